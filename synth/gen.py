@@ -1,0 +1,184 @@
+"""Seeded synthetic workloads (SURVEY.md §8(d) "Synthetic inputs").
+
+Every generator is keyed by integers only, so the oracle side and the CUDA side
+receive bit-identical p-bit inputs.  Nothing here implements the method:
+  * gaussian_records  — iid N(0, 1/2) reals (complex entries N(0,1/2)+iN(0,1/2)):
+                        a float64 normal deviate supplies the top 53 bits, the
+                        remaining p-53 mantissa bits are uniform random bits;
+  * haar_unitary      — complex Gaussian d x d, modified Gram-Schmidt twice in
+                        mpmath at p+32 bits (R's diagonal comes out real-positive,
+                        so Q is Haar distributed), rounded to p bits;
+  * circuits for BASELINE.json configs 1, 3, 4, 5 (brick-wall layouts).
+Seeds: 0x11113124 + config index (0-based, BASELINE order), streams keyed
+(seed, layer, position) through numpy SeedSequence.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import records as R
+
+SEED0 = 0x11113124
+
+
+def rng(*key) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence([int(k) & 0xFFFFFFFF for k in key])))
+
+
+def gaussian_records(p: int, n: int, *key, scale_exp: int = 0, sigma: float = 0.7071067811865476) -> np.ndarray:
+    """n real records ~ N(0, sigma^2) * 2^scale_exp with p random significant bits."""
+    g = rng(*key)
+    x = g.standard_normal(n) * sigma
+    a = R.empty(p, n)
+    L = R.nlimbs(p)
+    m, e = np.frexp(np.abs(x))                       # |x| = m 2^e, m in [0.5, 1)
+    man53 = np.ldexp(m, 53).astype(np.uint64)        # 53-bit integer mantissa (top bit set)
+    limbs = g.integers(0, 1 << 32, size=(n, L), dtype=np.uint64)
+    limbs[:, L - 1] = man53 >> np.uint64(21)
+    limbs[:, L - 2] = ((man53 & np.uint64((1 << 21) - 1)) << np.uint64(11)) | (limbs[:, L - 2] & np.uint64((1 << 11) - 1))
+    drop = 32 * L - p                                # low bits that must be zero
+    if drop:
+        limbs[:, 0] &= np.uint64((0xFFFFFFFF >> drop) << drop)
+    a["limb"] = limbs.astype(np.uint32)
+    a["exp"] = e.astype(np.int64) + scale_exp
+    a["sign"] = (x < 0).astype(np.uint32)
+    zero = x == 0
+    if zero.any():
+        a["exp"][zero] = R.INT64_MIN
+        a["limb"][zero] = 0
+    return a
+
+
+def gaussian_cplx(p: int, n: int, *key, scale_exp: int = 0) -> np.ndarray:
+    """n complex records (2n reals, re/im interleaved), entries N(0,1/2) + i N(0,1/2)."""
+    return gaussian_records(p, 2 * n, *key, scale_exp=scale_exp)
+
+
+def haar_unitary(p: int, d: int, *key) -> np.ndarray:
+    """d x d Haar unitary (row-major complex records)."""
+    import mpmath
+    z = gaussian_cplx(p + 32, d * d, *key)
+    with mpmath.workprec(p + 32):
+        vals = [R.to_mpf(z[i]) for i in range(2 * d * d)]
+        Z = [[mpmath.mpc(vals[2 * (r * d + c)], vals[2 * (r * d + c) + 1]) for c in range(d)] for r in range(d)]
+        cols = [[Z[r][c] for r in range(d)] for c in range(d)]
+        for _ in range(2):  # modified Gram-Schmidt, twice
+            for c in range(d):
+                v = cols[c]
+                for b in range(c):
+                    u = cols[b]
+                    h = mpmath.fsum(mpmath.conj(u[r]) * v[r] for r in range(d))
+                    v = [v[r] - h * u[r] for r in range(d)]
+                nrm = mpmath.sqrt(mpmath.fsum(abs(x) ** 2 for x in v))
+                cols[c] = [x / nrm for x in v]
+    out = R.empty(p, 2 * d * d)
+    with mpmath.workprec(p):
+        for r in range(d):
+            for c in range(d):
+                x = cols[c][r]
+                R.from_fraction(p, +mpmath.mpf(x.real), out[2 * (r * d + c)])
+                R.from_fraction(p, +mpmath.mpf(x.imag), out[2 * (r * d + c) + 1])
+    return out
+
+
+def const_gate(p: int, name: str) -> np.ndarray:
+    """Named gates (row-major complex records, p-bit rounded entries)."""
+    import mpmath
+    with mpmath.workprec(p):
+        h = +(1 / mpmath.sqrt(2))
+        I2 = [[1, 0], [0, 1]]
+        tbl = {
+            "I": I2,
+            "X": [[0, 1], [1, 0]],
+            "Z": [[1, 0], [0, -1]],
+            "H": [[h, h], [h, -h]],
+            "CNOT": [[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 0, 1], [0, 0, 1, 0]],
+            "SWAP": [[1, 0, 0, 0], [0, 0, 1, 0], [0, 1, 0, 0], [0, 0, 0, 1]],
+            "CZ": [[1, 0, 0, 0], [0, 1, 0, 0], [0, 0, 1, 0], [0, 0, 0, -1]],
+            "I4": [[1 if i == j else 0 for j in range(4)] for i in range(4)],
+        }
+        m = tbl[name]
+        d = len(m)
+        out = R.empty(p, 2 * d * d)
+        for r in range(d):
+            for c in range(d):
+                R.from_fraction(p, mpmath.mpf(m[r][c]), out[2 * (r * d + c)])
+                R.from_fraction(p, 0, out[2 * (r * d + c) + 1])
+    return out
+
+
+def phase_swap_gate(p: int, m: int) -> np.ndarray:
+    """SWAP . diag(1,1,1,e^{2 pi i / 2^(m+2)}) (the nearest-neighbour QFT network gate)."""
+    import mpmath
+    with mpmath.workprec(p + 32):
+        th = 2 * mpmath.pi / mpmath.mpf(2) ** (m + 2)
+        c, s = mpmath.cos(th), mpmath.sin(th)
+    D = [[(1, 0), (0, 0), (0, 0), (0, 0)], [(0, 0), (1, 0), (0, 0), (0, 0)],
+         [(0, 0), (0, 0), (1, 0), (0, 0)], [(0, 0), (0, 0), (0, 0), (c, s)]]
+    SW = [0, 2, 1, 3]  # SWAP row permutation: (SWAP.D)[r] = D[SW[r]]
+    out = R.empty(p, 32)
+    with mpmath.workprec(p):
+        for r in range(4):
+            for col in range(4):
+                re, im = D[SW[r]][col]
+                R.from_fraction(p, +mpmath.mpf(re), out[2 * (r * 4 + col)])
+                R.from_fraction(p, +mpmath.mpf(im), out[2 * (r * 4 + col) + 1])
+    return out
+
+
+# --------------------------------------------------------------------- circuits
+def brickwall(n: int, depth: int, p: int, seed: int, one_site_layer: bool = False):
+    """List of (U records, sites) for a brick-wall circuit of Haar U(4) on (s, s+1),
+    layer t acting on s = t%2, t%2+2, ...; optionally a Haar U(2) on every qubit
+    after each U(4) layer (BASELINE configs[0], [2], [4])."""
+    gates = []
+    for t in range(depth):
+        for s in range(t % 2, n - 1, 2):
+            gates.append((haar_unitary(p, 4, seed, t, s), (s, s + 1)))
+        if one_site_layer:
+            for q in range(n):
+                gates.append((haar_unitary(p, 2, seed, t, 1000 + q), (q,)))
+    return gates
+
+
+def triples(n: int, depth: int, p: int, seed: int):
+    """Haar U(8) on (o+3j, o+3j+1, o+3j+2), o = t mod 3 (BASELINE configs[3])."""
+    gates = []
+    for t in range(depth):
+        o = t % 3
+        s = o
+        while s + 2 <= n - 1:
+            gates.append((haar_unitary(p, 8, seed, t, s), (s, s + 1, s + 2)))
+            s += 3
+    return gates
+
+
+def config_circuit(idx: int, p: int | None = None, depth: int | None = None):
+    """(n, p, chi_max, thr, gates) for BASELINE.json configs[idx] (idx in 0, 2, 3, 4)."""
+    seed = SEED0 + idx
+    if idx == 0:
+        p = p or 280
+        return 8, p, 16, 2.0 ** -140, brickwall(8, depth or 8, p, seed)
+    if idx == 2:
+        p = p or 280
+        return 32, p, 64, 1e-60, brickwall(32, depth or 20, p, seed, one_site_layer=True)
+    if idx == 3:
+        p = p or 280
+        return 20, p, 128, 2.0 ** -140, triples(20, depth or 16, p, seed)
+    if idx == 4:
+        p = p or 512
+        return 64, p, 256, 2.0 ** -256, brickwall(64, depth or 40, p, seed)
+    raise ValueError(idx)
+
+
+def update_batch_inputs(p: int, chi: int, batch: int, seed: int = SEED0 + 1, first: int = 0):
+    """Configs[1] items first..first+batch-1: Gamma_A, Gamma_B in C^{2 x chi x chi} iid,
+    lambda = 1, Haar U(4).  Entry variance chosen so ||Theta||_F ~ 1 (a power-of-two scale,
+    SURVEY §8(c) ledger #17): E|Theta_ij|^2 = chi s^4 with s^2 = 2^(2*scale_exp)... we scale
+    each Gamma by 2^-e with e = round(log2(4 chi^3)/4)."""
+    import math
+    e = -int(round(math.log2(4.0 * chi ** 3) / 4.0))
+    A = np.concatenate([gaussian_cplx(p, 2 * chi * chi, seed, b, 0, scale_exp=e) for b in range(first, first + batch)])
+    B = np.concatenate([gaussian_cplx(p, 2 * chi * chi, seed, b, 1, scale_exp=e) for b in range(first, first + batch)])
+    U = np.concatenate([haar_unitary(p, 4, seed, b, 2) for b in range(first, first + batch)])
+    return A, B, U
