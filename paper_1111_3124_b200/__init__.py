@@ -1,0 +1,157 @@
+"""Python binding of libmps_b200.so (include/mps_b200.h) — argument marshalling only.
+
+Every step of the gate update runs in the sm_100a kernels behind the C ABI; this
+module converts numpy record arrays / torch device tensors to pointers and raises
+on error statuses.  There is no CPU fallback: if the CUDA library is missing or no
+CUDA device is present, calls fail loudly (MpsError / ImportError).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libmps_b200.so")
+
+STATUS = {0: "MPS_OK", -1: "MPS_EINVAL", -2: "MPS_ENOTUNITARY", -3: "MPS_ENOCONV", -4: "MPS_EZEROBOND",
+          -5: "MPS_EOVERLAP", -6: "MPS_EUNSUPPORTED", -7: "MPS_ENOMEM", -8: "MPS_ECUDA", -9: "MPS_ENCCL",
+          -10: "MPS_ETOOBIG"}
+
+# every symbol include/mps_b200.h declares
+EXPORTS = ["mps_svd_batch", "mps_debug_mpf", "mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
+           "mps_apply_gate", "mps_apply_layer", "mps_amplitude", "mps_expect", "mps_norm2", "mps_to_dense",
+           "mps_sync", "mps_n_qubits", "mps_bond_dims", "mps_schmidt", "mps_get_site", "mps_set_schmidt",
+           "mps_set_site", "mps_stats", "mps_bench_update_batch", "mps_update_batch_workspace",
+           "mps_update_batch_device", "mps_last_launch_count"]
+
+
+class MpsError(RuntimeError):
+    def __init__(self, rc: int, what: str = ""):
+        super().__init__(f"{STATUS.get(rc, rc)}{': ' + what if what else ''}")
+        self.rc = rc
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise ImportError(f"{_SO} not built: run python -c 'import __graft_entry__ as g; g.build()'")
+        L = ctypes.CDLL(_SO)
+        vp, ci, cd, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_size_t
+        L.mps_record_bytes.restype = sz
+        L.mps_strerror.restype = ctypes.c_char_p
+        L.mps_update_batch_workspace.restype = sz
+        L.mps_update_batch_workspace.argtypes = [ci, ci, ci]
+        L.mps_bench_update_batch.argtypes = [ci, ci, ci, ci, cd] + [vp] * 6 + [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.mps_update_batch_device.argtypes = [ci, ci, ci, ci, cd] + [vp] * 6 + [vp] * 8
+        L.mps_svd_batch.argtypes = [ci, ci, ci, ci, vp, vp, vp, vp]
+        L.mps_debug_mpf.argtypes = [ci, ci, ci, vp, vp, vp]
+        if hasattr(L, "mps_init"):
+            L.mps_init.argtypes = [ctypes.POINTER(vp), ci, ci, ci, cd]
+            L.mps_free.argtypes = [vp]
+            L.mps_set_stream.argtypes = [vp, vp]
+            L.mps_apply_gate.argtypes = [vp, vp, vp, ci]
+            L.mps_apply_layer.argtypes = [vp, ci, vp, vp, vp]
+            L.mps_amplitude.argtypes = [vp, vp, vp]
+            L.mps_expect.argtypes = [vp, vp, vp, ci, vp]
+            L.mps_norm2.argtypes = [vp, vp]
+            L.mps_to_dense.argtypes = [vp, vp]
+            L.mps_sync.argtypes = [vp]
+            L.mps_n_qubits.argtypes = [vp]
+            L.mps_bond_dims.argtypes = [vp, vp]
+            L.mps_schmidt.argtypes = [vp, ci, vp, vp]
+            L.mps_get_site.argtypes = [vp, ci, vp, vp, vp]
+            L.mps_set_schmidt.argtypes = [vp, ci, vp, ci]
+            L.mps_set_site.argtypes = [vp, ci, vp, ci, ci]
+            L.mps_stats.argtypes = [vp, vp, sz]
+        _lib = L
+    return _lib
+
+
+def _chk(rc: int, what: str = ""):
+    if rc != 0:
+        raise MpsError(rc, what)
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data_as(ctypes.c_void_p)
+    if hasattr(a, "data_ptr"):  # torch tensor
+        return ctypes.c_void_p(a.data_ptr())
+    return a
+
+
+def record_bytes(p: int) -> int:
+    return int(lib().mps_record_bytes(p))
+
+
+def _empty(p, n):
+    from synth import records as R  # record dtype helper (format only)
+    return R.empty(p, n)
+
+
+def update_batch(p: int, chi: int, batch: int, A, B, U, lam_l=None, lam_m=None, lam_r=None, chi_max: int | None = None,
+                 thr: float = 0.0, theta: bool = False, stream=None):
+    """Batched two-site update through mps_bench_update_batch (host records in/out)."""
+    chi_max = chi_max or chi
+    out = {}
+    if theta:
+        th = _empty(p, batch * 2 * 4 * chi * chi)
+        rc = lib().mps_bench_update_batch(p, chi, chi_max, batch, thr, _p(A), _p(B), _p(lam_l), _p(lam_m), _p(lam_r),
+                                          _p(U), None, None, None, None, None, None, _p(th), stream)
+        _chk(rc, "mps_bench_update_batch")
+        return {"theta": th}
+    sig = _empty(p, batch * 2 * chi)
+    k = np.zeros(batch, np.int32)
+    Ao = _empty(p, batch * 2 * 2 * chi * chi_max)
+    Bo = _empty(p, batch * 2 * 2 * chi_max * chi)
+    lam = _empty(p, batch * chi_max)
+    sw = np.zeros(batch, np.int32)
+    rc = lib().mps_bench_update_batch(p, chi, chi_max, batch, thr, _p(A), _p(B), _p(lam_l), _p(lam_m), _p(lam_r),
+                                      _p(U), _p(sig), _p(k), _p(Ao), _p(Bo), _p(lam), _p(sw), None, stream)
+    _chk(rc, "mps_bench_update_batch")
+    out.update(sigma=sig, k=k, GL=Ao, GR=Bo, lam=lam, sweeps=sw)
+    return out
+
+
+def update_batch_workspace(p: int, chi: int, batch: int) -> int:
+    return int(lib().mps_update_batch_workspace(p, chi, batch))
+
+
+def update_batch_device(p, chi, chi_max, batch, thr, dA, dB, dU, dsigma, dk, dA_out, dB_out, dlam, dsweeps, dws,
+                        stream=None, dlam_l=None, dlam_m=None, dlam_r=None):
+    """Same on torch CUDA tensors (no host copies)."""
+    rc = lib().mps_update_batch_device(p, chi, chi_max, batch, thr, _p(dA), _p(dB), _p(dlam_l), _p(dlam_m),
+                                       _p(dlam_r), _p(dU), _p(dsigma), _p(dk), _p(dA_out), _p(dB_out), _p(dlam),
+                                       _p(dsweeps), _p(dws), stream)
+    _chk(rc, "mps_update_batch_device")
+
+
+def last_launch_count() -> int:
+    return int(lib().mps_last_launch_count())
+
+
+def svd_batch(p: int, M: int, N: int, batch: int, A):
+    """sigma (descending), sweeps, rotations per sweep of column-major M x N matrices."""
+    n = min(M, N)
+    sig = _empty(p, batch * n)
+    sw = np.zeros(batch, np.int32)
+    rps = np.zeros(batch * 64, np.int32)
+    rc = lib().mps_svd_batch(p, M, N, batch, _p(A), _p(sig), _p(sw), _p(rps))
+    if rc not in (0, -3):
+        _chk(rc, "mps_svd_batch")
+    return sig, sw, rps.reshape(batch, 64), rc
+
+
+def debug_mpf(p: int, op: str, a, b=None):
+    ops = {"add": 0, "sub": 1, "mul": 2, "div": 3, "sqrt": 4, "rsqrt": 5, "recip": 6, "copy": 7, "fixed": 8}
+    out = _empty(p, len(a))
+    _chk(lib().mps_debug_mpf(p, ops[op], len(a), _p(a), _p(b), _p(out)), "mps_debug_mpf")
+    return out

@@ -1,0 +1,207 @@
+// C ABI (include/mps_b200.h): validation, tier dispatch, host<->device marshalling.
+// Every computation of the method runs in the kernels of kernels.cuh; this file only
+// moves records, checks arguments and sequences launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mps_b200.h"
+#include "common.h"
+
+using namespace mpsb;
+
+static thread_local int g_last_launches = 0;
+
+extern "C" {
+
+size_t mps_record_bytes(int p) { return 16 + 4 * (size_t)((p + 31) / 32); }
+
+const char* mps_strerror(int s) {
+  switch (s) {
+    case MPS_OK: return "ok";
+    case MPS_EINVAL: return "invalid argument";
+    case MPS_ENOTUNITARY: return "gate is not unitary at working precision";
+    case MPS_ENOCONV: return "Jacobi SVD did not converge";
+    case MPS_EZEROBOND: return "all Schmidt coefficients below the truncation floor";
+    case MPS_EOVERLAP: return "gates of a layer overlap";
+    case MPS_EUNSUPPORTED: return "unsupported precision or size";
+    case MPS_ENOMEM: return "out of device memory";
+    case MPS_ECUDA: return "CUDA error (or no CUDA device)";
+    case MPS_ENCCL: return "NCCL error";
+    case MPS_ETOOBIG: return "state too large";
+    default: return "unknown status";
+  }
+}
+
+int mps_max_chi(void) { return MAX_CHI; }
+int mps_last_launch_count(void) { return g_last_launches; }
+
+size_t mps_update_batch_workspace(int p, int chi, int batch) {
+  if (p < 64 || p > 512 || chi < 1 || chi > MAX_CHI || batch < 1) return 0;
+  return p <= 280 ? update2_workspace<Tier280>(chi, batch) : update2_workspace<Tier512>(chi, batch);
+}
+
+int mps_update_batch_device(int p, int chi, int chi_max, int batch, double thr, const void* dA,
+                            const void* dB, const void* dlam_l, const void* dlam_m, const void* dlam_r,
+                            const void* dU, void* dsigma, int* dk_out, void* dA_out, void* dB_out,
+                            void* dlam_out, int* dsweeps, void* dws, void* stream) {
+  if (p < 64 || p > 512 || chi < 1 || chi > MAX_CHI || batch < 1 || chi_max < 1 || !dA || !dB || !dU || !dws)
+    return MPS_EINVAL;
+  if (thr <= 0) thr = std::ldexp(1.0, -((p + 1) / 2));
+  BatchOut o{(uint32_t*)dsigma, dk_out, (uint32_t*)dA_out, (uint32_t*)dB_out, (uint32_t*)dlam_out, dsweeps, nullptr};
+  std::vector<unsigned char> hd;
+  cudaStream_t st = (cudaStream_t)stream;
+  int nl;
+  if (p <= 280)
+    nl = launch_update2_batch<Tier280>(p, chi, chi_max, batch, thr, (const uint32_t*)dA, (const uint32_t*)dB,
+                                       (const uint32_t*)dlam_l, (const uint32_t*)dlam_m, (const uint32_t*)dlam_r,
+                                       (const uint32_t*)dU, o, dws, st, hd);
+  else
+    nl = launch_update2_batch<Tier512>(p, chi, chi_max, batch, thr, (const uint32_t*)dA, (const uint32_t*)dB,
+                                       (const uint32_t*)dlam_l, (const uint32_t*)dlam_m, (const uint32_t*)dlam_r,
+                                       (const uint32_t*)dU, o, dws, st, hd);
+  // the host descriptor buffer must outlive the async copy
+  cudaStreamSynchronize(st);
+  g_last_launches = nl;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? MPS_OK : MPS_ECUDA;
+}
+
+int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, const void* A, const void* B,
+                           const void* lam_l, const void* lam_m, const void* lam_r, const void* U, void* sigma,
+                           int* k_out, void* A_out, void* B_out, void* lam_out, int* sweeps, void* theta_debug,
+                           void* stream) {
+  if (p < 64 || p > 512 || chi < 1 || chi > MAX_CHI || batch < 1 || chi_max < 1 || !A || !B || !U)
+    return MPS_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MPS_ECUDA;
+  if (thr <= 0) thr = std::ldexp(1.0, -((p + 1) / 2));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t rb = mps_record_bytes(p), cb = 2 * rb;
+  const size_t nA = (size_t)batch * 2 * chi * chi * cb;
+  const size_t nLam = (size_t)batch * chi * rb;
+  const size_t nU = (size_t)batch * 16 * cb;
+  const size_t nSig = (size_t)batch * 2 * chi * rb;
+  const size_t nAo = (size_t)batch * 2 * chi * chi_max * cb;
+  const size_t nLo = (size_t)batch * chi_max * rb;
+  const size_t nTh = (size_t)batch * 4 * chi * chi * cb;
+  const size_t ws = mps_update_batch_workspace(p, chi, batch);
+  size_t tot = 0;
+  auto slot = [&](size_t n) { size_t o = tot; tot += align_up(n); return o; };
+  size_t oA = slot(nA), oB = slot(nA), oll = slot(lam_l ? nLam : 0), olm = slot(lam_m ? nLam : 0),
+         olr = slot(lam_r ? nLam : 0), oU = slot(nU), oS = slot(nSig), oK = slot(4 * (size_t)batch),
+         oAo = slot(nAo), oBo = slot(nAo), oLo = slot(nLo), oSw = slot(4 * (size_t)batch),
+         oTh = slot(theta_debug ? nTh : 0), oWs = slot(ws);
+  char* d = nullptr;
+  if (cudaMalloc(&d, tot) != cudaSuccess) return MPS_ENOMEM;
+  cudaMemcpyAsync(d + oA, A, nA, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d + oB, B, nA, cudaMemcpyHostToDevice, st);
+  if (lam_l) cudaMemcpyAsync(d + oll, lam_l, nLam, cudaMemcpyHostToDevice, st);
+  if (lam_m) cudaMemcpyAsync(d + olm, lam_m, nLam, cudaMemcpyHostToDevice, st);
+  if (lam_r) cudaMemcpyAsync(d + olr, lam_r, nLam, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d + oU, U, nU, cudaMemcpyHostToDevice, st);
+  BatchOut o{(uint32_t*)(d + oS), (int*)(d + oK), (uint32_t*)(d + oAo), (uint32_t*)(d + oBo),
+             (uint32_t*)(d + oLo), (int*)(d + oSw), theta_debug ? (uint32_t*)(d + oTh) : nullptr};
+  cudaMemsetAsync(d + oAo, 0, nAo, st);
+  cudaMemsetAsync(d + oBo, 0, nAo, st);
+  std::vector<unsigned char> hd;
+  int nl;
+  const uint32_t* ll = lam_l ? (const uint32_t*)(d + oll) : nullptr;
+  const uint32_t* lm = lam_m ? (const uint32_t*)(d + olm) : nullptr;
+  const uint32_t* lr = lam_r ? (const uint32_t*)(d + olr) : nullptr;
+  if (p <= 280)
+    nl = launch_update2_batch<Tier280>(p, chi, chi_max, batch, thr, (const uint32_t*)(d + oA),
+                                       (const uint32_t*)(d + oB), ll, lm, lr, (const uint32_t*)(d + oU), o,
+                                       d + oWs, st, hd);
+  else
+    nl = launch_update2_batch<Tier512>(p, chi, chi_max, batch, thr, (const uint32_t*)(d + oA),
+                                       (const uint32_t*)(d + oB), ll, lm, lr, (const uint32_t*)(d + oU), o,
+                                       d + oWs, st, hd);
+  g_last_launches = nl;
+  if (theta_debug) cudaMemcpyAsync(theta_debug, d + oTh, nTh, cudaMemcpyDeviceToHost, st);
+  if (sigma) cudaMemcpyAsync(sigma, d + oS, nSig, cudaMemcpyDeviceToHost, st);
+  if (k_out) cudaMemcpyAsync(k_out, d + oK, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
+  if (A_out) cudaMemcpyAsync(A_out, d + oAo, nAo, cudaMemcpyDeviceToHost, st);
+  if (B_out) cudaMemcpyAsync(B_out, d + oBo, nAo, cudaMemcpyDeviceToHost, st);
+  if (lam_out) cudaMemcpyAsync(lam_out, d + oLo, nLo, cudaMemcpyDeviceToHost, st);
+  if (sweeps) cudaMemcpyAsync(sweeps, d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
+    return MPS_ECUDA;
+  }
+  if (!theta_debug && k_out) {
+    for (int b = 0; b < batch; ++b)
+      if (k_out[b] == 0) return MPS_EZEROBOND;
+  }
+  if (!theta_debug && sweeps) {
+    for (int b = 0; b < batch; ++b)
+      if (sweeps[b] > JACOBI_MAX_SWEEPS) return MPS_ENOCONV;
+  }
+  return MPS_OK;
+}
+
+int mps_svd_batch(int p, int M, int N, int batch, const void* A, void* sigma, int* sweeps, int* rot_per_sweep) {
+  if (p < 64 || p > 512 || M < 1 || N < 1 || batch < 1 || !A || !sigma || std::min(M, N) > 2 * MAX_CHI ||
+      std::max(M, N) > 4 * MAX_CHI)
+    return MPS_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MPS_ECUDA;
+  const size_t rb = mps_record_bytes(p);
+  const size_t nA = (size_t)batch * M * N * 2 * rb, nS = (size_t)batch * std::min(M, N) * rb;
+  const size_t ws = p <= 280 ? svd_workspace<Tier280>(M, N, batch) : svd_workspace<Tier512>(M, N, batch);
+  size_t tot = 0;
+  auto slot = [&](size_t n) { size_t o = tot; tot += align_up(n); return o; };
+  size_t oA = slot(nA), oS = slot(nS), oSw = slot(4 * (size_t)batch), oD = slot(256 * (size_t)batch), oW = slot(ws);
+  char* d = nullptr;
+  if (cudaMalloc(&d, tot) != cudaSuccess) return MPS_ENOMEM;
+  cudaStream_t st = 0;
+  cudaMemcpyAsync(d + oA, A, nA, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(d + oD, 0, 256 * (size_t)batch, st);
+  std::vector<unsigned char> hd;
+  int nl = p <= 280 ? run_svd_batch<Tier280>(p, M, N, batch, (const uint32_t*)(d + oA), (uint32_t*)(d + oS),
+                                             (int*)(d + oSw), (int*)(d + oD), d + oW, st, hd)
+                    : run_svd_batch<Tier512>(p, M, N, batch, (const uint32_t*)(d + oA), (uint32_t*)(d + oS),
+                                             (int*)(d + oSw), (int*)(d + oD), d + oW, st, hd);
+  g_last_launches = nl;
+  std::vector<int> sw(batch);
+  cudaMemcpyAsync(sigma, d + oS, nS, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(sw.data(), d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
+  if (rot_per_sweep) cudaMemcpyAsync(rot_per_sweep, d + oD, 256 * (size_t)batch, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  cudaFree(d);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
+    return MPS_ECUDA;
+  }
+  if (sweeps) std::memcpy(sweeps, sw.data(), 4 * (size_t)batch);
+  for (int b = 0; b < batch; ++b)
+    if (sw[b] > JACOBI_MAX_SWEEPS) return MPS_ENOCONV;
+  return MPS_OK;
+}
+
+int mps_debug_mpf(int p, int op, int n, const void* a, const void* b, void* out) {
+  if (p < 64 || p > 512 || n < 1 || op < 0 || op > 8 || !a || !out) return MPS_EINVAL;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MPS_ECUDA;
+  const size_t nb = (size_t)n * mps_record_bytes(p);
+  char* d = nullptr;
+  if (cudaMalloc(&d, 3 * align_up(nb)) != cudaSuccess) return MPS_ENOMEM;
+  cudaMemcpy(d, a, nb, cudaMemcpyHostToDevice);
+  if (b) cudaMemcpy(d + align_up(nb), b, nb, cudaMemcpyHostToDevice);
+  uint32_t* o = (uint32_t*)(d + 2 * align_up(nb));
+  if (p <= 280)
+    run_debug_mpf<Tier280>(p, op, n, (const uint32_t*)d, b ? (const uint32_t*)(d + align_up(nb)) : nullptr, o, 0);
+  else
+    run_debug_mpf<Tier512>(p, op, n, (const uint32_t*)d, b ? (const uint32_t*)(d + align_up(nb)) : nullptr, o, 0);
+  cudaError_t e = cudaMemcpy(out, o, nb, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? MPS_OK : MPS_ECUDA;
+}
+
+}  // extern "C"

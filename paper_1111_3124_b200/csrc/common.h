@@ -1,0 +1,42 @@
+// Host-visible declarations shared by the translation units (capi.cu, state.cu,
+// tier280.cu, tier512.cu).  Kernels are instantiated once per precision tier.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace mpsb {
+
+constexpr int MAX_CHI = 256;
+constexpr int JACOBI_MAX_SWEEPS = 60;  // then MPS_ENOCONV; a failed run reports 61 sweeps
+// precision tiers: L = radix-2^28 digits of the Jacobi format (W = 28L bits >= p),
+// NL = u32 limbs of the scalar mpf format (one guard limb above the record width)
+struct Tier280 { static constexpr int L = 10, NL = 10; };
+struct Tier512 { static constexpr int L = 19, NL = 17; };
+
+inline int record_words(int p) { return 4 + (p + 31) / 32; }
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct BatchOut {  // device pointers (records unless stated)
+  uint32_t* sigma; int* k; uint32_t* A_out; uint32_t* B_out; uint32_t* lam; int* sweeps;
+  uint32_t* theta_dbg;
+};
+
+template <class T>
+int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, const uint32_t* A,
+                         const uint32_t* B, const uint32_t* lam_l, const uint32_t* lam_m,
+                         const uint32_t* lam_r, const uint32_t* U, const BatchOut& out, void* ws,
+                         cudaStream_t st, std::vector<unsigned char>& hostdesc);
+template <class T>
+size_t update2_workspace(int chi, int batch);
+template <class T>
+size_t svd_workspace(int M, int N, int batch);
+template <class T>
+int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* dsig, int* dsweeps, int* ddbg,
+                  void* ws, cudaStream_t st, std::vector<unsigned char>& hd);
+template <class T>
+void run_debug_mpf(int p, int op, int n, const uint32_t* a, const uint32_t* b, uint32_t* out, cudaStream_t st);
+
+}  // namespace mpsb

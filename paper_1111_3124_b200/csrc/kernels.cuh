@@ -1,0 +1,955 @@
+// sm_100a kernels of the MPS gate update.
+// Every kernel works on a batch of independent "items" (gates or cfg2 matrices);
+// per-item geometry and pointers live in small device descriptor arrays.
+//
+// Fixed-point matrix layout (the Jacobi working format):
+//   digits  d[((col*2 + ri)*L + k)*ld + row]   (int32, balanced radix-2^28)
+//   value   (sum_k d_k 2^(28k)) * 2^(e_col - 28L),  ri = 0 re / 1 im
+// so a warp reading 32 consecutive rows of one digit plane issues one coalesced
+// 128-byte transaction.  Store records are AoS (include/mps_b200.h format).
+#pragma once
+#include <cstdint>
+
+#include "common.h"
+#include "mp.cuh"
+
+namespace mpsb {
+
+constexpr int NTHR = 256;  // threads per CTA of the per-item kernels
+constexpr int NWARP = NTHR / 32;
+constexpr int MAX_SWEEPS = JACOBI_MAX_SWEEPS;
+
+// ----------------------------------------------------------------------------
+// item descriptors
+// ----------------------------------------------------------------------------
+// Build a fixed matrix from a site tensor G [2][da][db] (records):
+//   mode 0: rows (i,a) = i*da + a, cols b      F = lamL(a) G^i(a,b) lamR(b)
+//   mode 1: rows a, cols (i,b) = i*db + b      F = lamL(a) G^i(a,b) lamR(b)
+struct PrepItem {
+  const uint32_t* G;        // records
+  const uint32_t* lamL;     // da records or null (= ones)
+  const uint32_t* lamR;     // db records or null
+  int da, db, mode;
+  int32_t* F;               // digits, ld = rows
+  int64_t* eF;              // block exponent (1 value)
+};
+
+// C = op(A) * B, op(A) = A or A^H ; block exponents; C rows x cols, inner K
+struct GemmItem {
+  const int32_t* A; int lda; const int64_t* eA;
+  const int32_t* B; int ldb; const int64_t* eB;
+  int32_t* C; int ldc; int64_t* eC;
+  int rows, cols, K, conjA;  // conjA: A stored K x rows, use conj transpose
+};
+
+// Theta'(x-block) = sum_y U[x][y] Theta(y-block); rows = RB*chiL, cols = 2*chiR,
+// x = 2*rowblock + colblock (qubit of the first site most significant).
+// Output in Jacobi layout: A (M x N) with per-column exponents; trans -> A = Theta'^H.
+struct MixItem {
+  const int32_t* T; int ldt; const int64_t* eT;   // Theta (block exponent)
+  const uint32_t* U;                              // D x D complex records
+  int RB, chiL, chiR;                             // D = 2*RB
+  int trans;
+  int32_t* A; int64_t* eA; int M, N;              // output Jacobi matrix (M >= N)
+};
+
+template <int NL>
+struct SvdItem {
+  int M, N;                 // Jacobi matrix, N <= M, N even (padded)
+  int32_t* A; int64_t* eA;  // [N][2][L][M], [N]
+  int32_t* V;               // [N][2][L][N], exponent fixed = 1
+  mpf<NL>* alpha;           // [N] squared column norms (output: final)
+  mpf<NL>* gam;             // [N/2][2] scratch
+  int32_t* coef;            // [N/2][9][L+1] scratch (L fractional digits + one integer digit)
+  int* dbg;                 // [64] rotations per sweep, or null
+  int* rot;                 // [N/2] scratch
+  int* negl;                // [N] scratch
+  int* status;              // out: 0 / MPS_ENOCONV
+  int* sweeps;              // out
+  long long* rotations;     // out
+};
+
+// Sort / truncate / renormalise one SVD result and produce the split outputs.
+template <int NL>
+struct FinItem {
+  int M, N, trans;          // Jacobi geometry; Theta' is (trans ? N x M : M x N)
+  const int32_t* A; const int64_t* eA; const int32_t* V;
+  const mpf<NL>* alpha;
+  int chi_max;
+  mpf<NL> thr;              // truncation threshold
+  // scratch / outputs (device)
+  int* ord;                 // [N] sorted column order
+  mpf<NL>* inv_sig;         // [N] 1/sigma of sorted kept columns
+  mpf<NL>* lam;             // [N] lambda' of kept (mpf)
+  int* k_out;               // 1
+  int* status;              // 1
+  uint32_t* sigma_rec;      // [nsig] records (sigma, descending) or null
+  int nsig;                 // number of sigma records to write (<= N)
+  uint32_t* lam_rec;        // [k] records or null
+  // split outputs (records) — left: Gamma_L[i][a][b] = Ul[(i,a),b] / lamL(a)
+  uint32_t* GL; int GL_ld;  // row stride (>= k) in complex records, or null
+  const uint32_t* lamL;     // chiL records (null = ones)
+  int chiL_out;             // rows of Ul = 2*chiL_out  (i, a)
+  // right: Gamma_R[j][b][c] = conj(Wr[(j,c),b]) / lamR(c)
+  uint32_t* GR; int GR_ld;  // GR[(j*GR_ld + b)*chiR + c]
+  const uint32_t* lamR;     // chiR records (null = ones)
+  int chiR_out;
+  // optional M2 build (three-site): M2[(i,a),(j,b)] = Ul[(2i+j)chiL2 + a, b] * w_b
+  int32_t* M2; int64_t* eM2; int M2_trans; int chiL2;
+};
+
+// ----------------------------------------------------------------------------
+// helpers
+// ----------------------------------------------------------------------------
+template <int L>
+__device__ __forceinline__ void ldfx(const int32_t* base, int ld, int col, int ri, int row, int32_t (&x)[L]) {
+  const int32_t* p = base + ((size_t)(col * 2 + ri) * L) * ld + row;
+#pragma unroll
+  for (int k = 0; k < L; ++k) x[k] = p[(size_t)k * ld];
+}
+template <int L>
+__device__ __forceinline__ void stfx(int32_t* base, int ld, int col, int ri, int row, const int32_t (&x)[L]) {
+  int32_t* p = base + ((size_t)(col * 2 + ri) * L) * ld + row;
+#pragma unroll
+  for (int k = 0; k < L; ++k) p[(size_t)k * ld] = x[k];
+}
+
+__device__ __forceinline__ int64_t rec_exp(const uint32_t* rec) { return rec_get_exp(rec); }
+
+// keep-carry normalisation of L+2 accumulator columns (the last one absorbs)
+template <int L>
+__device__ __forceinline__ void tnorm2(int64_t (&acc)[L + 2]) {
+  int64_t carry = 0;
+#pragma unroll
+  for (int c = 0; c <= L; ++c) {
+    int64_t v = acc[c] + carry;
+    carry = (v + HALF) >> RADIX;
+    acc[c] = v - (carry << RADIX);
+  }
+  acc[L + 1] += carry;
+}
+template <int L>
+__device__ __forceinline__ void tmul_acc2(int64_t (&acc)[L + 2], const int32_t (&x)[L], const int32_t (&y)[L]) {
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(x[i], y[j], acc[i + j - (L - 2)]);
+}
+template <int L>
+__device__ __forceinline__ void tmul_sub2(int64_t (&acc)[L + 2], const int32_t (&x)[L], const int32_t (&y)[L]) {
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(-x[i], y[j], acc[i + j - (L - 2)]);
+}
+
+// Round sum V (acc columns L-2 .. 2L-1, acc[L+1] the top column) to
+// round(V 2^(-g) / 2^(28L)) for 0 <= g <= 27 (used by the GEMMs for head-room).
+template <int L>
+__device__ __forceinline__ void tround_sr(int64_t (&acc)[L + 2], int g, int32_t (&out)[L]) {
+  tnorm2<L>(acc);
+  // multiply by 2^(28-g): digits <= 2^27 * 2^28 fits
+  const int sh = 28 - g;
+  int64_t ext[L + 3];
+  int64_t carry = 0;
+#pragma unroll
+  for (int c = 0; c <= L + 1; ++c) {
+    int64_t v = (acc[c] << sh) + carry;
+    carry = (v + HALF) >> RADIX;
+    ext[c] = v - (carry << RADIX);
+  }
+  ext[L + 2] = carry;
+  // now V' = V 2^(28-g) with columns L-2 .. 2L ; result = round(V' / 2^(28(L+1)))
+  // -> drop ext[0], ext[1], ext[2] (columns L-2, L-1, L); keep ext[3..L+2] (L digits)
+  int64_t c0 = (ext[0] + HALF) >> RADIX;
+  int64_t c1 = (ext[1] + c0 + HALF) >> RADIX;
+  int64_t c2 = (ext[2] + c1 + HALF) >> RADIX;
+  carry = c2;
+#pragma unroll
+  for (int j = 0; j < L - 1; ++j) {
+    int64_t v = ext[j + 3] + carry;
+    carry = (v + HALF) >> RADIX;
+    out[j] = (int32_t)(v - (carry << RADIX));
+  }
+  out[L - 1] = (int32_t)(ext[L + 2] + carry);
+}
+
+// acc (L+2 columns: L-2 .. 2L-1) += K * x with K an (L+1)-digit coefficient
+// (digit L = integer part, only formed when hasInt); x an L-digit number.
+template <int L>
+__device__ __forceinline__ void kmul_acc(int64_t (&acc)[L + 2], const int32_t (&K)[L + 1], const int32_t (&x)[L],
+                                         bool hasInt) {
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(K[i], x[j], acc[i + j - (L - 2)]);
+  if (hasInt) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) acc[j + 2] = madw(K[L], x[j], acc[j + 2]);
+  }
+}
+template <int L>
+__device__ __forceinline__ void kmul_sub(int64_t (&acc)[L + 2], const int32_t (&K)[L + 1], const int32_t (&x)[L],
+                                         bool hasInt) {
+#pragma unroll
+  for (int i = 0; i < L; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(-K[i], x[j], acc[i + j - (L - 2)]);
+  if (hasInt) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) acc[j + 2] = madw(-K[L], x[j], acc[j + 2]);
+  }
+}
+// round(V / 2^(28L)) of the L+2 accumulator columns (L-2 .. 2L-1) to L digits
+template <int L>
+__device__ __forceinline__ void tround2(int64_t (&acc)[L + 2], int32_t (&out)[L]) {
+  tnorm2<L>(acc);
+  int64_t c0 = (acc[0] + HALF) >> RADIX;
+  int64_t carry = (acc[1] + c0 + HALF) >> RADIX;
+#pragma unroll
+  for (int j = 0; j < L - 1; ++j) {
+    int64_t v = acc[j + 2] + carry;
+    carry = (v + HALF) >> RADIX;
+    out[j] = (int32_t)(v - (carry << RADIX));
+  }
+  out[L - 1] = (int32_t)(acc[L + 1] + carry);
+}
+// mpf -> (L+1)-digit coefficient at scale 1 (value = sum d_k 2^(28k) 2^(-28L)), |a| < 2^27
+template <int NL, int L>
+__device__ __forceinline__ void mpf_to_coef(const mpf<NL>& a, int32_t* out) {
+  int32_t d[L + 1];
+  mpf_to_fixed<NL, L + 1>(a, 28, d);  // L+1 digits at exponent 28: same digit weights as E = 0, one more digit
+#pragma unroll
+  for (int k = 0; k <= L; ++k) out[k] = d[k];
+}
+
+template <int L>
+__device__ __forceinline__ void fx_to_cols(const int32_t (&x)[L], int64_t (&c)[L]) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) c[k] = x[k];
+}
+
+// log2 |a| as double (a != 0)
+template <int NL>
+__device__ __forceinline__ double mpf_log2(const mpf<NL>& a) {
+  int64_t E;
+  double f = fabs(mpf_frexp(a, &E));
+  return (double)E + log2(f);
+}
+
+// 64-bit warp all-reduce (sum)
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+__device__ __forceinline__ void rr_pair(int N, int step, int i, int& p, int& q) {
+  const int m = N - 1;
+  if (i == 0) { p = step; q = m; }
+  else { p = (step + i) % m; q = (step - i + m) % m; }
+  if (p > q) { int t = p; p = q; q = t; }
+}
+
+// ----------------------------------------------------------------------------
+// a1 preparation: scaled site tensor -> fixed matrix with a block exponent
+// ----------------------------------------------------------------------------
+static __global__ void k_init_exp(int64_t* e, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) e[i] = INT64_MIN;
+}
+// eL, eR (first two int64 of each item's small area) <- INT64_MIN
+static __global__ void k_init_exp_items(char* small0, size_t stride, int n) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n) {
+    int64_t* e = (int64_t*)(small0 + (size_t)b * stride);
+    e[0] = INT64_MIN;
+    e[1] = INT64_MIN;
+  }
+}
+
+// pass 1: block exponent upper bound = max over entries of exp(lamL)+exp(G)+exp(lamR)
+static __global__ void k_prep_exp(const PrepItem* items, int RB) {
+  const PrepItem it = items[blockIdx.y];
+  const int rb = RB;  // bytes per real record / 4
+  const int n = 2 * it.da * it.db;
+  int64_t best = INT64_MIN;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int i = t / (it.da * it.db), a = (t / it.db) % it.da, b = t % it.db;
+    const uint32_t* g = it.G + (size_t)(2 * t) * rb;
+    int64_t eg = max(rec_exp(g), rec_exp(g + rb));
+    if (eg == INT64_MIN) continue;
+    int64_t e = eg;
+    if (it.lamL) { int64_t x = rec_exp(it.lamL + (size_t)a * rb); if (x == INT64_MIN) continue; e += x; }
+    if (it.lamR) { int64_t x = rec_exp(it.lamR + (size_t)b * rb); if (x == INT64_MIN) continue; e += x; }
+    (void)i;
+    best = max(best, e);
+  }
+  // block reduce via atomics on the item exponent
+  if (best != INT64_MIN) atomicMax((long long*)it.eF, (long long)best);
+}
+
+template <int L, int NL>
+__global__ void k_prep_conv(const PrepItem* items, int RB) {
+  const PrepItem it = items[blockIdx.y];
+  const int rb = RB;
+  const int n = 2 * it.da * it.db;
+  int64_t E = *it.eF;
+  if (E == INT64_MIN) E = 0;  // all-zero tensor
+  const int rows = it.mode == 0 ? 2 * it.da : it.da;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int i = t / (it.da * it.db), a = (t / it.db) % it.da, b = t % it.db;
+    const uint32_t* g = it.G + (size_t)(2 * t) * rb;
+    mpf<NL> s = mpf_from_int<NL>(1);
+    bool zero = false;
+    if (it.lamL) s = mpf_from_record<NL>(it.lamL + (size_t)a * rb, rb - 4);
+    if (it.lamR) s = mpf_mul(s, mpf_from_record<NL>(it.lamR + (size_t)b * rb, rb - 4));
+    if (mpf_is_zero(s)) zero = true;
+    int row, col;
+    if (it.mode == 0) { row = i * it.da + a; col = b; }
+    else { row = a; col = i * it.db + b; }
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t d[L];
+      mpf<NL> v = zero ? mpf_zero<NL>() : mpf_mul(s, mpf_from_record<NL>(g + ri * rb, rb - 4));
+      mpf_to_fixed<NL, L>(v, E, d);
+      stfx<L>(it.F, rows, col, ri, row, d);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a1 contraction: batched complex fixed-point GEMM (one thread per C entry)
+// ----------------------------------------------------------------------------
+template <int L>
+__global__ void k_gemm(const GemmItem* items) {
+  const GemmItem it = items[blockIdx.y];
+  const int n = it.rows * it.cols;
+  // head-room: sum of K complex products each |.| < 2^(eA+eB+1)
+  int g = 1;
+  while ((1 << (g - 1)) < it.K) ++g;  // 2^(g-1) >= K
+  g += 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *it.eC = *it.eA + *it.eB + g;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % it.rows, c = t / it.rows;
+    int64_t ar[L + 2], ai[L + 2];
+#pragma unroll
+    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    int cnt = 0;
+    for (int k = 0; k < it.K; ++k) {
+      int32_t xr[L], xi[L], yr[L], yi[L];
+      if (it.conjA) {  // A stored K x rows: op(A)(r,k) = conj(A(k, r))
+        ldfx<L>(it.A, it.lda, r, 0, k, xr);
+        ldfx<L>(it.A, it.lda, r, 1, k, xi);
+#pragma unroll
+        for (int j = 0; j < L; ++j) xi[j] = -xi[j];
+      } else {
+        ldfx<L>(it.A, it.lda, k, 0, r, xr);
+        ldfx<L>(it.A, it.lda, k, 1, r, xi);
+      }
+      ldfx<L>(it.B, it.ldb, c, 0, k, yr);
+      ldfx<L>(it.B, it.ldb, c, 1, k, yi);
+      tmul_acc2<L>(ar, xr, yr);
+      tmul_sub2<L>(ar, xi, yi);
+      tmul_acc2<L>(ai, xr, yi);
+      tmul_acc2<L>(ai, xi, yr);
+      if (++cnt == 8) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); }
+    }
+    int32_t o[L];
+    tround_sr<L>(ar, g, o);
+    stfx<L>(it.C, it.ldc, c, 0, r, o);
+    tround_sr<L>(ai, g, o);
+    stfx<L>(it.C, it.ldc, c, 1, r, o);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a2 gate application -> Jacobi layout (one thread per Theta' entry)
+// ----------------------------------------------------------------------------
+template <int L, int NL>
+__global__ void k_mix(const MixItem* items, int RBr) {
+  const MixItem it = items[blockIdx.y];
+  const int D = 2 * it.RB;
+  const int rows = it.RB * it.chiL, cols = 2 * it.chiR;
+  const int n = rows * cols;
+  // U as fixed digits at exponent 1 (|U_xy| <= 1 < 2^1) — staged in shared memory
+  extern __shared__ int32_t su[];  // [D*D][2][L]
+  for (int t = threadIdx.x; t < D * D; t += blockDim.x) {
+    for (int ri = 0; ri < 2; ++ri) {
+      mpf<NL> u = mpf_from_record<NL>(it.U + (size_t)(2 * t + ri) * RBr, RBr - 4);
+      int32_t d[L];
+      mpf_to_fixed<NL, L>(u, 1, d);
+      for (int k = 0; k < L; ++k) su[(t * 2 + ri) * L + k] = d[k];
+    }
+  }
+  __syncthreads();
+  int g = 2;
+  while ((1 << (g - 2)) < D) ++g;  // sum of D terms, |U| <= 1 (modulus < 2^0.5 per comp)
+  const int64_t eOut = *it.eT + 1 + g;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % rows, c = t / rows;
+    const int rb = r / it.chiL, a = r % it.chiL, cb = c / it.chiR, gg = c % it.chiR;
+    const int x = 2 * rb + cb;
+    int64_t ar[L + 2], ai[L + 2];
+#pragma unroll
+    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    for (int y = 0; y < D; ++y) {
+      const int rr = (y >> 1) * it.chiL + a, cc = (y & 1) * it.chiR + gg;
+      int32_t tr[L], ti[L], ur[L], ui[L];
+      ldfx<L>(it.T, it.ldt, cc, 0, rr, tr);
+      ldfx<L>(it.T, it.ldt, cc, 1, rr, ti);
+#pragma unroll
+      for (int k = 0; k < L; ++k) { ur[k] = su[((x * D + y) * 2 + 0) * L + k]; ui[k] = su[((x * D + y) * 2 + 1) * L + k]; }
+      tmul_acc2<L>(ar, ur, tr);
+      tmul_sub2<L>(ar, ui, ti);
+      tmul_acc2<L>(ai, ur, ti);
+      tmul_acc2<L>(ai, ui, tr);
+    }
+    int32_t o[L];
+    if (!it.trans) {
+      tround_sr<L>(ar, g, o); stfx<L>(it.A, it.M, c, 0, r, o);
+      tround_sr<L>(ai, g, o); stfx<L>(it.A, it.M, c, 1, r, o);
+      if (r == 0) it.eA[c] = eOut;
+    } else {  // A = Theta'^H : A(c, r) = conj(Theta'(r, c))
+      tround_sr<L>(ar, g, o); stfx<L>(it.A, it.M, r, 0, c, o);
+      tround_sr<L>(ai, g, o);
+#pragma unroll
+      for (int k = 0; k < L; ++k) o[k] = -o[k];
+      stfx<L>(it.A, it.M, r, 1, c, o);
+      if (c == 0) it.eA[r] = eOut;
+    }
+  }
+}
+
+// fixed matrix (Jacobi layout with per-column exponents, or block exponent if eCol==null)
+// -> column-major complex records (debug / theta output).  conjT: output (ThetaT)^H.
+template <int L, int NL>
+__global__ void k_fixed_to_records(const int32_t* F, int ld, const int64_t* eCol, const int64_t* eBlock,
+                                   int rows, int cols, int conjT, uint32_t* out, int RBr, int p) {
+  const int n = rows * cols;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % rows, c = t / rows;
+    const int64_t E = eCol ? eCol[c] : *eBlock;
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t x[L];
+      ldfx<L>(F, ld, c, ri, r, x);
+      int64_t cols_[L];
+      fx_to_cols<L>(x, cols_);
+      mpf<NL> v = mpf_from_cols<NL, L>(cols_, E - 28 * (int64_t)L);
+      if (conjT && ri == 1) v = mpf_neg(v);
+      // output index: column-major of the (possibly transposed) matrix
+      size_t o = conjT ? ((size_t)r * cols + c) : ((size_t)c * rows + r);
+      mpf_to_record<NL>(v, out + (2 * o + ri) * (size_t)RBr, RBr - 4, p);
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a3 one-sided Jacobi SVD (one CTA per matrix, round-robin ordering)
+// ----------------------------------------------------------------------------
+template <int L, int NL>
+__device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int W = 28 * L;
+  for (int j = warp; j < it.N; j += NWARP) {
+    int64_t acc[L + 2];
+#pragma unroll
+    for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+    int cnt = 0;
+    for (int r = lane; r < it.M; r += 32) {
+      int32_t xr[L], xi[L];
+      ldfx<L>(it.A, it.M, j, 0, r, xr);
+      ldfx<L>(it.A, it.M, j, 1, r, xi);
+      tmul_acc2<L>(acc, xr, xr);
+      tmul_acc2<L>(acc, xi, xi);
+      if (++cnt == 8) { cnt = 0; tnorm2<L>(acc); }
+    }
+    tnorm2<L>(acc);
+#pragma unroll
+    for (int c = 0; c < L + 2; ++c) acc[c] = warp_sum64(acc[c]);
+    int64_t ej = it.eA[j];
+    int shift = 0;
+    if (lane == 0) {
+      mpf<NL> a = mpf_from_cols<NL, L + 2>(acc, 28 * (int64_t)(L - 2) + 2 * ej - 2 * (int64_t)W);
+      // renormalise: target exponent = ceil(log2 ||a||) + 1
+      if (!mpf_is_zero(a)) {
+        double lg = 0.5 * mpf_log2(a);
+        int64_t target = (int64_t)ceil(lg + 1e-9) + 1;
+        if (ej - target >= 2) {
+          int64_t k = ej - target;
+          if (k > 28 * L - 2) k = 28 * L - 2;
+          shift = (int)k;
+        }
+      }
+      it.alpha[j] = a;
+      if (set_negl) it.negl[j] = (mpf_is_zero(a) || mpf_cmp(a, z) <= 0) ? 1 : 0;
+    }
+    shift = __shfl_sync(0xffffffffu, shift, 0);
+    if (shift) {
+      const int q = shift / 28, rbit = shift % 28;
+      for (int r = lane; r < it.M; r += 32) {
+        for (int ri = 0; ri < 2; ++ri) {
+          int32_t x[L];
+          ldfx<L>(it.A, it.M, j, ri, r, x);
+          int64_t y[L];
+#pragma unroll
+          for (int k = 0; k < L; ++k) y[k] = (k - q >= 0) ? ((int64_t)x[k - q] << rbit) : 0;
+          int64_t carry = 0;
+#pragma unroll
+          for (int k = 0; k < L; ++k) {
+            int64_t v = y[k] + carry;
+            carry = (v + HALF) >> RADIX;
+            x[k] = (int32_t)(v - (carry << RADIX));
+          }
+          x[L - 1] += (int32_t)(carry << RADIX);
+          stfx<L>(it.A, it.M, j, ri, r, x);
+        }
+      }
+      if (lane == 0) it.eA[j] = ej - shift;
+    }
+  }
+}
+
+template <int L, int NL>
+__global__ void __launch_bounds__(NTHR) k_jacobi(const SvdItem<NL>* items) {
+  const SvdItem<NL> it = items[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int M = it.M, N = it.N, NP = N / 2;
+  const int W = 28 * L;
+  __shared__ int s_any;
+  __shared__ mpf<NL> s_red[NWARP];
+  __shared__ mpf<NL> s_z;
+
+  // V = I (exponent 1: 1 = 2^27 * 2^(28(L-1)) * 2^(1 - 28L))
+  for (int t = tid; t < N * N; t += NTHR) {
+    const int r = t % N, c = t / N;
+    int32_t x[L], z0[L];
+#pragma unroll
+    for (int k = 0; k < L; ++k) { x[k] = 0; z0[k] = 0; }
+    if (r == c) x[L - 1] = 1 << 27;
+    stfx<L>(it.V, N, c, 0, r, x);
+    stfx<L>(it.V, N, c, 1, r, z0);
+  }
+  mpf<NL> z = mpf_zero<NL>();
+  jac_norms<L, NL>(it, false, z);
+  __syncthreads();
+  // ||A||_F^2 and the negligible-column floor z = tol^2 ||A||_F^2, tol = M 2^-W
+  if (warp == 0) {
+    mpf<NL> s = mpf_zero<NL>();
+    for (int j = lane; j < N; j += 32) s = mpf_add(s, it.alpha[j]);
+    if (lane < NWARP) s_red[lane] = mpf_zero<NL>();
+    __syncwarp();
+    // serialised lane sum (32 adds)
+    for (int l = 0; l < 32; ++l) {
+      if (lane == l) s_red[0] = mpf_add(s_red[0], s);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      mpf<NL> tol2 = mpf_ldexp(mpf_from_int<NL>((int64_t)M * M), 4 - 2 * (int64_t)W);
+      s_z = mpf_mul(tol2, s_red[0]);
+    }
+  }
+  __syncthreads();
+  z = s_z;
+  for (int j = tid; j < N; j += NTHR) {
+    const mpf<NL> a = it.alpha[j];
+    it.negl[j] = (mpf_is_zero(a) || mpf_cmp(a, z) <= 0) ? 1 : 0;
+  }
+  __syncthreads();
+  const mpf<NL> tol2 = mpf_ldexp(mpf_from_int<NL>((int64_t)M * M), 4 - 2 * (int64_t)W);  // tol = 4 M 2^-W
+
+  int sweep = 0, conv = 0;
+  long long nrot = 0;
+  for (sweep = 1; sweep <= MAX_SWEEPS; ++sweep) {
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    for (int step = 0; step < N - 1; ++step) {
+      // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows)
+      for (int i = warp; i < NP; i += NWARP) {
+        int p, q;
+        rr_pair(N, step, i, p, q);
+        if (it.negl[p] || it.negl[q]) continue;
+        int64_t gr[L + 2], gi[L + 2];
+#pragma unroll
+        for (int c = 0; c < L + 2; ++c) gr[c] = gi[c] = 0;
+        int cnt = 0;
+        for (int r = lane; r < M; r += 32) {
+          int32_t xrp[L], xip[L], xrq[L], xiq[L];
+          ldfx<L>(it.A, M, p, 0, r, xrp);
+          ldfx<L>(it.A, M, p, 1, r, xip);
+          ldfx<L>(it.A, M, q, 0, r, xrq);
+          ldfx<L>(it.A, M, q, 1, r, xiq);
+          tmul_acc2<L>(gr, xrp, xrq);
+          tmul_acc2<L>(gr, xip, xiq);
+          tmul_acc2<L>(gi, xrp, xiq);
+          tmul_sub2<L>(gi, xip, xrq);
+          if (++cnt == 8) { cnt = 0; tnorm2<L>(gr); tnorm2<L>(gi); }
+        }
+        tnorm2<L>(gr);
+        tnorm2<L>(gi);
+#pragma unroll
+        for (int c = 0; c < L + 2; ++c) { gr[c] = warp_sum64(gr[c]); gi[c] = warp_sum64(gi[c]); }
+        if (lane == 0) {
+          const int64_t E0 = 28 * (int64_t)(L - 2) + it.eA[p] + it.eA[q] - 2 * (int64_t)W;
+          it.gam[2 * i] = mpf_from_cols<NL, L + 2>(gr, E0);
+          it.gam[2 * i + 1] = mpf_from_cols<NL, L + 2>(gi, E0);
+        }
+      }
+      __syncthreads();
+      // ---- phase R: rotation parameters (thread per pair)
+      for (int i = tid; i < NP; i += NTHR) {
+        int p, q;
+        rr_pair(N, step, i, p, q);
+        int flag = 0;
+        if (!it.negl[p] && !it.negl[q]) {
+          mpf<NL> ap = it.alpha[p], aq = it.alpha[q];
+          const mpf<NL> gr = it.gam[2 * i], gi = it.gam[2 * i + 1];
+          const mpf<NL> g2 = mpf_add(mpf_mul(gr, gr), mpf_mul(gi, gi));
+          if (!mpf_is_zero(g2) && mpf_cmp(g2, mpf_mul(tol2, mpf_mul(ap, aq))) > 0) {
+            const mpf<NL> one = mpf_from_int<NL>(1);
+            const mpf<NL> rg = mpf_rsqrt(g2);
+            const mpf<NL> zeta = mpf_ldexp(mpf_mul(mpf_sub(aq, ap), rg), -1);
+            const mpf<NL> sq = mpf_sqrt(mpf_add(one, mpf_mul(zeta, zeta)));
+            mpf<NL> t = mpf_recip(mpf_add(mpf_abs(zeta), sq));
+            if (!mpf_is_zero(zeta) && zeta.neg) t = mpf_neg(t);
+            const mpf<NL> c = mpf_rsqrt(mpf_add(one, mpf_mul(t, t)));
+            const mpf<NL> ct = mpf_mul(c, t);
+            const mpf<NL> sr = mpf_mul(ct, mpf_mul(gr, rg));
+            const mpf<NL> si = mpf_mul(ct, mpf_mul(gi, rg));
+            const mpf<NL> tg = mpf_mul(t, mpf_mul(g2, rg));  // t |gamma|
+            ap = mpf_sub(ap, tg);
+            aq = mpf_add(aq, tg);
+            const int64_t ep = it.eA[p], eq = it.eA[q];
+            const int64_t eb = (ep > eq ? ep : eq) + 1;  // bound of every term's exponent
+            // tight output exponents from the predicted norms (slack for rounding), at most
+            // 27 bits below eb so that every scaled coefficient stays < 2^27 (one integer digit)
+            int64_t eo[2];
+            const mpf<NL>* an[2] = {&ap, &aq};
+            for (int u = 0; u < 2; ++u) {
+              const mpf<NL>& a = *an[u];
+              int64_t enew = eb - W + 14;
+              if (!mpf_is_zero(a) && !a.neg) {
+                int64_t e1 = (int64_t)ceil(0.5 * mpf_log2(a) + 1e-9) + 1;
+                if (e1 > enew) enew = e1;
+              }
+              if (enew < eb - 27) enew = eb - 27;
+              if (enew > eb) enew = eb;
+              eo[u] = enew;
+            }
+            // coefficients relative to the OUTPUT column scale (precision 2^-W of the output):
+            //   y_p = Cp x_p - Sp x_q,  Cp = c 2^(ep - eo_p), Sp = conj(s) 2^(eq - eo_p)
+            //   y_q = Sq x_p + Cq x_q,  Sq = s 2^(ep - eo_q),   Cq = c 2^(eq - eo_q)
+            int32_t* cf = it.coef + (size_t)i * 9 * (L + 1);
+            mpf_to_coef<NL, L>(mpf_ldexp(c, ep - eo[0]), cf + 0 * (L + 1));                 // Cp
+            mpf_to_coef<NL, L>(mpf_ldexp(sr, eq - eo[0]), cf + 1 * (L + 1));                // Spr
+            mpf_to_coef<NL, L>(mpf_neg(mpf_ldexp(si, eq - eo[0])), cf + 2 * (L + 1));       // Spi = -si
+            mpf_to_coef<NL, L>(mpf_ldexp(c, eq - eo[1]), cf + 3 * (L + 1));                 // Cq
+            mpf_to_coef<NL, L>(mpf_ldexp(sr, ep - eo[1]), cf + 4 * (L + 1));                // Sqr
+            mpf_to_coef<NL, L>(mpf_ldexp(si, ep - eo[1]), cf + 5 * (L + 1));                // Sqi
+            mpf_to_coef<NL, L>(c, cf + 6 * (L + 1));                                        // V: c
+            mpf_to_coef<NL, L>(sr, cf + 7 * (L + 1));                                       //    sr
+            mpf_to_coef<NL, L>(si, cf + 8 * (L + 1));                                       //    si
+            it.alpha[p] = ap;
+            it.alpha[q] = aq;
+            it.eA[p] = eo[0];
+            it.eA[q] = eo[1];
+            if (mpf_is_zero(ap) || ap.neg || mpf_cmp(ap, z) <= 0) it.negl[p] = 1;
+            if (mpf_is_zero(aq) || aq.neg || mpf_cmp(aq, z) <= 0) it.negl[q] = 1;
+            const int intp = (cf[0 * (L + 1) + L] | cf[1 * (L + 1) + L] | cf[2 * (L + 1) + L]) != 0;
+            const int intq = (cf[3 * (L + 1) + L] | cf[4 * (L + 1) + L] | cf[5 * (L + 1) + L]) != 0;
+            flag = 1 | (intp << 8) | (intq << 16);
+            s_any = 1;
+            ++nrot;
+            if (it.dbg) atomicAdd(&it.dbg[sweep < 63 ? sweep : 63], 1);
+          }
+        }
+        it.rot[i] = flag;
+      }
+      __syncthreads();
+      // ---- phase U: apply the rotations to columns p, q of A and V
+      for (int i = warp; i < NP; i += NWARP) {
+        const int flag = it.rot[i];
+        if (!(flag & 1)) continue;
+        int p, q;
+        rr_pair(N, step, i, p, q);
+        const bool ip = (flag >> 8) & 1, iq = (flag >> 16) & 1;  // integer digits present
+        const int32_t* cf = it.coef + (size_t)i * 9 * (L + 1);
+        int32_t Cp[L + 1], Spr[L + 1], Spi[L + 1], Cq[L + 1], Sqr[L + 1], Sqi[L + 1];
+#pragma unroll
+        for (int k = 0; k <= L; ++k) {
+          Cp[k] = cf[k]; Spr[k] = cf[(L + 1) + k]; Spi[k] = cf[2 * (L + 1) + k];
+          Cq[k] = cf[3 * (L + 1) + k]; Sqr[k] = cf[4 * (L + 1) + k]; Sqi[k] = cf[5 * (L + 1) + k];
+        }
+        for (int r = lane; r < M; r += 32) {
+          int32_t xrp[L], xip[L], xrq[L], xiq[L], o[L];
+          ldfx<L>(it.A, M, p, 0, r, xrp);
+          ldfx<L>(it.A, M, p, 1, r, xip);
+          ldfx<L>(it.A, M, q, 0, r, xrq);
+          ldfx<L>(it.A, M, q, 1, r, xiq);
+          int64_t acc[L + 2];
+          // y_p = Cp x_p - Sp x_q
+#pragma unroll
+          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+          kmul_acc<L>(acc, Cp, xrp, ip); kmul_sub<L>(acc, Spr, xrq, ip); kmul_acc<L>(acc, Spi, xiq, ip);
+          tround2<L>(acc, o); stfx<L>(it.A, M, p, 0, r, o);
+#pragma unroll
+          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+          kmul_acc<L>(acc, Cp, xip, ip); kmul_sub<L>(acc, Spr, xiq, ip); kmul_sub<L>(acc, Spi, xrq, ip);
+          tround2<L>(acc, o); stfx<L>(it.A, M, p, 1, r, o);
+          // y_q = Sq x_p + Cq x_q
+#pragma unroll
+          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+          kmul_acc<L>(acc, Sqr, xrp, iq); kmul_sub<L>(acc, Sqi, xip, iq); kmul_acc<L>(acc, Cq, xrq, iq);
+          tround2<L>(acc, o); stfx<L>(it.A, M, q, 0, r, o);
+#pragma unroll
+          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+          kmul_acc<L>(acc, Sqr, xip, iq); kmul_acc<L>(acc, Sqi, xrp, iq); kmul_acc<L>(acc, Cq, xiq, iq);
+          tround2<L>(acc, o); stfx<L>(it.A, M, q, 1, r, o);
+        }
+        // V: v_p' = c v_p - conj(s) v_q ; v_q' = s v_p + c v_q  (fixed scale, |c|,|s| <= 1)
+        int32_t c_[L], sr_[L], si_[L];
+#pragma unroll
+        for (int k = 0; k < L; ++k) { c_[k] = cf[6 * (L + 1) + k]; sr_[k] = cf[7 * (L + 1) + k]; si_[k] = cf[8 * (L + 1) + k]; }
+        // (an integer digit of c or s can only be 1 when the value is exactly 1: fold it)
+        const int32_t cI = cf[6 * (L + 1) + L], srI = cf[7 * (L + 1) + L], siI = cf[8 * (L + 1) + L];
+        c_[L - 1] += cI << 28; sr_[L - 1] += srI << 28; si_[L - 1] += siI << 28;
+        for (int r = lane; r < N; r += 32) {
+          int32_t vrp[L], vip[L], vrq[L], viq[L], o[L];
+          ldfx<L>(it.V, N, p, 0, r, vrp);
+          ldfx<L>(it.V, N, p, 1, r, vip);
+          ldfx<L>(it.V, N, q, 0, r, vrq);
+          ldfx<L>(it.V, N, q, 1, r, viq);
+          int64_t acc[L + 1];
+#pragma unroll
+          for (int c = 0; c <= L; ++c) acc[c] = 0;
+          tmul_acc<L>(acc, c_, vrp); tmul_sub<L>(acc, sr_, vrq); tmul_sub<L>(acc, si_, viq);
+          tround<L>(acc, 0, o); stfx<L>(it.V, N, p, 0, r, o);
+#pragma unroll
+          for (int c = 0; c <= L; ++c) acc[c] = 0;
+          tmul_acc<L>(acc, c_, vip); tmul_sub<L>(acc, sr_, viq); tmul_acc<L>(acc, si_, vrq);
+          tround<L>(acc, 0, o); stfx<L>(it.V, N, p, 1, r, o);
+#pragma unroll
+          for (int c = 0; c <= L; ++c) acc[c] = 0;
+          tmul_acc<L>(acc, sr_, vrp); tmul_sub<L>(acc, si_, vip); tmul_acc<L>(acc, c_, vrq);
+          tround<L>(acc, 0, o); stfx<L>(it.V, N, q, 0, r, o);
+#pragma unroll
+          for (int c = 0; c <= L; ++c) acc[c] = 0;
+          tmul_acc<L>(acc, sr_, vip); tmul_acc<L>(acc, si_, vrp); tmul_acc<L>(acc, c_, viq);
+          tround<L>(acc, 0, o); stfx<L>(it.V, N, q, 1, r, o);
+        }
+      }
+      __syncthreads();
+    }
+    // refresh exact column norms (and renormalise columns) for the next sweep / the result
+    const bool any = s_any != 0;
+    jac_norms<L, NL>(it, false, z);
+    __syncthreads();
+    if (!any) { conv = 1; break; }
+  }
+  // block-reduce the rotation count
+  __shared__ long long s_rot;
+  if (tid == 0) s_rot = 0;
+  __syncthreads();
+  atomicAdd((unsigned long long*)&s_rot, (unsigned long long)nrot);
+  __syncthreads();
+  if (tid == 0) {
+    *it.sweeps = conv ? sweep : MAX_SWEEPS + 1;
+    *it.status = conv ? 0 : -3;
+    *it.rotations = s_rot;
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a4 order / truncate / renormalise (one CTA per item)
+// ----------------------------------------------------------------------------
+template <int L, int NL>
+__global__ void __launch_bounds__(NTHR) k_finalize(const FinItem<NL>* items, int RBr, int p) {
+  const FinItem<NL> it = items[blockIdx.x];
+  const int N = it.N, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  extern __shared__ unsigned char fsm[];
+  mpf<NL>* sig = (mpf<NL>*)fsm;  // [N]
+  __shared__ int s_cnt, s_k;
+  __shared__ mpf<NL> s_sum[NWARP], s_all, s_kept, s_nu;
+  for (int j = tid; j < N; j += NTHR) sig[j] = mpf_sqrt(it.alpha[j]);
+  __syncthreads();
+  // stable descending rank
+  for (int j = tid; j < N; j += NTHR) {
+    int rank = 0;
+    for (int i = 0; i < N; ++i) {
+      int c = mpf_cmp(sig[i], sig[j]);
+      if (c > 0 || (c == 0 && i < j)) ++rank;
+    }
+    it.ord[rank] = j;
+  }
+  __syncthreads();
+  // sum of all sigma^2 (= alpha)
+  mpf<NL> s = mpf_zero<NL>();
+  for (int j = tid; j < N; j += NTHR) s = mpf_add(s, it.alpha[j]);
+  for (int l = 0; l < 32; ++l) {  // warp serial reduction
+    mpf<NL> o;
+    o.e = __shfl_sync(0xffffffffu, s.e, l);
+    o.neg = __shfl_sync(0xffffffffu, s.neg, l);
+#pragma unroll
+    for (int k = 0; k < NL; ++k) o.m[k] = __shfl_sync(0xffffffffu, s.m[k], l);
+    if (lane == 0 && l > 0) s = mpf_add(s, o);
+  }
+  if (lane == 0) s_sum[warp] = s;
+  __syncthreads();
+  if (tid == 0) {
+    mpf<NL> a = s_sum[0];
+    for (int w = 1; w < NWARP; ++w) a = mpf_add(a, s_sum[w]);
+    s_all = a;
+    const mpf<NL> cut = mpf_mul(it.thr, mpf_sqrt(a));
+    int cnt = 0;
+    while (cnt < N && !mpf_is_zero(sig[it.ord[cnt]]) && mpf_cmp(sig[it.ord[cnt]], cut) >= 0) ++cnt;
+    int k = cnt < it.chi_max ? cnt : it.chi_max;
+    s_k = k;
+    mpf<NL> kept = mpf_zero<NL>();
+    for (int b = 0; b < k; ++b) kept = mpf_add(kept, it.alpha[it.ord[b]]);
+    s_kept = kept;
+    s_nu = mpf_sqrt(kept);
+    *it.k_out = k;
+    *it.status = k == 0 ? -4 : 0;
+  }
+  __syncthreads();
+  const int k = s_k;
+  const mpf<NL> inv_nu = k ? mpf_recip(s_nu) : mpf_zero<NL>();
+  for (int b = tid; b < N; b += NTHR) {
+    const int j = it.ord[b];
+    if (it.sigma_rec && b < it.nsig) mpf_to_record<NL>(sig[j], it.sigma_rec + (size_t)b * RBr, RBr - 4, p);
+    if (b < k) {
+      mpf<NL> lam = mpf_mul(sig[j], inv_nu);
+      it.lam[b] = lam;
+      it.inv_sig[b] = mpf_recip(sig[j]);
+      if (it.lam_rec) mpf_to_record<NL>(lam, it.lam_rec + (size_t)b * RBr, RBr - 4, p);
+    }
+  }
+}
+
+// a5 split outputs: Gamma_L[i][a][b] = Ul[(i,a),b] / lamL(a), Gamma_R[j][b][c] = conj(Wr[(j,c),b]) / lamR(c)
+// Ul = X (= A col / sigma) or V (trans); Wr = V or X (trans). grid.x blocks over entries, grid.y items.
+template <int L, int NL>
+__global__ void k_split(const FinItem<NL>* items, int RBr, int p) {
+  const FinItem<NL> it = items[blockIdx.y];
+  const int k = *it.k_out;
+  if (k <= 0) return;
+  const int W = 28 * L;
+  const int nL = it.GL ? 2 * it.chiL_out * k : 0;
+  const int nR = it.GR ? 2 * it.chiR_out * k : 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < nL + nR; t += gridDim.x * blockDim.x) {
+    const bool left = t < nL;
+    const int u = left ? t : t - nL;
+    const int b = u % k, row = u / k;  // row = (i,a) or (j,c) index into the factor rows
+    const int j = it.ord[b];
+    // which stored matrix: X (A with exponent eA, scaled by 1/sigma) or V (exponent 1)
+    const bool fromA = left ? !it.trans : it.trans;
+    const int32_t* F = fromA ? it.A : it.V;
+    const int ld = fromA ? it.M : it.N;
+    const int64_t E = fromA ? it.eA[j] : 1;
+    mpf<NL> scale = fromA ? it.inv_sig[b] : mpf_from_int<NL>(1);
+    const int chi = left ? it.chiL_out : it.chiR_out;
+    const uint32_t* lam = left ? it.lamL : it.lamR;
+    const int a = row % chi;
+    if (lam) scale = mpf_mul(scale, mpf_recip(mpf_from_record<NL>(lam + (size_t)a * RBr, RBr - 4)));
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t x[L];
+      ldfx<L>(F, ld, j, ri, row, x);
+      int64_t cc[L];
+      fx_to_cols<L>(x, cc);
+      mpf<NL> v = mpf_mul(mpf_from_cols<NL, L>(cc, E - (int64_t)W), scale);
+      // trans: the left factor V (resp. right factor X) of Theta'^H relates by
+      // Theta' = V S X^H, so no extra conjugation is needed beyond Gamma_R's conj.
+      if (!left && ri == 1) v = mpf_neg(v);  // conj for Gamma_R
+      uint32_t* out;
+      if (left) {
+        const int i = row / it.chiL_out;
+        out = it.GL + ((size_t)(i * it.chiL_out + a) * it.GL_ld + b) * 2 * RBr;
+      } else {
+        const int jj = row / it.chiR_out;
+        out = it.GR + ((size_t)(jj * it.GR_ld + b) * it.chiR_out + a) * 2 * RBr;
+      }
+      mpf_to_record<NL>(v, out + ri * RBr, RBr - 4, p);
+    }
+  }
+}
+
+// three-site: M2[(i,a),(j,b)] = Ul[(2i+j) chiL2 + a, b] * w_b with w_b = lambda'_b/sigma_b
+// (Ul = X = A/sigma) or lambda'_b (Ul = V); written in Jacobi layout (trans -> M2^H).
+// Output exponent per column: E_b = E_src(b) + e(w_b); transposed, all columns share
+// E_max = max_b E_b (set by k_finalize in *eM2max) and entries are scaled by
+// kappa = w_b 2^(E_src - E_out) <= 1 (one truncated product per real).
+template <int NL>
+__device__ __forceinline__ void m2_weight(const FinItem<NL>& it, int b, mpf<NL>& w, int64_t& Es) {
+  const bool fromA = !it.trans;
+  const int j = it.ord[b];
+  w = fromA ? mpf_mul(it.lam[b], it.inv_sig[b]) : it.lam[b];
+  Es = fromA ? it.eA[j] : 1;
+}
+
+template <int L, int NL>
+__global__ void k_m2_exp(const FinItem<NL>* items, int64_t* eM2max) {
+  const FinItem<NL> it = items[blockIdx.x];
+  const int k = *it.k_out;
+  __shared__ long long s_max;
+  if (threadIdx.x == 0) s_max = INT64_MIN;
+  __syncthreads();
+  for (int b = threadIdx.x; b < k; b += blockDim.x) {
+    mpf<NL> w; int64_t Es;
+    m2_weight<NL>(it, b, w, Es);
+    atomicMax(&s_max, (long long)(Es + w.e));
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) eM2max[blockIdx.x] = s_max;
+}
+
+template <int L, int NL>
+__global__ void k_build_m2(const FinItem<NL>* items, const int64_t* eM2max) {
+  const FinItem<NL> it = items[blockIdx.y];
+  const int k = *it.k_out;
+  if (k <= 0) return;
+  const int chiL = it.chiL2;
+  const int rows = 2 * chiL, cols = 2 * k;  // M2 geometry
+  const int n = rows * cols;
+  const bool fromA = !it.trans;
+  const int trans = it.M2_trans;
+  const int Mrows = trans ? cols : rows;  // Jacobi matrix rows
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % rows, c = t / rows;
+    const int i = r / chiL, a = r % chiL, jj = c / k, b = c % k;
+    const int j = it.ord[b];
+    const int srow = (2 * i + jj) * chiL + a;
+    const int32_t* F = fromA ? it.A : it.V;
+    const int ld = fromA ? it.M : it.N;
+    mpf<NL> w; int64_t Es;
+    m2_weight<NL>(it, b, w, Es);
+    const int64_t Eout = trans ? eM2max[blockIdx.y] : Es + w.e;
+    int32_t wd[L];
+    mpf_to_fixed<NL, L>(mpf_ldexp(w, Es - Eout), 0, wd);
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t x[L], o[L];
+      ldfx<L>(F, ld, j, ri, srow, x);
+      int64_t acc[L + 1];
+#pragma unroll
+      for (int q = 0; q <= L; ++q) acc[q] = 0;
+      tmul_acc<L>(acc, wd, x);
+      tround<L>(acc, 0, o);
+      if (!trans) {
+        stfx<L>(it.M2, Mrows, c, ri, r, o);
+      } else {  // M2^H: row c, column r, conjugated
+        if (ri == 1) {
+#pragma unroll
+          for (int q = 0; q < L; ++q) o[q] = -o[q];
+        }
+        stfx<L>(it.M2, Mrows, r, ri, c, o);
+      }
+    }
+    if (!trans) { if (r == 0) it.eM2[c] = Eout; }
+    else { if (c == 0) it.eM2[r] = Eout; }
+  }
+}
+
+}  // namespace mpsb
