@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark: two-site gate updates/s at chi=128, 280-bit (BASELINE.json metric, configs[1]).
+
+A step = one pass of the whole hot path (contraction + gate, one-sided Jacobi SVD,
+truncation/renormalisation, split) over one batch of `--batch`
+synthetic Theta problems (configs[1]: Gamma_A, Gamma_B in C^{2 x chi x chi} complex
+Gaussian, Haar U(4), lambda = 1), inputs resident in HBM.  Multi-GPU (torchrun): every
+rank processes its own batch — the batch items are independent, so the path shards with
+no data-path collective ("scaling": "weak"); time = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the oracle (oracle/, the plain CPU implementation) on a bounded
+sample of the same workload on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import gen  # noqa: E402
+from synth import records as R  # noqa: E402
+
+METRIC = "two-site gate updates/sec at chi=128, 280-bit"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--chi", type=int, default=128)
+    ap.add_argument("--prec", type=int, default=280)
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--distinct", type=int, default=128, help="distinct seeded items, tiled to --batch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--oracle-pairs", type=int, default=1500)
+    return ap.parse_args()
+
+
+def jacobi_limb_macs(chi: int, p: int, sweeps) -> float:
+    """Algorithmic limb-MACs of the Jacobi kernel: per item
+    (S-1) N(N-1)/2 (20M + 12N) + N(N-1)/2 8M real multiplies, x L^2 limb-MACs, L = ceil(p/32)."""
+    M = N = 2 * chi
+    L = (p + 31) // 32
+    pairs = N * (N - 1) / 2
+    tot = 0.0
+    for S in sweeps:
+        tot += ((S - 1) * pairs * (20 * M + 12 * N) + pairs * 8 * M) * L * L
+    return tot
+
+
+def contraction_limb_macs(chi: int, p: int, n_items: int) -> float:
+    L = (p + 31) // 32
+    return n_items * (16 * chi ** 3 + 64 * chi ** 2) * L * L
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(args, nthreads: int):
+    """Bounded sample of the same workload on the oracle: thread t contracts item t and
+    runs the first --oracle-pairs Jacobi pair evaluations; extrapolated with the pair
+    count of a full update (N(N-1)/2 pairs per sweep x S sweeps)."""
+    import oracle
+    chi, p = args.chi, args.prec
+    A, B, U = gen.update_batch_inputs(p, chi, nthreads)
+    tc, tp = oracle.bench_update2(p, chi, nthreads, args.oracle_pairs, A, B, U)
+    return tc, tp
+
+
+def oracle_rate(args, tc, tp, sweeps_mean, nthreads):
+    N = 2 * args.chi
+    pairs_total = N * (N - 1) / 2 * sweeps_mean
+    per_gate = float(np.mean(tc)) + float(np.mean(tp)) / args.oracle_pairs * pairs_total
+    return nthreads / per_gate, per_gate
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    nthreads = os.cpu_count() or 1
+    S = 15.9  # mean sweeps of the chi=128/280-bit workload (measured on the GPU path)
+    times, vals = [], []
+    for it in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        tc, tp = oracle_sample(args, nthreads)
+        dt = time.perf_counter() - t0
+        v, per_gate = oracle_rate(args, tc, tp, S, nthreads)
+        if it >= args.warmup:
+            times.append(dt)
+            vals.append(v)
+    value = float(np.mean(vals))
+    sample = (f"per step: {nthreads} threads, each one chi={args.chi} {args.prec}-bit item: full contraction + first "
+              f"{args.oracle_pairs} Jacobi pair evaluations, extrapolated to {S} sweeps x N(N-1)/2 pairs")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gate_updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32-limb fixed/float p=280",
+            "data": "synthetic", "config": {"workload": f"configs[1] chi={args.chi} {args.prec}-bit (bounded oracle sample)",
+                                          "chi": args.chi, "prec_bits": args.prec},
+            "cpu_baseline": {"value": value, "unit": "gate_updates/s", "cores": nthreads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "gate_updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import paper_1111_3124_b200 as mps
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    chi, p, batch = args.chi, args.prec, args.batch
+    nd = min(args.distinct, batch)
+    # rank r generates items r*nd .. (r+1)*nd-1 (distinct across ranks), tiled to the batch
+    A, B, U = gen.update_batch_inputs(p, chi, nd, first=rank * nd)
+    reps = (batch + nd - 1) // nd
+    A = np.tile(A, reps)[: batch * 4 * chi * chi]
+    B = np.tile(B, reps)[: batch * 4 * chi * chi]
+    U = np.tile(U, reps)[: batch * 32]
+    rb = R.record_bytes(p)
+    tA = torch.from_numpy(A.view(np.uint8)).to(dev)
+    tB = torch.from_numpy(B.view(np.uint8)).to(dev)
+    tU = torch.from_numpy(U.view(np.uint8)).to(dev)
+    sig = torch.empty(batch * 2 * chi * rb, dtype=torch.uint8, device=dev)
+    kk = torch.empty(batch, dtype=torch.int32, device=dev)
+    Ao = torch.empty(batch * 2 * chi * chi * 2 * rb, dtype=torch.uint8, device=dev)
+    Bo = torch.empty_like(Ao)
+    lam = torch.empty(batch * chi * rb, dtype=torch.uint8, device=dev)
+    sw = torch.empty(batch, dtype=torch.int32, device=dev)
+    ws = torch.empty(mps.update_batch_workspace(p, chi, batch), dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        mps.update_batch_device(p, chi, chi, batch, 0.0, tA, tB, tU, sig, kk, Ao, Bo, lam, sw, ws,
+                                stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    launches_per_step = mps.last_launch_count()
+    sweeps = sw.cpu().numpy().astype(np.float64)
+    ks = kk.cpu().numpy()
+    assert (ks == chi).all(), "unexpected truncation in the benchmark workload"
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    mps.profile_enable(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    jac_ms, jac_n = mps.profile_query(mps.PROF_JACOBI)
+    con_ms, _ = mps.profile_query(mps.PROF_CONTRACT)
+    fin_ms, _ = mps.profile_query(mps.PROF_FINALIZE)
+    mps.profile_enable(False)
+    if dist is not None:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_items = batch * args.steps * world
+    value = total_items / (ms / 1e3)
+
+    # roofline of the dominant kernel (Jacobi SVD): algorithmic limb-MACs per launch / launch time
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_INT_PEAKS.json")))
+    peak = peaks["imad_wide_s32_per_s"]
+    jac_work = jacobi_limb_macs(chi, p, sweeps)
+    achieved = jac_work / (jac_ms / jac_n / 1e3) if jac_n else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        key = f"jacobi_chi{chi}_p{p}_batch{batch}"
+        if key in tj:
+            traffic = tj[key]
+
+    # end to end through the public C API with host buffers (pinned), one step
+    e2e = None
+    if not args.no_e2e:
+        pA = torch.from_numpy(A.view(np.uint8)).pin_memory().numpy().view(A.dtype)
+        pB = torch.from_numpy(B.view(np.uint8)).pin_memory().numpy().view(B.dtype)
+        pU = torch.from_numpy(U.view(np.uint8)).pin_memory().numpy().view(U.dtype)
+        barrier()
+        t0 = time.perf_counter()
+        out = mps.update_batch(p, chi, batch, pA, pB, pU)
+        t1 = time.perf_counter()
+        barrier()
+        dt = t1 - t0
+        if dist is not None:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = A.nbytes + B.nbytes + U.nbytes
+        d2h = sum(out[k_].nbytes for k_ in ("sigma", "k", "GL", "GR", "lam", "sweeps"))
+        e2e = {"value": batch * world / dt, "unit": "gate_updates/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        nthreads = os.cpu_count() or 1
+        tc, tp = oracle_sample(args, nthreads)
+        v, per_gate = oracle_rate(args, tc, tp, float(np.mean(sweeps)), nthreads)
+        cpu = {"value": v, "unit": "gate_updates/s", "cores": nthreads, "kind": "oracle",
+               "sample": f"{nthreads} threads x one chi={chi} {p}-bit item each: full contraction "
+                         f"({np.mean(tc):.1f}s) + first {args.oracle_pairs} Jacobi pairs ({np.mean(tp):.1f}s), "
+                         f"extrapolated to {np.mean(sweeps):.2f} sweeps x N(N-1)/2 pairs = {per_gate:.0f} s/gate/core"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "gate_updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p=280",
+            "data": "synthetic",
+            "config": {"workload": f"configs[1]: batch of {batch} Theta (2chi x 2chi), chi={chi}, {p}-bit, "
+                                   f"contraction+Jacobi SVD+truncate+split; {nd} distinct seeded items tiled",
+                       "chi": chi, "prec_bits": p, "batch_per_gpu": batch, "sweeps_mean": float(np.mean(sweeps)),
+                       "l2": "inputs+workspace >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world}"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "limb-MAC/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_jacobi", "peak_source": "MEASURED_INT_PEAKS.json imad_wide_s32_per_s (IMAD.WIDE)",
+                         "kernel_ms_per_launch": jac_ms / jac_n if jac_n else None,
+                         "share_of_step": jac_ms / ms if ms else None,
+                         "contraction_ms": con_ms, "finalize_ms": fin_ms},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

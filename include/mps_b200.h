@@ -146,6 +146,12 @@ int mps_update_batch_device(int prec_bits, int chi, int chi_max, int batch, doub
 /* Number of kernel launches issued by the last mps_update_batch_device / bench call. */
 int mps_last_launch_count(void);
 
+/* ---- measurement: CUDA events around the kernel classes of the batch path, on the
+ * launching stream.  which: 0 Jacobi SVD (a3), 1 contraction+gate (a1-a2), 2 truncate+split
+ * (a4-a5).  enable(1) clears and starts recording; query syncs and sums the durations. */
+int mps_profile_enable(int on);
+int mps_profile_query(int which, double* total_ms, int* launches);
+
 /* ---- kernel test surface --------------------------------------------------------
  * One-sided Jacobi SVD (a3) of `batch` column-major M x N complex matrices (host
  * records), sigma: batch*min(M,N) reals descending; sweeps: batch ints (may be NULL);

@@ -207,3 +207,14 @@ class OracleDense:
         out = R.empty(self.p, 2 << self.n)
         _chk(lib().orc_dense_get(self.h, _ptr(out)))
         return out
+
+
+def bench_update2(p: int, chi: int, nthreads: int, max_pairs: int, GL, GR, U):
+    """Per-thread (contraction seconds, seconds for max_pairs Jacobi pair evaluations)."""
+    tc = np.zeros(nthreads)
+    tp = np.zeros(nthreads)
+    pd = np.zeros(nthreads, np.int64)
+    L = lib()
+    L.orc_bench_update2.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long] + [ctypes.c_void_p] * 6
+    _chk(L.orc_bench_update2(p, nthreads, chi, max_pairs, _ptr(GL), _ptr(GR), _ptr(U), _ptr(tc), _ptr(tp), _ptr(pd)))
+    return tc, tp

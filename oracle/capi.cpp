@@ -4,6 +4,7 @@
 // boundary as interchange records (format restated in mp.hpp), complex = re record
 // then im record, tensors row-major [i][a][b], matrices column-major where stated.
 #include <atomic>
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -155,6 +156,44 @@ int orc_update2_batch(int p, int batch, int chi_l, int chi_m, int chi_r, int chi
   for (auto& t : th) t.join();
   if (status == -99) g_err = err;
   return status;
+  GUARD_END
+}
+
+// Bounded-sample timing of the two-site update (bench.py cpu_baseline / --impl reference):
+// thread t takes item t (inputs as orc_update2_batch, lambda = 1), times the contraction
+// (O3 steps 1-2) and the first max_pairs Jacobi pair evaluations (step 4).  Per-thread
+// seconds are returned; nothing is tuned for this.
+int orc_bench_update2(int p, int nthreads, int chi, long max_pairs, const uchar* GL, const uchar* GR,
+                      const uchar* U, double* t_contract, double* t_pairs, long* pairs_done) {
+  GUARD_BEGIN
+  set_prec(p);
+  const size_t cb = CB();
+  std::vector<std::thread> th;
+  std::string err;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back([&, t]() {
+      try {
+        set_prec(p);
+        CVec gl = read_c(GL + (size_t)t * 2 * chi * chi * cb, (size_t)2 * chi * chi);
+        CVec gr = read_c(GR + (size_t)t * 2 * chi * chi * cb, (size_t)2 * chi * chi);
+        CVec u = read_c(U + (size_t)t * 16 * cb, 16);
+        RVec ones(chi, from_int(1));
+        auto t0 = std::chrono::steady_clock::now();
+        CMat Tp = contract_two_site(gl, gr, ones, ones, ones, chi, chi, chi, u);
+        auto t1 = std::chrono::steady_clock::now();
+        SvdResult r = jacobi_svd(Tp, 60, max_pairs);
+        auto t2 = std::chrono::steady_clock::now();
+        t_contract[t] = std::chrono::duration<double>(t1 - t0).count();
+        t_pairs[t] = std::chrono::duration<double>(t2 - t1).count();
+        pairs_done[t] = max_pairs;
+        (void)r;
+      } catch (const std::exception& e) {
+        err = e.what();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (!err.empty()) { g_err = err; return -99; }
+  return 0;
   GUARD_END
 }
 

@@ -28,7 +28,7 @@ static Real dsum_abs2(const CMat& A, int col) {  // sum_r |a_r|^2, RN after each
 // (tested squared: |gamma|^2 <= tol^2 alpha_p alpha_q), or when either column is
 // negligible (alpha <= tol^2 ||A||_F^2, reading R3b), at most max_sweeps sweeps;
 // a sweep without any rotation means convergence (it is counted).
-SvdResult jacobi_svd(const CMat& A0, int max_sweeps) {
+SvdResult jacobi_svd(const CMat& A0, int max_sweeps, long max_pairs) {
   SvdResult r;
   const int M = A0.M, N = A0.N;
   r.A = A0;
@@ -45,11 +45,13 @@ SvdResult jacobi_svd(const CMat& A0, int max_sweeps) {
   for (int j = 0; j < N; ++j) fro2 = add(fro2, dsum_abs2(A, j));
   const Real zcol = mul(tol2, fro2);
   bool converged = false;
+  long pairs_seen = 0;  // bounded-sample timing only (bench.py cpu_baseline): stop early
   for (int sweep = 1; sweep <= max_sweeps; ++sweep) {
     r.sweeps = sweep;
     bool rotated = false;
     for (int p = 0; p < N - 1; ++p) {
       for (int q = p + 1; q < N; ++q) {
+        if (max_pairs >= 0 && pairs_seen++ >= max_pairs) { r.status = ORC_ENOCONV; r.rotations = pairs_seen - 1; return r; }
         // (4.1) alpha_p, alpha_q, gamma = sum conj(a_p) a_q
         Real ap = dsum_abs2(A, p), aq = dsum_abs2(A, q);
         Cplx g;
@@ -165,10 +167,8 @@ static inline const Cplx& T3(const CVec& g, int i, int a, int b, int da, int db)
 }
 
 // ---------------------------------------------------------------- two-site update
-Update2 update_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const RVec& lam_m,
-                        const RVec& lam_r, int chi_l, int chi_m, int chi_r, const CVec& U4,
-                        int chi_max, const Real& thr) {
-  Update2 out;
+CMat contract_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const RVec& lam_m,
+                       const RVec& lam_r, int chi_l, int chi_m, int chi_r, const CVec& U4) {
   // (1) L^i(a,b) = RN(RN(lam_l(a) G_s^i(a,b)) lam_m(b));  R^j(b,c) = RN(G_{s+1}^j(b,c) lam_r(c))
   CVec Lt((size_t)2 * chi_l * chi_m), Rt((size_t)2 * chi_m * chi_r);
   for (int i = 0; i < 2; ++i)
@@ -204,6 +204,14 @@ Update2 update_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const
               cfma(acc, U4[(size_t)(2 * i + j) * 4 + (2 * ip + jp)], Th.at(ip * chi_l + a, jp * chi_r + c));
           Tp.at(i * chi_l + a, j * chi_r + c) = acc;
         }
+  return Tp;
+}
+
+Update2 update_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const RVec& lam_m,
+                        const RVec& lam_r, int chi_l, int chi_m, int chi_r, const CVec& U4,
+                        int chi_max, const Real& thr) {
+  Update2 out;
+  CMat Tp = contract_two_site(GL, GR, lam_l, lam_m, lam_r, chi_l, chi_m, chi_r, U4);
   out.Theta = Tp;
   // (3)-(7)
   Split sp = svd_truncate(Tp, chi_max, thr);

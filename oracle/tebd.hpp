@@ -19,6 +19,9 @@ using CVec = std::vector<Cplx>;
 using RVec = std::vector<Real>;
 
 // Dense column-major M x N complex matrix: a[col*M + row].
+struct CMat;
+// Theta' = U (lam_l G_s lam_m G_{s+1} lam_r) of the two-site update, O3 steps 1-2.
+
 struct CMat {
   int M = 0, N = 0;
   CVec a;
@@ -39,7 +42,7 @@ struct SvdResult {
 };
 
 // Cyclic one-sided Jacobi SVD of A (M x N, N <= M), SURVEY §8(c) O3 step 4-5.
-SvdResult jacobi_svd(const CMat& A, int max_sweeps = 60);
+SvdResult jacobi_svd(const CMat& A, int max_sweeps = 60, long max_pairs = -1);
 
 // Left/right factorisation Theta = Ul diag(s) Wr^H, handling N > M by working on Theta^H
 // (O3 step 3).  Returns sorted (descending, ties by index) and truncated factors.
@@ -69,6 +72,8 @@ struct Update2 {
   RVec sigma_sorted;    // all singular values of Theta', descending
   CMat Theta;           // Theta' (2chi_l x 2chi_r) as contracted
 };
+struct CMat contract_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const RVec& lam_m,
+                              const RVec& lam_r, int chi_l, int chi_m, int chi_r, const CVec& U4);
 Update2 update_two_site(const CVec& GL, const CVec& GR, const RVec& lam_l, const RVec& lam_m,
                         const RVec& lam_r, int chi_l, int chi_m, int chi_r, const CVec& U4,
                         int chi_max, const Real& thr);

@@ -20,11 +20,12 @@ STATUS = {0: "MPS_OK", -1: "MPS_EINVAL", -2: "MPS_ENOTUNITARY", -3: "MPS_ENOCONV
           -10: "MPS_ETOOBIG"}
 
 # every symbol include/mps_b200.h declares
-EXPORTS = ["mps_svd_batch", "mps_debug_mpf", "mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
+EXPORTS = ["mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
            "mps_apply_gate", "mps_apply_layer", "mps_amplitude", "mps_expect", "mps_norm2", "mps_to_dense",
            "mps_sync", "mps_n_qubits", "mps_bond_dims", "mps_schmidt", "mps_get_site", "mps_set_schmidt",
            "mps_set_site", "mps_stats", "mps_bench_update_batch", "mps_update_batch_workspace",
-           "mps_update_batch_device", "mps_last_launch_count"]
+           "mps_update_batch_device", "mps_last_launch_count", "mps_profile_enable", "mps_profile_query",
+           "mps_svd_batch", "mps_debug_mpf"]
 
 
 class MpsError(RuntimeError):
@@ -49,6 +50,8 @@ def lib() -> ctypes.CDLL:
         L.mps_update_batch_workspace.argtypes = [ci, ci, ci]
         L.mps_bench_update_batch.argtypes = [ci, ci, ci, ci, cd] + [vp] * 6 + [vp, vp, vp, vp, vp, vp, vp, vp]
         L.mps_update_batch_device.argtypes = [ci, ci, ci, ci, cd] + [vp] * 6 + [vp] * 8
+        L.mps_profile_enable.argtypes = [ci]
+        L.mps_profile_query.argtypes = [ci, vp, vp]
         L.mps_svd_batch.argtypes = [ci, ci, ci, ci, vp, vp, vp, vp]
         L.mps_debug_mpf.argtypes = [ci, ci, ci, vp, vp, vp]
         if hasattr(L, "mps_init"):
@@ -155,3 +158,17 @@ def debug_mpf(p: int, op: str, a, b=None):
     out = _empty(p, len(a))
     _chk(lib().mps_debug_mpf(p, ops[op], len(a), _p(a), _p(b), _p(out)), "mps_debug_mpf")
     return out
+
+
+PROF_JACOBI, PROF_CONTRACT, PROF_FINALIZE = 0, 1, 2
+
+
+def profile_enable(on: bool = True):
+    _chk(lib().mps_profile_enable(1 if on else 0))
+
+
+def profile_query(which: int):
+    ms = ctypes.c_double(0)
+    n = ctypes.c_int(0)
+    _chk(lib().mps_profile_query(which, ctypes.byref(ms), ctypes.byref(n)))
+    return ms.value, n.value

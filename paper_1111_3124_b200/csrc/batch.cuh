@@ -141,6 +141,7 @@ int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, con
   }
   cudaMemcpyAsync(base, hostdesc.data(), d_end, cudaMemcpyHostToDevice, st);
   int nl = 0;
+  prof_mark(PROF_CONTRACT, 1, st);
   k_init_exp_items<<<(batch + 255) / 256, 256, 0, st>>>(items + w.o_small, w.per_item, batch); ++nl;
   dim3 gp(std::max(1, std::min(64, (2 * chi * chi + 255) / 256)), 2 * batch);
   k_prep_exp<<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
@@ -158,13 +159,18 @@ int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, con
     }
     return nl;
   }
+  prof_mark(PROF_CONTRACT, 0, st);
+  prof_mark(PROF_JACOBI, 1, st);
   k_jacobi<L, NL><<<batch, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  prof_mark(PROF_JACOBI, 0, st);
+  prof_mark(PROF_FINALIZE, 1, st);
   size_t fsm = sizeof(mpf<NL>) * (size_t)N;
   k_finalize<L, NL><<<batch, NTHR, fsm, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   if (out.A_out || out.B_out) {
     dim3 gs(std::max(1, std::min(64, (4 * chi * chi_max + 255) / 256)), batch);
     k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   }
+  prof_mark(PROF_FINALIZE, 0, st);
   return nl;
 }
 

@@ -16,6 +16,28 @@ using namespace mpsb;
 
 static thread_local int g_last_launches = 0;
 
+// ---- kernel event profiling (bench.py): accumulated ms per kernel class
+namespace {
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[PROF_N];
+  std::vector<cudaEvent_t> pending_begin[PROF_N];
+} g_prof;
+}  // namespace
+
+void mpsb::prof_mark(int which, int begin, cudaStream_t st) {
+  if (!g_prof.on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  if (begin) {
+    g_prof.pending_begin[which].push_back(e);
+  } else if (!g_prof.pending_begin[which].empty()) {
+    g_prof.ev[which].push_back({g_prof.pending_begin[which].back(), e});
+    g_prof.pending_begin[which].pop_back();
+  }
+}
+
 extern "C" {
 
 size_t mps_record_bytes(int p) { return 16 + 4 * (size_t)((p + 31) / 32); }
@@ -38,6 +60,31 @@ const char* mps_strerror(int s) {
 }
 
 int mps_max_chi(void) { return MAX_CHI; }
+
+int mps_profile_enable(int on) {
+  for (int k = 0; k < PROF_N; ++k) {
+    for (auto& pr : g_prof.ev[k]) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (auto& e : g_prof.pending_begin[k]) cudaEventDestroy(e);
+    g_prof.ev[k].clear();
+    g_prof.pending_begin[k].clear();
+  }
+  g_prof.on = on != 0;
+  return MPS_OK;
+}
+
+int mps_profile_query(int which, double* total_ms, int* launches) {
+  if (which < 0 || which >= PROF_N || !total_ms || !launches) return MPS_EINVAL;
+  double tot = 0;
+  for (auto& pr : g_prof.ev[which]) {
+    if (cudaEventSynchronize(pr.second) != cudaSuccess) return MPS_ECUDA;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (int)g_prof.ev[which].size();
+  return MPS_OK;
+}
 int mps_last_launch_count(void) { return g_last_launches; }
 
 size_t mps_update_batch_workspace(int p, int chi, int batch) {

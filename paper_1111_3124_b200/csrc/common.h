@@ -24,6 +24,10 @@ struct BatchOut {  // device pointers (records unless stated)
   uint32_t* theta_dbg;
 };
 
+// Optional CUDA-event bracketing of individual kernels (bench.py roofline): which = kernel id.
+enum { PROF_JACOBI = 0, PROF_CONTRACT = 1, PROF_FINALIZE = 2, PROF_N = 3 };
+void prof_mark(int which, int begin, cudaStream_t st);
+
 template <class T>
 int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, const uint32_t* A,
                          const uint32_t* B, const uint32_t* lam_l, const uint32_t* lam_m,
