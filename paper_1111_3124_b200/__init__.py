@@ -172,3 +172,91 @@ def profile_query(which: int):
     n = ctypes.c_int(0)
     _chk(lib().mps_profile_query(which, ctypes.byref(ms), ctypes.byref(n)))
     return ms.value, n.value
+
+
+class MPS:
+    """The on-device MPS state (mps_init ... mps_free).  Records in / out are synth.records arrays."""
+
+    def __init__(self, n: int, p: int, chi_max: int, thr: float = 0.0, stream=None):
+        self.n, self.p = n, p
+        h = ctypes.c_void_p()
+        _chk(lib().mps_init(ctypes.byref(h), n, p, chi_max, thr), "mps_init")
+        self.h = h
+        if stream is not None:
+            _chk(lib().mps_set_stream(self.h, stream))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mps_free(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def apply(self, U, sites):
+        s = (ctypes.c_int * len(sites))(*sites)
+        _chk(lib().mps_apply_gate(self.h, _p(U), s, len(sites)), "mps_apply_gate")
+
+    def apply_layer(self, gates):
+        """gates: list of (U records, sites)."""
+        n = len(gates)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[U.ctypes.data for U, _ in gates])
+        flat = [q for _, s in gates for q in s]
+        sf = (ctypes.c_int * max(len(flat), 1))(*flat)
+        ks = (ctypes.c_int * max(n, 1))(*[len(s) for _, s in gates])
+        _chk(lib().mps_apply_layer(self.h, n, ptrs, sf, ks), "mps_apply_layer")
+
+    def amplitude(self, bits):
+        b = np.asarray(bits, np.uint8)
+        out = _empty(self.p, 2)
+        _chk(lib().mps_amplitude(self.h, _p(b), _p(out)), "mps_amplitude")
+        return out
+
+    def to_dense(self):
+        out = _empty(self.p, 2 << self.n)
+        _chk(lib().mps_to_dense(self.h, _p(out)), "mps_to_dense")
+        return out
+
+    def norm2(self):
+        out = _empty(self.p, 1)
+        _chk(lib().mps_norm2(self.h, _p(out)), "mps_norm2")
+        return out
+
+    def expect(self, O, sites):
+        s = (ctypes.c_int * len(sites))(*sites)
+        out = _empty(self.p, 2)
+        _chk(lib().mps_expect(self.h, _p(O), s, len(sites), _p(out)), "mps_expect")
+        return out
+
+    def bond_dims(self):
+        out = np.zeros(max(self.n - 1, 1), np.int32)
+        _chk(lib().mps_bond_dims(self.h, _p(out)), "mps_bond_dims")
+        return out[: self.n - 1].tolist()
+
+    def schmidt(self, bond: int):
+        m = ctypes.c_int(0)
+        _chk(lib().mps_schmidt(self.h, bond, None, ctypes.byref(m)))
+        out = _empty(self.p, m.value)
+        _chk(lib().mps_schmidt(self.h, bond, _p(out), ctypes.byref(m)))
+        return out
+
+    def get_site(self, s: int):
+        ml, mr = ctypes.c_int(0), ctypes.c_int(0)
+        _chk(lib().mps_get_site(self.h, s, None, ctypes.byref(ml), ctypes.byref(mr)))
+        out = _empty(self.p, 4 * ml.value * mr.value)
+        _chk(lib().mps_get_site(self.h, s, _p(out), ctypes.byref(ml), ctypes.byref(mr)))
+        return out, ml.value, mr.value
+
+    def set_schmidt(self, bond: int, lam):
+        _chk(lib().mps_set_schmidt(self.h, bond, _p(lam), len(lam)))
+
+    def set_site(self, s: int, G, ml: int, mr: int):
+        _chk(lib().mps_set_site(self.h, s, _p(G), ml, mr))
+
+    def sync(self):
+        _chk(lib().mps_sync(self.h), "mps_sync")
+
+    def stats(self) -> dict:
+        import json
+        buf = ctypes.create_string_buffer(1 << 16)
+        _chk(lib().mps_stats(self.h, buf, len(buf)))
+        return json.loads(buf.value.decode())

@@ -99,7 +99,7 @@ int mps_update_batch_device(int p, int chi, int chi_max, int batch, double thr, 
   if (p < 64 || p > 512 || chi < 1 || chi > MAX_CHI || batch < 1 || chi_max < 1 || !dA || !dB || !dU || !dws)
     return MPS_EINVAL;
   if (thr <= 0) thr = std::ldexp(1.0, -((p + 1) / 2));
-  BatchOut o{(uint32_t*)dsigma, dk_out, (uint32_t*)dA_out, (uint32_t*)dB_out, (uint32_t*)dlam_out, dsweeps, nullptr};
+  BatchOut o{(uint32_t*)dsigma, dk_out, (uint32_t*)dA_out, (uint32_t*)dB_out, (uint32_t*)dlam_out, dsweeps, nullptr, nullptr};
   std::vector<unsigned char> hd;
   cudaStream_t st = (cudaStream_t)stream;
   int nl;
@@ -152,7 +152,7 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   if (lam_r) cudaMemcpyAsync(d + olr, lam_r, nLam, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(d + oU, U, nU, cudaMemcpyHostToDevice, st);
   BatchOut o{(uint32_t*)(d + oS), (int*)(d + oK), (uint32_t*)(d + oAo), (uint32_t*)(d + oBo),
-             (uint32_t*)(d + oLo), (int*)(d + oSw), theta_debug ? (uint32_t*)(d + oTh) : nullptr};
+             (uint32_t*)(d + oLo), (int*)(d + oSw), theta_debug ? (uint32_t*)(d + oTh) : nullptr, nullptr};
   cudaMemsetAsync(d + oAo, 0, nAo, st);
   cudaMemsetAsync(d + oBo, 0, nAo, st);
   std::vector<unsigned char> hd;

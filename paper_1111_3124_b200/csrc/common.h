@@ -21,7 +21,7 @@ inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
 struct BatchOut {  // device pointers (records unless stated)
   uint32_t* sigma; int* k; uint32_t* A_out; uint32_t* B_out; uint32_t* lam; int* sweeps;
-  uint32_t* theta_dbg;
+  uint32_t* theta_dbg; int* status;
 };
 
 // Optional CUDA-event bracketing of individual kernels (bench.py roofline): which = kernel id.

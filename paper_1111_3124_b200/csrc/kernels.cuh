@@ -82,7 +82,8 @@ struct FinItem {
   mpf<NL>* inv_sig;         // [N] 1/sigma of sorted kept columns
   mpf<NL>* lam;             // [N] lambda' of kept (mpf)
   int* k_out;               // 1
-  int* status;              // 1
+  int* status;              // 1 (out: svd status if nonzero, else -4 when k = 0, else 0)
+  const int* svd_status;    // the Jacobi status of this problem, or null
   uint32_t* sigma_rec;      // [nsig] records (sigma, descending) or null
   int nsig;                 // number of sigma records to write (<= N)
   uint32_t* lam_rec;        // [k] records or null
@@ -261,6 +262,16 @@ __device__ __forceinline__ void rr_pair(int N, int step, int i, int& p, int& q) 
 static __global__ void k_init_exp(int64_t* e, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) e[i] = INT64_MIN;
+}
+// every PrepItem's block exponent <- INT64_MIN
+static __global__ void k_init_prep(const PrepItem* items, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) *items[i].eF = INT64_MIN;
+}
+// *acc += *add ; if (*st == 0) *st = *st2
+static __global__ void k_add_int(int* acc, const int* add, int* st, const int* st2) {
+  *acc += *add;
+  if (*st == 0) *st = *st2;
 }
 // eL, eR (first two int64 of each item's small area) <- INT64_MIN
 static __global__ void k_init_exp_items(char* small0, size_t stride, int n) {
@@ -813,7 +824,8 @@ __global__ void __launch_bounds__(NTHR) k_finalize(const FinItem<NL>* items, int
     s_kept = kept;
     s_nu = mpf_sqrt(kept);
     *it.k_out = k;
-    *it.status = k == 0 ? -4 : 0;
+    const int js = it.svd_status ? *it.svd_status : 0;
+    *it.status = js ? js : (k == 0 ? -4 : 0);
   }
   __syncthreads();
   const int k = s_k;

@@ -1,0 +1,524 @@
+// The MPS state behind include/mps_b200.h (mps_init ... mps_stats): the on-device store
+// of Eq. 1 in Vidal Gamma-lambda form and the host sequencing of gate updates.
+// Every arithmetic step runs in the sm_100a kernels (update.cuh, query.cuh); this file only
+// validates arguments, moves records and repacks updated tensors into the store.
+//
+// Store layout (device): site s holds [2][m_{s-1}][m_s] complex records packed at the
+// current dims inside a buffer of capacity 2 cap_{s-1} cap_s; bond b holds m_b reals in a
+// buffer of capacity cap_b = min(chi_max, 2^min(b+1, n-b-1)) (the Schmidt-rank bound).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mps_b200.h"
+#include "common.h"
+#include "tierops.h"
+#include "update.cuh"
+
+using namespace mpsb;
+
+struct mps_state {
+  int n = 0, p = 0, chi_max = 0, RBr = 0;
+  size_t rb = 0, cb = 0;
+  double thr = 0;
+  cudaStream_t st = 0;
+  int sticky = MPS_OK;
+  std::vector<int> m, cap;
+  std::vector<uint32_t*> G, lam;
+  const TierOps* ops = nullptr;
+  void* ws = nullptr;
+  size_t ws_sz = 0;
+  char* tmp = nullptr;
+  size_t tmp_sz = 0;
+  int* dint = nullptr;  // 256 device ints
+  long long gates = 0, sweeps_total = 0;
+  int last_sweeps = 0;
+  int dl(int s) const { return s == 0 ? 1 : m[s - 1]; }
+  int dr(int s) const { return s == n - 1 ? 1 : m[s]; }
+  int capl(int s) const { return s == 0 ? 1 : cap[s - 1]; }
+  int capr(int s) const { return s == n - 1 ? 1 : cap[s]; }
+};
+
+namespace {
+
+int cuda_ok(mps_state* s, cudaError_t e) {
+  if (e == cudaSuccess) return MPS_OK;
+  fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
+  if (s) s->sticky = MPS_ECUDA;
+  return MPS_ECUDA;
+}
+
+bool grow(void** buf, size_t* sz, size_t need) {
+  if (*sz >= need) return true;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *sz = 0;
+  if (cudaMalloc(buf, need) != cudaSuccess) return false;
+  *sz = need;
+  return true;
+}
+
+// host record of +1 / 0 at precision p
+void host_record(int p, int one, std::vector<uint32_t>& out) {
+  const int L = (p + 31) / 32;
+  out.assign(4 + L, 0);
+  int64_t e = one ? 1 : INT64_MIN;
+  std::memcpy(out.data(), &e, 8);
+  if (one) out[3 + L] = 0x80000000u;  // value = 2^31 2^(32(L-1)) 2^(1-32L) = 1
+}
+
+int check_sites(const mps_state* s, const int* sites, int k) {
+  if (!sites || k < 1 || k > 3) return MPS_EINVAL;
+  for (int i = 0; i < k; ++i) {
+    if (sites[i] < 0 || sites[i] >= s->n) return MPS_EINVAL;
+    if (i && sites[i] <= sites[i - 1]) return MPS_EINVAL;
+  }
+  if (k == 2 && sites[1] - sites[0] > 2) return MPS_EINVAL;  // spans > 3 rejected
+  if (k == 3 && sites[2] != sites[0] + 2) return MPS_EINVAL;
+  return MPS_OK;
+}
+
+// U(4) on (s, s+2) -> U(8) on (s, s+1, s+2) with identity on s+1
+void embed_u8(const unsigned char* U4, size_t cb, std::vector<unsigned char>& U8, int p) {
+  std::vector<uint32_t> z;
+  host_record(p, 0, z);
+  U8.assign(64 * cb, 0);
+  for (int x = 0; x < 8; ++x)
+    for (int y = 0; y < 8; ++y) {
+      unsigned char* dst = U8.data() + (size_t)(x * 8 + y) * cb;
+      int mi = (x >> 1) & 1, mj = (y >> 1) & 1;
+      if (mi != mj) {
+        std::memcpy(dst, z.data(), cb / 2);
+        std::memcpy(dst + cb / 2, z.data(), cb / 2);
+        continue;
+      }
+      int a = ((x >> 2) << 1) | (x & 1), b = ((y >> 2) << 1) | (y & 1);
+      std::memcpy(dst, U4 + (size_t)(a * 4 + b) * cb, cb);
+    }
+}
+
+// Upload U (d x d complex records) and check unitarity on the device.
+int upload_gate(mps_state* s, const void* U, int d, uint32_t* dU) {
+  cudaMemcpyAsync(dU, U, (size_t)d * d * s->cb, cudaMemcpyHostToDevice, s->st);
+  cudaMemsetAsync(s->dint, 0, sizeof(int), s->st);
+  s->ops->unitary(s->p, dU, d, s->dint, s->st);
+  int bad = 0;
+  cudaMemcpyAsync(&bad, s->dint, sizeof(int), cudaMemcpyDeviceToHost, s->st);
+  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  return bad ? MPS_ENOTUNITARY : MPS_OK;
+}
+
+// copy the packed sub-block [rows][k] of a [rows][ld] record matrix into dst
+void repack_rows(mps_state* s, uint32_t* dst, const uint32_t* src, int rows, int k, int ld) {
+  cudaMemcpy2DAsync(dst, (size_t)k * s->cb, src, (size_t)ld * s->cb, (size_t)k * s->cb, rows,
+                    cudaMemcpyDeviceToDevice, s->st);
+}
+// [2][ld][cols] -> [2][k][cols]
+void repack_blocks(mps_state* s, uint32_t* dst, const uint32_t* src, int k, int ld, int cols) {
+  cudaMemcpy2DAsync(dst, (size_t)k * cols * s->cb, src, (size_t)ld * cols * s->cb, (size_t)k * cols * s->cb, 2,
+                    cudaMemcpyDeviceToDevice, s->st);
+}
+
+struct TwoSitePlan {
+  int s, ld;
+  uint32_t *GL, *GR, *lam, *sig;
+  int* ints;  // k, sweeps, status
+};
+
+}  // namespace
+
+extern "C" {
+
+int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
+  if (!out) return MPS_EINVAL;
+  *out = nullptr;
+  if (n < 1 || chi_max < 1) return MPS_EINVAL;
+  if (p < 64 || p > 512 || chi_max > MAX_CHI) return MPS_EUNSUPPORTED;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MPS_ECUDA;
+  auto* s = new mps_state();
+  s->n = n;
+  s->p = p;
+  s->chi_max = chi_max;
+  s->RBr = record_words(p);
+  s->rb = 4 * (size_t)s->RBr;
+  s->cb = 2 * s->rb;
+  s->thr = thr > 0 ? thr : std::ldexp(1.0, -((p + 1) / 2));
+  s->ops = &tier_ops(p);
+  s->m.assign(n > 1 ? n - 1 : 0, 1);
+  s->cap.resize(n > 1 ? n - 1 : 0);
+  for (int b = 0; b + 1 < n; ++b) {
+    int e = std::min(b + 1, n - b - 1);
+    long long c = e >= 30 ? (1LL << 30) : (1LL << e);
+    s->cap[b] = (int)std::min<long long>(chi_max, c);
+  }
+  std::vector<uint32_t> one, zero;
+  host_record(p, 1, one);
+  host_record(p, 0, zero);
+  s->G.assign(n, nullptr);
+  s->lam.assign(n > 1 ? n - 1 : 0, nullptr);
+  bool ok = cudaMalloc(&s->dint, 256 * sizeof(int)) == cudaSuccess;
+  for (int i = 0; ok && i < n; ++i) {
+    ok = cudaMalloc(&s->G[i], (size_t)2 * s->capl(i) * s->capr(i) * s->cb) == cudaSuccess;
+    if (!ok) break;
+    // Gamma^0 = [1], Gamma^1 = [0]
+    std::vector<uint32_t> g;
+    g.insert(g.end(), one.begin(), one.end());
+    g.insert(g.end(), zero.begin(), zero.end());
+    g.insert(g.end(), zero.begin(), zero.end());
+    g.insert(g.end(), zero.begin(), zero.end());
+    cudaMemcpy(s->G[i], g.data(), 2 * s->cb, cudaMemcpyHostToDevice);
+  }
+  for (int b = 0; ok && b + 1 < n; ++b) {
+    ok = cudaMalloc(&s->lam[b], (size_t)s->cap[b] * s->rb) == cudaSuccess;
+    if (ok) cudaMemcpy(s->lam[b], one.data(), s->rb, cudaMemcpyHostToDevice);
+  }
+  if (!ok) {
+    mps_free(s);
+    return MPS_ENOMEM;
+  }
+  *out = s;
+  return MPS_OK;
+}
+
+void mps_free(mps_state* s) {
+  if (!s) return;
+  for (auto* g : s->G) cudaFree(g);
+  for (auto* l : s->lam) cudaFree(l);
+  if (s->ws) cudaFree(s->ws);
+  if (s->tmp) cudaFree(s->tmp);
+  if (s->dint) cudaFree(s->dint);
+  delete s;
+}
+
+int mps_set_stream(mps_state* s, void* stream) {
+  if (!s) return MPS_EINVAL;
+  s->st = (cudaStream_t)stream;
+  return MPS_OK;
+}
+
+int mps_sync(mps_state* s) {
+  if (!s) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+int mps_n_qubits(mps_state* s) { return s ? s->n : MPS_EINVAL; }
+
+int mps_bond_dims(mps_state* s, int* out) {
+  if (!s || !out) return MPS_EINVAL;
+  for (int b = 0; b + 1 < s->n; ++b) out[b] = s->m[b];
+  return s->sticky;
+}
+
+// ---------------------------------------------------------------- gates
+static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, const std::vector<const void*>& Us) {
+  const int ng = (int)first.size();
+  // temp layout per gate: U (16 cplx), GL out [2][dl][ld], GR out [2][ld][dr], lam [ld], sigma [N]
+  std::vector<size_t> off(ng + 1, 0);
+  for (int g = 0; g < ng; ++g) {
+    const int q = first[g], ld = s->cap[q];
+    const int dl = s->dl(q), dr = s->dr(q + 1);
+    size_t need = align_up(16 * s->cb) + align_up((size_t)2 * dl * ld * s->cb) + align_up((size_t)2 * ld * dr * s->cb) +
+                  align_up((size_t)ld * s->rb) + align_up((size_t)2 * std::max(dl, dr) * s->rb);
+    off[g + 1] = off[g] + need;
+  }
+  if (!grow((void**)&s->tmp, &s->tmp_sz, off[ng] + 4096)) return s->sticky = MPS_ENOMEM;
+  std::vector<Upd2Args> args(ng);
+  for (int g = 0; g < ng; ++g) {
+    const int q = first[g], ld = s->cap[q];
+    const int dl = s->dl(q), dr = s->dr(q + 1);
+    char* b = s->tmp + off[g];
+    uint32_t* dU = (uint32_t*)b;
+    if (int rc = upload_gate(s, Us[g], 4, dU)) return rc;
+    Upd2Args a;
+    std::memset(&a, 0, sizeof(a));
+    a.chiL = dl; a.chiM = s->m[q]; a.chiR = dr; a.chi_max = s->chi_max;
+    a.GL = s->G[q]; a.GR = s->G[q + 1];
+    a.lamL = q > 0 ? s->lam[q - 1] : nullptr;
+    a.lamM = s->lam[q];
+    a.lamR = q + 1 < s->n - 1 ? s->lam[q + 1] : nullptr;
+    a.U = dU;
+    b += align_up(16 * s->cb);
+    a.GL_out = (uint32_t*)b; b += align_up((size_t)2 * dl * ld * s->cb);
+    a.GR_out = (uint32_t*)b; b += align_up((size_t)2 * ld * dr * s->cb);
+    a.lam_out = (uint32_t*)b; b += align_up((size_t)ld * s->rb);
+    a.sigma_out = (uint32_t*)b;
+    a.out_ld = ld;
+    a.k_out = s->dint + 3 * g; a.sweeps_out = s->dint + 3 * g + 1; a.status_out = s->dint + 3 * g + 2;
+    args[g] = a;
+  }
+  if (3 * ng > 256) return MPS_EINVAL;
+  size_t need = s->ops->upd2_ws(args.data(), ng);
+  if (!grow(&s->ws, &s->ws_sz, need)) return s->sticky = MPS_ENOMEM;
+  std::vector<unsigned char> hd;
+  s->ops->upd2(s->p, s->thr, args.data(), ng, s->ws, s->st, hd);
+  std::vector<int> res(3 * ng);
+  cudaMemcpyAsync(res.data(), s->dint, sizeof(int) * 3 * ng, cudaMemcpyDeviceToHost, s->st);
+  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  for (int g = 0; g < ng; ++g) {
+    const int k = res[3 * g], sw = res[3 * g + 1], stt = res[3 * g + 2];
+    s->sweeps_total += sw;
+    s->last_sweeps = sw;
+    s->gates++;
+    if (stt) return s->sticky = stt;
+    const int q = first[g], ld = s->cap[q];
+    const int dl = s->dl(q), dr = s->dr(q + 1);
+    repack_rows(s, s->G[q], args[g].GL_out, 2 * dl, k, ld);
+    repack_blocks(s, s->G[q + 1], args[g].GR_out, k, ld, dr);
+    cudaMemcpyAsync(s->lam[q], args[g].lam_out, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
+    s->m[q] = k;
+  }
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+static int apply_three_site(mps_state* s, int q, const void* U8) {
+  const int dl = s->dl(q), d1 = s->m[q], d2 = s->m[q + 1], dr = s->dr(q + 2);
+  const int ld = std::max(s->cap[q], s->cap[q + 1]);
+  size_t o_U = 0, o_G0 = align_up(64 * s->cb), o_G1 = o_G0 + align_up((size_t)2 * dl * ld * s->cb),
+         o_G2 = o_G1 + align_up((size_t)2 * ld * ld * s->cb), o_l1 = o_G2 + align_up((size_t)2 * ld * dr * s->cb),
+         o_l2 = o_l1 + align_up((size_t)ld * s->rb), o_end = o_l2 + align_up((size_t)ld * s->rb);
+  if (!grow((void**)&s->tmp, &s->tmp_sz, o_end + 4096)) return s->sticky = MPS_ENOMEM;
+  uint32_t* dU = (uint32_t*)(s->tmp + o_U);
+  if (int rc = upload_gate(s, U8, 8, dU)) return rc;
+  Upd3Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.chiL = dl; a.chi1 = d1; a.chi2 = d2; a.chiR = dr; a.chi_max = s->chi_max;
+  a.G0 = s->G[q]; a.G1 = s->G[q + 1]; a.G2 = s->G[q + 2];
+  a.lamL = q > 0 ? s->lam[q - 1] : nullptr;
+  a.lam1 = s->lam[q];
+  a.lam2 = s->lam[q + 1];
+  a.lamR = q + 2 < s->n - 1 ? s->lam[q + 2] : nullptr;
+  a.U = dU;
+  a.G0_out = (uint32_t*)(s->tmp + o_G0);
+  a.G1_out = (uint32_t*)(s->tmp + o_G1);
+  a.G2_out = (uint32_t*)(s->tmp + o_G2);
+  a.lam1_out = (uint32_t*)(s->tmp + o_l1);
+  a.lam2_out = (uint32_t*)(s->tmp + o_l2);
+  a.ld = ld;
+  a.k1 = s->dint; a.k2 = s->dint + 1; a.sweeps = s->dint + 2; a.status = s->dint + 3;
+  size_t need = s->ops->upd3_ws(a);
+  if (!grow(&s->ws, &s->ws_sz, need)) return s->sticky = MPS_ENOMEM;
+  cudaMemsetAsync(s->dint, 0, 4 * sizeof(int), s->st);
+  std::vector<unsigned char> hd1, hd2;
+  s->ops->upd3_s1(s->p, s->thr, a, s->ws, s->st, hd1);
+  int r1[4];
+  cudaMemcpyAsync(r1, s->dint, sizeof(r1), cudaMemcpyDeviceToHost, s->st);
+  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  if (r1[3]) { s->sweeps_total += r1[2]; return s->sticky = r1[3]; }
+  const int k1 = r1[0];
+  s->ops->upd3_s2(s->p, s->thr, a, k1, s->ws, s->st, hd2);
+  int r2[4];
+  cudaMemcpyAsync(r2, s->dint, sizeof(r2), cudaMemcpyDeviceToHost, s->st);
+  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  s->sweeps_total += r2[2];
+  s->last_sweeps = r2[2];
+  s->gates++;
+  if (r2[3]) return s->sticky = r2[3];
+  const int k2 = r2[1];
+  repack_rows(s, s->G[q], a.G0_out, 2 * dl, k2, ld);
+  repack_blocks(s, s->G[q + 1], a.G1_out, k2, ld, k1);
+  repack_blocks(s, s->G[q + 2], a.G2_out, k1, ld, dr);
+  cudaMemcpyAsync(s->lam[q], a.lam1_out, (size_t)k2 * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  cudaMemcpyAsync(s->lam[q + 1], a.lam2_out, (size_t)k1 * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  s->m[q] = k2;
+  s->m[q + 1] = k1;
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+static int apply_one(mps_state* s, const void* U, const int* sites, int k) {
+  const int q = sites[0];
+  if (k == 1) {
+    const int nab = s->dl(q) * s->dr(q);
+    size_t o_G = align_up(4 * s->cb);
+    if (!grow((void**)&s->tmp, &s->tmp_sz, o_G + (size_t)2 * nab * s->cb + 4096)) return s->sticky = MPS_ENOMEM;
+    uint32_t* dU = (uint32_t*)s->tmp;
+    if (int rc = upload_gate(s, U, 2, dU)) return rc;
+    uint32_t* out = (uint32_t*)(s->tmp + o_G);
+    s->ops->onesite(s->p, s->G[q], out, dU, nab, s->st);
+    cudaMemcpyAsync(s->G[q], out, (size_t)2 * nab * s->cb, cudaMemcpyDeviceToDevice, s->st);
+    s->gates++;
+    return cuda_ok(s, cudaStreamSynchronize(s->st));
+  }
+  if (k == 2 && sites[1] == q + 1) return apply_two_site_batch(s, {q}, {U});
+  if (k == 2) {
+    std::vector<unsigned char> U8;
+    embed_u8((const unsigned char*)U, s->cb, U8, s->p);
+    return apply_three_site(s, q, U8.data());
+  }
+  return apply_three_site(s, q, U);
+}
+
+int mps_apply_gate(mps_state* s, const void* U, const int* sites, int k) {
+  if (!s || !U) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  if (int rc = check_sites(s, sites, k)) return rc;
+  return apply_one(s, U, sites, k);
+}
+
+int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites_flat, const int* k) {
+  if (!s || ng < 0 || (ng && (!U || !sites_flat || !k))) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  std::vector<int> used(s->n, 0);
+  int o = 0;
+  for (int g = 0; g < ng; ++g) {
+    if (int rc = check_sites(s, sites_flat + o, k[g])) return rc;
+    const int lo = sites_flat[o], hi = sites_flat[o + k[g] - 1];
+    for (int q = lo; q <= hi; ++q)
+      if (used[q]++) return MPS_EOVERLAP;
+    o += k[g];
+  }
+  // batched launch of every adjacent two-site gate, the rest one by one
+  std::vector<int> first;
+  std::vector<const void*> us;
+  o = 0;
+  for (int g = 0; g < ng; ++g) {
+    if (k[g] == 2 && sites_flat[o + 1] == sites_flat[o] + 1) {
+      first.push_back(sites_flat[o]);
+      us.push_back(U[g]);
+    }
+    o += k[g];
+  }
+  for (size_t i = 0; i < first.size(); i += 64) {
+    std::vector<int> f(first.begin() + i, first.begin() + std::min(first.size(), i + 64));
+    std::vector<const void*> u(us.begin() + i, us.begin() + std::min(us.size(), i + 64));
+    if (int rc = apply_two_site_batch(s, f, u)) return rc;
+  }
+  o = 0;
+  for (int g = 0; g < ng; ++g) {
+    if (!(k[g] == 2 && sites_flat[o + 1] == sites_flat[o] + 1))
+      if (int rc = apply_one(s, U[g], sites_flat + o, k[g])) return rc;
+    o += k[g];
+  }
+  return MPS_OK;
+}
+
+// ---------------------------------------------------------------- queries
+static int amplitudes(mps_state* s, const uint8_t* bits_host, long long nstates, void* out) {
+  const int n = s->n;
+  int maxchi = 1;
+  for (int b = 0; b + 1 < n; ++b) maxchi = std::max(maxchi, s->m[b]);
+  const int nblocks = (int)std::min<long long>(nstates, 1184);
+  std::vector<int> dims(n + 1);
+  dims[0] = 1;
+  for (int q = 1; q < n; ++q) dims[q] = s->m[q - 1];
+  dims[n] = 1;
+  const size_t o_ptr = 0, o_lam = align_up(8 * (size_t)n), o_dims = o_lam + align_up(8 * (size_t)n),
+               o_bits = o_dims + align_up(4 * (size_t)(n + 1)), o_out = o_bits + align_up((size_t)nstates * n),
+               o_scr = o_out + align_up((size_t)nstates * s->cb),
+               o_end = o_scr + s->ops->amp_scratch(maxchi, nblocks);
+  if (!grow((void**)&s->tmp, &s->tmp_sz, o_end)) return MPS_ENOMEM;
+  std::vector<const uint32_t*> lam(std::max(1, n - 1));
+  for (int b = 0; b + 1 < n; ++b) lam[b] = s->lam[b];
+  cudaMemcpyAsync(s->tmp + o_ptr, s->G.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s->st);
+  cudaMemcpyAsync(s->tmp + o_lam, lam.data(), 8 * lam.size(), cudaMemcpyHostToDevice, s->st);
+  cudaMemcpyAsync(s->tmp + o_dims, dims.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s->st);
+  cudaMemcpyAsync(s->tmp + o_bits, bits_host, (size_t)nstates * n, cudaMemcpyHostToDevice, s->st);
+  s->ops->amplitudes(s->p, (const uint32_t* const*)(s->tmp + o_ptr), (const uint32_t* const*)(s->tmp + o_lam),
+                     (const int*)(s->tmp + o_dims), n, (const uint8_t*)(s->tmp + o_bits), nstates, maxchi,
+                     s->tmp + o_scr, nblocks, (uint32_t*)(s->tmp + o_out), s->st);
+  cudaMemcpyAsync(out, s->tmp + o_out, (size_t)nstates * s->cb, cudaMemcpyDeviceToHost, s->st);
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+int mps_amplitude(mps_state* s, const uint8_t* bits, void* out) {
+  if (!s || !bits || !out) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  for (int q = 0; q < s->n; ++q)
+    if (bits[q] > 1) return MPS_EINVAL;
+  return amplitudes(s, bits, 1, out);
+}
+
+int mps_to_dense(mps_state* s, void* out) {
+  if (!s || !out) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  if (s->n > 24) return MPS_ETOOBIG;
+  const long long ns = 1LL << s->n;
+  std::vector<uint8_t> bits((size_t)ns * s->n);
+  for (long long x = 0; x < ns; ++x)
+    for (int q = 0; q < s->n; ++q) bits[(size_t)x * s->n + q] = (x >> (s->n - 1 - q)) & 1;
+  return amplitudes(s, bits.data(), ns, out);
+}
+
+static int transfer(mps_state* s, const void* O, const int* sites, int k, void* out, void* den_out) {
+  const int n = s->n;
+  int maxchi = 1;
+  for (int b = 0; b + 1 < n; ++b) maxchi = std::max(maxchi, s->m[b]);
+  std::vector<int> dims(n + 1);
+  dims[0] = 1;
+  for (int q = 1; q < n; ++q) dims[q] = s->m[q - 1];
+  dims[n] = 1;
+  const size_t o_O = 0, o_res = align_up(64 * s->cb), o_scr = o_res + align_up(2 * s->cb),
+               o_end = o_scr + s->ops->transfer_scratch(maxchi);
+  if (!grow((void**)&s->tmp, &s->tmp_sz, o_end)) return MPS_ENOMEM;
+  const int D = O ? (1 << k) : 0;
+  if (O) cudaMemcpyAsync(s->tmp + o_O, O, (size_t)D * D * s->cb, cudaMemcpyHostToDevice, s->st);
+  std::vector<const uint32_t*> G(s->G.begin(), s->G.end()), lam(s->lam.begin(), s->lam.end());
+  uint32_t* res = (uint32_t*)(s->tmp + o_res);
+  s->ops->transfer(s->p, n, G.data(), lam.data(), dims.data(), O ? (const uint32_t*)(s->tmp + o_O) : nullptr,
+                   O ? sites[0] : 0, k, s->tmp + o_scr, maxchi, out ? res : nullptr,
+                   den_out ? (uint32_t*)((char*)res + s->cb) : nullptr, s->st);
+  if (out) cudaMemcpyAsync(out, res, s->cb, cudaMemcpyDeviceToHost, s->st);
+  if (den_out) cudaMemcpyAsync(den_out, (char*)res + s->cb, s->rb, cudaMemcpyDeviceToHost, s->st);
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+int mps_norm2(mps_state* s, void* out) {
+  if (!s || !out) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  return transfer(s, nullptr, nullptr, 0, nullptr, out);
+}
+
+int mps_expect(mps_state* s, const void* O, const int* sites, int k, void* out) {
+  if (!s || !O || !out || !sites || k < 1 || k > 3) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  for (int i = 0; i < k; ++i)
+    if (sites[i] != sites[0] + i || sites[i] < 0 || sites[i] >= s->n) return MPS_EINVAL;
+  return transfer(s, O, sites, k, out, nullptr);
+}
+
+int mps_schmidt(mps_state* s, int bond, void* out, int* m) {
+  if (!s || !m || bond < 0 || bond >= s->n - 1) return MPS_EINVAL;
+  *m = s->m[bond];
+  if (out && cudaMemcpy(out, s->lam[bond], (size_t)s->m[bond] * s->rb, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return MPS_ECUDA;
+  return s->sticky;
+}
+
+int mps_get_site(mps_state* s, int site, void* out, int* ml, int* mr) {
+  if (!s || !ml || !mr || site < 0 || site >= s->n) return MPS_EINVAL;
+  *ml = s->dl(site);
+  *mr = s->dr(site);
+  if (out && cudaMemcpy(out, s->G[site], (size_t)2 * *ml * *mr * s->cb, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return MPS_ECUDA;
+  return s->sticky;
+}
+
+int mps_set_schmidt(mps_state* s, int bond, const void* in, int m) {
+  if (!s || !in || bond < 0 || bond >= s->n - 1 || m < 1 || m > s->cap[bond]) return MPS_EINVAL;
+  s->m[bond] = m;
+  return cudaMemcpy(s->lam[bond], in, (size_t)m * s->rb, cudaMemcpyHostToDevice) == cudaSuccess ? MPS_OK : MPS_ECUDA;
+}
+
+int mps_set_site(mps_state* s, int site, const void* in, int ml, int mr) {
+  if (!s || !in || site < 0 || site >= s->n) return MPS_EINVAL;
+  if (ml != s->dl(site) || mr != s->dr(site)) return MPS_EINVAL;
+  return cudaMemcpy(s->G[site], in, (size_t)2 * ml * mr * s->cb, cudaMemcpyHostToDevice) == cudaSuccess ? MPS_OK
+                                                                                                       : MPS_ECUDA;
+}
+
+int mps_stats(mps_state* s, char* json, size_t cap) {
+  if (!s || !json || !cap) return MPS_EINVAL;
+  std::string j = "{\"gates\": " + std::to_string(s->gates) + ", \"sweeps_total\": " + std::to_string(s->sweeps_total) +
+                  ", \"last_sweeps\": " + std::to_string(s->last_sweeps) + ", \"bond_dims\": [";
+  for (int b = 0; b + 1 < s->n; ++b) j += (b ? ", " : "") + std::to_string(s->m[b]);
+  j += "], \"status\": " + std::to_string(s->sticky) + "}";
+  std::snprintf(json, cap, "%s", j.c_str());
+  return j.size() < cap ? MPS_OK : MPS_EINVAL;
+}
+
+}  // extern "C"

@@ -3,7 +3,7 @@
 // gate update; only the input conversion differs.
 #pragma once
 #include "common.h"
-#include "kernels.cuh"
+#include "update.cuh"
 
 namespace mpsb {
 
@@ -143,7 +143,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     std::memset(&fi, 0, sizeof(fi));
     fi.M = Mj; fi.N = Nj; fi.trans = trans; fi.A = A; fi.eA = eA; fi.V = V; fi.alpha = alpha;
     fi.chi_max = Nj; fi.thr = mpf_host_from_double<NL>(0.0); fi.ord = ord; fi.inv_sig = inv_sig; fi.lam = lam;
-    fi.k_out = ip + 1; fi.status = ip + 2; fi.sigma_rec = dsig + (size_t)b * Nj0 * RBr; fi.nsig = Nj0;
+    fi.k_out = ip + 1; fi.status = ip + 2; fi.svd_status = ip; fi.sigma_rec = dsig + (size_t)b * Nj0 * RBr; fi.nsig = Nj0;
     hf[b] = fi;
   }
   cudaMemcpyAsync(base, hd.data(), d_end, cudaMemcpyHostToDevice, st);

@@ -1,0 +1,392 @@
+// Generic (per-item dimensions) drivers of the two-site and three-site gate updates.
+// Used by the MPS state (mps_apply_gate / mps_apply_layer: a layer of disjoint gates is
+// one batched launch per kernel class) and by the configs[1] batch entry.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.h"
+#include "kernels.cuh"
+
+namespace mpsb {
+
+// host construction of an mpf from a double (exact)
+template <int NL>
+inline mpf<NL> mpf_host_from_double(double v) {
+  mpf<NL> r;
+  std::memset(&r, 0, sizeof(r));
+  if (v == 0.0) { r.e = MPF_ZERO; return r; }
+  int k;
+  double f = std::frexp(std::fabs(v), &k);
+  uint64_t man = (uint64_t)std::ldexp(f, 64);
+  r.m[NL - 1] = (uint32_t)(man >> 32);
+  r.m[NL - 2] = (uint32_t)man;
+  r.e = k;
+  r.neg = v < 0;
+  return r;
+}
+
+// Scratch of one Jacobi problem (M x N, N even) + finalize bookkeeping
+template <int L, int NL>
+struct SvdScratch {
+  int64_t* eA; mpf<NL>* alpha; mpf<NL>* gam; mpf<NL>* inv_sig; mpf<NL>* lam; int32_t* coef;
+  int* rot; int* negl; int* ord; int* status; int* sweeps; int* fstatus; int* k; long long* rots;
+  int64_t* e_misc;  // 4 spare exponents
+  static size_t bytes(int N) {
+    return align_up(8 * (size_t)N + 64) + align_up(sizeof(mpf<NL>) * (size_t)N * 4) +
+           align_up(4 * (size_t)N / 2 * 9 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256;
+  }
+  static SvdScratch carve(char* p, int N) {
+    SvdScratch s;
+    s.eA = (int64_t*)p;
+    char* q = p + align_up(8 * (size_t)N + 64);
+    s.alpha = (mpf<NL>*)q;
+    s.gam = s.alpha + N;
+    s.inv_sig = s.gam + N;
+    s.lam = s.inv_sig + N;
+    q += align_up(sizeof(mpf<NL>) * (size_t)N * 4);
+    s.coef = (int32_t*)q;
+    q += align_up(4 * (size_t)N / 2 * 9 * (L + 1));
+    s.rot = (int*)q;
+    s.negl = s.rot + N / 2;
+    s.ord = s.negl + N;
+    q += align_up(4 * (size_t)N * 3);
+    s.status = (int*)q;
+    s.sweeps = s.status + 1;
+    s.fstatus = s.status + 2;
+    s.k = s.status + 3;
+    s.rots = (long long*)(q + 16);
+    s.e_misc = (int64_t*)(q + 32);
+    return s;
+  }
+};
+
+inline size_t mat_bytes(int rows, int cols, int L) { return align_up((size_t)rows * cols * 2 * L * 4); }
+
+// ---------------------------------------------------------------------------- two-site
+struct Upd2Args {
+  int chiL, chiM, chiR, chi_max;
+  const uint32_t *GL, *GR, *lamL, *lamM, *lamR, *U;  // device records (lamL / lamR may be null)
+  uint32_t *GL_out, *GR_out, *lam_out, *sigma_out;    // GL_out [2][chiL][ld], GR_out [2][ld][chiR]
+  int out_ld;
+  int *k_out, *sweeps_out, *status_out;               // device ints (may be null)
+  uint32_t* theta_dbg;                                // column-major Theta' records or null
+};
+
+template <int L, int NL>
+inline size_t upd2_item_bytes(const Upd2Args& a) {
+  const int M = 2 * std::max(a.chiL, a.chiR), N = 2 * std::min(a.chiL, a.chiR);
+  size_t lr = mat_bytes(2 * a.chiL, a.chiM, L) + mat_bytes(a.chiM, 2 * a.chiR, L);
+  size_t r1 = std::max(lr, mat_bytes(M, N, L));
+  return r1 + mat_bytes(2 * a.chiL, 2 * a.chiR, L) + mat_bytes(N, N, L) + SvdScratch<L, NL>::bytes(N) + 256;
+}
+
+template <class T>
+size_t upd2_workspace(const Upd2Args* a, int n) {
+  constexpr int L = T::L, NL = T::NL;
+  size_t s = align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
+             align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + 4096;
+  for (int i = 0; i < n; ++i) s += align_up(upd2_item_bytes<L, NL>(a[i]));
+  return s;
+}
+
+// Launch the update of n independent items (one batched launch per kernel class).
+template <class T>
+int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaStream_t st,
+                   std::vector<unsigned char>& hd) {
+  constexpr int L = T::L, NL = T::NL;
+  const int RBr = record_words(p);
+  const size_t cplx = 2 * (size_t)RBr;
+  char* base = (char*)ws;
+  const size_t d_prep = 0, d_gemm = align_up(sizeof(PrepItem) * 2 * n),
+               d_mix = d_gemm + align_up(sizeof(GemmItem) * n), d_svd = d_mix + align_up(sizeof(MixItem) * n),
+               d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_end = d_fin + align_up(sizeof(FinItem<NL>) * n);
+  hd.assign(d_end, 0);
+  PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
+  GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
+  MixItem* hm = (MixItem*)(hd.data() + d_mix);
+  SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
+  FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
+  const mpf<NL> thr_m = mpf_host_from_double<NL>(thr);
+  char* items = base + d_end;
+  int maxMN = 0, maxLR = 0, maxOut = 0;
+  bool any_dbg = false;
+  std::vector<int64_t*> einit;
+  size_t off = 0;
+  for (int b = 0; b < n; ++b) {
+    const Upd2Args& g = a[b];
+    const int chiL = g.chiL, chiM = g.chiM, chiR = g.chiR;
+    const bool trans = chiR > chiL;
+    const int M = 2 * std::max(chiL, chiR), N = 2 * std::min(chiL, chiR);
+    char* ib = items + off;
+    off += align_up(upd2_item_bytes<L, NL>(g));
+    int32_t* Lf = (int32_t*)ib;
+    int32_t* Rf = (int32_t*)(ib + mat_bytes(2 * chiL, chiM, L));
+    int32_t* Af = (int32_t*)ib;
+    size_t lr = mat_bytes(2 * chiL, chiM, L) + mat_bytes(chiM, 2 * chiR, L);
+    char* p2 = ib + std::max(lr, mat_bytes(M, N, L));
+    int32_t* Tf = (int32_t*)p2;
+    int32_t* Vf = (int32_t*)(p2 + mat_bytes(2 * chiL, 2 * chiR, L));
+    char* sp = (char*)Vf + mat_bytes(N, N, L);
+    auto S = SvdScratch<L, NL>::carve(sp, N);
+    int64_t* eL = S.e_misc;
+    int64_t* eR = S.e_misc + 1;
+    int64_t* eT = S.e_misc + 2;
+    einit.push_back(eL);
+    einit.push_back(eR);
+    hp[2 * b] = PrepItem{g.GL, g.lamL, g.lamM, chiL, chiM, 0, Lf, eL};
+    hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
+    hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
+    hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, Af, S.eA, M, N};
+    SvdItem<NL> si;
+    si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
+    si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
+    si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
+    hs[b] = si;
+    FinItem<NL> fi;
+    std::memset(&fi, 0, sizeof(fi));
+    fi.M = M; fi.N = N; fi.trans = trans ? 1 : 0; fi.A = Af; fi.eA = S.eA; fi.V = Vf; fi.alpha = S.alpha;
+    fi.chi_max = g.chi_max; fi.thr = thr_m; fi.ord = S.ord; fi.inv_sig = S.inv_sig; fi.lam = S.lam;
+    fi.k_out = g.k_out ? g.k_out : S.k; fi.status = g.status_out ? g.status_out : S.fstatus;
+    fi.svd_status = S.status;
+    fi.sigma_rec = g.sigma_out; fi.nsig = N; fi.lam_rec = g.lam_out;
+    fi.GL = g.GL_out; fi.GL_ld = g.out_ld; fi.lamL = g.lamL; fi.chiL_out = chiL;
+    fi.GR = g.GR_out; fi.GR_ld = g.out_ld; fi.lamR = g.lamR; fi.chiR_out = chiR;
+    hf[b] = fi;
+    maxMN = std::max(maxMN, M * N);
+    maxLR = std::max(maxLR, 2 * std::max(chiL, chiR) * chiM);
+    maxOut = std::max(maxOut, 2 * std::max(chiL, chiR) * std::min(g.chi_max, N));
+    any_dbg |= g.theta_dbg != nullptr;
+  }
+  cudaMemcpyAsync(base, hd.data(), d_end, cudaMemcpyHostToDevice, st);
+  int nl = 0;
+  prof_mark(PROF_CONTRACT, 1, st);
+  k_init_prep<<<(2 * n + 255) / 256, 256, 0, st>>>((const PrepItem*)(base + d_prep), 2 * n); ++nl;
+  dim3 gp(std::max(1, std::min(64, (maxLR + 255) / 256)), 2 * n);
+  k_prep_exp<<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
+  k_prep_conv<L, NL><<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
+  dim3 gg(std::max(1, std::min(128, (maxMN + 127) / 128)), n);
+  k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
+  k_mix<L, NL><<<gg, 128, 16 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
+  prof_mark(PROF_CONTRACT, 0, st);
+  if (any_dbg) {
+    for (int b = 0; b < n; ++b) {
+      if (!a[b].theta_dbg) continue;
+      const MixItem& mi = hm[b];
+      k_fixed_to_records<L, NL><<<64, 256, 0, st>>>(mi.A, mi.M, mi.eA, nullptr, mi.M, mi.N, mi.trans,
+                                                    a[b].theta_dbg, RBr, p);
+      ++nl;
+    }
+    return nl;
+  }
+  prof_mark(PROF_JACOBI, 1, st);
+  k_jacobi<L, NL><<<n, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  prof_mark(PROF_JACOBI, 0, st);
+  prof_mark(PROF_FINALIZE, 1, st);
+  int maxN = 0;
+  for (int b = 0; b < n; ++b) maxN = std::max(maxN, hs[b].N);
+  k_finalize<L, NL><<<n, NTHR, sizeof(mpf<NL>) * (size_t)maxN, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p);
+  ++nl;
+  dim3 gs(std::max(1, std::min(64, (2 * maxOut + 255) / 256)), n);
+  k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
+  prof_mark(PROF_FINALIZE, 0, st);
+  (void)cplx;
+  return nl;
+}
+
+// ---------------------------------------------------------------------------- three-site
+// Theta (4chiL x 2chiR) = U8 (lamL G0 lam1 G1 lam2 G2 lamR); SVD#1 splits off site s+2
+// (lambda_{s+1}', Gamma_{s+2}'), M2 = X1 lambda' reshaped (2chiL x 2k1), SVD#2 gives
+// lambda_s', Gamma_s', Gamma_{s+1}' (right site first).
+struct Upd3Args {
+  int chiL, chi1, chi2, chiR, chi_max;
+  const uint32_t *G0, *G1, *G2, *lamL, *lam1, *lam2, *lamR, *U;  // lamL/lamR may be null
+  // outputs (device): G0_out [2][chiL][ld], G1_out [2][ld][ld] (k2 x k1), G2_out [2][ld][chiR]
+  uint32_t *G0_out, *G1_out, *G2_out, *lam1_out, *lam2_out;      // lam1 = lambda_s' (k2), lam2 = lambda_{s+1}' (k1)
+  int ld;
+  int *k1, *k2, *sweeps, *status;  // device
+};
+
+// workspace of one three-site update (bounded by the capacities: k1 <= min(chi_max, 2chiR, 4chiL))
+template <int L, int NL>
+inline size_t upd3_item_bytes(const Upd3Args& a) {
+  const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
+  const int k1max = std::min(a.chi_max, N1);
+  const int M2 = std::max(2 * a.chiL, 2 * k1max), N2 = std::min(2 * a.chiL, 2 * k1max);
+  size_t s = mat_bytes(2 * a.chiL, a.chi1, L) + mat_bytes(a.chi1, 2 * a.chi2, L) + mat_bytes(a.chi2, 2 * a.chiR, L) +
+             mat_bytes(2 * a.chiL, 2 * a.chi2, L) + mat_bytes(4 * a.chiL, a.chi2, L) + mat_bytes(4 * a.chiL, 2 * a.chiR, L) +
+             mat_bytes(M1, N1, L) + mat_bytes(N1, N1, L) + mat_bytes(M2 + 2, N2 + 2, L) + mat_bytes(N2 + 2, N2 + 2, L) +
+             SvdScratch<L, NL>::bytes(N1) + SvdScratch<L, NL>::bytes(N2 + 2) + 1024;
+  return s;
+}
+
+// T (2chiL x 2chi2) -> T' (4chiL x chi2): T'[(2i+j)chiL + a, g] = T[(i chiL + a), (j chi2 + g)]
+template <int L>
+__global__ void k_relayout_T(const int32_t* T, int32_t* Tp, int chiL, int chi2) {
+  const int n = 4 * chiL * chi2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const int r = t % (4 * chiL), g = t / (4 * chiL);
+    const int ij = r / chiL, a = r % chiL, i = ij >> 1, j = ij & 1;
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t x[L];
+      ldfx<L>(T, 2 * chiL, j * chi2 + g, ri, i * chiL + a, x);
+      stfx<L>(Tp, 4 * chiL, g, ri, r, x);
+    }
+  }
+}
+
+template <class T>
+size_t upd3_workspace(const Upd3Args& a) {
+  return upd3_item_bytes<T::L, T::NL>(a) + 4 * 4096;
+}
+
+// Stage 1: contraction, SVD#1, truncation, Gamma_{s+2}' and lambda_{s+1}'.  k1 lands in *a.k1.
+template <class T>
+int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaStream_t st,
+                          std::vector<unsigned char>& hd) {
+  constexpr int L = T::L, NL = T::NL;
+  const int RBr = record_words(p);
+  char* base = (char*)ws;
+  const size_t d_prep = 0, d_gemm = 1024, d_mix = 2048, d_svd = 2560, d_fin = 4096, d_end = 4 * 4096;
+  hd.assign(d_end, 0);
+  char* q = base + d_end;
+  const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
+  const bool trans1 = 2 * a.chiR > 4 * a.chiL;
+  int32_t* Lf = (int32_t*)q; q += mat_bytes(2 * a.chiL, a.chi1, L);
+  int32_t* Mf = (int32_t*)q; q += mat_bytes(a.chi1, 2 * a.chi2, L);
+  int32_t* Rf = (int32_t*)q; q += mat_bytes(a.chi2, 2 * a.chiR, L);
+  int32_t* Tf = (int32_t*)q; q += mat_bytes(2 * a.chiL, 2 * a.chi2, L);
+  int32_t* Tp = (int32_t*)q; q += mat_bytes(4 * a.chiL, a.chi2, L);
+  int32_t* Th = (int32_t*)q; q += mat_bytes(4 * a.chiL, 2 * a.chiR, L);
+  int32_t* A1 = (int32_t*)q; q += mat_bytes(M1, N1, L);
+  int32_t* V1 = (int32_t*)q; q += mat_bytes(N1, N1, L);
+  auto S1 = SvdScratch<L, NL>::carve(q, N1);
+  int64_t* e = S1.e_misc;  // eL, eM, eR, eT ; eTh in S1.e_misc[3]
+  PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
+  hp[0] = PrepItem{a.G0, a.lamL, a.lam1, a.chiL, a.chi1, 0, Lf, e + 0};
+  hp[1] = PrepItem{a.G1, nullptr, a.lam2, a.chi1, a.chi2, 1, Mf, e + 1};
+  hp[2] = PrepItem{a.G2, nullptr, a.lamR, a.chi2, a.chiR, 1, Rf, e + 2};
+  GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
+  static thread_local int64_t dummy;
+  (void)dummy;
+  hg[0] = GemmItem{Lf, 2 * a.chiL, e + 0, Mf, a.chi1, e + 1, Tf, 2 * a.chiL, e + 3, 2 * a.chiL, 2 * a.chi2, a.chi1, 0};
+  // GEMM2 output exponent goes to S1.e_misc... reuse e+0 after GEMM1 consumed it? keep separate: use eA[N1] region
+  int64_t* eTh = S1.eA + N1;  // spare slot after the column exponents (64 bytes of slack)
+  hg[1] = GemmItem{Tp, 4 * a.chiL, e + 3, Rf, a.chi2, e + 2, Th, 4 * a.chiL, eTh, 4 * a.chiL, 2 * a.chiR, a.chi2, 0};
+  MixItem* hm = (MixItem*)(hd.data() + d_mix);
+  hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, A1, S1.eA, M1, N1};
+  SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
+  SvdItem<NL> si;
+  si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
+  si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
+  si.sweeps = S1.sweeps; si.rotations = S1.rots;
+  hs[0] = si;
+  FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
+  FinItem<NL> fi;
+  std::memset(&fi, 0, sizeof(fi));
+  fi.M = M1; fi.N = N1; fi.trans = trans1 ? 1 : 0; fi.A = A1; fi.eA = S1.eA; fi.V = V1; fi.alpha = S1.alpha;
+  fi.chi_max = a.chi_max; fi.thr = mpf_host_from_double<NL>(thr); fi.ord = S1.ord; fi.inv_sig = S1.inv_sig;
+  fi.lam = S1.lam; fi.k_out = a.k1; fi.status = a.status; fi.sigma_rec = nullptr; fi.nsig = 0;
+  fi.svd_status = S1.status;
+  fi.lam_rec = a.lam2_out; fi.GL = nullptr;
+  fi.GR = a.G2_out; fi.GR_ld = a.ld; fi.lamR = a.lamR; fi.chiR_out = a.chiR;
+  fi.chiL2 = a.chiL;
+  hf[0] = fi;
+  cudaMemcpyAsync(base, hd.data(), d_end, cudaMemcpyHostToDevice, st);
+  int nl = 0;
+  k_init_exp<<<1, 32, 0, st>>>(e, 3); ++nl;
+  dim3 gp(std::max(1, std::min(64, (2 * a.chi1 * std::max(a.chiL, a.chi2) + 255) / 256)), 1);
+  for (int i = 0; i < 3; ++i) {
+    k_prep_exp<<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep) + i, RBr); ++nl;
+    k_prep_conv<L, NL><<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep) + i, RBr); ++nl;
+  }
+  dim3 g1(std::max(1, std::min(128, (4 * a.chiL * a.chi2 + 127) / 128)), 1);
+  k_gemm<L><<<g1, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
+  k_relayout_T<L><<<64, 256, 0, st>>>(Tf, Tp, a.chiL, a.chi2); ++nl;
+  dim3 g2(std::max(1, std::min(128, (8 * a.chiL * a.chiR + 127) / 128)), 1);
+  k_gemm<L><<<g2, 128, 0, st>>>((const GemmItem*)(base + d_gemm) + 1); ++nl;
+  k_mix<L, NL><<<g2, 128, 64 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
+  k_jacobi<L, NL><<<1, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N1, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
+  dim3 gs(std::max(1, std::min(64, (2 * a.chiR * N1 + 255) / 256)), 1);
+  k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
+  // sweeps of SVD#1 accumulate into *a.sweeps by the host (stage 2 reads S1.sweeps)
+  cudaMemcpyAsync(a.sweeps, S1.sweeps, sizeof(int), cudaMemcpyDeviceToDevice, st);
+  return nl;
+}
+
+// Stage 2 (k1 known on the host): M2 from SVD#1's left factor, SVD#2, split into G0', G1'.
+template <class T>
+int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws, cudaStream_t st,
+                          std::vector<unsigned char>& hd) {
+  constexpr int L = T::L, NL = T::NL;
+  const int RBr = record_words(p);
+  char* base = (char*)ws;
+  const size_t d_fin = 4096, d_svd2 = 8192, d_fin2 = 12288, d_end = 4 * 4096;
+  // recover the stage-1 layout
+  char* q = base + d_end;
+  const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
+  const int k1max = std::min(a.chi_max, N1);
+  q += mat_bytes(2 * a.chiL, a.chi1, L) + mat_bytes(a.chi1, 2 * a.chi2, L) + mat_bytes(a.chi2, 2 * a.chiR, L) +
+       mat_bytes(2 * a.chiL, 2 * a.chi2, L) + mat_bytes(4 * a.chiL, a.chi2, L) + mat_bytes(4 * a.chiL, 2 * a.chiR, L) +
+       mat_bytes(M1, N1, L) + mat_bytes(N1, N1, L);
+  auto S1 = SvdScratch<L, NL>::carve(q, N1);
+  q += SvdScratch<L, NL>::bytes(N1);
+  const int rows2 = 2 * a.chiL, cols2 = 2 * k1;
+  const bool trans2 = cols2 > rows2;
+  const int M2 = std::max(rows2, cols2), N2 = std::min(rows2, cols2);
+  const int M2c = std::max(2 * a.chiL, 2 * k1max), N2c = std::min(2 * a.chiL, 2 * k1max);
+  int32_t* A2 = (int32_t*)q; q += mat_bytes(M2c + 2, N2c + 2, L);
+  int32_t* V2 = (int32_t*)q; q += mat_bytes(N2c + 2, N2c + 2, L);
+  auto S2 = SvdScratch<L, NL>::carve(q, N2c + 2);
+  hd.assign(d_end, 0);
+  // the FinItem of SVD#1 (re-sent with the M2 target filled in)
+  FinItem<NL>* hf1 = (FinItem<NL>*)(hd.data() + d_fin);
+  {
+    FinItem<NL> fi;
+    std::memset(&fi, 0, sizeof(fi));
+    const int32_t* A1 = (const int32_t*)(base + d_end + mat_bytes(2 * a.chiL, a.chi1, L) +
+                                         mat_bytes(a.chi1, 2 * a.chi2, L) + mat_bytes(a.chi2, 2 * a.chiR, L) +
+                                         mat_bytes(2 * a.chiL, 2 * a.chi2, L) + mat_bytes(4 * a.chiL, a.chi2, L) +
+                                         mat_bytes(4 * a.chiL, 2 * a.chiR, L));
+    fi.M = M1; fi.N = N1; fi.trans = 2 * a.chiR > 4 * a.chiL; fi.A = A1; fi.eA = S1.eA;
+    fi.V = (const int32_t*)((const char*)A1 + mat_bytes(M1, N1, L));
+    fi.alpha = S1.alpha; fi.ord = S1.ord; fi.inv_sig = S1.inv_sig; fi.lam = S1.lam; fi.k_out = a.k1;
+    fi.status = a.status; fi.chiL2 = a.chiL; fi.M2 = A2; fi.eM2 = S2.eA; fi.M2_trans = trans2 ? 1 : 0;
+    hf1[0] = fi;
+  }
+  SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd2);
+  SvdItem<NL> si;
+  si.M = M2; si.N = N2; si.A = A2; si.eA = S2.eA; si.V = V2; si.alpha = S2.alpha; si.gam = S2.gam;
+  si.coef = S2.coef; si.dbg = nullptr; si.rot = S2.rot; si.negl = S2.negl; si.status = S2.status;
+  si.sweeps = S2.sweeps; si.rotations = S2.rots;
+  hs[0] = si;
+  FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
+  FinItem<NL> fi;
+  std::memset(&fi, 0, sizeof(fi));
+  fi.M = M2; fi.N = N2; fi.trans = trans2 ? 1 : 0; fi.A = A2; fi.eA = S2.eA; fi.V = V2; fi.alpha = S2.alpha;
+  fi.chi_max = a.chi_max; fi.thr = mpf_host_from_double<NL>(thr); fi.ord = S2.ord; fi.inv_sig = S2.inv_sig;
+  fi.lam = S2.lam; fi.k_out = a.k2; fi.status = S2.fstatus; fi.sigma_rec = nullptr; fi.nsig = 0;
+  fi.svd_status = S2.status;
+  fi.lam_rec = a.lam1_out;
+  fi.GL = a.G0_out; fi.GL_ld = a.ld; fi.lamL = a.lamL; fi.chiL_out = a.chiL;
+  fi.GR = a.G1_out; fi.GR_ld = a.ld; fi.lamR = a.lam2_out; fi.chiR_out = k1;
+  hf[0] = fi;
+  cudaMemcpyAsync(base + d_fin, hd.data() + d_fin, d_end - d_fin, cudaMemcpyHostToDevice, st);
+  int nl = 0;
+  k_m2_exp<L, NL><<<1, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
+  dim3 gb(std::max(1, std::min(64, (rows2 * cols2 + 255) / 256)), 1);
+  k_build_m2<L, NL><<<gb, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
+  k_jacobi<L, NL><<<1, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd2)); ++nl;
+  k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N2, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
+  dim3 gs(std::max(1, std::min(64, (2 * std::max(a.chiL, k1) * N2 + 255) / 256)), 1);
+  k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
+  k_add_int<<<1, 1, 0, st>>>(a.sweeps, S2.sweeps, a.status, S2.fstatus); ++nl;
+  return nl;
+}
+
+}  // namespace mpsb
