@@ -526,7 +526,7 @@ __device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z
 }
 
 template <int L, int NL>
-__global__ void __launch_bounds__(NTHR) k_jacobi(const SvdItem<NL>* items) {
+__global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdItem<NL>* items) {
   const SvdItem<NL> it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int M = it.M, N = it.N, NP = N / 2;

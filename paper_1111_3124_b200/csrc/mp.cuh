@@ -190,7 +190,7 @@ __device__ __forceinline__ int mpf_cmp(const mpf<NL>& a, const mpf<NL>& b) {
 }
 
 template <int NL>
-__device__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
+__device__ __noinline__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
   if (mpf_is_zero(a) || mpf_is_zero(b)) return mpf_zero<NL>();
   // full product (2NL limbs), keep the top NL+1
   uint32_t p[2 * NL];
@@ -217,7 +217,7 @@ __device__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
 
 // a + b
 template <int NL>
-__device__ mpf<NL> mpf_add(mpf<NL> a, mpf<NL> b) {
+__device__ __noinline__ mpf<NL> mpf_add(mpf<NL> a, mpf<NL> b) {
   if (mpf_is_zero(a)) return b;
   if (mpf_is_zero(b)) return a;
   if (mpf_cmp_abs(a, b) < 0) { mpf<NL> t = a; a = b; b = t; }
@@ -315,7 +315,7 @@ __device__ __forceinline__ mpf<NL> mpf_from_frexp(double f, int64_t E) {
 
 // 1/b by Newton: y <- y + y(1 - b y), quadratic from a 53-bit seed
 template <int NL>
-__device__ mpf<NL> mpf_recip(const mpf<NL>& b) {
+__device__ __noinline__ mpf<NL> mpf_recip(const mpf<NL>& b) {
   int64_t E;
   double f = mpf_frexp(b, &E);
   mpf<NL> y = mpf_from_frexp<NL>(1.0 / f, -E);
@@ -331,7 +331,7 @@ __device__ mpf<NL> mpf_recip(const mpf<NL>& b) {
 
 // 1/sqrt(x), x > 0: y <- y + y(1 - x y^2)/2
 template <int NL>
-__device__ mpf<NL> mpf_rsqrt(const mpf<NL>& x) {
+__device__ __noinline__ mpf<NL> mpf_rsqrt(const mpf<NL>& x) {
   int64_t E;
   double f = mpf_frexp(x, &E);  // x = f 2^E
   if (E & 1) { f *= 0.5; E += 1; }
@@ -435,7 +435,7 @@ __device__ __forceinline__ void mpf_to_record(const mpf<NL>& a, uint32_t* rec, i
 // fixed digits (value = sum d_k 2^(28k) * 2^(E - 28L)) -> mpf.
 // Digits may be unnormalised (any int64 column values); cols = number of digit columns.
 template <int NL, int NC>
-__device__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t E_of_col0) {
+__device__ __noinline__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t E_of_col0) {
   // value = sum_c col[c] 2^(28c) * 2^(E_of_col0).  Resolve carries into a two's-complement
   // integer of 32-bit words, then take sign and magnitude.
   constexpr int NW = (28 * NC + 64) / 32 + 2;
@@ -493,7 +493,7 @@ __device__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t E_of_col0) {
 // mpf -> L fixed digits at column exponent E (value = sum d_k 2^(28k) 2^(E - 28L)),
 // rounded to nearest; requires |a| < 2^E (else the top digit is simply large).
 template <int NL, int L>
-__device__ void mpf_to_fixed(const mpf<NL>& a, int64_t E, int32_t (&d)[L]) {
+__device__ __noinline__ void mpf_to_fixed(const mpf<NL>& a, int64_t E, int32_t (&d)[L]) {
 #pragma unroll
   for (int k = 0; k < L; ++k) d[k] = 0;
   if (mpf_is_zero(a)) return;
