@@ -525,12 +525,53 @@ __device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z
   }
 }
 
+// cp.async staging helpers (4-byte copies, zero-fill past the matrix edge)
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NW>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
+
+// Stage rows [row0, row0+32) of the four operand columns (p re, p im, q re, q im) of a
+// fixed matrix into buf[4][L][32] (one row per lane).
+template <int L>
+__device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int ld, int p, int q, int row0, int rows,
+                                          int lane) {
+  const int r = row0 + lane;
+  const bool ok = r < rows;
+  const int rr = ok ? r : 0;
+#pragma unroll
+  for (int op = 0; op < 4; ++op) {
+    const int col = op < 2 ? p : q, ri = op & 1;
+    const int32_t* g = F + ((size_t)(col * 2 + ri) * L) * ld + rr;
+#pragma unroll
+    for (int k = 0; k < L; ++k) cp_async4(buf + (op * L + k) * 32 + lane, g + (size_t)k * ld, ok);
+  }
+}
+
+// Per output o of (y_p.re, y_p.im, y_q.re, y_q.im): operand index of its three terms
+// (0 x_p.re, 1 x_p.im, 2 x_q.re, 3 x_q.im); coefficients (sign folded) are stored as
+// [mat][o][t] in the same order:
+//   y_p.re = +Cp xrp - Psr xrq - Psi xiq     y_p.im = +Cp xip - Psr xiq + Psi xrq
+//   y_q.re = +Qsr xrp - Qsi xip + Cq xrq     y_q.im = +Qsr xip + Qsi xrp + Cq xiq
+// with Psr+iPsi = s 2^(eq-eo_p) (conj(s) multiplies x_q), Qsr+iQsi = s 2^(ep-eo_q),
+// Cp = c 2^(ep-eo_p), Cq = c 2^(eq-eo_q); for V all scales are 1.
+__constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {0, 1, 2}, {1, 0, 3}};
+
 template <int L, int NL>
 __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdItem<NL>* items) {
   const SvdItem<NL> it = items[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int M = it.M, N = it.N, NP = N / 2;
   const int W = 28 * L;
+  constexpr int CW = L + 1;              // words per coefficient vector
+  constexpr int STAGE = 4 * L * 32;      // words per staging buffer
+  extern __shared__ int32_t jsm[];
+  int32_t* wbuf = jsm + warp * (2 * STAGE + 24 * CW);  // per-warp: 2 stage buffers + 24 coefficients
+  int32_t* wcoef = wbuf + 2 * STAGE;
   __shared__ int s_any;
   __shared__ mpf<NL> s_red[NWARP];
   __shared__ mpf<NL> s_z;
@@ -548,13 +589,12 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   mpf<NL> z = mpf_zero<NL>();
   jac_norms<L, NL>(it, false, z);
   __syncthreads();
-  // ||A||_F^2 and the negligible-column floor z = tol^2 ||A||_F^2, tol = M 2^-W
+  // ||A||_F^2 and the negligible-column floor z = tol^2 ||A||_F^2
   if (warp == 0) {
     mpf<NL> s = mpf_zero<NL>();
     for (int j = lane; j < N; j += 32) s = mpf_add(s, it.alpha[j]);
-    if (lane < NWARP) s_red[lane] = mpf_zero<NL>();
+    if (lane == 0) s_red[0] = mpf_zero<NL>();
     __syncwarp();
-    // serialised lane sum (32 adds)
     for (int l = 0; l < 32; ++l) {
       if (lane == l) s_red[0] = mpf_add(s_red[0], s);
       __syncwarp();
@@ -572,6 +612,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   }
   __syncthreads();
   const mpf<NL> tol2 = mpf_ldexp(mpf_from_int<NL>((int64_t)M * M), 4 - 2 * (int64_t)W);  // tol = 4 M 2^-W
+  const int nchA = (M + 31) / 32, nchV = (N + 31) / 32;
 
   int sweep = 0, conv = 0;
   long long nrot = 0;
@@ -579,7 +620,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     if (tid == 0) s_any = 0;
     __syncthreads();
     for (int step = 0; step < N - 1; ++step) {
-      // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows)
+      // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows, cp.async staging)
       for (int i = warp; i < NP; i += NWARP) {
         int p, q;
         rr_pair(N, step, i, p, q);
@@ -587,18 +628,34 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         int64_t gr[L + 2], gi[L + 2];
 #pragma unroll
         for (int c = 0; c < L + 2; ++c) gr[c] = gi[c] = 0;
-        int cnt = 0;
-        for (int r = lane; r < M; r += 32) {
-          int32_t xrp[L], xip[L], xrq[L], xiq[L];
-          ldfx<L>(it.A, M, p, 0, r, xrp);
-          ldfx<L>(it.A, M, p, 1, r, xip);
-          ldfx<L>(it.A, M, q, 0, r, xrq);
-          ldfx<L>(it.A, M, q, 1, r, xiq);
-          tmul_acc2<L>(gr, xrp, xrq);
-          tmul_acc2<L>(gr, xip, xiq);
-          tmul_acc2<L>(gi, xrp, xiq);
-          tmul_sub2<L>(gi, xip, xrq);
-          if (++cnt == 8) { cnt = 0; tnorm2<L>(gr); tnorm2<L>(gi); }
+        stage_rows<L>(wbuf, it.A, M, p, q, 0, M, lane);
+        cp_commit();
+        for (int ch = 0; ch < nchA; ++ch) {
+          if (ch + 1 < nchA) {
+            stage_rows<L>(wbuf + ((ch + 1) & 1) * STAGE, it.A, M, p, q, (ch + 1) * 32, M, lane);
+            cp_commit();
+            cp_wait<1>();
+          } else {
+            cp_wait<0>();
+          }
+          __syncwarp();
+          const int32_t* b = wbuf + (ch & 1) * STAGE;
+          int32_t xa[L], xb[L];
+          // rows past M were zero-filled: their products vanish
+#pragma unroll
+          for (int k = 0; k < L; ++k) { xa[k] = b[(0 * L + k) * 32 + lane]; xb[k] = b[(2 * L + k) * 32 + lane]; }
+          tmul_acc2<L>(gr, xa, xb);  // xrp xrq
+#pragma unroll
+          for (int k = 0; k < L; ++k) xb[k] = b[(3 * L + k) * 32 + lane];
+          tmul_acc2<L>(gi, xa, xb);  // xrp xiq
+#pragma unroll
+          for (int k = 0; k < L; ++k) xa[k] = b[(1 * L + k) * 32 + lane];
+          tmul_acc2<L>(gr, xa, xb);  // xip xiq
+#pragma unroll
+          for (int k = 0; k < L; ++k) xb[k] = b[(2 * L + k) * 32 + lane];
+          tmul_sub2<L>(gi, xa, xb);  // - xip xrq
+          if ((ch & 7) == 7) { tnorm2<L>(gr); tnorm2<L>(gi); }
+          __syncwarp();
         }
         tnorm2<L>(gr);
         tnorm2<L>(gi);
@@ -651,28 +708,27 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
               if (enew > eb) enew = eb;
               eo[u] = enew;
             }
-            // coefficients relative to the OUTPUT column scale (precision 2^-W of the output):
-            //   y_p = Cp x_p - Sp x_q,  Cp = c 2^(ep - eo_p), Sp = conj(s) 2^(eq - eo_p)
-            //   y_q = Sq x_p + Cq x_q,  Sq = s 2^(ep - eo_q),   Cq = c 2^(eq - eo_q)
-            int32_t* cf = it.coef + (size_t)i * 9 * (L + 1);
-            mpf_to_coef<NL, L>(mpf_ldexp(c, ep - eo[0]), cf + 0 * (L + 1));                 // Cp
-            mpf_to_coef<NL, L>(mpf_ldexp(sr, eq - eo[0]), cf + 1 * (L + 1));                // Spr
-            mpf_to_coef<NL, L>(mpf_neg(mpf_ldexp(si, eq - eo[0])), cf + 2 * (L + 1));       // Spi = -si
-            mpf_to_coef<NL, L>(mpf_ldexp(c, eq - eo[1]), cf + 3 * (L + 1));                 // Cq
-            mpf_to_coef<NL, L>(mpf_ldexp(sr, ep - eo[1]), cf + 4 * (L + 1));                // Sqr
-            mpf_to_coef<NL, L>(mpf_ldexp(si, ep - eo[1]), cf + 5 * (L + 1));                // Sqi
-            mpf_to_coef<NL, L>(c, cf + 6 * (L + 1));                                        // V: c
-            mpf_to_coef<NL, L>(sr, cf + 7 * (L + 1));                                       //    sr
-            mpf_to_coef<NL, L>(si, cf + 8 * (L + 1));                                       //    si
+            // 24 signed coefficient vectors [mat][o][t] (layout: see c_opidx)
+            int32_t* cf = it.coef + (size_t)i * 24 * CW;
+            const mpf<NL> Cp = mpf_ldexp(c, ep - eo[0]), Cq = mpf_ldexp(c, eq - eo[1]);
+            const mpf<NL> Psr = mpf_ldexp(sr, eq - eo[0]), Psi = mpf_ldexp(si, eq - eo[0]);
+            const mpf<NL> Qsr = mpf_ldexp(sr, ep - eo[1]), Qsi = mpf_ldexp(si, ep - eo[1]);
+            const mpf<NL> A12[12] = {Cp, mpf_neg(Psr), mpf_neg(Psi), Cp, mpf_neg(Psr), Psi,
+                                     Qsr, mpf_neg(Qsi), Cq, Qsr, Qsi, Cq};
+            const mpf<NL> V12[12] = {c, mpf_neg(sr), mpf_neg(si), c, mpf_neg(sr), si,
+                                     sr, mpf_neg(si), c, sr, si, c};
+            for (int u = 0; u < 12; ++u) mpf_to_coef<NL, L>(A12[u], cf + u * CW);
+            for (int u = 0; u < 12; ++u) mpf_to_coef<NL, L>(V12[u], cf + (12 + u) * CW);
+            int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
+            for (int u = 0; u < 24; ++u)
+              if (cf[u * CW + L]) ints |= 1 << (u / 3);
             it.alpha[p] = ap;
             it.alpha[q] = aq;
             it.eA[p] = eo[0];
             it.eA[q] = eo[1];
             if (mpf_is_zero(ap) || ap.neg || mpf_cmp(ap, z) <= 0) it.negl[p] = 1;
             if (mpf_is_zero(aq) || aq.neg || mpf_cmp(aq, z) <= 0) it.negl[q] = 1;
-            const int intp = (cf[0 * (L + 1) + L] | cf[1 * (L + 1) + L] | cf[2 * (L + 1) + L]) != 0;
-            const int intq = (cf[3 * (L + 1) + L] | cf[4 * (L + 1) + L] | cf[5 * (L + 1) + L]) != 0;
-            flag = 1 | (intp << 8) | (intq << 16);
+            flag = 1 | (ints << 8);
             s_any = 1;
             ++nrot;
             if (it.dbg) atomicAdd(&it.dbg[sweep < 63 ? sweep : 63], 1);
@@ -687,70 +743,49 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         if (!(flag & 1)) continue;
         int p, q;
         rr_pair(N, step, i, p, q);
-        const bool ip = (flag >> 8) & 1, iq = (flag >> 16) & 1;  // integer digits present
-        const int32_t* cf = it.coef + (size_t)i * 9 * (L + 1);
-        int32_t Cp[L + 1], Spr[L + 1], Spi[L + 1], Cq[L + 1], Sqr[L + 1], Sqi[L + 1];
+        const int32_t* cfg = it.coef + (size_t)i * 24 * CW;
+        for (int w = lane; w < 24 * CW; w += 32) wcoef[w] = cfg[w];
+        __syncwarp();
+        for (int mat = 0; mat < 2; ++mat) {
+          int32_t* F = mat ? it.V : it.A;
+          const int rows = mat ? N : M;
+          const int nch = mat ? nchV : nchA;
+          stage_rows<L>(wbuf, F, rows, p, q, 0, rows, lane);
+          cp_commit();
+          for (int ch = 0; ch < nch; ++ch) {
+            if (ch + 1 < nch) {
+              stage_rows<L>(wbuf + ((ch + 1) & 1) * STAGE, F, rows, p, q, (ch + 1) * 32, rows, lane);
+              cp_commit();
+              cp_wait<1>();
+            } else {
+              cp_wait<0>();
+            }
+            __syncwarp();
+            const int32_t* b = wbuf + (ch & 1) * STAGE;
+            const int r = ch * 32 + lane;
+#pragma unroll 1
+            for (int o = 0; o < 4; ++o) {
+              const bool hasInt = (flag >> (8 + mat * 4 + o)) & 1;
+              int64_t acc[L + 2];
 #pragma unroll
-        for (int k = 0; k <= L; ++k) {
-          Cp[k] = cf[k]; Spr[k] = cf[(L + 1) + k]; Spi[k] = cf[2 * (L + 1) + k];
-          Cq[k] = cf[3 * (L + 1) + k]; Sqr[k] = cf[4 * (L + 1) + k]; Sqi[k] = cf[5 * (L + 1) + k];
-        }
-        for (int r = lane; r < M; r += 32) {
-          int32_t xrp[L], xip[L], xrq[L], xiq[L], o[L];
-          ldfx<L>(it.A, M, p, 0, r, xrp);
-          ldfx<L>(it.A, M, p, 1, r, xip);
-          ldfx<L>(it.A, M, q, 0, r, xrq);
-          ldfx<L>(it.A, M, q, 1, r, xiq);
-          int64_t acc[L + 2];
-          // y_p = Cp x_p - Sp x_q
+              for (int c = 0; c < L + 2; ++c) acc[c] = 0;
 #pragma unroll
-          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
-          kmul_acc<L>(acc, Cp, xrp, ip); kmul_sub<L>(acc, Spr, xrq, ip); kmul_acc<L>(acc, Spi, xiq, ip);
-          tround2<L>(acc, o); stfx<L>(it.A, M, p, 0, r, o);
+              for (int t = 0; t < 3; ++t) {
+                const int32_t* Kp = wcoef + ((mat * 4 + o) * 3 + t) * CW;
+                const int32_t* xp = b + c_opidx[o][t] * L * 32 + lane;
+                int32_t K[L + 1], x[L];
 #pragma unroll
-          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
-          kmul_acc<L>(acc, Cp, xip, ip); kmul_sub<L>(acc, Spr, xiq, ip); kmul_sub<L>(acc, Spi, xrq, ip);
-          tround2<L>(acc, o); stfx<L>(it.A, M, p, 1, r, o);
-          // y_q = Sq x_p + Cq x_q
+                for (int k = 0; k <= L; ++k) K[k] = Kp[k];
 #pragma unroll
-          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
-          kmul_acc<L>(acc, Sqr, xrp, iq); kmul_sub<L>(acc, Sqi, xip, iq); kmul_acc<L>(acc, Cq, xrq, iq);
-          tround2<L>(acc, o); stfx<L>(it.A, M, q, 0, r, o);
-#pragma unroll
-          for (int c = 0; c < L + 2; ++c) acc[c] = 0;
-          kmul_acc<L>(acc, Sqr, xip, iq); kmul_acc<L>(acc, Sqi, xrp, iq); kmul_acc<L>(acc, Cq, xiq, iq);
-          tround2<L>(acc, o); stfx<L>(it.A, M, q, 1, r, o);
-        }
-        // V: v_p' = c v_p - conj(s) v_q ; v_q' = s v_p + c v_q  (fixed scale, |c|,|s| <= 1)
-        int32_t c_[L], sr_[L], si_[L];
-#pragma unroll
-        for (int k = 0; k < L; ++k) { c_[k] = cf[6 * (L + 1) + k]; sr_[k] = cf[7 * (L + 1) + k]; si_[k] = cf[8 * (L + 1) + k]; }
-        // (an integer digit of c or s can only be 1 when the value is exactly 1: fold it)
-        const int32_t cI = cf[6 * (L + 1) + L], srI = cf[7 * (L + 1) + L], siI = cf[8 * (L + 1) + L];
-        c_[L - 1] += cI << 28; sr_[L - 1] += srI << 28; si_[L - 1] += siI << 28;
-        for (int r = lane; r < N; r += 32) {
-          int32_t vrp[L], vip[L], vrq[L], viq[L], o[L];
-          ldfx<L>(it.V, N, p, 0, r, vrp);
-          ldfx<L>(it.V, N, p, 1, r, vip);
-          ldfx<L>(it.V, N, q, 0, r, vrq);
-          ldfx<L>(it.V, N, q, 1, r, viq);
-          int64_t acc[L + 1];
-#pragma unroll
-          for (int c = 0; c <= L; ++c) acc[c] = 0;
-          tmul_acc<L>(acc, c_, vrp); tmul_sub<L>(acc, sr_, vrq); tmul_sub<L>(acc, si_, viq);
-          tround<L>(acc, 0, o); stfx<L>(it.V, N, p, 0, r, o);
-#pragma unroll
-          for (int c = 0; c <= L; ++c) acc[c] = 0;
-          tmul_acc<L>(acc, c_, vip); tmul_sub<L>(acc, sr_, viq); tmul_acc<L>(acc, si_, vrq);
-          tround<L>(acc, 0, o); stfx<L>(it.V, N, p, 1, r, o);
-#pragma unroll
-          for (int c = 0; c <= L; ++c) acc[c] = 0;
-          tmul_acc<L>(acc, sr_, vrp); tmul_sub<L>(acc, si_, vip); tmul_acc<L>(acc, c_, vrq);
-          tround<L>(acc, 0, o); stfx<L>(it.V, N, q, 0, r, o);
-#pragma unroll
-          for (int c = 0; c <= L; ++c) acc[c] = 0;
-          tmul_acc<L>(acc, sr_, vip); tmul_acc<L>(acc, si_, vrp); tmul_acc<L>(acc, c_, viq);
-          tround<L>(acc, 0, o); stfx<L>(it.V, N, q, 1, r, o);
+                for (int k = 0; k < L; ++k) x[k] = xp[k * 32];
+                kmul_acc<L>(acc, K, x, hasInt);
+              }
+              int32_t out[L];
+              tround2<L>(acc, out);
+              if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
+            }
+            __syncwarp();
+          }
         }
       }
       __syncthreads();
@@ -771,6 +806,19 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     *it.sweeps = conv ? sweep : MAX_SWEEPS + 1;
     *it.status = conv ? 0 : -3;
     *it.rotations = s_rot;
+  }
+}
+
+template <int L>
+constexpr size_t jacobi_smem_bytes() { return (size_t)NWARP * (2 * 4 * L * 32 + 24 * (L + 1)) * 4; }
+
+// opt in to > 48 KB of dynamic shared memory (once per instantiation)
+template <int L, int NL>
+inline void jacobi_prepare() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(k_jacobi<L, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jacobi_smem_bytes<L>());
+    done = true;
   }
 }
 

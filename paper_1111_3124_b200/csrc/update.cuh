@@ -38,7 +38,7 @@ struct SvdScratch {
   int64_t* e_misc;  // 4 spare exponents
   static size_t bytes(int N) {
     return align_up(8 * (size_t)N + 64) + align_up(sizeof(mpf<NL>) * (size_t)N * 4) +
-           align_up(4 * (size_t)N / 2 * 9 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256;
+           align_up(4 * (size_t)N / 2 * 24 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256;
   }
   static SvdScratch carve(char* p, int N) {
     SvdScratch s;
@@ -50,7 +50,7 @@ struct SvdScratch {
     s.lam = s.inv_sig + N;
     q += align_up(sizeof(mpf<NL>) * (size_t)N * 4);
     s.coef = (int32_t*)q;
-    q += align_up(4 * (size_t)N / 2 * 9 * (L + 1));
+    q += align_up(4 * (size_t)N / 2 * 24 * (L + 1));
     s.rot = (int*)q;
     s.negl = s.rot + N / 2;
     s.ord = s.negl + N;
@@ -184,7 +184,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     return nl;
   }
   prof_mark(PROF_JACOBI, 1, st);
-  k_jacobi<L, NL><<<n, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  jacobi_prepare<L, NL>();
+  k_jacobi<L, NL><<<n, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
   prof_mark(PROF_JACOBI, 0, st);
   prof_mark(PROF_FINALIZE, 1, st);
   int maxN = 0;
@@ -310,7 +311,8 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   dim3 g2(std::max(1, std::min(128, (8 * a.chiL * a.chiR + 127) / 128)), 1);
   k_gemm<L><<<g2, 128, 0, st>>>((const GemmItem*)(base + d_gemm) + 1); ++nl;
   k_mix<L, NL><<<g2, 128, 64 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
-  k_jacobi<L, NL><<<1, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  jacobi_prepare<L, NL>();
+  k_jacobi<L, NL><<<1, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N1, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * a.chiR * N1 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
@@ -381,7 +383,8 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   k_m2_exp<L, NL><<<1, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
   dim3 gb(std::max(1, std::min(64, (rows2 * cols2 + 255) / 256)), 1);
   k_build_m2<L, NL><<<gb, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
-  k_jacobi<L, NL><<<1, NTHR, 0, st>>>((const SvdItem<NL>*)(base + d_svd2)); ++nl;
+  jacobi_prepare<L, NL>();
+  k_jacobi<L, NL><<<1, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd2)); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N2, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * std::max(a.chiL, k1) * N2 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
