@@ -135,6 +135,15 @@ class OracleMPS:
         s = (ctypes.c_int * len(sites))(*sites)
         _chk(lib().orc_mps_apply(self.h, _ptr(U), s, len(sites)))
 
+    def apply_layer(self, gates, nthreads=None):
+        """gates: list of (U records, sites); disjoint gates computed in parallel threads."""
+        n = len(gates)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[U.ctypes.data for U, _ in gates])
+        flat = [q for _, s in gates for q in s]
+        sf = (ctypes.c_int * max(len(flat), 1))(*flat)
+        ks = (ctypes.c_int * max(n, 1))(*[len(s) for _, s in gates])
+        _chk(lib().orc_mps_apply_layer(self.h, n, ptrs, sf, ks, nthreads or os.cpu_count()))
+
     def amplitude(self, bits) -> np.ndarray:
         b = np.asarray(bits, np.uint8)
         out = R.empty(self.p, 2)

@@ -226,6 +226,84 @@ int orc_mps_apply(void* hv, const uchar* U, const int* sites, int k) {
   GUARD_END
 }
 
+// A layer of pairwise-disjoint gates: the updates (pure functions of the current tensors)
+// are computed in parallel threads and committed in gate order; the arithmetic of every
+// gate is exactly mps_apply's (parallelism over disjoint gates only).
+int orc_mps_apply_layer(void* hv, int ng, const uchar* const* U, const int* sites_flat, const int* k, int nthreads) {
+  GUARD_BEGIN
+  auto* h = (OrcMps*)hv;
+  set_prec(h->p);
+  Mps& st = h->st;
+  std::vector<int> off(ng + 1, 0), used(st.n, 0);
+  for (int g = 0; g < ng; ++g) {
+    off[g + 1] = off[g] + k[g];
+    const int* s = sites_flat + off[g];
+    for (int i = 0; i < k[g]; ++i) if (s[i] < 0 || s[i] >= st.n || (i && s[i] <= s[i - 1])) return ORC_EINVAL;
+    for (int q = s[0]; q <= s[k[g] - 1]; ++q) if (used[q]++) return ORC_EOVERLAP;
+  }
+  // one-site gates and anything but plain adjacent two-site / three-site run sequentially
+  std::vector<int> par;
+  for (int g = 0; g < ng; ++g) {
+    const int* s = sites_flat + off[g];
+    bool adj2 = k[g] == 2 && s[1] == s[0] + 1, adj3 = k[g] == 3;
+    if (adj2 || adj3) par.push_back(g);
+  }
+  std::vector<Update2> r2(ng);
+  std::vector<Update3> r3(ng);
+  std::vector<CVec> Us(ng);
+  for (int g = 0; g < ng; ++g) Us[g] = read_c(U[g], (size_t)1 << (2 * k[g]));
+  std::atomic<int> next(0);
+  std::string err;
+  auto lamL = [&](int s) { return s == 0 ? RVec(1, from_int(1)) : st.lam[s - 1]; };
+  auto lamR = [&](int s) { return s == st.n - 1 ? RVec(1, from_int(1)) : st.lam[s]; };
+  auto work = [&]() {
+    set_prec(h->p);
+    try {
+      for (int j; (j = next++) < (int)par.size();) {
+        const int g = par[j];
+        const int s = sites_flat[off[g]];
+        if (k[g] == 2)
+          r2[g] = update_two_site(st.G[s], st.G[s + 1], lamL(s), st.lam[s], lamR(s + 1), st.dl(s), st.m[s],
+                                  st.dr(s + 1), Us[g], st.chi_max, st.thr);
+        else
+          r3[g] = update_three_site(st.G[s], st.G[s + 1], st.G[s + 2], lamL(s), st.lam[s], st.lam[s + 1],
+                                    lamR(s + 2), st.dl(s), st.m[s], st.m[s + 1], st.dr(s + 2), Us[g], st.chi_max,
+                                    st.thr);
+      }
+    } catch (const std::exception& e) {
+      err = e.what();
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 0; t < std::max(1, nthreads); ++t) th.emplace_back(work);
+  for (auto& t : th) t.join();
+  if (!err.empty()) { g_err = err; return -99; }
+  int rc = 0;
+  for (int g = 0; g < ng && !rc; ++g) {
+    const int* s = sites_flat + off[g];
+    const int q = s[0];
+    bool adj2 = k[g] == 2 && s[1] == s[0] + 1;
+    if (adj2) {
+      Update2& u = r2[g];
+      st.sweeps_total += u.sweeps;
+      st.gates++;
+      if (u.status) { rc = u.status; break; }
+      st.G[q] = u.GL; st.G[q + 1] = u.GR; st.lam[q] = u.lam; st.m[q] = u.k;
+    } else if (k[g] == 3) {
+      Update3& u = r3[g];
+      st.sweeps_total += u.sweeps;
+      st.gates++;
+      if (u.status) { rc = u.status; break; }
+      st.G[q] = u.G0; st.G[q + 1] = u.G1; st.G[q + 2] = u.G2;
+      st.lam[q] = u.lam1; st.lam[q + 1] = u.lam2; st.m[q] = u.k2; st.m[q + 1] = u.k1;
+    } else {
+      rc = mps_apply(st, Us[g], s, k[g]);
+    }
+  }
+  return rc;
+  GUARD_END
+}
+
 int orc_mps_amplitude(void* hv, const uint8_t* bits, uchar* out) {
   GUARD_BEGIN
   auto* h = (OrcMps*)hv;
