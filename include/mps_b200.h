@@ -102,6 +102,33 @@ int mps_norm2(mps_state* st, void* out);
 int mps_to_dense(mps_state* st, void* out);
 int mps_sync(mps_state* st); /* first sticky error or MPS_OK */
 
+/* ---- site-sharded blocks -----------------------------------------
+ * A block state holds the global sites [site_lo, site_hi) of an n_total-site chain (one
+ * block per GPU, contiguous).  The bonds site_lo-1 and site_hi-1 are external: their
+ * Schmidt vectors are mirrored in both neighbouring blocks.  Gates fully inside a block use
+ * mps_apply_gate / mps_apply_layer with LOCAL site indices.  A two-site gate on the block
+ * edge (site_hi-1, site_hi) runs on the left block: the right block exports its first site
+ * and the Schmidt vector right of it (device buffers), the left block applies the update and
+ * returns the new first site of the right block and the new shared Schmidt vector, which the
+ * right block imports.  The halo buffers move between GPUs by NCCL send/recv (the Python
+ * driver, paper_1111_3124_b200/dist.py).  Device pointers below are CUDA device memory. */
+int mps_init_block(mps_state** out, int n_total, int site_lo, int site_hi, int prec_bits, int chi_max,
+                   double trunc_thr);
+int mps_block_dims(mps_state* st, int* site_lo, int* n_local, int* m_ext_l, int* m_ext_r);
+/* first local site [2][m_l][m_r] -> dG (device), Schmidt vector right of it (m_r reals) -> dlam (device, may be NULL) */
+int mps_block_export_first(mps_state* st, void* dG, void* dlam, int* m_l, int* m_r);
+/* U (host 4x4 records) on (last local site, halo site); dG_halo [2][m_ext_r][m_h] (device), dlam_h the
+ * Schmidt vector right of the halo site (device, NULL at the chain end).  Outputs (device): the halo
+ * site [2][k][m_h] and the new shared Schmidt vector (k reals); k_out host int. */
+int mps_block_boundary_apply(mps_state* st, const void* U, const void* dG_halo, int m_h, const void* dlam_h,
+                             void* dG_halo_out, void* dlam_mid_out, int* k_out);
+/* replace the first local site by dG0 [2][k][m_r] and the external left Schmidt vector by dlam_mid (k) */
+int mps_block_import_first(mps_state* st, const void* dG0, const void* dlam_mid, int k);
+/* amplitude chain over the block: v_out = (v_in lambda_ext_l) Gamma_lo^{b0} lambda ... Gamma_hi-1^{b};
+ * v_in: m_ext_l complex (host; ignored for the first block), v_out: m_ext_r complex (host; the
+ * amplitude itself for the last block). bits: n_local entries. */
+int mps_amplitude_block(mps_state* st, const uint8_t* bits, const void* v_in, void* v_out);
+
 /* ---- diagnostics / test surface ----------------------------------------------- */
 int mps_n_qubits(mps_state* st);
 int mps_bond_dims(mps_state* st, int* out /* n-1 ints */);

@@ -55,26 +55,29 @@ __global__ void k_onesite(const uint32_t* G, uint32_t* Gout, const uint32_t* U, 
 }
 
 // Amplitudes c(b) = G_0^{b0} lam_0 G_1^{b1} ... (Eq. 1), one CTA per basis state (grid-stride),
-// vector ping-pong in global scratch (2 * maxchi cmpf per CTA).
+// vector ping-pong in global scratch (2 * maxchi cmpf per CTA).  Block form (site-sharded
+// state): the chain starts from v_in (dims[0] complex records, null = [1]) and lam[s] is the
+// Schmidt vector left of local site s (lam[0] = the external left bond or null); the output
+// per state is the dims[n]-vector (the amplitude itself for a whole chain).
 template <int NL>
 __global__ void k_amplitudes(const uint32_t* const* G, const uint32_t* const* lam, const int* dims, int n,
-                             const uint8_t* bits, long long nstates, int maxchi, cmpf<NL>* scratch, uint32_t* out,
-                             int RBr, int p) {
+                             const uint8_t* bits, long long nstates, int maxchi, cmpf<NL>* scratch,
+                             const uint32_t* v_in, uint32_t* out, int RBr, int p) {
   for (long long st = blockIdx.x; st < nstates; st += gridDim.x) {
     cmpf<NL>* v0 = scratch + (size_t)blockIdx.x * 2 * maxchi;
     cmpf<NL>* v1 = v0 + maxchi;
     const uint8_t* b = bits + st * n;
-    // site 0: v(c) = G_0^{b0}(0, c)
-    int dr = dims[1];
-    for (int c = threadIdx.x; c < dr; c += blockDim.x) v0[c] = cm_from_rec<NL>(G[0] + (size_t)(2 * (b[0] * dr + c)) * RBr, RBr);
+    for (int a = threadIdx.x; a < dims[0]; a += blockDim.x)
+      v0[a] = v_in ? cm_from_rec<NL>(v_in + (size_t)(2 * a) * RBr, RBr)
+                   : cmpf<NL>{mpf_from_int<NL>(1), mpf_zero<NL>()};
     __syncthreads();
-    for (int s = 1; s < n; ++s) {
+    for (int s = 0; s < n; ++s) {
       const int dl = dims[s], drs = dims[s + 1];
       const uint32_t* g = G[s] + (size_t)(2 * b[s] * dl * drs) * RBr;
       for (int c = threadIdx.x; c < drs; c += blockDim.x) {
         cmpf<NL> acc = cm_zero<NL>();
         for (int a = 0; a < dl; ++a) {
-          const cmpf<NL> w = cm_scale(mpf_from_record<NL>(lam[s - 1] + (size_t)a * RBr, RBr - 4), v0[a]);
+          const cmpf<NL> w = lam[s] ? cm_scale(mpf_from_record<NL>(lam[s] + (size_t)a * RBr, RBr - 4), v0[a]) : v0[a];
           acc = cm_add(acc, cm_mul(w, cm_from_rec<NL>(g + (size_t)(2 * (a * drs + c)) * RBr, RBr)));
         }
         v1[c] = acc;
@@ -82,7 +85,8 @@ __global__ void k_amplitudes(const uint32_t* const* G, const uint32_t* const* la
       __syncthreads();
       cmpf<NL>* t = v0; v0 = v1; v1 = t;
     }
-    if (threadIdx.x == 0) cm_to_rec<NL>(v0[0], out + (size_t)(2 * st) * RBr, RBr, p);
+    for (int c = threadIdx.x; c < dims[n]; c += blockDim.x)
+      cm_to_rec<NL>(v0[c], out + (size_t)(2 * (st * dims[n] + c)) * RBr, RBr, p);
     __syncthreads();
   }
 }
@@ -169,10 +173,10 @@ size_t amp_scratch_bytes(int maxchi, int nblocks) { return sizeof(cmpf<T::NL>) *
 
 template <class T>
 void run_amplitudes(int p, const uint32_t* const* G, const uint32_t* const* lam, const int* dims, int n,
-                    const uint8_t* bits, long long nstates, int maxchi, void* scratch, int nblocks, uint32_t* out,
-                    cudaStream_t st) {
-  k_amplitudes<T::NL><<<nblocks, 128, 0, st>>>(G, lam, dims, n, bits, nstates, maxchi, (cmpf<T::NL>*)scratch, out,
-                                              record_words(p), p);
+                    const uint8_t* bits, long long nstates, int maxchi, void* scratch, int nblocks,
+                    const uint32_t* v_in, uint32_t* out, cudaStream_t st) {
+  k_amplitudes<T::NL><<<nblocks, 128, 0, st>>>(G, lam, dims, n, bits, nstates, maxchi, (cmpf<T::NL>*)scratch, v_in,
+                                              out, record_words(p), p);
 }
 
 template <class T>

@@ -23,6 +23,13 @@ using namespace mpsb;
 
 struct mps_state {
   int n = 0, p = 0, chi_max = 0, RBr = 0;
+  // block (site-sharded) state: local sites are global [lo, lo+n) of ntot; the bonds
+  // outside the block (lo-1 and lo+n-1) are external, with their Schmidt vectors mirrored
+  int lo = 0, ntot = 0;
+  bool has_l = false, has_r = false;
+  int m_el = 1, m_er = 1, cap_el = 1, cap_er = 1;
+  uint32_t* lam_el = nullptr;
+  uint32_t* lam_er = nullptr;
   size_t rb = 0, cb = 0;
   double thr = 0;
   cudaStream_t st = 0;
@@ -37,10 +44,14 @@ struct mps_state {
   int* dint = nullptr;  // 256 device ints
   long long gates = 0, sweeps_total = 0;
   int last_sweeps = 0;
-  int dl(int s) const { return s == 0 ? 1 : m[s - 1]; }
-  int dr(int s) const { return s == n - 1 ? 1 : m[s]; }
-  int capl(int s) const { return s == 0 ? 1 : cap[s - 1]; }
-  int capr(int s) const { return s == n - 1 ? 1 : cap[s]; }
+  int dl(int s) const { return s == 0 ? (has_l ? m_el : 1) : m[s - 1]; }
+  int dr(int s) const { return s == n - 1 ? (has_r ? m_er : 1) : m[s]; }
+  int capl(int s) const { return s == 0 ? (has_l ? cap_el : 1) : cap[s - 1]; }
+  int capr(int s) const { return s == n - 1 ? (has_r ? cap_er : 1) : cap[s]; }
+  // Schmidt vector left of site s / right of site s (null = the trivial [1] of a chain end)
+  const uint32_t* lamL(int s) const { return s > 0 ? lam[s - 1] : (has_l ? lam_el : nullptr); }
+  const uint32_t* lamR(int s) const { return s < n - 1 ? lam[s] : (has_r ? lam_er : nullptr); }
+  int capR(int s) const { return s < n - 1 ? cap[s] : cap_er; }  // capacity of the bond right of s
 };
 
 namespace {
@@ -133,15 +144,27 @@ struct TwoSitePlan {
 
 extern "C" {
 
-int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
+// global bond b capacity: Schmidt rank <= min(2^(b+1), 2^(N-b-1)), and <= chi_max
+static int gcap(int b, int N, int chi_max) {
+  int e = std::min(b + 1, N - b - 1);
+  long long c = e >= 30 ? (1LL << 30) : (1LL << e);
+  return (int)std::min<long long>(chi_max, c);
+}
+
+int mps_init_block(mps_state** out, int ntot, int lo, int hi, int p, int chi_max, double thr) {
   if (!out) return MPS_EINVAL;
   *out = nullptr;
-  if (n < 1 || chi_max < 1) return MPS_EINVAL;
+  if (ntot < 1 || chi_max < 1 || lo < 0 || hi > ntot || hi <= lo) return MPS_EINVAL;
   if (p < 64 || p > 512 || chi_max > MAX_CHI) return MPS_EUNSUPPORTED;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return MPS_ECUDA;
+  const int n = hi - lo;
   auto* s = new mps_state();
   s->n = n;
+  s->lo = lo;
+  s->ntot = ntot;
+  s->has_l = lo > 0;
+  s->has_r = hi < ntot;
   s->p = p;
   s->chi_max = chi_max;
   s->RBr = record_words(p);
@@ -151,11 +174,9 @@ int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
   s->ops = &tier_ops(p);
   s->m.assign(n > 1 ? n - 1 : 0, 1);
   s->cap.resize(n > 1 ? n - 1 : 0);
-  for (int b = 0; b + 1 < n; ++b) {
-    int e = std::min(b + 1, n - b - 1);
-    long long c = e >= 30 ? (1LL << 30) : (1LL << e);
-    s->cap[b] = (int)std::min<long long>(chi_max, c);
-  }
+  for (int b = 0; b + 1 < n; ++b) s->cap[b] = gcap(lo + b, ntot, chi_max);
+  if (s->has_l) s->cap_el = gcap(lo - 1, ntot, chi_max);
+  if (s->has_r) s->cap_er = gcap(hi - 1, ntot, chi_max);
   std::vector<uint32_t> one, zero;
   host_record(p, 1, one);
   host_record(p, 0, zero);
@@ -177,6 +198,14 @@ int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
     ok = cudaMalloc(&s->lam[b], (size_t)s->cap[b] * s->rb) == cudaSuccess;
     if (ok) cudaMemcpy(s->lam[b], one.data(), s->rb, cudaMemcpyHostToDevice);
   }
+  if (ok && s->has_l) {
+    ok = cudaMalloc(&s->lam_el, (size_t)s->cap_el * s->rb) == cudaSuccess;
+    if (ok) cudaMemcpy(s->lam_el, one.data(), s->rb, cudaMemcpyHostToDevice);
+  }
+  if (ok && s->has_r) {
+    ok = cudaMalloc(&s->lam_er, (size_t)s->cap_er * s->rb) == cudaSuccess;
+    if (ok) cudaMemcpy(s->lam_er, one.data(), s->rb, cudaMemcpyHostToDevice);
+  }
   if (!ok) {
     mps_free(s);
     return MPS_ENOMEM;
@@ -185,10 +214,16 @@ int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
   return MPS_OK;
 }
 
+int mps_init(mps_state** out, int n, int p, int chi_max, double thr) {
+  return mps_init_block(out, n, 0, n, p, chi_max, thr);
+}
+
 void mps_free(mps_state* s) {
   if (!s) return;
   for (auto* g : s->G) cudaFree(g);
   for (auto* l : s->lam) cudaFree(l);
+  if (s->lam_el) cudaFree(s->lam_el);
+  if (s->lam_er) cudaFree(s->lam_er);
   if (s->ws) cudaFree(s->ws);
   if (s->tmp) cudaFree(s->tmp);
   if (s->dint) cudaFree(s->dint);
@@ -221,7 +256,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
   // temp layout per gate: U (16 cplx), GL out [2][dl][ld], GR out [2][ld][dr], lam [ld], sigma [N]
   std::vector<size_t> off(ng + 1, 0);
   for (int g = 0; g < ng; ++g) {
-    const int q = first[g], ld = s->cap[q];
+    const int q = first[g], ld = s->capR(q);
     const int dl = s->dl(q), dr = s->dr(q + 1);
     size_t need = align_up(16 * s->cb) + align_up((size_t)2 * dl * ld * s->cb) + align_up((size_t)2 * ld * dr * s->cb) +
                   align_up((size_t)ld * s->rb) + align_up((size_t)2 * std::max(dl, dr) * s->rb);
@@ -230,7 +265,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
   if (!grow((void**)&s->tmp, &s->tmp_sz, off[ng] + 4096)) return s->sticky = MPS_ENOMEM;
   std::vector<Upd2Args> args(ng);
   for (int g = 0; g < ng; ++g) {
-    const int q = first[g], ld = s->cap[q];
+    const int q = first[g], ld = s->capR(q);
     const int dl = s->dl(q), dr = s->dr(q + 1);
     char* b = s->tmp + off[g];
     uint32_t* dU = (uint32_t*)b;
@@ -239,9 +274,9 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
     std::memset(&a, 0, sizeof(a));
     a.chiL = dl; a.chiM = s->m[q]; a.chiR = dr; a.chi_max = s->chi_max;
     a.GL = s->G[q]; a.GR = s->G[q + 1];
-    a.lamL = q > 0 ? s->lam[q - 1] : nullptr;
+    a.lamL = s->lamL(q);
     a.lamM = s->lam[q];
-    a.lamR = q + 1 < s->n - 1 ? s->lam[q + 1] : nullptr;
+    a.lamR = s->lamR(q + 1);
     a.U = dU;
     b += align_up(16 * s->cb);
     a.GL_out = (uint32_t*)b; b += align_up((size_t)2 * dl * ld * s->cb);
@@ -266,7 +301,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
     s->last_sweeps = sw;
     s->gates++;
     if (stt) return s->sticky = stt;
-    const int q = first[g], ld = s->cap[q];
+    const int q = first[g], ld = s->capR(q);
     const int dl = s->dl(q), dr = s->dr(q + 1);
     repack_rows(s, s->G[q], args[g].GL_out, 2 * dl, k, ld);
     repack_blocks(s, s->G[q + 1], args[g].GR_out, k, ld, dr);
@@ -289,10 +324,10 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
   std::memset(&a, 0, sizeof(a));
   a.chiL = dl; a.chi1 = d1; a.chi2 = d2; a.chiR = dr; a.chi_max = s->chi_max;
   a.G0 = s->G[q]; a.G1 = s->G[q + 1]; a.G2 = s->G[q + 2];
-  a.lamL = q > 0 ? s->lam[q - 1] : nullptr;
+  a.lamL = s->lamL(q);
   a.lam1 = s->lam[q];
   a.lam2 = s->lam[q + 1];
-  a.lamR = q + 2 < s->n - 1 ? s->lam[q + 2] : nullptr;
+  a.lamR = s->lamR(q + 2);
   a.U = dU;
   a.G0_out = (uint32_t*)(s->tmp + o_G0);
   a.G1_out = (uint32_t*)(s->tmp + o_G1);
@@ -398,53 +433,60 @@ int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites
 }
 
 // ---------------------------------------------------------------- queries
-static int amplitudes(mps_state* s, const uint8_t* bits_host, long long nstates, void* out) {
+// amplitude chains of nstates bit strings over the local sites; v_in (host, dl(0) complex
+// records) or null; out receives dr(n-1) complex records per state
+static int amplitudes(mps_state* s, const uint8_t* bits_host, long long nstates, const void* v_in, void* out) {
   const int n = s->n;
-  int maxchi = 1;
+  int maxchi = std::max(s->dl(0), s->dr(n - 1));
   for (int b = 0; b + 1 < n; ++b) maxchi = std::max(maxchi, s->m[b]);
   const int nblocks = (int)std::min<long long>(nstates, 1184);
   std::vector<int> dims(n + 1);
-  dims[0] = 1;
-  for (int q = 1; q < n; ++q) dims[q] = s->m[q - 1];
-  dims[n] = 1;
+  for (int q = 0; q < n; ++q) dims[q] = s->dl(q);
+  dims[n] = s->dr(n - 1);
   const size_t o_ptr = 0, o_lam = align_up(8 * (size_t)n), o_dims = o_lam + align_up(8 * (size_t)n),
-               o_bits = o_dims + align_up(4 * (size_t)(n + 1)), o_out = o_bits + align_up((size_t)nstates * n),
-               o_scr = o_out + align_up((size_t)nstates * s->cb),
+               o_vin = o_dims + align_up(4 * (size_t)(n + 1)), o_bits = o_vin + align_up((size_t)dims[0] * s->cb),
+               o_out = o_bits + align_up((size_t)nstates * n),
+               o_scr = o_out + align_up((size_t)nstates * dims[n] * s->cb),
                o_end = o_scr + s->ops->amp_scratch(maxchi, nblocks);
   if (!grow((void**)&s->tmp, &s->tmp_sz, o_end)) return MPS_ENOMEM;
-  std::vector<const uint32_t*> lam(std::max(1, n - 1));
-  for (int b = 0; b + 1 < n; ++b) lam[b] = s->lam[b];
+  std::vector<const uint32_t*> lam(n);
+  for (int q = 0; q < n; ++q) lam[q] = s->lamL(q);
   cudaMemcpyAsync(s->tmp + o_ptr, s->G.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s->st);
-  cudaMemcpyAsync(s->tmp + o_lam, lam.data(), 8 * lam.size(), cudaMemcpyHostToDevice, s->st);
+  cudaMemcpyAsync(s->tmp + o_lam, lam.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s->st);
   cudaMemcpyAsync(s->tmp + o_dims, dims.data(), 4 * (size_t)(n + 1), cudaMemcpyHostToDevice, s->st);
+  if (v_in) cudaMemcpyAsync(s->tmp + o_vin, v_in, (size_t)dims[0] * s->cb, cudaMemcpyHostToDevice, s->st);
   cudaMemcpyAsync(s->tmp + o_bits, bits_host, (size_t)nstates * n, cudaMemcpyHostToDevice, s->st);
   s->ops->amplitudes(s->p, (const uint32_t* const*)(s->tmp + o_ptr), (const uint32_t* const*)(s->tmp + o_lam),
                      (const int*)(s->tmp + o_dims), n, (const uint8_t*)(s->tmp + o_bits), nstates, maxchi,
-                     s->tmp + o_scr, nblocks, (uint32_t*)(s->tmp + o_out), s->st);
-  cudaMemcpyAsync(out, s->tmp + o_out, (size_t)nstates * s->cb, cudaMemcpyDeviceToHost, s->st);
+                     s->tmp + o_scr, nblocks, v_in ? (const uint32_t*)(s->tmp + o_vin) : nullptr,
+                     (uint32_t*)(s->tmp + o_out), s->st);
+  cudaMemcpyAsync(out, s->tmp + o_out, (size_t)nstates * dims[n] * s->cb, cudaMemcpyDeviceToHost, s->st);
   return cuda_ok(s, cudaStreamSynchronize(s->st));
 }
 
 int mps_amplitude(mps_state* s, const uint8_t* bits, void* out) {
   if (!s || !bits || !out) return MPS_EINVAL;
   if (s->sticky) return s->sticky;
+  if (s->has_l || s->has_r) return MPS_EINVAL;  // block states: mps_amplitude_block
   for (int q = 0; q < s->n; ++q)
     if (bits[q] > 1) return MPS_EINVAL;
-  return amplitudes(s, bits, 1, out);
+  return amplitudes(s, bits, 1, nullptr, out);
 }
 
 int mps_to_dense(mps_state* s, void* out) {
   if (!s || !out) return MPS_EINVAL;
   if (s->sticky) return s->sticky;
+  if (s->has_l || s->has_r) return MPS_EINVAL;
   if (s->n > 24) return MPS_ETOOBIG;
   const long long ns = 1LL << s->n;
   std::vector<uint8_t> bits((size_t)ns * s->n);
   for (long long x = 0; x < ns; ++x)
     for (int q = 0; q < s->n; ++q) bits[(size_t)x * s->n + q] = (x >> (s->n - 1 - q)) & 1;
-  return amplitudes(s, bits.data(), ns, out);
+  return amplitudes(s, bits.data(), ns, nullptr, out);
 }
 
 static int transfer(mps_state* s, const void* O, const int* sites, int k, void* out, void* den_out) {
+  if (s->has_l || s->has_r) return MPS_EINVAL;
   const int n = s->n;
   int maxchi = 1;
   for (int b = 0; b + 1 < n; ++b) maxchi = std::max(maxchi, s->m[b]);
@@ -479,6 +521,85 @@ int mps_expect(mps_state* s, const void* O, const int* sites, int k, void* out) 
   for (int i = 0; i < k; ++i)
     if (sites[i] != sites[0] + i || sites[i] < 0 || sites[i] >= s->n) return MPS_EINVAL;
   return transfer(s, O, sites, k, out, nullptr);
+}
+
+// ---------------------------------------------------------------- site-sharded blocks
+int mps_amplitude_block(mps_state* s, const uint8_t* bits, const void* v_in, void* v_out) {
+  if (!s || !bits || !v_out || (s->has_l && !v_in)) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  for (int q = 0; q < s->n; ++q)
+    if (bits[q] > 1) return MPS_EINVAL;
+  return amplitudes(s, bits, 1, s->has_l ? v_in : nullptr, v_out);
+}
+
+int mps_block_dims(mps_state* s, int* lo, int* n, int* m_ext_l, int* m_ext_r) {
+  if (!s) return MPS_EINVAL;
+  if (lo) *lo = s->lo;
+  if (n) *n = s->n;
+  if (m_ext_l) *m_ext_l = s->dl(0);
+  if (m_ext_r) *m_ext_r = s->dr(s->n - 1);
+  return s->sticky;
+}
+
+int mps_block_export_first(mps_state* s, void* dG, void* dlam, int* m_l, int* m_r) {
+  if (!s || !dG || !m_l || !m_r || !s->has_l) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  *m_l = s->dl(0);
+  *m_r = s->dr(0);
+  cudaMemcpyAsync(dG, s->G[0], (size_t)2 * *m_l * *m_r * s->cb, cudaMemcpyDeviceToDevice, s->st);
+  const uint32_t* lr = s->lamR(0);
+  if (dlam && lr) cudaMemcpyAsync(dlam, lr, (size_t)*m_r * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+int mps_block_boundary_apply(mps_state* s, const void* U, const void* dG_halo, int m_h, const void* dlam_h,
+                             void* dG_halo_out, void* dlam_mid_out, int* k_out) {
+  if (!s || !U || !dG_halo || !dG_halo_out || !dlam_mid_out || !k_out || !s->has_r || m_h < 1) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  const int q = s->n - 1, ld = s->cap_er, dl = s->dl(q), dm = s->m_er;
+  const size_t o_U = 0, o_GL = align_up(16 * s->cb), o_GR = o_GL + align_up((size_t)2 * dl * ld * s->cb),
+               o_lam = o_GR + align_up((size_t)2 * ld * m_h * s->cb), o_end = o_lam + align_up((size_t)ld * s->rb);
+  if (!grow((void**)&s->tmp, &s->tmp_sz, o_end + 4096)) return s->sticky = MPS_ENOMEM;
+  uint32_t* dU = (uint32_t*)(s->tmp + o_U);
+  if (int rc = upload_gate(s, U, 4, dU)) return rc;
+  Upd2Args a;
+  std::memset(&a, 0, sizeof(a));
+  a.chiL = dl; a.chiM = dm; a.chiR = m_h; a.chi_max = s->chi_max;
+  a.GL = s->G[q]; a.GR = (const uint32_t*)dG_halo;
+  a.lamL = s->lamL(q); a.lamM = s->lam_er; a.lamR = (const uint32_t*)dlam_h;
+  a.U = dU;
+  a.GL_out = (uint32_t*)(s->tmp + o_GL);
+  a.GR_out = (uint32_t*)(s->tmp + o_GR);
+  a.lam_out = (uint32_t*)(s->tmp + o_lam);
+  a.out_ld = ld;
+  a.k_out = s->dint; a.sweeps_out = s->dint + 1; a.status_out = s->dint + 2;
+  if (!grow(&s->ws, &s->ws_sz, s->ops->upd2_ws(&a, 1))) return s->sticky = MPS_ENOMEM;
+  std::vector<unsigned char> hd;
+  s->ops->upd2(s->p, s->thr, &a, 1, s->ws, s->st, hd);
+  int res[3];
+  cudaMemcpyAsync(res, s->dint, sizeof(res), cudaMemcpyDeviceToHost, s->st);
+  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  s->sweeps_total += res[1];
+  s->last_sweeps = res[1];
+  s->gates++;
+  if (res[2]) return s->sticky = res[2];
+  const int k = res[0];
+  repack_rows(s, s->G[q], a.GL_out, 2 * dl, k, ld);
+  repack_blocks(s, (uint32_t*)dG_halo_out, a.GR_out, k, ld, m_h);
+  cudaMemcpyAsync(s->lam_er, a.lam_out, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  cudaMemcpyAsync(dlam_mid_out, a.lam_out, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  s->m_er = k;
+  *k_out = k;
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
+int mps_block_import_first(mps_state* s, const void* dG0, const void* dlam_mid, int k) {
+  if (!s || !dG0 || !dlam_mid || !s->has_l || k < 1 || k > s->cap_el) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  s->m_el = k;
+  cudaMemcpyAsync(s->G[0], dG0, (size_t)2 * k * s->dr(0) * s->cb, cudaMemcpyDeviceToDevice, s->st);
+  cudaMemcpyAsync(s->lam_el, dlam_mid, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
 }
 
 int mps_schmidt(mps_state* s, int bond, void* out, int* m) {

@@ -19,8 +19,8 @@ struct TierOps {
   void (*onesite)(int p, const uint32_t* G, uint32_t* Gout, const uint32_t* U, int nab, cudaStream_t st);
   size_t (*amp_scratch)(int maxchi, int nblocks);
   void (*amplitudes)(int p, const uint32_t* const* G, const uint32_t* const* lam, const int* dims, int n,
-                     const uint8_t* bits, long long nstates, int maxchi, void* scratch, int nblocks, uint32_t* out,
-                     cudaStream_t st);
+                     const uint8_t* bits, long long nstates, int maxchi, void* scratch, int nblocks,
+                     const uint32_t* v_in, uint32_t* out, cudaStream_t st);
   void (*unitary)(int p, const uint32_t* U, int d, int* bad, cudaStream_t st);
   size_t (*transfer_scratch)(int maxchi);
   int (*transfer)(int p, int n, const uint32_t* const* Gh, const uint32_t* const* lamh, const int* dims,
