@@ -10,6 +10,10 @@
 #pragma once
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+
 #include "common.h"
 #include "mp.cuh"
 
@@ -67,6 +71,8 @@ struct SvdItem {
   int* status;              // out: 0 / MPS_ENOCONV
   int* sweeps;              // out
   long long* rotations;     // out
+  int* sync;                // scratch flag ("some pair rotated in this sweep")
+  mpf<NL>* zbuf;            // scratch: negligible-column floor
 };
 
 // Sort / truncate / renormalise one SVD result and produce the split outputs.
@@ -463,10 +469,10 @@ __global__ void k_fixed_to_records(const int32_t* F, int ld, const int64_t* eCol
 // a3 one-sided Jacobi SVD (one CTA per matrix, round-robin ordering)
 // ----------------------------------------------------------------------------
 template <int L, int NL>
-__device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z, int gw, int GW) {
+  const int lane = threadIdx.x & 31;
   const int W = 28 * L;
-  for (int j = warp; j < it.N; j += NWARP) {
+  for (int j = gw; j < it.N; j += GW) {
     int64_t acc[L + 2];
 #pragma unroll
     for (int c = 0; c < L + 2; ++c) acc[c] = 0;
@@ -561,10 +567,22 @@ __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int l
 // Cp = c 2^(ep-eo_p), Cq = c 2^(eq-eo_q); for V all scales are 1.
 __constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {0, 1, 2}, {1, 0, 3}};
 
+// C CTAs (a thread-block cluster when C > 1) cooperate on one matrix: pairs, columns and
+// rows are distributed over all C*NWARP warps, column state lives in global memory, and
+// the phases are separated by cluster barriers.  The arithmetic of every pair is the same
+// whatever C is, so results are bitwise independent of C.
 template <int L, int NL>
-__global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdItem<NL>* items) {
-  const SvdItem<NL> it = items[blockIdx.x];
+__global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdItem<NL>* items, int C) {
+  namespace cg = cooperative_groups;
+  const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
+  const SvdItem<NL> it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
+  auto csync = [&]() {
+    if (C > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int gw = crank * NWARP + warp, GW = C * NWARP;       // global warp id / count
+  const int gt = crank * NTHR + tid, GT = C * NTHR;          // global thread id / count
   const int M = it.M, N = it.N, NP = N / 2;
   const int W = 28 * L;
   constexpr int CW = L + 1;              // words per coefficient vector
@@ -572,12 +590,11 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   extern __shared__ int32_t jsm[];
   int32_t* wbuf = jsm + warp * (2 * STAGE + 24 * CW);  // per-warp: 2 stage buffers + 24 coefficients
   int32_t* wcoef = wbuf + 2 * STAGE;
-  __shared__ int s_any;
-  __shared__ mpf<NL> s_red[NWARP];
-  __shared__ mpf<NL> s_z;
+  __shared__ mpf<NL> s_red[1];
 
+  if (crank == 0 && tid == 0) *it.rotations = 0;
   // V = I (exponent 1: 1 = 2^27 * 2^(28(L-1)) * 2^(1 - 28L))
-  for (int t = tid; t < N * N; t += NTHR) {
+  for (int t = gt; t < N * N; t += GT) {
     const int r = t % N, c = t / N;
     int32_t x[L], z0[L];
 #pragma unroll
@@ -587,10 +604,10 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     stfx<L>(it.V, N, c, 1, r, z0);
   }
   mpf<NL> z = mpf_zero<NL>();
-  jac_norms<L, NL>(it, false, z);
-  __syncthreads();
-  // ||A||_F^2 and the negligible-column floor z = tol^2 ||A||_F^2
-  if (warp == 0) {
+  jac_norms<L, NL>(it, false, z, gw, GW);
+  csync();
+  // ||A||_F^2 and the negligible-column floor z = tol^2 ||A||_F^2 (CTA rank 0, warp 0)
+  if (crank == 0 && warp == 0) {
     mpf<NL> s = mpf_zero<NL>();
     for (int j = lane; j < N; j += 32) s = mpf_add(s, it.alpha[j]);
     if (lane == 0) s_red[0] = mpf_zero<NL>();
@@ -601,27 +618,27 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     }
     if (lane == 0) {
       mpf<NL> tol2 = mpf_ldexp(mpf_from_int<NL>((int64_t)M * M), 4 - 2 * (int64_t)W);
-      s_z = mpf_mul(tol2, s_red[0]);
+      *it.zbuf = mpf_mul(tol2, s_red[0]);
     }
   }
-  __syncthreads();
-  z = s_z;
-  for (int j = tid; j < N; j += NTHR) {
+  csync();
+  z = *it.zbuf;
+  for (int j = gt; j < N; j += GT) {
     const mpf<NL> a = it.alpha[j];
     it.negl[j] = (mpf_is_zero(a) || mpf_cmp(a, z) <= 0) ? 1 : 0;
   }
-  __syncthreads();
+  csync();
   const mpf<NL> tol2 = mpf_ldexp(mpf_from_int<NL>((int64_t)M * M), 4 - 2 * (int64_t)W);  // tol = 4 M 2^-W
   const int nchA = (M + 31) / 32, nchV = (N + 31) / 32;
 
   int sweep = 0, conv = 0;
   long long nrot = 0;
   for (sweep = 1; sweep <= MAX_SWEEPS; ++sweep) {
-    if (tid == 0) s_any = 0;
-    __syncthreads();
+    if (crank == 0 && tid == 0) *(volatile int*)it.sync = 0;
+    csync();
     for (int step = 0; step < N - 1; ++step) {
       // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows, cp.async staging)
-      for (int i = warp; i < NP; i += NWARP) {
+      for (int i = gw; i < NP; i += GW) {
         int p, q;
         rr_pair(N, step, i, p, q);
         if (it.negl[p] || it.negl[q]) continue;
@@ -667,9 +684,9 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
           it.gam[2 * i + 1] = mpf_from_cols<NL, L + 2>(gi, E0);
         }
       }
-      __syncthreads();
+      csync();
       // ---- phase R: rotation parameters (thread per pair)
-      for (int i = tid; i < NP; i += NTHR) {
+      for (int i = gt; i < NP; i += GT) {
         int p, q;
         rr_pair(N, step, i, p, q);
         int flag = 0;
@@ -729,16 +746,16 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             if (mpf_is_zero(ap) || ap.neg || mpf_cmp(ap, z) <= 0) it.negl[p] = 1;
             if (mpf_is_zero(aq) || aq.neg || mpf_cmp(aq, z) <= 0) it.negl[q] = 1;
             flag = 1 | (ints << 8);
-            s_any = 1;
+            *(volatile int*)it.sync = 1;
             ++nrot;
             if (it.dbg) atomicAdd(&it.dbg[sweep < 63 ? sweep : 63], 1);
           }
         }
         it.rot[i] = flag;
       }
-      __syncthreads();
+      csync();
       // ---- phase U: apply the rotations to columns p, q of A and V
-      for (int i = warp; i < NP; i += NWARP) {
+      for (int i = gw; i < NP; i += GW) {
         const int flag = it.rot[i];
         if (!(flag & 1)) continue;
         int p, q;
@@ -788,29 +805,27 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
           }
         }
       }
-      __syncthreads();
+      csync();
     }
     // refresh exact column norms (and renormalise columns) for the next sweep / the result
-    const bool any = s_any != 0;
-    jac_norms<L, NL>(it, false, z);
-    __syncthreads();
+    const bool any = *(volatile int*)it.sync != 0;
+    jac_norms<L, NL>(it, false, z, gw, GW);
+    csync();
     if (!any) { conv = 1; break; }
   }
-  // block-reduce the rotation count
-  __shared__ long long s_rot;
-  if (tid == 0) s_rot = 0;
-  __syncthreads();
-  atomicAdd((unsigned long long*)&s_rot, (unsigned long long)nrot);
-  __syncthreads();
-  if (tid == 0) {
+  atomicAdd((unsigned long long*)it.rotations, (unsigned long long)nrot);
+  if (crank == 0 && tid == 0) {
     *it.sweeps = conv ? sweep : MAX_SWEEPS + 1;
     *it.status = conv ? 0 : -3;
-    *it.rotations = s_rot;
   }
 }
 
 template <int L>
 constexpr size_t jacobi_smem_bytes() { return (size_t)NWARP * (2 * 4 * L * 32 + 24 * (L + 1)) * 4; }
+
+// Launch n items with C CTAs each (a cluster of C when C > 1).
+template <int L, int NL>
+inline void launch_jacobi(const SvdItem<NL>* d_items, int n, int C, cudaStream_t st);
 
 // opt in to > 48 KB of dynamic shared memory (once per instantiation)
 template <int L, int NL>
@@ -820,6 +835,44 @@ inline void jacobi_prepare() {
     cudaFuncSetAttribute(k_jacobi<L, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jacobi_smem_bytes<L>());
     done = true;
   }
+}
+
+template <int L, int NL>
+inline void launch_jacobi(const SvdItem<NL>* d_items, int n, int C, cudaStream_t st) {
+  jacobi_prepare<L, NL>();
+  if (C <= 1) {
+    k_jacobi<L, NL><<<n, NTHR, jacobi_smem_bytes<L>(), st>>>(d_items, 1);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n * C, 1, 1);
+  cfg.blockDim = dim3(NTHR, 1, 1);
+  cfg.dynamicSmemBytes = jacobi_smem_bytes<L>();
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_jacobi<L, NL>, d_items, C);
+}
+
+// CTAs per matrix: fill ~2 CTAs per SM when few matrices are in flight, at least one pair
+// per warp, power of two, at most 8 (portable cluster size).
+// MPS_JACOBI_MAX_CLUSTER (env, default 8) caps C; tests use it to compare C = 1 and C > 1.
+inline int jacobi_cluster_size(int n_items, int min_N) {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("MPS_JACOBI_MAX_CLUSTER");
+    cap = e ? atoi(e) : 8;
+    if (cap < 1) cap = 1;
+    if (cap > 8) cap = 8;
+  }
+  int C = 1;
+  while (C < cap && n_items * C * 2 <= 2 * 148 && (C * 2) * NWARP <= min_N / 2) C *= 2;
+  return C;
 }
 
 // ----------------------------------------------------------------------------

@@ -91,7 +91,7 @@ size_t svd_workspace(int M, int N, int batch) {
   const int Nj = Nj0 + (Nj0 & 1);
   size_t per = align_up((size_t)Mj * Nj * 2 * L * 4) + align_up((size_t)Nj * Nj * 2 * L * 4) +
                align_up(8 * (size_t)Nj + 64) + align_up(sizeof(mpf<NL>) * (size_t)Nj * 4) +
-               align_up(4 * (size_t)Nj / 2 * 24 * (L + 1)) + align_up(4 * (size_t)Nj * 3 + 64);
+               align_up(4 * (size_t)Nj / 2 * 24 * (L + 1)) + align_up(4 * (size_t)Nj * 3 + 64) + 512;
   return align_up(sizeof(MatItem) * batch) + align_up(sizeof(SvdItem<NL>) * batch) +
          align_up(sizeof(FinItem<NL>) * batch) + (size_t)batch * per + 4096;
 }
@@ -133,11 +133,14 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     int* rot = (int*)((char*)coef + align_up(4 * (size_t)Nj / 2 * 24 * (L + 1)));
     int* negl = rot + Nj / 2;
     int* ord = negl + Nj;
+    int* syncp = (int*)align_up((size_t)(ord + Nj) + 64, 16);
+    mpf<NL>* zbuf = (mpf<NL>*)(syncp + 16);
     hm[b] = MatItem{dR + (size_t)b * M * N * 2 * RBr, M, N, trans ? 1 : 0, A, eA, eblk};
     SvdItem<NL> si;
     si.M = Mj; si.N = Nj; si.A = A; si.eA = eA; si.V = V; si.alpha = alpha; si.gam = gam; si.coef = coef;
     si.dbg = ddbg ? ddbg + 64 * b : nullptr;
     si.rot = rot; si.negl = negl; si.status = ip; si.sweeps = dsweeps + b; si.rotations = rots;
+    si.sync = syncp; si.zbuf = zbuf;
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -156,8 +159,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
   dim3 g(std::max(1, std::min(64, (M * N + 255) / 256)), batch);
   k_mat_exp<<<g, 256, 0, st>>>((const MatItem*)(base + d_mat), RBr); ++nl;
   k_mat_conv<L, NL><<<g, 256, 0, st>>>((const MatItem*)(base + d_mat), RBr); ++nl;
-  jacobi_prepare<L, NL>();
-  k_jacobi<L, NL><<<batch, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), batch, jacobi_cluster_size(batch, Nj), st); ++nl;
   // the sigma records of the padded zero column are not part of the output
   k_finalize<L, NL><<<batch, NTHR, sizeof(mpf<NL>) * (size_t)Nj, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p);
   ++nl;

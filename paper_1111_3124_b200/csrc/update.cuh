@@ -36,9 +36,11 @@ struct SvdScratch {
   int64_t* eA; mpf<NL>* alpha; mpf<NL>* gam; mpf<NL>* inv_sig; mpf<NL>* lam; int32_t* coef;
   int* rot; int* negl; int* ord; int* status; int* sweeps; int* fstatus; int* k; long long* rots;
   int64_t* e_misc;  // 4 spare exponents
+  int* sync;
+  mpf<NL>* zbuf;
   static size_t bytes(int N) {
     return align_up(8 * (size_t)N + 64) + align_up(sizeof(mpf<NL>) * (size_t)N * 4) +
-           align_up(4 * (size_t)N / 2 * 24 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256;
+           align_up(4 * (size_t)N / 2 * 24 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256 + 256;
   }
   static SvdScratch carve(char* p, int N) {
     SvdScratch s;
@@ -61,6 +63,8 @@ struct SvdScratch {
     s.k = s.status + 3;
     s.rots = (long long*)(q + 16);
     s.e_misc = (int64_t*)(q + 32);
+    s.sync = (int*)(q + 64);
+    s.zbuf = (mpf<NL>*)(q + 128);
     return s;
   }
 };
@@ -146,6 +150,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
+    si.sync = S.sync; si.zbuf = S.zbuf;
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -184,8 +189,12 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     return nl;
   }
   prof_mark(PROF_JACOBI, 1, st);
-  jacobi_prepare<L, NL>();
-  k_jacobi<L, NL><<<n, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  {
+    int minN = 1 << 30;
+    for (int b = 0; b < n; ++b) minN = std::min(minN, hs[b].N);
+    launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n, minN), st);
+    ++nl;
+  }
   prof_mark(PROF_JACOBI, 0, st);
   prof_mark(PROF_FINALIZE, 1, st);
   int maxN = 0;
@@ -284,7 +293,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   SvdItem<NL> si;
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
   si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
-  si.sweeps = S1.sweeps; si.rotations = S1.rots;
+  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   FinItem<NL> fi;
@@ -311,8 +320,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   dim3 g2(std::max(1, std::min(128, (8 * a.chiL * a.chiR + 127) / 128)), 1);
   k_gemm<L><<<g2, 128, 0, st>>>((const GemmItem*)(base + d_gemm) + 1); ++nl;
   k_mix<L, NL><<<g2, 128, 64 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
-  jacobi_prepare<L, NL>();
-  k_jacobi<L, NL><<<1, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd)); ++nl;
+  launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), 1, jacobi_cluster_size(1, N1), st); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N1, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * a.chiR * N1 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
@@ -365,7 +373,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   SvdItem<NL> si;
   si.M = M2; si.N = N2; si.A = A2; si.eA = S2.eA; si.V = V2; si.alpha = S2.alpha; si.gam = S2.gam;
   si.coef = S2.coef; si.dbg = nullptr; si.rot = S2.rot; si.negl = S2.negl; si.status = S2.status;
-  si.sweeps = S2.sweeps; si.rotations = S2.rots;
+  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
   FinItem<NL> fi;
@@ -383,8 +391,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   k_m2_exp<L, NL><<<1, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
   dim3 gb(std::max(1, std::min(64, (rows2 * cols2 + 255) / 256)), 1);
   k_build_m2<L, NL><<<gb, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
-  jacobi_prepare<L, NL>();
-  k_jacobi<L, NL><<<1, NTHR, jacobi_smem_bytes<L>(), st>>>((const SvdItem<NL>*)(base + d_svd2)); ++nl;
+  launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd2), 1, jacobi_cluster_size(1, N2), st); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N2, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * std::max(a.chiL, k1) * N2 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
