@@ -503,7 +503,7 @@ __device__ void jac_norms(const SvdItem<NL>& it, bool set_negl, const mpf<NL>& z
         }
       }
       it.alpha[j] = a;
-      if (set_negl) it.negl[j] = (mpf_is_zero(a) || mpf_cmp(a, z) <= 0) ? 1 : 0;
+      if (set_negl && (mpf_is_zero(a) || mpf_cmp(a, z) <= 0)) it.negl[j] = 1;
     }
     shift = __shfl_sync(0xffffffffu, shift, 0);
     if (shift) {
@@ -710,18 +710,26 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             aq = mpf_add(aq, tg);
             const int64_t ep = it.eA[p], eq = it.eA[q];
             const int64_t eb = (ep > eq ? ep : eq) + 1;  // bound of every term's exponent
-            // tight output exponents from the predicted norms (slack for rounding), at most
-            // 27 bits below eb so that every scaled coefficient stays < 2^27 (one integer digit)
+            // Output exponents: tight from the predicted norms (slack for rounding), but no
+            // lower than (largest term exponent) - 26 so that every scaled coefficient
+            // |coef| 2^(e_in - e_out) stays < 2^26 (one integer digit).  A term's exponent is
+            // e_in + e(coef) with |coef| < 2^e(coef); only genuine cancellation (output much
+            // smaller than its terms) leaves a column under-normalised, as in floating point.
+            const int64_t ec = mpf_is_zero(c) ? INT64_MIN / 4 : c.e;
+            const int64_t es = (mpf_is_zero(sr) && mpf_is_zero(si)) ? INT64_MIN / 4
+                               : (mpf_is_zero(sr) ? si.e : (mpf_is_zero(si) ? sr.e : (sr.e > si.e ? sr.e : si.e)));
+            const int64_t tmax[2] = {(ep + ec > eq + es ? ep + ec : eq + es) + 1,
+                                     (ep + es > eq + ec ? ep + es : eq + ec) + 1};
             int64_t eo[2];
             const mpf<NL>* an[2] = {&ap, &aq};
             for (int u = 0; u < 2; ++u) {
               const mpf<NL>& a = *an[u];
-              int64_t enew = eb - W + 14;
+              int64_t enew = tmax[u] - W + 14;
               if (!mpf_is_zero(a) && !a.neg) {
                 int64_t e1 = (int64_t)ceil(0.5 * mpf_log2(a) + 1e-9) + 1;
                 if (e1 > enew) enew = e1;
               }
-              if (enew < eb - 27) enew = eb - 27;
+              if (enew < tmax[u] - 26) enew = tmax[u] - 26;
               if (enew > eb) enew = eb;
               eo[u] = enew;
             }
@@ -809,7 +817,8 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     }
     // refresh exact column norms (and renormalise columns) for the next sweep / the result
     const bool any = *(volatile int*)it.sync != 0;
-    jac_norms<L, NL>(it, false, z, gw, GW);
+    // exact norms; the negligible-column rule (R3b) is re-evaluated on them
+    jac_norms<L, NL>(it, true, z, gw, GW);
     csync();
     if (!any) { conv = 1; break; }
   }

@@ -490,6 +490,24 @@ __device__ __noinline__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t 
   return mpf_pack<NL>(t, E_of_col0 + 32 * (int64_t)(top - NL) + 32 * (int64_t)(NL + 1), neg);
 }
 
+// 28 bits of the NL-limb magnitude m starting at bit position b0 (bits outside
+// [0, 32 NL) read as zero; b0 may be negative)
+template <int NL>
+__device__ __forceinline__ uint32_t mpf_bits28(const uint32_t (&m)[NL], int64_t b0) {
+  uint32_t v = 0;
+  if (b0 >= 32 * NL || b0 <= -28) return 0;
+  if (b0 < 0) {
+    // bits [0, b0 + 28) of m land at positions [-b0, 28)
+    const uint32_t lo = m[0];
+    v = (lo << (int)(-b0)) & 0x0FFFFFFFu;
+    return v;
+  }
+  const int q = (int)(b0 >> 5), r = (int)(b0 & 31);
+  uint64_t lo = m[q];
+  uint64_t hi = (q + 1 < NL) ? m[q + 1] : 0;
+  return (uint32_t)((((hi << 32) | lo) >> r) & 0x0FFFFFFFu);
+}
+
 // mpf -> L fixed digits at column exponent E (value = sum d_k 2^(28k) 2^(E - 28L)),
 // rounded to nearest; requires |a| < 2^E (else the top digit is simply large).
 template <int NL, int L>
@@ -497,34 +515,19 @@ __device__ __noinline__ void mpf_to_fixed(const mpf<NL>& a, int64_t E, int32_t (
 #pragma unroll
   for (int k = 0; k < L; ++k) d[k] = 0;
   if (mpf_is_zero(a)) return;
-  // integer X = round(m * 2^(a.e - 32NL - E + 28L)); shift s = a.e - 32NL - E + 28L (usually < 0)
-  int64_t s = a.e - 32 * (int64_t)NL - E + 28 * (int64_t)L;
-  // Build digits: bit position b of X (b >= 0) comes from bit (b - s) of m.
-  // round: add half of the lowest kept unit
-  // Extract 28-bit chunks of m >> (-s) (s <= 0) with rounding.
-  if (s > 0) {  // value larger than representable (should not happen): saturate via top digit
-    s = 0;
-  }
-  int64_t sh = -s;  // right shift of m
+  // integer X = round(m * 2^s), s = a.e - 32NL - E + 28L; digit k = bits [28k - s, 28k - s + 28) of m
+  const int64_t s = a.e - 32 * (int64_t)NL - E + 28 * (int64_t)L;
+  const int64_t sh = -s;  // bit of m that becomes bit 0 of X (negative: X = m shifted left)
   if (sh >= 32 * NL + 1) return;  // rounds to zero
-  // rounding bit
-  int64_t rb = sh - 1;
-  uint32_t rbit = 0;
-  if (rb >= 0 && rb < 32 * NL) rbit = (a.m[rb >> 5] >> (rb & 31)) & 1u;
-  uint32_t carry = rbit;
+  uint32_t carry = 0;
+  if (sh >= 1) {  // round to nearest on bit sh-1
+    const int64_t rb = sh - 1;
+    if (rb < 32 * NL) carry = (a.m[rb >> 5] >> (rb & 31)) & 1u;
+  }
 #pragma unroll
   for (int k = 0; k < L; ++k) {
-    // 28 bits starting at bit (sh + 28k) of m
-    int64_t b0 = sh + 28 * (int64_t)k;
-    uint32_t v = 0;
-    if (b0 < 32 * NL) {
-      int q = (int)(b0 >> 5), r = (int)(b0 & 31);
-      uint64_t lo = a.m[q];
-      uint64_t hi = (q + 1 < NL) ? a.m[q + 1] : 0;
-      uint64_t both = lo | (hi << 32);
-      v = (uint32_t)((both >> r) & 0x0FFFFFFFu);
-    }
-    uint32_t sum = v + carry;
+    const uint32_t v = mpf_bits28<NL>(a.m, sh + 28 * (int64_t)k);
+    const uint32_t sum = v + carry;
     carry = sum >> 28;
     d[k] = (int32_t)(sum & 0x0FFFFFFFu);
   }

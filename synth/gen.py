@@ -153,8 +153,12 @@ def triples(n: int, depth: int, p: int, seed: int):
     return gates
 
 
-def config_circuit(idx: int, p: int | None = None, depth: int | None = None):
-    """(n, p, chi_max, thr, gates) for BASELINE.json configs[idx] (idx in 0, 2, 3, 4)."""
+def config_circuit(idx: int, p: int | None = None, depth: int | None = None, chi_max: int | None = None):
+    """(n, p, chi_max, thr, gates) for BASELINE.json configs[idx] (idx in 0, 2, 3, 4);
+    depth / chi_max override the config's (scaled-down parity runs)."""
+    if chi_max is not None:
+        n, p_, chi, thr, gates = config_circuit(idx, p, depth)
+        return n, p_, chi_max, thr, gates
     seed = SEED0 + idx
     if idx == 0:
         p = p or 280

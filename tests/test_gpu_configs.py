@@ -43,7 +43,7 @@ def layers_of(gates):
 def test_config_vs_cached_oracle(path):
     import paper_1111_3124_b200 as m
     g = json.load(open(path))
-    n, p, chi, thr, gates = gen.config_circuit(g["config"], depth=g["depth"])
+    n, p, chi, thr, gates = gen.config_circuit(g["config"], depth=g["depth"], chi_max=g.get("chi_override"))
     assert len(gates) == g["gates"]
     st = m.MPS(n, p, chi, thr)
     for layer in layers_of(gates):

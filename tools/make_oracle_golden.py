@@ -50,9 +50,10 @@ def main():
     ap.add_argument("--config", type=int, required=True)
     ap.add_argument("--depth", type=int, default=None)
     ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--chi", type=int, default=None, help="override chi_max (scaled-down run)")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    n, p, chi, thr, gates = gen.config_circuit(a.config, depth=a.depth)
+    n, p, chi, thr, gates = gen.config_circuit(a.config, depth=a.depth, chi_max=a.chi)
     t0 = time.time()
     m = oracle.OracleMPS(n, p, chi, thr)
     ls = layers_of(gates)
@@ -64,7 +65,7 @@ def main():
     bits = sample_bits(n, gen.SEED0 + a.config)
     res = {
         "config": a.config, "n": n, "prec": p, "chi_max": chi, "thr": thr,
-        "depth": a.depth, "gates": len(gates), "layers": len(ls),
+        "depth": a.depth, "chi_override": a.chi, "gates": len(gates), "layers": len(ls),
         "bond_dims": m.bond_dims(),
         "schmidt": [hexrec(m.schmidt(b)) for b in range(n - 1)],
         "bits": bits,
@@ -74,7 +75,7 @@ def main():
         "seconds": secs, "threads": a.threads, "cpu": platform.processor() or platform.machine(),
         "generator": "tools/make_oracle_golden.py (oracle/ only)",
     }
-    out = a.out or os.path.join(ROOT, "tests", "golden", f"cfg{a.config}_oracle{'' if a.depth is None else f'_d{a.depth}'}.json")
+    out = a.out or os.path.join(ROOT, "tests", "golden", f"cfg{a.config}_oracle{'' if a.depth is None else f'_d{a.depth}'}{'' if a.chi is None else f'_chi{a.chi}'}.json")
     json.dump(res, open(out, "w"))
     print("wrote", out, f"{secs:.0f}s")
 
