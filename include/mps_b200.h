@@ -96,6 +96,11 @@ int mps_apply_layer(mps_state* st, int n_gates, const void* const* U, const int*
 int mps_amplitude(mps_state* st, const uint8_t* bits, void* out);
 /* <Psi|O|Psi> / <Psi|Psi> for O on contiguous ascending sites (k = 1..3). out: 1 complex. */
 int mps_expect(mps_state* st, const void* O, const int* sites, int k, void* out);
+/* Reduced density operator of k ascending sites (k <= 6), the paper's RDO_block(a,b) /
+ * RDO(list): rho(x, x') = sum_rest psi(x, rest) conj(psi(x', rest)) / trace,
+ * computed by transfer contraction (no 2^n state).  out: 2^k x 2^k complex, row-major,
+ * x = first listed site most significant (the |000> labels of P:351). */
+int mps_rdo(mps_state* st, const int* sites, int k, void* out);
 /* <Psi|Psi> of the stored tensors. out: 1 real. */
 int mps_norm2(mps_state* st, void* out);
 /* All 2^n amplitudes, qubit 0 = MSB (n <= 24). out: 2^n complex. */

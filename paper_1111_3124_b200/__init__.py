@@ -20,7 +20,8 @@ STATUS = {0: "MPS_OK", -1: "MPS_EINVAL", -2: "MPS_ENOTUNITARY", -3: "MPS_ENOCONV
           -10: "MPS_ETOOBIG"}
 
 # every symbol include/mps_b200.h declares
-EXPORTS = ["mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
+EXPORTS = ["mps_rdo", "mps_init_block", "mps_block_dims", "mps_block_export_first", "mps_block_boundary_apply",
+           "mps_block_import_first", "mps_amplitude_block", "mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
            "mps_apply_gate", "mps_apply_layer", "mps_amplitude", "mps_expect", "mps_norm2", "mps_to_dense",
            "mps_sync", "mps_n_qubits", "mps_bond_dims", "mps_schmidt", "mps_get_site", "mps_set_schmidt",
            "mps_set_site", "mps_stats", "mps_bench_update_batch", "mps_update_batch_workspace",
@@ -214,6 +215,15 @@ class MPS:
     def to_dense(self):
         out = _empty(self.p, 2 << self.n)
         _chk(lib().mps_to_dense(self.h, _p(out)), "mps_to_dense")
+        return out
+
+    def rdo(self, sites):
+        """Reduced density operator, 2^k x 2^k complex records, row-major."""
+        k = len(sites)
+        s = (ctypes.c_int * k)(*sites)
+        out = _empty(self.p, 2 << (2 * k))
+        lib().mps_rdo.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+        _chk(lib().mps_rdo(self.h, s, k, _p(out)), "mps_rdo")
         return out
 
     def norm2(self):

@@ -130,6 +130,22 @@ __global__ void k_caxpy_rec(const uint32_t* s, const cmpf<NL>* X, cmpf<NL>* Y, i
   }
 }
 
+// rho(a, b) = E_(b,a) / sum_x E_(x,x) ; E_j are 1x1 at stride X
+template <int NL>
+__global__ void k_rdo_out(const cmpf<NL>* E, int X, int D, uint32_t* out, int RBr, int p) {
+  __shared__ mpf<NL> s_inv;
+  if (threadIdx.x == 0) {
+    mpf<NL> tr = mpf_zero<NL>();
+    for (int x = 0; x < D; ++x) tr = mpf_add(tr, E[(size_t)(x * D + x) * X].re);
+    s_inv = mpf_recip(tr);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < D * D; t += blockDim.x) {
+    const int a = t / D, b = t % D;
+    cm_to_rec<NL>(cm_scale(s_inv, E[(size_t)(b * D + a) * X]), out + (size_t)(2 * t) * RBr, RBr, p);
+  }
+}
+
 template <int NL>
 __global__ void k_set_one(cmpf<NL>* E) {
   E[0] = {mpf_from_int<NL>(1), mpf_zero<NL>()};
@@ -269,6 +285,67 @@ int run_transfer(int p, int n, const uint32_t* const* Gh, const uint32_t* const*
     num = Ec;
   }
   k_ratio<NL><<<1, 1, 0, st>>>(num, tmp, out, den_out, RBr, p); ++nl;
+  return nl;
+}
+
+}  // namespace mpsb
+
+namespace mpsb {
+
+// Reduced density operator of the kept sites (ascending, k <= 6) by transfer contraction
+// (P:322-341 RDO_block / RDO): environments E_{(x,x')}(b,b') = sum conj(A_x(b)) A_{x'}(b')
+// over the open kept multi-indices; traced sites apply sum_i T_i^H E T_i, kept sites split
+// every environment into its 4 children conj(T_i)^T E T_i'.  rho(a,b) = E_{(b,a)} / trace.
+template <class T>
+int run_rdo(int p, int n, const uint32_t* const* Gh, const uint32_t* const* lamh, const int* dims,
+            const int* keep, int k, void* scratch, int maxchi, uint32_t* out, cudaStream_t st) {
+  constexpr int NL = T::NL;
+  using C = cmpf<NL>;
+  const int RBr = record_words(p);
+  const size_t X = (size_t)maxchi * maxchi;
+  const int D = 1 << k, NE = D * D;   // final number of environments
+  C* base = (C*)scratch;
+  C* Ea = base;                 // NE environments (ping)
+  C* Eb = base + NE * X;        // NE environments (pong)
+  C* Tm = base + 2 * NE * X;    // [2][dl][dr]
+  C* F = Tm + 2 * X;            // work
+  int nl = 0;
+  auto blocks = [](size_t m) { return (int)std::max<size_t>(1, std::min<size_t>(1184, (m + 127) / 128)); };
+  auto gemm = [&](const C* A, int lda, int conjT, const C* B, int ldb, C* Cc, int ldc, int rows, int cols, int K,
+                  int acc) {
+    k_cgemm_mpf<NL><<<blocks((size_t)rows * cols), 128, 0, st>>>(A, lda, conjT, B, ldb, Cc, ldc, rows, cols, K, acc);
+    ++nl;
+  };
+  k_set_one<NL><<<1, 1, 0, st>>>(Ea); ++nl;
+  int ne = 1, kk = 0;  // current number of environments, kept sites so far
+  for (int s = 0; s < n; ++s) {
+    const int dl = dims[s], dr = dims[s + 1];
+    k_tmat<NL><<<blocks(2 * (size_t)dl * dr), 128, 0, st>>>(Gh[s], s ? lamh[s - 1] : nullptr, dl, dr, Tm, RBr); ++nl;
+    const bool kept = kk < k && keep[kk] == s;
+    if (!kept) {
+      for (int e = 0; e < ne; ++e) {
+        for (int i = 0; i < 2; ++i) gemm(Ea + e * X, dl, 0, Tm + (size_t)i * dl * dr, dr, F + (size_t)i * X, dr, dl, dr, dl, 0);
+        for (int i = 0; i < 2; ++i) gemm(Tm + (size_t)i * dl * dr, dr, 1, F + (size_t)i * X, dr, Eb + e * X, dr, dr, dr, dl, i);
+      }
+    } else {
+      // child (x i, x' i') of environment (x, x'): index ((x*2+i)*(2D') + (x'*2+i')) with D' = 2^(kk+1)
+      const int Dold = 1 << kk, Dnew = Dold * 2;
+      for (int x = 0; x < Dold; ++x)
+        for (int xp = 0; xp < Dold; ++xp) {
+          const C* E = Ea + (x * Dold + xp) * X;
+          for (int ip = 0; ip < 2; ++ip) gemm(E, dl, 0, Tm + (size_t)ip * dl * dr, dr, F + (size_t)ip * X, dr, dl, dr, dl, 0);
+          for (int i = 0; i < 2; ++i)
+            for (int ip = 0; ip < 2; ++ip)
+              gemm(Tm + (size_t)i * dl * dr, dr, 1, F + (size_t)ip * X, dr,
+                   Eb + ((x * 2 + i) * Dnew + (xp * 2 + ip)) * X, dr, dr, dr, dl, 0);
+        }
+      ne = Dnew * Dnew;
+      ++kk;
+    }
+    C* t = Ea; Ea = Eb; Eb = t;
+  }
+  // trace and output rho(a, b) = E_(b,a) / trace
+  k_rdo_out<NL><<<1, 64, 0, st>>>(Ea, (int)X, D, out, RBr, p); ++nl;
   return nl;
 }
 

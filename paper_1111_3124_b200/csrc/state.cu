@@ -509,6 +509,34 @@ static int transfer(mps_state* s, const void* O, const int* sites, int k, void* 
   return cuda_ok(s, cudaStreamSynchronize(s->st));
 }
 
+// Reduced density operator of ascending sites (P:322-341 RDO_block / RDO), normalised by its trace.
+int mps_rdo(mps_state* s, const int* sites, int k, void* out) {
+  if (!s || !sites || !out || k < 1 || k > 6) return MPS_EINVAL;
+  if (s->sticky) return s->sticky;
+  if (s->has_l || s->has_r) return MPS_EINVAL;
+  for (int i = 0; i < k; ++i)
+    if (sites[i] < 0 || sites[i] >= s->n || (i && sites[i] <= sites[i - 1])) return MPS_EINVAL;
+  const int n = s->n, D = 1 << k;
+  int maxchi = 1;
+  for (int b = 0; b + 1 < n; ++b) maxchi = std::max(maxchi, s->m[b]);
+  std::vector<int> dims(n + 1);
+  dims[0] = 1;
+  for (int q = 1; q < n; ++q) dims[q] = s->m[q - 1];
+  dims[n] = 1;
+  const size_t X = (size_t)maxchi * maxchi;
+  const size_t cm = s->ops->transfer_scratch(1) / 24;  // sizeof(cmpf) (scratch of 24 1x1 matrices, minus slack)
+  (void)cm;
+  const size_t scr = s->ops->transfer_scratch(maxchi) / 24 * (2 * (size_t)D * D + 6) + 4096;
+  const size_t o_res = 0, o_scr = align_up((size_t)D * D * s->cb), o_end = o_scr + scr;
+  if (!grow((void**)&s->tmp, &s->tmp_sz, o_end)) return MPS_ENOMEM;
+  std::vector<const uint32_t*> G(s->G.begin(), s->G.end()), lam(s->lam.begin(), s->lam.end());
+  s->ops->rdo(s->p, n, G.data(), lam.data(), dims.data(), sites, k, s->tmp + o_scr, maxchi,
+              (uint32_t*)(s->tmp + o_res), s->st);
+  cudaMemcpyAsync(out, s->tmp + o_res, (size_t)D * D * s->cb, cudaMemcpyDeviceToHost, s->st);
+  (void)X;
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
 int mps_norm2(mps_state* s, void* out) {
   if (!s || !out) return MPS_EINVAL;
   if (s->sticky) return s->sticky;

@@ -20,6 +20,6 @@ const TierOps tier512_ops = {
     &upd2_workspace<Tier512>, &launch_update2<Tier512>,
     &upd3_workspace<Tier512>, &launch_update3_stage1<Tier512>, &launch_update3_stage2<Tier512>,
     &run_onesite<Tier512>, &amp_scratch_bytes<Tier512>, &run_amplitudes<Tier512>, &run_unitary<Tier512>,
-    &transfer_scratch_bytes<Tier512>, &run_transfer<Tier512>,
+    &transfer_scratch_bytes<Tier512>, &run_rdo<Tier512>, &run_transfer<Tier512>,
 };
 }  // namespace mpsb

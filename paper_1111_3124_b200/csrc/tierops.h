@@ -23,6 +23,8 @@ struct TierOps {
                      const uint32_t* v_in, uint32_t* out, cudaStream_t st);
   void (*unitary)(int p, const uint32_t* U, int d, int* bad, cudaStream_t st);
   size_t (*transfer_scratch)(int maxchi);
+  int (*rdo)(int p, int n, const uint32_t* const* Gh, const uint32_t* const* lamh, const int* dims, const int* keep,
+             int k, void* scratch, int maxchi, uint32_t* out, cudaStream_t st);
   int (*transfer)(int p, int n, const uint32_t* const* Gh, const uint32_t* const* lamh, const int* dims,
                   const uint32_t* O, int s0, int k, void* scratch, int maxchi, uint32_t* out, uint32_t* den_out,
                   cudaStream_t st);

@@ -70,8 +70,13 @@ def fmt(x, digits):
     return f"{mant}e{'+' if e >= 0 else '-'}{abs(e):02d}"
 
 
-def partial_trace_dense(psi, n: int, keep):
-    """rho_keep = Tr_{others} |psi><psi| for a dense state (qubit 0 = MSB)."""
+def partial_trace_dense(psi, n: int, keep, prec: int = 1200):
+    """rho_keep = Tr_{others} |psi><psi| for a dense state (qubit 0 = MSB), at `prec` bits."""
+    with mpmath.workprec(prec):
+        return _ptrace(psi, n, keep)
+
+
+def _ptrace(psi, n, keep):
     keep = list(keep)
     k = len(keep)
     others = [q for q in range(n) if q not in keep]

@@ -211,3 +211,37 @@ def test_error_contract():
         m.MPS(0, p, 4)
     # the failed calls had no side effects
     assert st.bond_dims() == [1, 1, 1]
+
+
+def rho_of(rec, k):
+    v = cplx(rec)
+    D = 1 << k
+    return [[v[r * D + c] for c in range(D)] for r in range(D)]
+
+
+def test_paper_golden_via_gpu_rdo():
+    """§3.2 end to end on the GPU path: RDO_block(0,2) of |000>, then RDO({0,2}) after
+    H(0), CNOT(0,2), printed at 8 digits."""
+    p = 256
+    st = M().MPS(3, p, 8, 2.0 ** -128)
+    assert showb(rho_of(st.rdo([0, 1, 2]), 3), 3) == GOLDEN[0]
+    st.apply(gen.const_gate(p, "H"), [0])
+    st.apply(gen.const_gate(p, "CNOT"), [0, 2])
+    assert showb(rho_of(st.rdo([0, 2]), 2), 2) == GOLDEN[1]
+
+
+def test_rdo_vs_dense_partial_trace():
+    p = 280
+    n = 7
+    gates = gen.brickwall(n, 4, p, 96, one_site_layer=True)
+    st = M().MPS(n, p, 16, 2.0 ** -140)
+    for U, s in gates:
+        st.apply(U, s)
+    psi = dense_of(gates, n, p)
+    for keep in ([2], [0, 6], [1, 3, 4], [0, 1, 2, 3]):
+        got = rho_of(st.rdo(keep), len(keep))
+        want = partial_trace_dense(psi, n, keep)
+        with mpmath.workprec(2 * p):
+            tr = mpmath.fsum(want[i][i] for i in range(1 << len(keep)))
+            err = max(abs(got[r][c] - want[r][c] / tr) for r in range(1 << len(keep)) for c in range(1 << len(keep)))
+        assert err <= tau(p), (keep, err)
