@@ -64,7 +64,7 @@ struct SvdItem {
   int32_t* V;               // [N][2][L][N], exponent fixed = 1
   mpf<NL>* alpha;           // [N] squared column norms (output: final)
   mpf<NL>* gam;             // [N/2][2] scratch
-  int32_t* coef;            // [N/2][9][L+1] scratch (L fractional digits + one integer digit)
+  int32_t* coef;            // [N/2][33][L+1] scratch: 24 signed coefficient slots + 9 values (L+1 digits)
   int* dbg;                 // [64] rotations per sweep, or null
   int* rot;                 // [N/2] scratch
   int* negl;                // [N] scratch
@@ -73,6 +73,7 @@ struct SvdItem {
   long long* rotations;     // out
   int* sync;                // scratch flag ("some pair rotated in this sweep")
   mpf<NL>* zbuf;            // scratch: negligible-column floor
+  unsigned long long* phase_cycles;  // null, or [6]: D, R, U, norms, init, total (summed over CTAs)
 };
 
 // Sort / truncate / renormalise one SVD result and produce the split outputs.
@@ -633,6 +634,17 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
 
   int sweep = 0, conv = 0;
   long long nrot = 0;
+  const bool prof = it.phase_cycles != nullptr && tid == 0;
+  unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
+  long long t_start = clock64(), t_mark = t_start;
+  auto mark = [&](int slot) {
+    if (prof) {
+      const long long t = clock64();
+      pc[slot] += (unsigned long long)(t - t_mark);
+      t_mark = t;
+    }
+  };
+  mark(4);
   for (sweep = 1; sweep <= MAX_SWEEPS; ++sweep) {
     if (crank == 0 && tid == 0) *(volatile int*)it.sync = 0;
     csync();
@@ -676,15 +688,41 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         }
         tnorm2<L>(gr);
         tnorm2<L>(gi);
+        // cross-lane column sums through shared memory (the staging buffer is free now):
+        // lane l writes its 2(L+2) columns, lanes 0..2(L+2)-1 each sum one column over 32 lanes
+        {
+          int64_t* red = (int64_t*)wbuf;  // [2(L+2)][32]
+          __syncwarp();
 #pragma unroll
-        for (int c = 0; c < L + 2; ++c) { gr[c] = warp_sum64(gr[c]); gi[c] = warp_sum64(gi[c]); }
-        if (lane == 0) {
-          const int64_t E0 = 28 * (int64_t)(L - 2) + it.eA[p] + it.eA[q] - 2 * (int64_t)W;
-          it.gam[2 * i] = mpf_from_cols<NL, L + 2>(gr, E0);
-          it.gam[2 * i + 1] = mpf_from_cols<NL, L + 2>(gi, E0);
+          for (int c = 0; c < L + 2; ++c) { red[c * 32 + lane] = gr[c]; red[(L + 2 + c) * 32 + lane] = gi[c]; }
+          __syncwarp();
+          int64_t sum[2] = {0, 0};  // 2(L+2) columns over 32 lanes (two rounds when L > 14)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            if (c < 2 * (L + 2)) {
+#pragma unroll 8
+              for (int l = 0; l < 32; ++l) sum[h] += red[c * 32 + ((l + lane) & 31)];
+            }
+          }
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (lane + 32 * h < 2 * (L + 2)) red[lane + 32 * h] = sum[h];
+          __syncwarp();
+          // lane 0 converts gamma_re, lane 1 gamma_im (in parallel)
+          if (lane < 2) {
+            int64_t cols[L + 2];
+#pragma unroll
+            for (int c = 0; c < L + 2; ++c) cols[c] = red[lane * (L + 2) + c];
+            const int64_t E0 = 28 * (int64_t)(L - 2) + it.eA[p] + it.eA[q] - 2 * (int64_t)W;
+            it.gam[2 * i + lane] = mpf_from_cols<NL, L + 2>(cols, E0);
+          }
+          __syncwarp();
         }
       }
       csync();
+      mark(0);
       // ---- phase R: rotation parameters (thread per pair)
       for (int i = gt; i < NP; i += GT) {
         int p, q;
@@ -734,16 +772,22 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
               eo[u] = enew;
             }
             // 24 signed coefficient vectors [mat][o][t] (layout: see c_opidx)
-            int32_t* cf = it.coef + (size_t)i * 24 * CW;
+            int32_t* cf = it.coef + (size_t)i * 33 * CW;
             const mpf<NL> Cp = mpf_ldexp(c, ep - eo[0]), Cq = mpf_ldexp(c, eq - eo[1]);
             const mpf<NL> Psr = mpf_ldexp(sr, eq - eo[0]), Psi = mpf_ldexp(si, eq - eo[0]);
             const mpf<NL> Qsr = mpf_ldexp(sr, ep - eo[1]), Qsi = mpf_ldexp(si, ep - eo[1]);
-            const mpf<NL> A12[12] = {Cp, mpf_neg(Psr), mpf_neg(Psi), Cp, mpf_neg(Psr), Psi,
-                                     Qsr, mpf_neg(Qsi), Cq, Qsr, Qsi, Cq};
-            const mpf<NL> V12[12] = {c, mpf_neg(sr), mpf_neg(si), c, mpf_neg(sr), si,
-                                     sr, mpf_neg(si), c, sr, si, c};
-            for (int u = 0; u < 12; ++u) mpf_to_coef<NL, L>(A12[u], cf + u * CW);
-            for (int u = 0; u < 12; ++u) mpf_to_coef<NL, L>(V12[u], cf + (12 + u) * CW);
+            // 9 distinct values; the 24 signed slots are copies / negations of their digits
+            const mpf<NL> vals[9] = {Cp, Psr, Psi, Qsr, Qsi, Cq, c, sr, si};
+            // slot u <- (+/-) vals[src[u]]; sign bit in bit 4
+            const int8_t src[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 3, 4 | 16, 5, 3, 4, 5,
+                                    6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 7, 8 | 16, 6, 7, 8, 6};
+            int32_t* tmpc = cf + 24 * CW;  // 9 scratch vectors after the 24 slots
+            for (int v = 0; v < 9; ++v) mpf_to_coef<NL, L>(vals[v], tmpc + v * CW);
+            for (int u = 0; u < 24; ++u) {
+              const int32_t* sv = tmpc + (src[u] & 15) * CW;
+              const bool ng = src[u] & 16;
+              for (int d = 0; d < CW; ++d) cf[u * CW + d] = ng ? -sv[d] : sv[d];
+            }
             int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
             for (int u = 0; u < 24; ++u)
               if (cf[u * CW + L]) ints |= 1 << (u / 3);
@@ -762,13 +806,14 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         it.rot[i] = flag;
       }
       csync();
+      mark(1);
       // ---- phase U: apply the rotations to columns p, q of A and V
       for (int i = gw; i < NP; i += GW) {
         const int flag = it.rot[i];
         if (!(flag & 1)) continue;
         int p, q;
         rr_pair(N, step, i, p, q);
-        const int32_t* cfg = it.coef + (size_t)i * 24 * CW;
+        const int32_t* cfg = it.coef + (size_t)i * 33 * CW;
         for (int w = lane; w < 24 * CW; w += 32) wcoef[w] = cfg[w];
         __syncwarp();
         for (int mat = 0; mat < 2; ++mat) {
@@ -814,15 +859,21 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         }
       }
       csync();
+      mark(2);
     }
     // refresh exact column norms (and renormalise columns) for the next sweep / the result
     const bool any = *(volatile int*)it.sync != 0;
     // exact norms; the negligible-column rule (R3b) is re-evaluated on them
     jac_norms<L, NL>(it, true, z, gw, GW);
     csync();
+    mark(3);
     if (!any) { conv = 1; break; }
   }
   atomicAdd((unsigned long long*)it.rotations, (unsigned long long)nrot);
+  if (prof) {
+    pc[5] = (unsigned long long)(clock64() - t_start);
+    for (int i = 0; i < 6; ++i) atomicAdd(&it.phase_cycles[i], pc[i]);
+  }
   if (crank == 0 && tid == 0) {
     *it.sweeps = conv ? sweep : MAX_SWEEPS + 1;
     *it.status = conv ? 0 : -3;

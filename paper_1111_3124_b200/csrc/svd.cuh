@@ -91,7 +91,7 @@ size_t svd_workspace(int M, int N, int batch) {
   const int Nj = Nj0 + (Nj0 & 1);
   size_t per = align_up((size_t)Mj * Nj * 2 * L * 4) + align_up((size_t)Nj * Nj * 2 * L * 4) +
                align_up(8 * (size_t)Nj + 64) + align_up(sizeof(mpf<NL>) * (size_t)Nj * 4) +
-               align_up(4 * (size_t)Nj / 2 * 24 * (L + 1)) + align_up(4 * (size_t)Nj * 3 + 64) + 512;
+               align_up(4 * (size_t)Nj / 2 * 33 * (L + 1)) + align_up(4 * (size_t)Nj * 3 + 64) + 512;
   return align_up(sizeof(MatItem) * batch) + align_up(sizeof(SvdItem<NL>) * batch) +
          align_up(sizeof(FinItem<NL>) * batch) + (size_t)batch * per + 4096;
 }
@@ -130,7 +130,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     mpf<NL>* inv_sig = gam + Nj;
     mpf<NL>* lam = inv_sig + Nj;
     int32_t* coef = (int32_t*)((char*)alpha + align_up(sizeof(mpf<NL>) * (size_t)Nj * 4));
-    int* rot = (int*)((char*)coef + align_up(4 * (size_t)Nj / 2 * 24 * (L + 1)));
+    int* rot = (int*)((char*)coef + align_up(4 * (size_t)Nj / 2 * 33 * (L + 1)));
     int* negl = rot + Nj / 2;
     int* ord = negl + Nj;
     int* syncp = (int*)align_up((size_t)(ord + Nj) + 64, 16);
@@ -140,7 +140,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     si.M = Mj; si.N = Nj; si.A = A; si.eA = eA; si.V = V; si.alpha = alpha; si.gam = gam; si.coef = coef;
     si.dbg = ddbg ? ddbg + 64 * b : nullptr;
     si.rot = rot; si.negl = negl; si.status = ip; si.sweeps = dsweeps + b; si.rotations = rots;
-    si.sync = syncp; si.zbuf = zbuf;
+    si.sync = syncp; si.zbuf = zbuf; si.phase_cycles = nullptr;
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));

@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -40,7 +42,7 @@ struct SvdScratch {
   mpf<NL>* zbuf;
   static size_t bytes(int N) {
     return align_up(8 * (size_t)N + 64) + align_up(sizeof(mpf<NL>) * (size_t)N * 4) +
-           align_up(4 * (size_t)N / 2 * 24 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256 + 256;
+           align_up(4 * (size_t)N / 2 * 33 * (L + 1)) + align_up(4 * (size_t)N * 3) + 256 + 256;
   }
   static SvdScratch carve(char* p, int N) {
     SvdScratch s;
@@ -52,7 +54,7 @@ struct SvdScratch {
     s.lam = s.inv_sig + N;
     q += align_up(sizeof(mpf<NL>) * (size_t)N * 4);
     s.coef = (int32_t*)q;
-    q += align_up(4 * (size_t)N / 2 * 24 * (L + 1));
+    q += align_up(4 * (size_t)N / 2 * 33 * (L + 1));
     s.rot = (int*)q;
     s.negl = s.rot + N / 2;
     s.ord = s.negl + N;
@@ -70,6 +72,22 @@ struct SvdScratch {
 };
 
 inline size_t mat_bytes(int rows, int cols, int L) { return align_up((size_t)rows * cols * 2 * L * 4); }
+
+// MPS_JACOBI_PHASES=1 (debug): per-phase cycle counters of the batched Jacobi, printed to
+// stderr after each launch_update2 (D, R, U, norms, init, total; summed over CTAs).
+inline unsigned long long* phase_dbg() {
+  static unsigned long long* d = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_JACOBI_PHASES");
+    on = e && atoi(e) ? 1 : 0;
+    if (on) {
+      cudaMalloc(&d, 6 * sizeof(unsigned long long));
+      cudaMemset(d, 0, 6 * sizeof(unsigned long long));
+    }
+  }
+  return on ? d : nullptr;
+}
 
 // ---------------------------------------------------------------------------- two-site
 struct Upd2Args {
@@ -150,7 +168,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
-    si.sync = S.sync; si.zbuf = S.zbuf;
+    si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -196,6 +214,14 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     ++nl;
   }
   prof_mark(PROF_JACOBI, 0, st);
+  if (unsigned long long* pd = phase_dbg()) {
+    unsigned long long h[6];
+    cudaMemcpyAsync(h, pd, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "jacobi phase cycles (sum over CTAs): D %.4e R %.4e U %.4e norms %.4e init %.4e total %.4e\n",
+            (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5]);
+    cudaMemsetAsync(pd, 0, sizeof(h), st);
+  }
   prof_mark(PROF_FINALIZE, 1, st);
   int maxN = 0;
   for (int b = 0; b < n; ++b) maxN = std::max(maxN, hs[b].N);
@@ -293,7 +319,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   SvdItem<NL> si;
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
   si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
-  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf;
+  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   FinItem<NL> fi;
@@ -373,7 +399,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   SvdItem<NL> si;
   si.M = M2; si.N = N2; si.A = A2; si.eA = S2.eA; si.V = V2; si.alpha = S2.alpha; si.gam = S2.gam;
   si.coef = S2.coef; si.dbg = nullptr; si.rot = S2.rot; si.negl = S2.negl; si.status = S2.status;
-  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf;
+  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
   FinItem<NL> fi;
