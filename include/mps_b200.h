@@ -183,6 +183,10 @@ int mps_last_launch_count(void);
  * (a4-a5).  enable(1) clears and starts recording; query syncs and sums the durations. */
 int mps_profile_enable(int on);
 int mps_profile_query(int which, double* total_ms, int* launches);
+/* Totals over the Jacobi problems run since mps_profile_enable(1): [0] rotations applied,
+ * [1] pair evaluations (gamma computed), [2] sum (sweeps+1) M N (norm passes),
+ * [3] sum N N M (recovery of V).  Used to count the executed IMAD.WIDE of the kernel. */
+int mps_profile_counts(long long* out4);
 
 /* ---- kernel test surface --------------------------------------------------------
  * One-sided Jacobi SVD (a3) of `batch` column-major M x N complex matrices (host

@@ -20,10 +20,13 @@ static thread_local int g_last_launches = 0;
 namespace {
 struct Prof {
   bool on = false;
+  unsigned long long* counts = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[PROF_N];
   std::vector<cudaEvent_t> pending_begin[PROF_N];
 } g_prof;
 }  // namespace
+
+unsigned long long* mpsb::prof_counts() { return g_prof.on ? g_prof.counts : nullptr; }
 
 void mpsb::prof_mark(int which, int begin, cudaStream_t st) {
   if (!g_prof.on) return;
@@ -69,6 +72,19 @@ int mps_profile_enable(int on) {
     g_prof.pending_begin[k].clear();
   }
   g_prof.on = on != 0;
+  if (g_prof.on) {
+    if (!g_prof.counts && cudaMalloc(&g_prof.counts, 4 * sizeof(unsigned long long)) != cudaSuccess) return MPS_ENOMEM;
+    cudaMemset(g_prof.counts, 0, 4 * sizeof(unsigned long long));
+  }
+  return MPS_OK;
+}
+
+int mps_profile_counts(long long* out4) {
+  if (!out4 || !g_prof.counts) return MPS_EINVAL;
+  cudaDeviceSynchronize();
+  unsigned long long h[4];
+  if (cudaMemcpy(h, g_prof.counts, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return MPS_ECUDA;
+  for (int i = 0; i < 4; ++i) out4[i] = (long long)h[i];
   return MPS_OK;
 }
 

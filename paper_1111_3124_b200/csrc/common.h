@@ -27,6 +27,8 @@ struct BatchOut {  // device pointers (records unless stated)
 // Optional CUDA-event bracketing of individual kernels (bench.py roofline): which = kernel id.
 enum { PROF_JACOBI = 0, PROF_CONTRACT = 1, PROF_FINALIZE = 2, PROF_N = 3 };
 void prof_mark(int which, int begin, cudaStream_t st);
+// device buffer of 4 running totals while profiling is on (else null), see k_accum_stats
+unsigned long long* prof_counts();
 
 template <class T>
 int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, const uint32_t* A,

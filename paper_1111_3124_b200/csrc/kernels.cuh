@@ -74,6 +74,11 @@ struct SvdItem {
   int* sync;                // scratch flag ("some pair rotated in this sweep")
   mpf<NL>* zbuf;            // scratch: negligible-column floor
   unsigned long long* phase_cycles;  // null, or [6]: D, R, U, norms, init, total (summed over CTAs)
+  int32_t* A0;              // non-null: V is NOT accumulated; the input Theta' is kept here (M x N,
+                            // block exponent eA0) and V is recovered after convergence (k_recover_v)
+  int64_t* eA0;             // [1]
+  int64_t* eV;              // [N] exponents of the recovered V columns
+  long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
 };
 
 // Sort / truncate / renormalise one SVD result and produce the split outputs.
@@ -91,6 +96,7 @@ struct FinItem {
   int* k_out;               // 1
   int* status;              // 1 (out: svd status if nonzero, else -4 when k = 0, else 0)
   const int* svd_status;    // the Jacobi status of this problem, or null
+  const int64_t* eV;        // per-column exponents of V (recovered V), or null (= 1)
   uint32_t* sigma_rec;      // [nsig] records (sigma, descending) or null
   int nsig;                 // number of sigma records to write (<= N)
   uint32_t* lam_rec;        // [k] records or null
@@ -593,9 +599,15 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   int32_t* wcoef = wbuf + 2 * STAGE;
   __shared__ mpf<NL> s_red[1];
 
-  if (crank == 0 && tid == 0) *it.rotations = 0;
+  if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; }
+  const bool accV = it.A0 == nullptr;
+  if (!accV) {  // keep the input (block exponent from k_mix) for the recovery of V
+    const size_t nw = (size_t)M * N * 2 * L;
+    for (size_t t = gt; t < nw; t += GT) it.A0[t] = it.A[t];
+    if (gt == 0) *it.eA0 = it.eA[0];
+  }
   // V = I (exponent 1: 1 = 2^27 * 2^(28(L-1)) * 2^(1 - 28L))
-  for (int t = gt; t < N * N; t += GT) {
+  for (int t = gt; accV && t < N * N; t += GT) {
     const int r = t % N, c = t / N;
     int32_t x[L], z0[L];
 #pragma unroll
@@ -633,7 +645,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   const int nchA = (M + 31) / 32, nchV = (N + 31) / 32;
 
   int sweep = 0, conv = 0;
-  long long nrot = 0;
+  long long nrot = 0, nev = 0;
   const bool prof = it.phase_cycles != nullptr && tid == 0;
   unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
   long long t_start = clock64(), t_mark = t_start;
@@ -729,6 +741,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         rr_pair(N, step, i, p, q);
         int flag = 0;
         if (!it.negl[p] && !it.negl[q]) {
+          ++nev;
           mpf<NL> ap = it.alpha[p], aq = it.alpha[q];
           const mpf<NL> gr = it.gam[2 * i], gi = it.gam[2 * i + 1];
           const mpf<NL> g2 = mpf_add(mpf_mul(gr, gr), mpf_mul(gi, gi));
@@ -816,7 +829,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         const int32_t* cfg = it.coef + (size_t)i * 33 * CW;
         for (int w = lane; w < 24 * CW; w += 32) wcoef[w] = cfg[w];
         __syncwarp();
-        for (int mat = 0; mat < 2; ++mat) {
+        for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
           int32_t* F = mat ? it.V : it.A;
           const int rows = mat ? N : M;
           const int nch = mat ? nchV : nchA;
@@ -870,6 +883,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
     if (!any) { conv = 1; break; }
   }
   atomicAdd((unsigned long long*)it.rotations, (unsigned long long)nrot);
+  atomicAdd((unsigned long long*)it.evals, (unsigned long long)nev);
   if (prof) {
     pc[5] = (unsigned long long)(clock64() - t_start);
     for (int i = 0; i < 6; ++i) atomicAdd(&it.phase_cycles[i], pc[i]);
@@ -933,6 +947,81 @@ inline int jacobi_cluster_size(int n_items, int min_N) {
   int C = 1;
   while (C < cap && n_items * C * 2 <= 2 * 148 && (C * 2) * NWARP <= min_N / 2) C *= 2;
   return C;
+}
+
+// per-item counters -> running totals (profiling): [0] rotations, [1] pair evaluations,
+// [2] sum over items of sweeps * M * N (norm passes), [3] sum of N*N*M (recovery GEMMs)
+template <int NL>
+__global__ void k_accum_stats(const SvdItem<NL>* items, int n, unsigned long long* tot) {
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
+    const SvdItem<NL>& it = items[b];
+    atomicAdd(&tot[0], (unsigned long long)*it.rotations);
+    atomicAdd(&tot[1], (unsigned long long)*it.evals);
+    atomicAdd(&tot[2], (unsigned long long)(*it.sweeps + 1) * it.M * it.N);
+    if (it.A0) atomicAdd(&tot[3], (unsigned long long)it.N * it.N * it.M);
+  }
+}
+
+// ----------------------------------------------------------------------------
+// a3' recovery of the right factor: V(c,b) = sum_r conj(A0(r,c)) A(r,b) / alpha_b
+// (A = A0 V with A's columns a_b = sigma_b x_b, so V = A0^H A diag(1/sigma^2)).  A0 has one
+// block exponent, A per-column exponents; column b of V gets its own exponent
+// eV[b] = e0 + e_b + g + e(1/alpha_b) and the digits are scaled by the mantissa of 1/alpha_b.
+template <int L, int NL>
+__global__ void k_recover_v(const SvdItem<NL>* items) {
+  const SvdItem<NL> it = items[blockIdx.y];
+  if (!it.A0) return;
+  const int M = it.M, N = it.N, W = 28 * L;
+  int g = 1;
+  while ((1 << (g - 1)) < M) ++g;
+  g += 1;  // sum of M complex products, each |.| < 2^(e0 + e_b + 1)
+  const int64_t e0 = *it.eA0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * N; t += gridDim.x * blockDim.x) {
+    const int c = t % N, b = t / N;
+    const mpf<NL> al = it.alpha[b];
+    int32_t o[L];
+    if (mpf_is_zero(al)) {
+#pragma unroll
+      for (int k = 0; k < L; ++k) o[k] = 0;
+      stfx<L>(it.V, N, b, 0, c, o);
+      stfx<L>(it.V, N, b, 1, c, o);
+      if (c == 0) it.eV[b] = 1;
+      continue;
+    }
+    int64_t ar[L + 2], ai[L + 2];
+#pragma unroll
+    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    int cnt = 0;
+    for (int r = 0; r < M; ++r) {
+      int32_t xr[L], xi[L], yr[L], yi[L];
+      ldfx<L>(it.A0, M, c, 0, r, xr);
+      ldfx<L>(it.A0, M, c, 1, r, xi);
+      ldfx<L>(it.A, M, b, 0, r, yr);
+      ldfx<L>(it.A, M, b, 1, r, yi);
+      tmul_acc2<L>(ar, xr, yr);  // conj(x) y: re = xr yr + xi yi, im = xr yi - xi yr
+      tmul_acc2<L>(ar, xi, yi);
+      tmul_acc2<L>(ai, xr, yi);
+      tmul_sub2<L>(ai, xi, yr);
+      if (++cnt == 8) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); }
+    }
+    // 1/alpha_b = m 2^ei, m in [0.5, 1): digits x m as a fractional coefficient
+    const mpf<NL> inv = mpf_recip(al);
+    const int64_t ei = inv.e;
+    int32_t kd[L + 1];
+    mpf_to_coef<NL, L>(mpf_ldexp(inv, -ei), kd);
+    const int64_t eOut = e0 + it.eA[b] + g + ei;
+    for (int ri = 0; ri < 2; ++ri) {
+      int32_t d[L];
+      tround_sr<L>(ri ? ai : ar, g, d);
+      int64_t acc[L + 2];
+#pragma unroll
+      for (int j = 0; j < L + 2; ++j) acc[j] = 0;
+      kmul_acc<L>(acc, kd, d, kd[L] != 0);
+      tround2<L>(acc, o);
+      stfx<L>(it.V, N, b, ri, c, o);
+    }
+    if (c == 0) it.eV[b] = eOut;
+  }
 }
 
 // ----------------------------------------------------------------------------
@@ -1022,7 +1111,7 @@ __global__ void k_split(const FinItem<NL>* items, int RBr, int p) {
     const bool fromA = left ? !it.trans : it.trans;
     const int32_t* F = fromA ? it.A : it.V;
     const int ld = fromA ? it.M : it.N;
-    const int64_t E = fromA ? it.eA[j] : 1;
+    const int64_t E = fromA ? it.eA[j] : (it.eV ? it.eV[j] : 1);
     mpf<NL> scale = fromA ? it.inv_sig[b] : mpf_from_int<NL>(1);
     const int chi = left ? it.chiL_out : it.chiR_out;
     const uint32_t* lam = left ? it.lamL : it.lamR;
@@ -1060,7 +1149,7 @@ __device__ __forceinline__ void m2_weight(const FinItem<NL>& it, int b, mpf<NL>&
   const bool fromA = !it.trans;
   const int j = it.ord[b];
   w = fromA ? mpf_mul(it.lam[b], it.inv_sig[b]) : it.lam[b];
-  Es = fromA ? it.eA[j] : 1;
+  Es = fromA ? it.eA[j] : (it.eV ? it.eV[j] : 1);
 }
 
 template <int L, int NL>

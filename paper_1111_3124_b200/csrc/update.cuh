@@ -104,7 +104,8 @@ inline size_t upd2_item_bytes(const Upd2Args& a) {
   const int M = 2 * std::max(a.chiL, a.chiR), N = 2 * std::min(a.chiL, a.chiR);
   size_t lr = mat_bytes(2 * a.chiL, a.chiM, L) + mat_bytes(a.chiM, 2 * a.chiR, L);
   size_t r1 = std::max(lr, mat_bytes(M, N, L));
-  return r1 + mat_bytes(2 * a.chiL, 2 * a.chiR, L) + mat_bytes(N, N, L) + SvdScratch<L, NL>::bytes(N) + 256;
+  return r1 + mat_bytes(2 * a.chiL, 2 * a.chiR, L) + mat_bytes(N, N, L) + mat_bytes(M, N, L) +
+         SvdScratch<L, NL>::bytes(N) + 8 * (size_t)N + 512;
 }
 
 template <class T>
@@ -153,8 +154,10 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     char* p2 = ib + std::max(lr, mat_bytes(M, N, L));
     int32_t* Tf = (int32_t*)p2;
     int32_t* Vf = (int32_t*)(p2 + mat_bytes(2 * chiL, 2 * chiR, L));
-    char* sp = (char*)Vf + mat_bytes(N, N, L);
+    int32_t* A0f = (int32_t*)((char*)Vf + mat_bytes(N, N, L));
+    char* sp = (char*)A0f + mat_bytes(M, N, L);
     auto S = SvdScratch<L, NL>::carve(sp, N);
+    int64_t* eV = (int64_t*)align_up((size_t)sp + SvdScratch<L, NL>::bytes(N), 16);
     int64_t* eL = S.e_misc;
     int64_t* eR = S.e_misc + 1;
     int64_t* eT = S.e_misc + 2;
@@ -169,6 +172,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
+    si.A0 = A0f; si.eA0 = S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -176,6 +180,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     fi.chi_max = g.chi_max; fi.thr = thr_m; fi.ord = S.ord; fi.inv_sig = S.inv_sig; fi.lam = S.lam;
     fi.k_out = g.k_out ? g.k_out : S.k; fi.status = g.status_out ? g.status_out : S.fstatus;
     fi.svd_status = S.status;
+    fi.eV = eV;
     fi.sigma_rec = g.sigma_out; fi.nsig = N; fi.lam_rec = g.lam_out;
     fi.GL = g.GL_out; fi.GL_ld = g.out_ld; fi.lamL = g.lamL; fi.chiL_out = chiL;
     fi.GR = g.GR_out; fi.GR_ld = g.out_ld; fi.lamR = g.lamR; fi.chiR_out = chiR;
@@ -212,6 +217,17 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     for (int b = 0; b < n; ++b) minN = std::min(minN, hs[b].N);
     launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n, minN), st);
     ++nl;
+  }
+  {
+    int maxNN = 0;
+    for (int b = 0; b < n; ++b) maxNN = std::max(maxNN, hs[b].N * hs[b].N);
+    dim3 gr(std::max(1, std::min(64, (maxNN + 127) / 128)), n);
+    k_recover_v<L, NL><<<gr, 128, 0, st>>>((const SvdItem<NL>*)(base + d_svd));
+    ++nl;
+    if (unsigned long long* pc = prof_counts()) {
+      k_accum_stats<NL><<<(n + 127) / 128, 128, 0, st>>>((const SvdItem<NL>*)(base + d_svd), n, pc);
+      ++nl;
+    }
   }
   prof_mark(PROF_JACOBI, 0, st);
   if (unsigned long long* pd = phase_dbg()) {
@@ -319,7 +335,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   SvdItem<NL> si;
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
   si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
-  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr;
+  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr; si.A0 = nullptr; si.eA0 = nullptr; si.eV = nullptr; si.evals = S1.rots + 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   FinItem<NL> fi;
@@ -399,7 +415,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   SvdItem<NL> si;
   si.M = M2; si.N = N2; si.A = A2; si.eA = S2.eA; si.V = V2; si.alpha = S2.alpha; si.gam = S2.gam;
   si.coef = S2.coef; si.dbg = nullptr; si.rot = S2.rot; si.negl = S2.negl; si.status = S2.status;
-  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr;
+  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr; si.A0 = nullptr; si.eA0 = nullptr; si.eV = nullptr; si.evals = S2.rots + 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
   FinItem<NL> fi;
