@@ -573,6 +573,10 @@ __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int l
 // with Psr+iPsi = s 2^(eq-eo_p) (conj(s) multiplies x_q), Qsr+iQsi = s 2^(ep-eo_q),
 // Cp = c 2^(ep-eo_p), Cq = c 2^(eq-eo_q); for V all scales are 1.
 __constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {0, 1, 2}, {1, 0, 3}};
+// slot u <- (+/-) vals[src & 15] of the 9 distinct values {Cp, Psr, Psi, Qsr, Qsi, Cq, c,
+// sr, si}; bit 4 = negate
+__constant__ int8_t c_coefsrc[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 3, 4 | 16, 5, 3, 4, 5,
+                                     6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 7, 8 | 16, 6, 7, 8, 6};
 
 // C CTAs (a thread-block cluster when C > 1) cooperate on one matrix: pairs, columns and
 // rows are distributed over all C*NWARP warps, column state lives in global memory, and
@@ -746,17 +750,22 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
           const mpf<NL> gr = it.gam[2 * i], gi = it.gam[2 * i + 1];
           const mpf<NL> g2 = mpf_add(mpf_mul(gr, gr), mpf_mul(gi, gi));
           if (!mpf_is_zero(g2) && mpf_cmp(g2, mpf_mul(tol2, mpf_mul(ap, aq))) > 0) {
-            const mpf<NL> one = mpf_from_int<NL>(1);
-            const mpf<NL> rg = mpf_rsqrt(g2);
-            const mpf<NL> zeta = mpf_ldexp(mpf_mul(mpf_sub(aq, ap), rg), -1);
-            const mpf<NL> sq = mpf_sqrt(mpf_add(one, mpf_mul(zeta, zeta)));
-            mpf<NL> t = mpf_recip(mpf_add(mpf_abs(zeta), sq));
-            if (!mpf_is_zero(zeta) && zeta.neg) t = mpf_neg(t);
-            const mpf<NL> c = mpf_rsqrt(mpf_add(one, mpf_mul(t, t)));
-            const mpf<NL> ct = mpf_mul(c, t);
-            const mpf<NL> sr = mpf_mul(ct, mpf_mul(gr, rg));
-            const mpf<NL> si = mpf_mul(ct, mpf_mul(gi, rg));
-            const mpf<NL> tg = mpf_mul(t, mpf_mul(g2, rg));  // t |gamma|
+            // The oracle's zeta = d/(2|g|), t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
+            // c = 1/sqrt(1 + t^2), s = c t g/|g| (d = a_q - a_p, g = gamma), rewritten with
+            // r = sqrt(d^2 + 4|g|^2) and c^2 = (|d| + r)/(2r) (no cancellation, both terms
+            // >= 0) so that only two inverse square roots are needed:
+            //   s = sgn(d) g / (r c),  t |g| = sgn(d) |g|^2 / (r c^2)      (R17)
+            const mpf<NL> d = mpf_sub(aq, ap);
+            const mpf<NL> w = mpf_add(mpf_mul(d, d), mpf_ldexp(g2, 2));
+            const mpf<NL> rr = mpf_rsqrt(w);                       // 1/r
+            const mpf<NL> c2 = mpf_ldexp(mpf_mul(mpf_add(mpf_abs(d), mpf_mul(w, rr)), rr), -1);
+            const mpf<NL> ic = mpf_rsqrt(c2);                      // 1/c
+            const mpf<NL> c = mpf_mul(c2, ic);
+            mpf<NL> sc = mpf_mul(rr, ic);                          // 1/(r c)
+            if (!mpf_is_zero(d) && d.neg) sc = mpf_neg(sc);
+            const mpf<NL> sr = mpf_mul(sc, gr);
+            const mpf<NL> si = mpf_mul(sc, gi);
+            const mpf<NL> tg = mpf_mul(mpf_mul(g2, sc), ic);      // t |gamma|
             ap = mpf_sub(ap, tg);
             aq = mpf_add(aq, tg);
             const int64_t ep = it.eA[p], eq = it.eA[q];
@@ -791,19 +800,34 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             const mpf<NL> Qsr = mpf_ldexp(sr, ep - eo[1]), Qsi = mpf_ldexp(si, ep - eo[1]);
             // 9 distinct values; the 24 signed slots are copies / negations of their digits
             const mpf<NL> vals[9] = {Cp, Psr, Psi, Qsr, Qsi, Cq, c, sr, si};
-            // slot u <- (+/-) vals[src[u]]; sign bit in bit 4
-            const int8_t src[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 3, 4 | 16, 5, 3, 4, 5,
-                                    6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 7, 8 | 16, 6, 7, 8, 6};
-            int32_t* tmpc = cf + 24 * CW;  // 9 scratch vectors after the 24 slots
-            for (int v = 0; v < 9; ++v) mpf_to_coef<NL, L>(vals[v], tmpc + v * CW);
-            for (int u = 0; u < 24; ++u) {
-              const int32_t* sv = tmpc + (src[u] & 15) * CW;
-              const bool ng = src[u] & 16;
-              for (int d = 0; d < CW; ++d) cf[u * CW + d] = ng ? -sv[d] : sv[d];
+            // the U warp expands them into the 24 signed slots (c_coefsrc)
+            int vint = 0;
+            for (int v = 0; v < 9; ++v) {
+              mpf_to_coef<NL, L>(vals[v], cf + v * CW);
+              if (cf[v * CW + L]) vint |= 1 << v;
             }
             int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
             for (int u = 0; u < 24; ++u)
-              if (cf[u * CW + L]) ints |= 1 << (u / 3);
+              if ((vint >> (c_coefsrc[u] & 15)) & 1) ints |= 1 << (u / 3);
+            if (it.phase_cycles) {  // debug: digit products a leading-zero-aware U would need
+              unsigned long long full = 0, need = 0;
+              for (int u = 0; u < 12; ++u) {
+                const int32_t* kv = cf + (c_coefsrc[u] & 15) * CW;
+                int top = -1;
+                for (int k = L - 1; k >= 0; --k)
+                  if (top < 0 && kv[k]) top = k;
+                for (int i = 0; i < L; ++i) {
+                  const int nj = i >= L - 2 ? L : i + 2;
+                  full += nj;
+                  if (i <= top) need += nj;
+                }
+                full += L;
+                if (kv[L]) need += L;
+              }
+              const int sw = sweep < 63 ? sweep : 63;
+              atomicAdd(&it.phase_cycles[6 + 2 * sw], full);
+              atomicAdd(&it.phase_cycles[7 + 2 * sw], need);
+            }
             it.alpha[p] = ap;
             it.alpha[q] = aq;
             it.eA[p] = eo[0];
@@ -827,7 +851,11 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         int p, q;
         rr_pair(N, step, i, p, q);
         const int32_t* cfg = it.coef + (size_t)i * 33 * CW;
-        for (int w = lane; w < 24 * CW; w += 32) wcoef[w] = cfg[w];
+        for (int w = lane; w < 24 * CW; w += 32) {
+          const int src = c_coefsrc[w / CW];
+          const int32_t v = cfg[(src & 15) * CW + w % CW];
+          wcoef[w] = (src & 16) ? -v : v;
+        }
         __syncwarp();
         for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
           int32_t* F = mat ? it.V : it.A;

@@ -189,10 +189,13 @@ __device__ __forceinline__ int mpf_cmp(const mpf<NL>& a, const mpf<NL>& b) {
   return sa > 0 ? c : -c;
 }
 
+// a * b.  Partial products a_i b_j with i + j < NL - 2 are skipped: their sum (and the
+// carries they would send up) is < NL^2/2 units of limb NL-1, the guard limb that
+// mpf_pack rounds on, so the result is faithful to ~2^-(32 NL - 6) relative.
 template <int NL>
 __device__ __noinline__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
   if (mpf_is_zero(a) || mpf_is_zero(b)) return mpf_zero<NL>();
-  // full product (2NL limbs), keep the top NL+1
+  constexpr int LO = NL > 2 ? NL - 2 : 0;  // lowest product column kept
   uint32_t p[2 * NL];
 #pragma unroll
   for (int i = 0; i < 2 * NL; ++i) p[i] = 0;
@@ -201,6 +204,7 @@ __device__ __noinline__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
     uint64_t carry = 0;
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
+      if (i + j < LO) continue;
       uint64_t t = (uint64_t)a.m[i] * b.m[j] + p[i + j] + carry;
       p[i + j] = (uint32_t)t;
       carry = t >> 32;
@@ -213,6 +217,20 @@ __device__ __noinline__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
   // value = p * 2^(ea + eb - 64NL) = t * 2^(ea + eb - 64NL + 32(NL-1)) ; t has NL+1 limbs
   int64_t e = a.e + b.e - 64 * (int64_t)NL + 32 * (int64_t)(NL - 1) + 32 * (int64_t)(NL + 1);
   return mpf_pack<NL>(t, e, a.neg ^ b.neg);
+}
+
+// precision change: the top K limbs (truncation) / zero extension
+template <int K, int NL>
+__device__ __forceinline__ mpf<K> mpf_resize(const mpf<NL>& a) {
+  mpf<K> r;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int src = NL - K + i;
+    r.m[i] = src >= 0 ? a.m[src] : 0u;
+  }
+  r.e = a.e;
+  r.neg = a.neg;
+  return r;
 }
 
 // a + b
@@ -313,37 +331,55 @@ __device__ __forceinline__ mpf<NL> mpf_from_frexp(double f, int64_t E) {
   return mpf_pack<NL>(t, E + k, neg);
 }
 
-// 1/b by Newton: y <- y + y(1 - b y), quadratic from a 53-bit seed
+// Newton iterations with precision doubling: the iteration that takes b correct bits to
+// 2b runs with K limbs, K the smallest of 4, 7, 13, ... (2K-1) that holds 2b bits, and the
+// last one with all NL limbs (53 -> ~100 -> ~200 -> ~400 bits).
+template <int K, int NL>
+struct NewtonNext {
+  static constexpr int value = (2 * K - 1 < NL) ? 2 * K - 1 : NL;
+};
+
+// 1/b: y <- y + y(1 - b y)
+template <int NL, int K>
+__device__ __forceinline__ mpf<NL> recip_chain(const mpf<NL>& b, mpf<K> y) {
+  const mpf<K> bk = mpf_resize<K>(b);
+  const mpf<K> r = mpf_sub(mpf_from_int<K>(1), mpf_mul(bk, y));
+  y = mpf_add(y, mpf_mul(y, r));
+  if constexpr (K == NL) {
+    return y;
+  } else {
+    constexpr int K2 = NewtonNext<K, NL>::value;
+    return recip_chain<NL, K2>(b, mpf_resize<K2>(y));
+  }
+}
 template <int NL>
 __device__ __noinline__ mpf<NL> mpf_recip(const mpf<NL>& b) {
   int64_t E;
   double f = mpf_frexp(b, &E);
-  mpf<NL> y = mpf_from_frexp<NL>(1.0 / f, -E);
-  const mpf<NL> one = mpf_from_int<NL>(1);
-  int bits = 50;
-  while (bits < 32 * NL + 8) {
-    mpf<NL> r = mpf_sub(one, mpf_mul(b, y));
-    y = mpf_add(y, mpf_mul(y, r));
-    bits *= 2;
-  }
-  return y;
+  constexpr int K0 = NL < 4 ? NL : 4;
+  return recip_chain<NL, K0>(b, mpf_from_frexp<K0>(1.0 / f, -E));
 }
 
 // 1/sqrt(x), x > 0: y <- y + y(1 - x y^2)/2
+template <int NL, int K>
+__device__ __forceinline__ mpf<NL> rsqrt_chain(const mpf<NL>& x, mpf<K> y) {
+  const mpf<K> xk = mpf_resize<K>(x);
+  const mpf<K> r = mpf_sub(mpf_from_int<K>(1), mpf_mul(xk, mpf_mul(y, y)));
+  y = mpf_add(y, mpf_ldexp(mpf_mul(y, r), -1));
+  if constexpr (K == NL) {
+    return y;
+  } else {
+    constexpr int K2 = NewtonNext<K, NL>::value;
+    return rsqrt_chain<NL, K2>(x, mpf_resize<K2>(y));
+  }
+}
 template <int NL>
 __device__ __noinline__ mpf<NL> mpf_rsqrt(const mpf<NL>& x) {
   int64_t E;
   double f = mpf_frexp(x, &E);  // x = f 2^E
   if (E & 1) { f *= 0.5; E += 1; }
-  mpf<NL> y = mpf_from_frexp<NL>(1.0 / sqrt(f), -E / 2);
-  const mpf<NL> one = mpf_from_int<NL>(1);
-  int bits = 50;
-  while (bits < 32 * NL + 8) {
-    mpf<NL> r = mpf_sub(one, mpf_mul(x, mpf_mul(y, y)));
-    y = mpf_add(y, mpf_ldexp(mpf_mul(y, r), -1));
-    bits *= 2;
-  }
-  return y;
+  constexpr int K0 = NL < 4 ? NL : 4;
+  return rsqrt_chain<NL, K0>(x, mpf_from_frexp<K0>(1.0 / sqrt(f), -E / 2));
 }
 template <int NL>
 __device__ __forceinline__ mpf<NL> mpf_sqrt(const mpf<NL>& x) {

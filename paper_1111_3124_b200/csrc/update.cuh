@@ -82,8 +82,8 @@ inline unsigned long long* phase_dbg() {
     const char* e = getenv("MPS_JACOBI_PHASES");
     on = e && atoi(e) ? 1 : 0;
     if (on) {
-      cudaMalloc(&d, 6 * sizeof(unsigned long long));
-      cudaMemset(d, 0, 6 * sizeof(unsigned long long));
+      cudaMalloc(&d, (6 + 128) * sizeof(unsigned long long));
+      cudaMemset(d, 0, (6 + 128) * sizeof(unsigned long long));
     }
   }
   return on ? d : nullptr;
@@ -231,11 +231,15 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   }
   prof_mark(PROF_JACOBI, 0, st);
   if (unsigned long long* pd = phase_dbg()) {
-    unsigned long long h[6];
+    unsigned long long h[6 + 128];
     cudaMemcpyAsync(h, pd, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "jacobi phase cycles (sum over CTAs): D %.4e R %.4e U %.4e norms %.4e init %.4e total %.4e\n",
             (double)h[0], (double)h[1], (double)h[2], (double)h[3], (double)h[4], (double)h[5]);
+    for (int sw = 1; sw < 64; ++sw)
+      if (h[6 + 2 * sw])
+        fprintf(stderr, "  sweep %2d: U digit products per row %.4e, needed with leading-zero skipping %.4e (%.3f)\n", sw,
+                (double)h[6 + 2 * sw], (double)h[7 + 2 * sw], (double)h[7 + 2 * sw] / (double)h[6 + 2 * sw]);
     cudaMemsetAsync(pd, 0, sizeof(h), st);
   }
   prof_mark(PROF_FINALIZE, 1, st);
