@@ -548,11 +548,34 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int NW>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NW)); }
 
+// 16-byte copy of `bytes` (0..16) valid bytes, the rest zero-filled (L2 only: streamed data)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
 // Stage rows [row0, row0+32) of the four operand columns (p re, p im, q re, q im) of a
-// fixed matrix into buf[4][L][32] (one row per lane).
+// fixed matrix into buf[4][L][32] (one row per lane of the consumer).  When ld is a
+// multiple of 4 words each lane moves 16 bytes (4 rows of one digit plane): lanes 8o..8o+7
+// copy operand o, L copies per lane; otherwise one 4-byte copy per row and plane.
 template <int L>
 __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int ld, int p, int q, int row0, int rows,
                                           int lane) {
+  if ((ld & 3) == 0) {
+    const int op = lane >> 3, sub = lane & 7;
+    const int col = op < 2 ? p : q, ri = op & 1;
+    const int r = row0 + 4 * sub;
+    int nv = rows - r;
+    nv = nv < 0 ? 0 : (nv > 4 ? 4 : nv);
+    const int32_t* g = F + ((size_t)(col * 2 + ri) * L) * ld + (nv ? r : 0);
+    int32_t* d = buf + op * L * 32 + 4 * sub;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      cp_async16(d + k * 32, g, 4 * nv);
+      g += ld;
+    }
+    return;
+  }
   const int r = row0 + lane;
   const bool ok = r < rows;
   const int rr = ok ? r : 0;
