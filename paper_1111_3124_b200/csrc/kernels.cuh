@@ -804,9 +804,9 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             const int64_t tmax[2] = {(ep + ec > eq + es ? ep + ec : eq + es) + 1,
                                      (ep + es > eq + ec ? ep + es : eq + ec) + 1};
             int64_t eo[2];
-            const mpf<NL>* an[2] = {&ap, &aq};
+#pragma unroll
             for (int u = 0; u < 2; ++u) {
-              const mpf<NL>& a = *an[u];
+              const mpf<NL>& a = u ? aq : ap;
               int64_t enew = tmax[u] - W + 14;
               if (!mpf_is_zero(a) && !a.neg) {
                 int64_t e1 = (int64_t)ceil(0.5 * mpf_log2(a) + 1e-9) + 1;
@@ -818,16 +818,21 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             }
             // 24 signed coefficient vectors [mat][o][t] (layout: see c_opidx)
             int32_t* cf = it.coef + (size_t)i * 33 * CW;
-            const mpf<NL> Cp = mpf_ldexp(c, ep - eo[0]), Cq = mpf_ldexp(c, eq - eo[1]);
-            const mpf<NL> Psr = mpf_ldexp(sr, eq - eo[0]), Psi = mpf_ldexp(si, eq - eo[0]);
-            const mpf<NL> Qsr = mpf_ldexp(sr, ep - eo[1]), Qsi = mpf_ldexp(si, ep - eo[1]);
-            // 9 distinct values; the 24 signed slots are copies / negations of their digits
-            const mpf<NL> vals[9] = {Cp, Psr, Psi, Qsr, Qsi, Cq, c, sr, si};
+            // 9 distinct values {Cp, Psr, Psi, Qsr, Qsi, Cq, c, sr, si}:
+            //   Cp = c 2^(ep-eo_p), Psr + i Psi = s 2^(eq-eo_p), Qsr + i Qsi = s 2^(ep-eo_q),
+            //   Cq = c 2^(eq-eo_q), and c, sr, si unscaled (V);
             // the U warp expands them into the 24 signed slots (c_coefsrc)
             int vint = 0;
+#pragma unroll
             for (int v = 0; v < 9; ++v) {
-              mpf_to_coef<NL, L>(vals[v], cf + v * CW);
-              if (cf[v * CW + L]) vint |= 1 << v;
+              const mpf<NL>& base = (v == 0 || v == 5 || v == 6) ? c : ((v == 1 || v == 3 || v == 7) ? sr : si);
+              const int64_t sc = v == 0 ? ep - eo[0] : v == 1 || v == 2 ? eq - eo[0] : v == 3 || v == 4 ? ep - eo[1]
+                                 : v == 5 ? eq - eo[1] : 0;
+              int32_t dg[L + 1];
+              mpf_to_fixed<NL, L + 1>(mpf_ldexp(base, sc), 28, dg);  // coefficient digits (scale 1)
+#pragma unroll
+              for (int k = 0; k <= L; ++k) cf[v * CW + k] = dg[k];
+              if (dg[L]) vint |= 1 << v;
             }
             int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
             for (int u = 0; u < 24; ++u)

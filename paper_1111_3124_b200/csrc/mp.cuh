@@ -98,6 +98,37 @@ __device__ __forceinline__ void tround(int64_t (&acc)[L + 1], int k, int32_t (&o
 }
 
 // ----------------------------------------------------------------------------
+// register-only word shifters (runtime shift counts without runtime array indices,
+// which would put the arrays in local memory): log2(N) passes of selects
+// ----------------------------------------------------------------------------
+// w[i] <- w[i - s] (zeros shifted in), s >= 0
+template <int N>
+__device__ __forceinline__ void words_up(uint32_t (&w)[N], int s) {
+  const bool all = s >= N;
+#pragma unroll
+  for (int b = 1; b < N; b <<= 1) {
+    const bool on = (s & b) != 0;
+#pragma unroll
+    for (int i = N - 1; i >= 0; --i) w[i] = on ? (i >= b ? w[i - b] : 0u) : w[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = all ? 0u : w[i];
+}
+// w[i] <- w[i + s] (zeros shifted in), s >= 0
+template <int N>
+__device__ __forceinline__ void words_down(uint32_t (&w)[N], int s) {
+  const bool all = s >= N;
+#pragma unroll
+  for (int b = 1; b < N; b <<= 1) {
+    const bool on = (s & b) != 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) w[i] = on ? (i + b < N ? w[i + b] : 0u) : w[i];
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = all ? 0u : w[i];
+}
+
+// ----------------------------------------------------------------------------
 // mpf: scalar multiprecision floating point
 // ----------------------------------------------------------------------------
 template <int NL>
@@ -131,12 +162,9 @@ __device__ __forceinline__ mpf<NL> mpf_pack(uint32_t (&t)[NL + 1], int64_t e, in
     if (top < 0 && t[i]) top = i;
   if (top < 0) return mpf_zero<NL>();
   // shift left by whole limbs so that t[NL] != 0
-  int ls = NL - top;
-  if (ls) {
-#pragma unroll
-    for (int i = NL; i >= 0; --i) t[i] = (i - ls >= 0) ? t[i - ls] : 0u;
-    e -= 32 * (int64_t)ls;
-  }
+  const int ls = NL - top;
+  words_up<NL + 1>(t, ls);
+  e -= 32 * (int64_t)ls;
   int sh = __clz(t[NL]);
   if (sh) {
 #pragma unroll
@@ -193,7 +221,7 @@ __device__ __forceinline__ int mpf_cmp(const mpf<NL>& a, const mpf<NL>& b) {
 // carries they would send up) is < NL^2/2 units of limb NL-1, the guard limb that
 // mpf_pack rounds on, so the result is faithful to ~2^-(32 NL - 6) relative.
 template <int NL>
-__device__ __noinline__ mpf<NL> mpf_mul(const mpf<NL>& a, const mpf<NL>& b) {
+__device__ __noinline__ mpf<NL> mpf_mul(mpf<NL> a, mpf<NL> b) {
   if (mpf_is_zero(a) || mpf_is_zero(b)) return mpf_zero<NL>();
   constexpr int LO = NL > 2 ? NL - 2 : 0;  // lowest product column kept
   uint32_t p[2 * NL];
@@ -241,22 +269,16 @@ __device__ __noinline__ mpf<NL> mpf_add(mpf<NL> a, mpf<NL> b) {
   if (mpf_cmp_abs(a, b) < 0) { mpf<NL> t = a; a = b; b = t; }
   int64_t d = a.e - b.e;  // >= 0
   if (d > 32 * (NL + 1)) return a;
-  // a and b as NL+1 limbs (one guard limb at the bottom)
+  // a and b as NL+1 limbs (one guard limb at the bottom); tb = (b << 32 guard) >> d
   uint32_t ta[NL + 1], tb[NL + 1];
   ta[0] = 0;
+  tb[0] = 0;
 #pragma unroll
-  for (int i = 0; i < NL; ++i) ta[i + 1] = a.m[i];
-  int q = (int)(d >> 5), r = (int)(d & 31);
-  uint32_t sticky = 0;
+  for (int i = 0; i < NL; ++i) { ta[i + 1] = a.m[i]; tb[i + 1] = b.m[i]; }
+  const int q = (int)(d >> 5), r = (int)(d & 31);
+  words_down<NL + 1>(tb, q);
 #pragma unroll
-  for (int i = 0; i <= NL; ++i) {
-    // tb[i] = (b << 32 guard) >> d
-    int src = i + q;  // index into (0, b.m[0..NL-1]) shifted
-    uint32_t lo = (src >= 1 && src <= NL) ? b.m[src - 1] : 0u;
-    uint32_t hi = (src + 1 >= 1 && src + 1 <= NL) ? b.m[src] : 0u;
-    tb[i] = r ? ((lo >> r) | (hi << (32 - r))) : lo;
-  }
-  (void)sticky;
+  for (int i = 0; i <= NL; ++i) tb[i] = __funnelshift_r(tb[i], i < NL ? tb[i + 1] : 0u, r);
   uint32_t t[NL + 1];
   int64_t e = a.e + 32;  // t[NL] top limb has the weight of a.m[NL-1]*2^32...
   if (a.neg == b.neg) {
@@ -471,7 +493,7 @@ __device__ __forceinline__ void mpf_to_record(const mpf<NL>& a, uint32_t* rec, i
 // fixed digits (value = sum d_k 2^(28k) * 2^(E - 28L)) -> mpf.
 // Digits may be unnormalised (any int64 column values); cols = number of digit columns.
 template <int NL, int NC>
-__device__ __noinline__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t E_of_col0) {
+__device__ __forceinline__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t E_of_col0) {
   // value = sum_c col[c] 2^(28c) * 2^(E_of_col0).  Resolve carries into a two's-complement
   // integer of 32-bit words, then take sign and magnitude.
   constexpr int NW = (28 * NC + 64) / 32 + 2;
@@ -515,54 +537,52 @@ __device__ __noinline__ mpf<NL> mpf_from_cols(const int64_t (&col)[NC], int64_t 
   for (int i = NW - 1; i >= 0; --i)
     if (top < 0 && w[i]) top = i;
   if (top < 0) return mpf_zero<NL>();
+  // bring word `top` to index NW-1, then take the NL+1 words below it
+  words_up<NW>(w, NW - 1 - top);
   uint32_t t[NL + 1];
 #pragma unroll
   for (int i = 0; i <= NL; ++i) {
-    int src = top - NL + i;
-    t[i] = (src >= 0 && src < NW) ? w[src] : 0u;
+    const int src = NW - 1 - NL + i;
+    t[i] = src >= 0 ? w[src] : 0u;
   }
   // value = w * 2^E0 ; t[NL] = w[top] -> value ~= t * 2^(E0 + 32(top - NL))
   //   mpf_pack expects value = t * 2^(E - 32(NL+1))  =>  E = E0 + 32(top - NL) + 32(NL+1)
   return mpf_pack<NL>(t, E_of_col0 + 32 * (int64_t)(top - NL) + 32 * (int64_t)(NL + 1), neg);
 }
 
-// 28 bits of the NL-limb magnitude m starting at bit position b0 (bits outside
-// [0, 32 NL) read as zero; b0 may be negative)
-template <int NL>
-__device__ __forceinline__ uint32_t mpf_bits28(const uint32_t (&m)[NL], int64_t b0) {
-  uint32_t v = 0;
-  if (b0 >= 32 * NL || b0 <= -28) return 0;
-  if (b0 < 0) {
-    // bits [0, b0 + 28) of m land at positions [-b0, 28)
-    const uint32_t lo = m[0];
-    v = (lo << (int)(-b0)) & 0x0FFFFFFFu;
-    return v;
-  }
-  const int q = (int)(b0 >> 5), r = (int)(b0 & 31);
-  uint64_t lo = m[q];
-  uint64_t hi = (q + 1 < NL) ? m[q + 1] : 0;
-  return (uint32_t)((((hi << 32) | lo) >> r) & 0x0FFFFFFFu);
-}
-
 // mpf -> L fixed digits at column exponent E (value = sum d_k 2^(28k) 2^(E - 28L)),
 // rounded to nearest; requires |a| < 2^E (else the top digit is simply large).
 template <int NL, int L>
-__device__ __noinline__ void mpf_to_fixed(const mpf<NL>& a, int64_t E, int32_t (&d)[L]) {
+__device__ __forceinline__ void mpf_to_fixed(const mpf<NL>& a, int64_t E, int32_t (&d)[L]) {
 #pragma unroll
   for (int k = 0; k < L; ++k) d[k] = 0;
   if (mpf_is_zero(a)) return;
-  // integer X = round(m * 2^s), s = a.e - 32NL - E + 28L; digit k = bits [28k - s, 28k - s + 28) of m
-  const int64_t s = a.e - 32 * (int64_t)NL - E + 28 * (int64_t)L;
-  const int64_t sh = -s;  // bit of m that becomes bit 0 of X (negative: X = m shifted left)
-  if (sh >= 32 * NL + 1) return;  // rounds to zero
-  uint32_t carry = 0;
-  if (sh >= 1) {  // round to nearest on bit sh-1
-    const int64_t rb = sh - 1;
-    if (rb < 32 * NL) carry = (a.m[rb >> 5] >> (rb & 31)) & 1u;
-  }
+  // integer X = round(m * 2^s), s = a.e - 32NL - E + 28L; digit k = bits [28k + sh, 28k + sh + 28)
+  // of m (sh = -s), the rounding bit is bit sh - 1.  Y = m >> (sh - 1) (bits outside m are 0):
+  // Y bit 0 = rounding bit, digit k = Y bits [1 + 28k, 29 + 28k).
+  const int64_t sh = -(a.e - 32 * (int64_t)NL - E + 28 * (int64_t)L);
+  if (sh >= 32 * (int64_t)NL + 1) return;  // rounds to zero
+  constexpr int NY = (1 + 28 * L + 31) / 32 + 1;
+  constexpr int OFF = NY + 1;
+  constexpr int NE = OFF + NL + 1;
+  const int64_t s1 = sh - 1;
+  const int64_t qw = s1 >> 5;  // floor
+  const int r = (int)(s1 & 31);
+  int64_t sw = qw + OFF;       // E'[i] = E[i + sw] = m[i + qw]
+  uint32_t Ex[NE];
+#pragma unroll
+  for (int j = 0; j < NE; ++j) Ex[j] = (j >= OFF && j < OFF + NL) ? a.m[j - OFF] : 0u;
+  if (sw < 0) sw = NE;         // |a| far above 2^E: outside the contract, digits 0
+  words_down<NE>(Ex, (int)(sw > NE ? NE : sw));
+  uint32_t Y[NY];
+#pragma unroll
+  for (int i = 0; i < NY; ++i) Y[i] = __funnelshift_r(Ex[i], Ex[i + 1], r);
+  uint32_t carry = Y[0] & 1u;
 #pragma unroll
   for (int k = 0; k < L; ++k) {
-    const uint32_t v = mpf_bits28<NL>(a.m, sh + 28 * (int64_t)k);
+    const int bit = 1 + 28 * k, w = bit >> 5, b = bit & 31;
+    const uint32_t hi = (w + 1 < NY) ? Y[w + 1] : 0u;
+    const uint32_t v = __funnelshift_r(Y[w], hi, b) & 0x0FFFFFFFu;
     const uint32_t sum = v + carry;
     carry = sum >> 28;
     d[k] = (int32_t)(sum & 0x0FFFFFFFu);
