@@ -83,12 +83,20 @@ void mps_free(mps_state* st); /* NULL-safe */
 int mps_set_stream(mps_state* st, void* cuda_stream);
 
 /* ---- gates ------------------------------------------------------------------ */
-/* Apply U (2^k x 2^k complex records, host) on ascending sites[0..k), k = 1..3.
- * k = 2 needs sites (s, s+1) or (s, s+2) (embedded into U(8)); k = 3 needs (s, s+1, s+2).
- * Validates unitarity at p bits.  Synchronous w.r.t. the handle's stream. */
+/* Apply U (2^k x 2^k complex records, host) on the k = 1..3 distinct qubits sites[0..k)
+ * in any order and at any distance (the paper's applyU on chosen qubits, §3.2;
+ * the n factor of O(g n m^3)).  sites[0] is the most significant bit of U's
+ * row/column index.  Placement (R18): U is rewritten on ascending sites; (s, s+1)
+ * and (s, s+1, s+2) are applied directly, (s, s+2) is embedded into U(8) with identity on
+ * s+1; any other placement is routed with exact SWAP gates (each a two-site update,
+ * truncating like any other) that bring the far qubits next to the lowest one and are
+ * undone afterwards.  Validates unitarity at p bits.  MPS_EINVAL: k out of range, a site
+ * out of range or repeated.  Synchronous w.r.t. the handle's stream. */
 int mps_apply_gate(mps_state* st, const void* U, const int* sites, int k);
-/* A layer of pairwise disjoint gates, executed as batched launches.
- * U[g] points to gate g's records; sites_flat holds the k[g] sites of each gate in order. */
+/* A layer of gates whose site spans [min, max] are pairwise disjoint (MPS_EOVERLAP
+ * otherwise).  Adjacent two-site gates in ascending order run as batched launches; the
+ * others one by one as mps_apply_gate.  U[g] points to gate g's records; sites_flat holds
+ * the k[g] sites of each gate in order. */
 int mps_apply_layer(mps_state* st, int n_gates, const void* const* U, const int* sites_flat, const int* k);
 
 /* ---- queries (synchronise; results on the host) ------------------------------ */

@@ -238,14 +238,22 @@ int orc_mps_apply_layer(void* hv, int ng, const uchar* const* U, const int* site
   for (int g = 0; g < ng; ++g) {
     off[g + 1] = off[g] + k[g];
     const int* s = sites_flat + off[g];
-    for (int i = 0; i < k[g]; ++i) if (s[i] < 0 || s[i] >= st.n || (i && s[i] <= s[i - 1])) return ORC_EINVAL;
-    for (int q = s[0]; q <= s[k[g] - 1]; ++q) if (used[q]++) return ORC_EOVERLAP;
+    if (k[g] < 1 || k[g] > 3) return ORC_EINVAL;
+    int lo = st.n, hi = -1;
+    for (int i = 0; i < k[g]; ++i) {
+      if (s[i] < 0 || s[i] >= st.n) return ORC_EINVAL;
+      for (int j = 0; j < i; ++j) if (s[j] == s[i]) return ORC_EINVAL;
+      lo = std::min(lo, s[i]);
+      hi = std::max(hi, s[i]);
+    }
+    for (int q = lo; q <= hi; ++q) if (used[q]++) return ORC_EOVERLAP;  // whole span
   }
-  // one-site gates and anything but plain adjacent two-site / three-site run sequentially
+  // plain adjacent two-site and consecutive three-site gates run in parallel; the rest
+  // (one-site, span-3 two-site, reordered or routed gates) sequentially through mps_apply
   std::vector<int> par;
   for (int g = 0; g < ng; ++g) {
     const int* s = sites_flat + off[g];
-    bool adj2 = k[g] == 2 && s[1] == s[0] + 1, adj3 = k[g] == 3;
+    bool adj2 = k[g] == 2 && s[1] == s[0] + 1, adj3 = k[g] == 3 && s[1] == s[0] + 1 && s[2] == s[0] + 2;
     if (adj2 || adj3) par.push_back(g);
   }
   std::vector<Update2> r2(ng);
@@ -282,14 +290,14 @@ int orc_mps_apply_layer(void* hv, int ng, const uchar* const* U, const int* site
   for (int g = 0; g < ng && !rc; ++g) {
     const int* s = sites_flat + off[g];
     const int q = s[0];
-    bool adj2 = k[g] == 2 && s[1] == s[0] + 1;
+    bool adj2 = k[g] == 2 && s[1] == s[0] + 1, adj3 = k[g] == 3 && s[1] == s[0] + 1 && s[2] == s[0] + 2;
     if (adj2) {
       Update2& u = r2[g];
       st.sweeps_total += u.sweeps;
       st.gates++;
       if (u.status) { rc = u.status; break; }
       st.G[q] = u.GL; st.G[q + 1] = u.GR; st.lam[q] = u.lam; st.m[q] = u.k;
-    } else if (k[g] == 3) {
+    } else if (adj3) {
       Update3& u = r3[g];
       st.sweeps_total += u.sweeps;
       st.gates++;

@@ -362,15 +362,8 @@ static bool is_unitary(const CVec& U, int d) {
   return true;
 }
 
-int mps_apply(Mps& st, const CVec& U, const int* sites, int k) {
-  if (k < 1 || k > 3) return ORC_EINVAL;
-  for (int i = 0; i < k; ++i) {
-    if (sites[i] < 0 || sites[i] >= st.n) return ORC_EINVAL;
-    if (i && sites[i] <= sites[i - 1]) return ORC_EINVAL;
-  }
-  const int d = 1 << k;
-  if ((int)U.size() != d * d) return ORC_EINVAL;
-  if (!is_unitary(U, d)) return ORC_ENOTUNITARY;
+// One gate on ascending sites spanning at most three consecutive sites.
+static int apply_local(Mps& st, const CVec& U, const int* sites, int k) {
   st.gates++;
   const int s = sites[0];
   if (k == 1) {
@@ -399,7 +392,7 @@ int mps_apply(Mps& st, const CVec& U, const int* sites, int k) {
   }
   CVec U8;
   if (k == 2) {
-    if (sites[1] != s + 2) return ORC_EINVAL;  // spans > 3 rejected
+    if (sites[1] != s + 2) return ORC_EINVAL;  // routed by mps_apply
     // U8[4i+2m+k, 4i'+2m'+k'] = U[2i+k, 2i'+k'] delta(m, m')
     U8.assign(64, Cplx());
     for (int x = 0; x < 8; ++x)
@@ -426,6 +419,67 @@ int mps_apply(Mps& st, const CVec& U, const int* sites, int k) {
   st.m[s] = u.k2;
   st.m[s + 1] = u.k1;
   return ORC_OK;
+}
+
+// General placement (R18; the paper's applyU on "chosen qubits", §3.2,
+// and the n factor of O(g n m^3)): a gate on k distinct qubits in any order is
+// first written on ascending sites (its index bits permuted), and a gate whose sites do not
+// fit three consecutive sites is routed with exact SWAPs: the far qubits are moved next to
+// the lowest one, the gate acts on consecutive sites, and the SWAPs are undone in reverse.
+int mps_apply(Mps& st, const CVec& U, const int* sites, int k) {
+  if (k < 1 || k > 3) return ORC_EINVAL;
+  for (int i = 0; i < k; ++i) {
+    if (sites[i] < 0 || sites[i] >= st.n) return ORC_EINVAL;
+    for (int j = 0; j < i; ++j)
+      if (sites[j] == sites[i]) return ORC_EINVAL;
+  }
+  const int d = 1 << k;
+  if ((int)U.size() != d * d) return ORC_EINVAL;
+  if (!is_unitary(U, d)) return ORC_ENOTUNITARY;
+  if (k == 1) return apply_local(st, U, sites, 1);
+  // pos[t] = index into `sites` of the t-th smallest site
+  int pos[3] = {0, 1, 2};
+  for (int a = 0; a < k; ++a)
+    for (int b = a + 1; b < k; ++b)
+      if (sites[pos[b]] < sites[pos[a]]) std::swap(pos[a], pos[b]);
+  int q[3];
+  for (int t = 0; t < k; ++t) q[t] = sites[pos[t]];
+  // W[x][y] = U[x_orig][y_orig]: bit t of x (MSB first) is bit pos[t] of x_orig
+  auto to_orig = [&](int x) {
+    int r = 0;
+    for (int t = 0; t < k; ++t)
+      if ((x >> (k - 1 - t)) & 1) r |= 1 << (k - 1 - pos[t]);
+    return r;
+  };
+  CVec W((size_t)d * d);
+  for (int x = 0; x < d; ++x)
+    for (int y = 0; y < d; ++y) W[(size_t)x * d + y] = U[(size_t)to_orig(x) * d + to_orig(y)];
+  if ((k == 2 && q[1] - q[0] <= 2) || (k == 3 && q[2] == q[0] + 2)) return apply_local(st, W, q, k);
+  // SWAP = [[1,0,0,0],[0,0,1,0],[0,1,0,0],[0,0,0,1]]
+  CVec S(16, Cplx());
+  S[0] = cone(); S[6] = cone(); S[9] = cone(); S[15] = cone();
+  int rc = ORC_OK;
+  auto swp = [&](int t) {
+    const int pr[2] = {t - 1, t};
+    return apply_local(st, S, pr, 2);
+  };
+  const int a = q[0];
+  if (k == 2) {
+    for (int t = q[1]; t > a + 1 && !rc; --t) rc = swp(t);
+    if (rc) return rc;
+    const int pr[2] = {a, a + 1};
+    if ((rc = apply_local(st, W, pr, 2))) return rc;
+    for (int t = a + 2; t <= q[1] && !rc; ++t) rc = swp(t);
+    return rc;
+  }
+  for (int t = q[1]; t > a + 1 && !rc; --t) rc = swp(t);
+  for (int t = q[2]; t > a + 2 && !rc; --t) rc = swp(t);
+  if (rc) return rc;
+  const int tr[3] = {a, a + 1, a + 2};
+  if ((rc = apply_local(st, W, tr, 3))) return rc;
+  for (int t = a + 3; t <= q[2] && !rc; ++t) rc = swp(t);
+  for (int t = a + 2; t <= q[1] && !rc; ++t) rc = swp(t);
+  return rc;
 }
 
 // c(b) = Gamma_0^{b0} lam_0 Gamma_1^{b1} lam_1 ... Gamma_{n-1}^{b_{n-1}}, left to right (Eq. 1)

@@ -42,7 +42,7 @@ int launch_update2_batch(int p, int chi, int chi_max, int batch, double thr, con
                          const uint32_t* lam_r, const uint32_t* U, const BatchOut& out, void* ws,
                          cudaStream_t st, std::vector<unsigned char>& hostdesc) {
   std::vector<Upd2Args> v = batch_args(p, chi, chi_max, batch, A, B, lam_l, lam_m, lam_r, U, out);
-  return launch_update2<T>(p, thr, v.data(), batch, ws, st, hostdesc);
+  return run_update2<T>(p, thr, v.data(), batch, ws, st, hostdesc);
 }
 
 template <class T>

@@ -78,6 +78,7 @@ struct SvdItem {
                             // block exponent eA0) and V is recovered after convergence (k_recover_v)
   int64_t* eA0;             // [1]
   int64_t* eV;              // [N] exponents of the recovered V columns
+  int a0_ready;             // 1: A0 / eA0 were written by the producer (k_build_m2), not copied here
   long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
 };
 
@@ -110,6 +111,10 @@ struct FinItem {
   int chiR_out;
   // optional M2 build (three-site): M2[(i,a),(j,b)] = Ul[(2i+j)chiL2 + a, b] * w_b
   int32_t* M2; int64_t* eM2; int M2_trans; int chiL2;
+  int32_t* M2_A0; int64_t* M2_eA0;  // optional copy of M2 at one block exponent (V recovery of SVD#2)
+  // V was recovered (eV != null): *redo = 1 when the kept spectrum spans more than 2^redo_bits
+  // (sigma_1 / sigma_k), where the recovered V is not accurate enough (R16)
+  int* redo; int redo_bits;
 };
 
 // ----------------------------------------------------------------------------
@@ -628,7 +633,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
 
   if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; }
   const bool accV = it.A0 == nullptr;
-  if (!accV) {  // keep the input (block exponent from k_mix) for the recovery of V
+  if (!accV && !it.a0_ready) {  // keep the input (block exponent from k_mix) for the recovery of V
     const size_t nw = (size_t)M * N * 2 * L;
     for (size_t t = gt; t < nw; t += GT) it.A0[t] = it.A[t];
     if (gt == 0) *it.eA0 = it.eA[0];
@@ -823,9 +828,9 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             //   Cq = c 2^(eq-eo_q), and c, sr, si unscaled (V);
             // the U warp expands them into the 24 signed slots (c_coefsrc)
             int vint = 0;
-#pragma unroll
-            for (int v = 0; v < 9; ++v) {
-              const mpf<NL>& base = (v == 0 || v == 5 || v == 6) ? c : ((v == 1 || v == 3 || v == 7) ? sr : si);
+#pragma unroll 1
+            for (int v = 0; v < 9; ++v) {  // one copy of the conversion code (i-cache)
+              const mpf<NL> base = (v == 0 || v == 5 || v == 6) ? c : ((v == 1 || v == 3 || v == 7) ? sr : si);
               const int64_t sc = v == 0 ? ep - eo[0] : v == 1 || v == 2 ? eq - eo[0] : v == 3 || v == 4 ? ep - eo[1]
                                  : v == 5 ? eq - eo[1] : 0;
               int32_t dg[L + 1];
@@ -860,8 +865,10 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             it.alpha[q] = aq;
             it.eA[p] = eo[0];
             it.eA[q] = eo[1];
-            if (mpf_is_zero(ap) || ap.neg || mpf_cmp(ap, z) <= 0) it.negl[p] = 1;
-            if (mpf_is_zero(aq) || aq.neg || mpf_cmp(aq, z) <= 0) it.negl[q] = 1;
+            // No negligible flag from these incremental norms: a column whose norm collapses
+            // by cancellation has an incremental alpha with absolute error ~2^-W alpha_old,
+            // which could mark a still-significant column negligible for good.  The flag is
+            // only set from exact norms (jac_norms at the end of the sweep).
             flag = 1 | (ints << 8);
             *(volatile int*)it.sync = 1;
             ++nrot;
@@ -1130,6 +1137,11 @@ __global__ void __launch_bounds__(NTHR) k_finalize(const FinItem<NL>* items, int
     s_kept = kept;
     s_nu = mpf_sqrt(kept);
     *it.k_out = k;
+    if (it.redo && it.eV && k > 0) {
+      const mpf<NL>& smax = sig[it.ord[0]];
+      const mpf<NL>& smin = sig[it.ord[k - 1]];
+      if (!mpf_is_zero(smin) && smax.e - smin.e > it.redo_bits) *it.redo = 1;
+    }
     const int js = it.svd_status ? *it.svd_status : 0;
     *it.status = js ? js : (k == 0 ? -4 : 0);
   }
@@ -1264,6 +1276,30 @@ __global__ void k_build_m2(const FinItem<NL>* items, const int64_t* eM2max) {
         }
         stfx<L>(it.M2, Mrows, r, ri, c, o);
       }
+    }
+    if (it.M2_A0) {  // the same entries at the block exponent eM2max (input kept for V recovery)
+      const int64_t E0 = eM2max[blockIdx.y];
+      int32_t wd0[L];
+      mpf_to_fixed<NL, L>(mpf_ldexp(w, Es - E0), 0, wd0);
+      for (int ri = 0; ri < 2; ++ri) {
+        int32_t x[L], o[L];
+        ldfx<L>(F, ld, j, ri, srow, x);
+        int64_t acc[L + 1];
+#pragma unroll
+        for (int q = 0; q <= L; ++q) acc[q] = 0;
+        tmul_acc<L>(acc, wd0, x);
+        tround<L>(acc, 0, o);
+        if (!trans) {
+          stfx<L>(it.M2_A0, Mrows, c, ri, r, o);
+        } else {
+          if (ri == 1) {
+#pragma unroll
+            for (int q = 0; q < L; ++q) o[q] = -o[q];
+          }
+          stfx<L>(it.M2_A0, Mrows, r, ri, c, o);
+        }
+      }
+      if (t == 0) *it.M2_eA0 = E0;
     }
     if (!trans) { if (r == 0) it.eM2[c] = Eout; }
     else { if (c == 0) it.eM2[r] = Eout; }

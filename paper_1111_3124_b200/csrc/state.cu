@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -82,15 +83,50 @@ void host_record(int p, int one, std::vector<uint32_t>& out) {
   if (one) out[3 + L] = 0x80000000u;  // value = 2^31 2^(32(L-1)) 2^(1-32L) = 1
 }
 
+// sites: k distinct qubits in range, any order (general placement, R18)
 int check_sites(const mps_state* s, const int* sites, int k) {
   if (!sites || k < 1 || k > 3) return MPS_EINVAL;
   for (int i = 0; i < k; ++i) {
     if (sites[i] < 0 || sites[i] >= s->n) return MPS_EINVAL;
-    if (i && sites[i] <= sites[i - 1]) return MPS_EINVAL;
+    for (int j = 0; j < i; ++j)
+      if (sites[j] == sites[i]) return MPS_EINVAL;
   }
-  if (k == 2 && sites[1] - sites[0] > 2) return MPS_EINVAL;  // spans > 3 rejected
-  if (k == 3 && sites[2] != sites[0] + 2) return MPS_EINVAL;
   return MPS_OK;
+}
+
+// Reorder a k-qubit gate given on `sites` (sites[0] = most significant bit of the gate
+// index, any order) to ascending sites: ss = sorted sites, Us[x'][y'] = U[x][y] where x' has
+// bit t (MSB first) equal to bit idx[t] of x and ss[t] = sites[idx[t]].
+void sort_gate(const unsigned char* U, size_t cb, int k, const int* sites, int* ss, std::vector<unsigned char>& Us) {
+  int idx[3] = {0, 1, 2};
+  std::sort(idx, idx + k, [&](int a, int b) { return sites[a] < sites[b]; });
+  for (int t = 0; t < k; ++t) ss[t] = sites[idx[t]];
+  const int D = 1 << k;
+  auto orig = [&](int xs) {  // sorted-order index -> original-order index
+    int x = 0;
+    for (int t = 0; t < k; ++t)
+      if ((xs >> (k - 1 - t)) & 1) x |= 1 << (k - 1 - idx[t]);
+    return x;
+  };
+  Us.resize((size_t)D * D * cb);
+  for (int xs = 0; xs < D; ++xs)
+    for (int ys = 0; ys < D; ++ys)
+      std::memcpy(Us.data() + ((size_t)xs * D + ys) * cb, U + ((size_t)orig(xs) * D + orig(ys)) * cb, cb);
+}
+
+// exact SWAP gate (4 x 4 complex records)
+void swap_gate(int p, size_t cb, std::vector<unsigned char>& S) {
+  std::vector<uint32_t> z, o;
+  host_record(p, 0, z);
+  host_record(p, 1, o);
+  S.assign(16 * cb, 0);
+  const int perm[4] = {0, 2, 1, 3};
+  for (int x = 0; x < 4; ++x)
+    for (int y = 0; y < 4; ++y) {
+      unsigned char* dst = S.data() + (size_t)(x * 4 + y) * cb;
+      std::memcpy(dst, (perm[x] == y ? o : z).data(), cb / 2);
+      std::memcpy(dst + cb / 2, z.data(), cb / 2);
+    }
 }
 
 // U(4) on (s, s+2) -> U(8) on (s, s+1, s+2) with identity on s+1
@@ -133,6 +169,20 @@ void repack_blocks(mps_state* s, uint32_t* dst, const uint32_t* src, int k, int 
   cudaMemcpy2DAsync(dst, (size_t)k * cols * s->cb, src, (size_t)ld * cols * s->cb, (size_t)k * cols * s->cb, 2,
                     cudaMemcpyDeviceToDevice, s->st);
 }
+
+// Range (bits) of a stored Schmidt vector (descending records): log2(lam_0 / lam_{m-1}).
+// Used to predict whether an update's kept spectrum will be too wide for the recovered V (R16);
+// a wrong guess is caught by the device check (FinItem::redo) and re-run.
+int lam_range_bits(mps_state* s, const uint32_t* lam, int m) {
+  if (!lam || m <= 1) return 0;
+  int64_t e0 = 0, e1 = 0;
+  cudaMemcpyAsync(&e0, lam, 8, cudaMemcpyDeviceToHost, s->st);
+  cudaMemcpyAsync(&e1, (const char*)lam + (size_t)(m - 1) * s->rb, 8, cudaMemcpyDeviceToHost, s->st);
+  cudaStreamSynchronize(s->st);
+  if (e1 == INT64_MIN) return 1 << 20;
+  return (int)std::min<int64_t>(e0 - e1, 1 << 20);
+}
+int recover_bits(const mps_state* s) { return s->ops->L <= 10 ? redo_bits<10>() : redo_bits<19>(); }
 
 struct TwoSitePlan {
   int s, ld;
@@ -285,6 +335,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
     a.sigma_out = (uint32_t*)b;
     a.out_ld = ld;
     a.k_out = s->dint + 3 * g; a.sweeps_out = s->dint + 3 * g + 1; a.status_out = s->dint + 3 * g + 2;
+    a.accumulate_v = lam_range_bits(s, s->lam[q], s->m[q]) > recover_bits(s) ? 1 : 0;
     args[g] = a;
   }
   if (3 * ng > 256) return MPS_EINVAL;
@@ -338,18 +389,35 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
   a.k1 = s->dint; a.k2 = s->dint + 1; a.sweeps = s->dint + 2; a.status = s->dint + 3;
   size_t need = s->ops->upd3_ws(a);
   if (!grow(&s->ws, &s->ws_sz, need)) return s->sticky = MPS_ENOMEM;
-  cudaMemsetAsync(s->dint, 0, 4 * sizeof(int), s->st);
+  a.redo = s->dint + 4;
   std::vector<unsigned char> hd1, hd2;
-  s->ops->upd3_s1(s->p, s->thr, a, s->ws, s->st, hd1);
-  int r1[4];
-  cudaMemcpyAsync(r1, s->dint, sizeof(r1), cudaMemcpyDeviceToHost, s->st);
-  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  // each stage recovers V unless its kept spectrum is too wide; then it is re-run with
+  // accumulated V (R16)
+  int r1[5];
+  const int rb1 = lam_range_bits(s, s->lam[q + 1], s->m[q + 1]), rb2 = lam_range_bits(s, s->lam[q], s->m[q]);
+  for (int pass = rb1 > recover_bits(s) ? 1 : 0; pass < 2; ++pass) {
+    a.accumulate_v = pass;
+    cudaMemsetAsync(s->dint, 0, 5 * sizeof(int), s->st);
+    s->ops->upd3_s1(s->p, s->thr, a, s->ws, s->st, hd1);
+    cudaMemcpyAsync(r1, s->dint, sizeof(r1), cudaMemcpyDeviceToHost, s->st);
+    if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+    if (!r1[4] || r1[3]) break;
+    if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 1 at %d: re-run with accumulated V\n", q);
+  }
   if (r1[3]) { s->sweeps_total += r1[2]; return s->sticky = r1[3]; }
   const int k1 = r1[0];
-  s->ops->upd3_s2(s->p, s->thr, a, k1, s->ws, s->st, hd2);
-  int r2[4];
-  cudaMemcpyAsync(r2, s->dint, sizeof(r2), cudaMemcpyDeviceToHost, s->st);
-  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  a.s1_accumulated = a.accumulate_v;
+  int r2[5];
+  for (int pass = rb2 > recover_bits(s) ? 1 : 0; pass < 2; ++pass) {
+    a.accumulate_v = pass;
+    cudaMemcpyAsync(s->dint + 2, &r1[2], sizeof(int), cudaMemcpyHostToDevice, s->st);  // stage-1 sweeps
+    cudaMemsetAsync(s->dint + 4, 0, sizeof(int), s->st);
+    s->ops->upd3_s2(s->p, s->thr, a, k1, s->ws, s->st, hd2);
+    cudaMemcpyAsync(r2, s->dint, sizeof(r2), cudaMemcpyDeviceToHost, s->st);
+    if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+    if (!r2[4] || r2[3]) break;
+    if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 2 at %d: re-run with accumulated V\n", q);
+  }
   s->sweeps_total += r2[2];
   s->last_sweeps = r2[2];
   s->gates++;
@@ -388,11 +456,49 @@ static int apply_one(mps_state* s, const void* U, const int* sites, int k) {
   return apply_three_site(s, q, U);
 }
 
+// General placement (R18): sort the sites (permuting U), then a gate that spans
+// more than three consecutive sites is routed with exact SWAP gates: the far qubits are
+// moved next to the first one, the gate is applied on consecutive sites, and the SWAPs are
+// undone in reverse order.  A two-qubit gate on (s, s+2) keeps the U(8) embedding.
+static int apply_general(mps_state* s, const void* U, const int* sites, int k) {
+  if (k == 1) return apply_one(s, U, sites, k);
+  int ss[3];
+  std::vector<unsigned char> Us;
+  sort_gate((const unsigned char*)U, s->cb, k, sites, ss, Us);
+  const int a = ss[0];
+  if ((k == 2 && ss[1] - a <= 2) || (k == 3 && ss[2] == a + 2)) return apply_one(s, Us.data(), ss, k);
+  std::vector<unsigned char> S;
+  swap_gate(s->p, s->cb, S);
+  auto sw = [&](int t) {  // SWAP on (t-1, t)
+    const int q[2] = {t - 1, t};
+    return apply_one(s, S.data(), q, 2);
+  };
+  int rc = MPS_OK;
+  if (k == 2) {
+    const int b = ss[1];
+    for (int t = b; t > a + 1 && !rc; --t) rc = sw(t);  // qubit b -> a+1
+    if (rc) return rc;
+    const int q[2] = {a, a + 1};
+    if ((rc = apply_one(s, Us.data(), q, 2))) return rc;
+    for (int t = a + 2; t <= b && !rc; ++t) rc = sw(t);  // back to b
+    return rc;
+  }
+  const int b = ss[1], c = ss[2];
+  for (int t = b; t > a + 1 && !rc; --t) rc = sw(t);  // qubit b -> a+1
+  for (int t = c; t > a + 2 && !rc; --t) rc = sw(t);  // qubit c -> a+2
+  if (rc) return rc;
+  const int q[3] = {a, a + 1, a + 2};
+  if ((rc = apply_one(s, Us.data(), q, 3))) return rc;
+  for (int t = a + 3; t <= c && !rc; ++t) rc = sw(t);  // a+2 -> c
+  for (int t = a + 2; t <= b && !rc; ++t) rc = sw(t);  // a+1 -> b
+  return rc;
+}
+
 int mps_apply_gate(mps_state* s, const void* U, const int* sites, int k) {
   if (!s || !U) return MPS_EINVAL;
   if (s->sticky) return s->sticky;
   if (int rc = check_sites(s, sites, k)) return rc;
-  return apply_one(s, U, sites, k);
+  return apply_general(s, U, sites, k);
 }
 
 int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites_flat, const int* k) {
@@ -402,8 +508,9 @@ int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites
   int o = 0;
   for (int g = 0; g < ng; ++g) {
     if (int rc = check_sites(s, sites_flat + o, k[g])) return rc;
-    const int lo = sites_flat[o], hi = sites_flat[o + k[g] - 1];
-    for (int q = lo; q <= hi; ++q)
+    const int lo = *std::min_element(sites_flat + o, sites_flat + o + k[g]);
+    const int hi = *std::max_element(sites_flat + o, sites_flat + o + k[g]);
+    for (int q = lo; q <= hi; ++q)  // the whole span (routed gates swap through it)
       if (used[q]++) return MPS_EOVERLAP;
     o += k[g];
   }
@@ -426,7 +533,7 @@ int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites
   o = 0;
   for (int g = 0; g < ng; ++g) {
     if (!(k[g] == 2 && sites_flat[o + 1] == sites_flat[o] + 1))
-      if (int rc = apply_one(s, U[g], sites_flat + o, k[g])) return rc;
+      if (int rc = apply_general(s, U[g], sites_flat + o, k[g])) return rc;
     o += k[g];
   }
   return MPS_OK;

@@ -136,7 +136,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     int* syncp = (int*)align_up((size_t)(ord + Nj) + 64, 16);
     mpf<NL>* zbuf = (mpf<NL>*)(syncp + 16);
     hm[b] = MatItem{dR + (size_t)b * M * N * 2 * RBr, M, N, trans ? 1 : 0, A, eA, eblk};
-    SvdItem<NL> si;
+    SvdItem<NL> si = {};
     si.M = Mj; si.N = Nj; si.A = A; si.eA = eA; si.V = V; si.alpha = alpha; si.gam = gam; si.coef = coef;
     si.dbg = ddbg ? ddbg + 64 * b : nullptr;
     si.rot = rot; si.negl = negl; si.status = ip; si.sweeps = dsweeps + b; si.rotations = rots;

@@ -17,7 +17,7 @@ template void run_debug_mpf<Tier280>(int, int, int, const uint32_t*, const uint3
 
 const TierOps tier280_ops = {
     Tier280::L, Tier280::NL,
-    &upd2_workspace<Tier280>, &launch_update2<Tier280>,
+    &upd2_workspace<Tier280>, &run_update2<Tier280>,
     &upd3_workspace<Tier280>, &launch_update3_stage1<Tier280>, &launch_update3_stage2<Tier280>,
     &run_onesite<Tier280>, &amp_scratch_bytes<Tier280>, &run_amplitudes<Tier280>, &run_unitary<Tier280>,
     &transfer_scratch_bytes<Tier280>, &run_rdo<Tier280>, &run_transfer<Tier280>,

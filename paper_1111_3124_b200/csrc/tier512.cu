@@ -17,7 +17,7 @@ template void run_debug_mpf<Tier512>(int, int, int, const uint32_t*, const uint3
 
 const TierOps tier512_ops = {
     Tier512::L, Tier512::NL,
-    &upd2_workspace<Tier512>, &launch_update2<Tier512>,
+    &upd2_workspace<Tier512>, &run_update2<Tier512>,
     &upd3_workspace<Tier512>, &launch_update3_stage1<Tier512>, &launch_update3_stage2<Tier512>,
     &run_onesite<Tier512>, &amp_scratch_bytes<Tier512>, &run_amplitudes<Tier512>, &run_unitary<Tier512>,
     &transfer_scratch_bytes<Tier512>, &run_rdo<Tier512>, &run_transfer<Tier512>,

@@ -75,6 +75,16 @@ inline size_t mat_bytes(int rows, int cols, int L) { return align_up((size_t)row
 
 // MPS_JACOBI_PHASES=1 (debug): per-phase cycle counters of the batched Jacobi, printed to
 // stderr after each launch_update2 (D, R, U, norms, init, total; summed over CTAs).
+// MPS_ACCUMULATE_V=1 (debug): accumulate V in every SVD instead of recovering it (R16).
+inline bool force_accumulate_v() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_ACCUMULATE_V");
+    on = e && atoi(e) ? 1 : 0;
+  }
+  return on != 0;
+}
+
 inline unsigned long long* phase_dbg() {
   static unsigned long long* d = nullptr;
   static int on = -1;
@@ -97,7 +107,17 @@ struct Upd2Args {
   int out_ld;
   int *k_out, *sweeps_out, *status_out;               // device ints (may be null)
   uint32_t* theta_dbg;                                // column-major Theta' records or null
+  int accumulate_v;                                   // 1: accumulate V (else recover it, R16)
 };
+
+// kept-spectrum range (bits) above which a recovered V is replaced by an accumulated one:
+// the recovered V_b carries ~2^-W (sigma_1 / sigma_b)^2 (A's column b has absolute error
+// ~2^-W sigma_1 after the rotations, divided by sigma_b^2), and its loss of orthonormality
+// propagates through later updates (measured: configs[3] amplitudes 2^13 worse than with
+// accumulated V for kept ranges < 2^12).  At 280 bits (W = p, no guard digits) the budget is
+// small: R = 4 (<= 2^8 amplification); at 512 bits (20 guard bits) R = 16.
+template <int L>
+constexpr int redo_bits() { return L <= 10 ? 4 : 16; }
 
 template <int L, int NL>
 inline size_t upd2_item_bytes(const Upd2Args& a) {
@@ -112,7 +132,7 @@ template <class T>
 size_t upd2_workspace(const Upd2Args* a, int n) {
   constexpr int L = T::L, NL = T::NL;
   size_t s = align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
-             align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + 4096;
+             align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(4 * (size_t)n) + 4096;
   for (int i = 0; i < n; ++i) s += align_up(upd2_item_bytes<L, NL>(a[i]));
   return s;
 }
@@ -128,6 +148,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   const size_t d_prep = 0, d_gemm = align_up(sizeof(PrepItem) * 2 * n),
                d_mix = d_gemm + align_up(sizeof(GemmItem) * n), d_svd = d_mix + align_up(sizeof(MixItem) * n),
                d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_end = d_fin + align_up(sizeof(FinItem<NL>) * n);
+  int* redo = (int*)(base + d_end);  // [n] flags (run_update2)
   hd.assign(d_end, 0);
   PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
   GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
@@ -135,7 +156,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   const mpf<NL> thr_m = mpf_host_from_double<NL>(thr);
-  char* items = base + d_end;
+  char* items = base + d_end + align_up(4 * (size_t)n);
   int maxMN = 0, maxLR = 0, maxOut = 0;
   bool any_dbg = false;
   std::vector<int64_t*> einit;
@@ -167,12 +188,13 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
     hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
     hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, Af, S.eA, M, N};
-    SvdItem<NL> si;
+    SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
-    si.A0 = A0f; si.eA0 = S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
+    const bool recover = !force_accumulate_v() && !g.accumulate_v;
+    si.A0 = recover ? A0f : nullptr; si.eA0 = S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -180,7 +202,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     fi.chi_max = g.chi_max; fi.thr = thr_m; fi.ord = S.ord; fi.inv_sig = S.inv_sig; fi.lam = S.lam;
     fi.k_out = g.k_out ? g.k_out : S.k; fi.status = g.status_out ? g.status_out : S.fstatus;
     fi.svd_status = S.status;
-    fi.eV = eV;
+    fi.eV = recover ? eV : nullptr;
+    fi.redo = recover ? redo + b : nullptr; fi.redo_bits = redo_bits<L>();
     fi.sigma_rec = g.sigma_out; fi.nsig = N; fi.lam_rec = g.lam_out;
     fi.GL = g.GL_out; fi.GL_ld = g.out_ld; fi.lamL = g.lamL; fi.chiL_out = chiL;
     fi.GR = g.GR_out; fi.GR_ld = g.out_ld; fi.lamR = g.lamR; fi.chiR_out = chiR;
@@ -191,6 +214,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     any_dbg |= g.theta_dbg != nullptr;
   }
   cudaMemcpyAsync(base, hd.data(), d_end, cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(redo, 0, 4 * (size_t)n, st);
   int nl = 0;
   prof_mark(PROF_CONTRACT, 1, st);
   k_init_prep<<<(2 * n + 255) / 256, 256, 0, st>>>((const PrepItem*)(base + d_prep), 2 * n); ++nl;
@@ -254,6 +278,35 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   return nl;
 }
 
+// launch_update2, then (synchronously) re-run with accumulated V every item whose kept
+// spectrum was too wide for the recovered V (FinItem::redo).  Returns the launch count.
+template <class T>
+int run_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaStream_t st,
+                std::vector<unsigned char>& hd) {
+  constexpr int NL = T::NL;
+  int nl = launch_update2<T>(p, thr, a, n, ws, st, hd);
+  if (force_accumulate_v()) return nl;
+  const size_t d_end = align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) +
+                       align_up(sizeof(MixItem) * n) + align_up(sizeof(SvdItem<NL>) * n) +
+                       align_up(sizeof(FinItem<NL>) * n);
+  std::vector<int> redo(n, 0);
+  cudaMemcpyAsync(redo.data(), (char*)ws + d_end, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  std::vector<Upd2Args> sub;
+  for (int b = 0; b < n; ++b)
+    if (redo[b]) {
+      Upd2Args c = a[b];
+      c.accumulate_v = 1;
+      sub.push_back(c);
+    }
+  if (!sub.empty()) {
+    std::vector<unsigned char> hd2;
+    nl += launch_update2<T>(p, thr, sub.data(), (int)sub.size(), ws, st, hd2);
+    cudaStreamSynchronize(st);
+  }
+  return nl;
+}
+
 // ---------------------------------------------------------------------------- three-site
 // Theta (4chiL x 2chiR) = U8 (lamL G0 lam1 G1 lam2 G2 lamR); SVD#1 splits off site s+2
 // (lambda_{s+1}', Gamma_{s+2}'), M2 = X1 lambda' reshaped (2chiL x 2k1), SVD#2 gives
@@ -265,6 +318,9 @@ struct Upd3Args {
   uint32_t *G0_out, *G1_out, *G2_out, *lam1_out, *lam2_out;      // lam1 = lambda_s' (k2), lam2 = lambda_{s+1}' (k1)
   int ld;
   int *k1, *k2, *sweeps, *status;  // device
+  int* redo;                        // device flag (one int) or null: recovered V too inaccurate
+  int accumulate_v;                 // 1: accumulate V in this stage (the re-run)
+  int s1_accumulated;               // stage 2: stage 1 ran with accumulated V (its V exponent is 1)
 };
 
 // workspace of one three-site update (bounded by the capacities: k1 <= min(chi_max, 2chiR, 4chiL))
@@ -277,8 +333,34 @@ inline size_t upd3_item_bytes(const Upd3Args& a) {
              mat_bytes(2 * a.chiL, 2 * a.chi2, L) + mat_bytes(4 * a.chiL, a.chi2, L) + mat_bytes(4 * a.chiL, 2 * a.chiR, L) +
              mat_bytes(M1, N1, L) + mat_bytes(N1, N1, L) + mat_bytes(M2 + 2, N2 + 2, L) + mat_bytes(N2 + 2, N2 + 2, L) +
              SvdScratch<L, NL>::bytes(N1) + SvdScratch<L, NL>::bytes(N2 + 2) + 1024;
+  // V recovery (R16): the inputs of both SVDs and the per-column exponents of V
+  s += mat_bytes(M1, N1, L) + mat_bytes(M2 + 2, N2 + 2, L) + align_up(8 * (size_t)N1) + align_up(8 * (size_t)(N2 + 2)) +
+       256;
   return s;
 }
+
+// V-recovery buffers of a three-site update, after everything stage 1 and stage 2 carve
+template <int L, int NL>
+struct Upd3Rec {
+  int32_t *A0a, *A0b;
+  int64_t *eVa, *eVb, *eA0a, *eA0b;
+  Upd3Rec(char* base_end, const Upd3Args& a) {
+    const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
+    const int k1max = std::min(a.chi_max, N1);
+    const int M2 = std::max(2 * a.chiL, 2 * k1max), N2 = std::min(2 * a.chiL, 2 * k1max);
+    char* q = base_end + mat_bytes(2 * a.chiL, a.chi1, L) + mat_bytes(a.chi1, 2 * a.chi2, L) +
+              mat_bytes(a.chi2, 2 * a.chiR, L) + mat_bytes(2 * a.chiL, 2 * a.chi2, L) +
+              mat_bytes(4 * a.chiL, a.chi2, L) + mat_bytes(4 * a.chiL, 2 * a.chiR, L) + mat_bytes(M1, N1, L) +
+              mat_bytes(N1, N1, L) + SvdScratch<L, NL>::bytes(N1) + mat_bytes(M2 + 2, N2 + 2, L) +
+              mat_bytes(N2 + 2, N2 + 2, L) + SvdScratch<L, NL>::bytes(N2 + 2);
+    A0a = (int32_t*)q; q += mat_bytes(M1, N1, L);
+    A0b = (int32_t*)q; q += mat_bytes(M2 + 2, N2 + 2, L);
+    eVa = (int64_t*)q; q += align_up(8 * (size_t)N1);
+    eVb = (int64_t*)q; q += align_up(8 * (size_t)(N2 + 2));
+    eA0a = (int64_t*)q;
+    eA0b = eA0a + 1;
+  }
+};
 
 // T (2chiL x 2chi2) -> T' (4chiL x chi2): T'[(2i+j)chiL + a, g] = T[(i chiL + a), (j chi2 + g)]
 template <int L>
@@ -336,10 +418,13 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
   hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, A1, S1.eA, M1, N1};
   SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
-  SvdItem<NL> si;
+  SvdItem<NL> si = {};
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
   si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
-  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr; si.A0 = nullptr; si.eA0 = nullptr; si.eV = nullptr; si.evals = S1.rots + 1;
+  const Upd3Rec<L, NL> rec(base + d_end, a);
+  si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr;
+  const bool recover = !force_accumulate_v() && !a.accumulate_v;
+  si.A0 = recover ? rec.A0a : nullptr; si.eA0 = rec.eA0a; si.eV = rec.eVa; si.evals = S1.rots + 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   FinItem<NL> fi;
@@ -351,6 +436,8 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   fi.lam_rec = a.lam2_out; fi.GL = nullptr;
   fi.GR = a.G2_out; fi.GR_ld = a.ld; fi.lamR = a.lamR; fi.chiR_out = a.chiR;
   fi.chiL2 = a.chiL;
+  fi.eV = recover ? rec.eVa : nullptr;
+  fi.redo = recover ? a.redo : nullptr; fi.redo_bits = redo_bits<L>();
   hf[0] = fi;
   cudaMemcpyAsync(base, hd.data(), d_end, cudaMemcpyHostToDevice, st);
   int nl = 0;
@@ -367,6 +454,8 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   k_gemm<L><<<g2, 128, 0, st>>>((const GemmItem*)(base + d_gemm) + 1); ++nl;
   k_mix<L, NL><<<g2, 128, 64 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
   launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), 1, jacobi_cluster_size(1, N1), st); ++nl;
+  k_recover_v<L, NL><<<dim3(std::max(1, std::min(64, (N1 * N1 + 127) / 128)), 1), 128, 0, st>>>(
+      (const SvdItem<NL>*)(base + d_svd)); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N1, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * a.chiR * N1 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
@@ -413,13 +502,19 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
     fi.V = (const int32_t*)((const char*)A1 + mat_bytes(M1, N1, L));
     fi.alpha = S1.alpha; fi.ord = S1.ord; fi.inv_sig = S1.inv_sig; fi.lam = S1.lam; fi.k_out = a.k1;
     fi.status = a.status; fi.chiL2 = a.chiL; fi.M2 = A2; fi.eM2 = S2.eA; fi.M2_trans = trans2 ? 1 : 0;
+    const Upd3Rec<L, NL> r1(base + d_end, a);
+    fi.eV = (force_accumulate_v() || a.s1_accumulated) ? nullptr : r1.eVa;  // M2 from V1 when trans
+    fi.M2_A0 = r1.A0b; fi.M2_eA0 = r1.eA0b;
     hf1[0] = fi;
   }
   SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd2);
-  SvdItem<NL> si;
+  SvdItem<NL> si = {};
   si.M = M2; si.N = N2; si.A = A2; si.eA = S2.eA; si.V = V2; si.alpha = S2.alpha; si.gam = S2.gam;
   si.coef = S2.coef; si.dbg = nullptr; si.rot = S2.rot; si.negl = S2.negl; si.status = S2.status;
-  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr; si.A0 = nullptr; si.eA0 = nullptr; si.eV = nullptr; si.evals = S2.rots + 1;
+  const Upd3Rec<L, NL> rec(base + d_end, a);
+  si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr;
+  const bool recover = !force_accumulate_v() && !a.accumulate_v;
+  si.A0 = recover ? rec.A0b : nullptr; si.eA0 = rec.eA0b; si.eV = rec.eVb; si.evals = S2.rots + 1; si.a0_ready = 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
   FinItem<NL> fi;
@@ -431,6 +526,8 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   fi.lam_rec = a.lam1_out;
   fi.GL = a.G0_out; fi.GL_ld = a.ld; fi.lamL = a.lamL; fi.chiL_out = a.chiL;
   fi.GR = a.G1_out; fi.GR_ld = a.ld; fi.lamR = a.lam2_out; fi.chiR_out = k1;
+  fi.eV = recover ? rec.eVb : nullptr;
+  fi.redo = recover ? a.redo : nullptr; fi.redo_bits = redo_bits<L>();
   hf[0] = fi;
   cudaMemcpyAsync(base + d_fin, hd.data() + d_fin, d_end - d_fin, cudaMemcpyHostToDevice, st);
   int nl = 0;
@@ -438,6 +535,8 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   dim3 gb(std::max(1, std::min(64, (rows2 * cols2 + 255) / 256)), 1);
   k_build_m2<L, NL><<<gb, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
   launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd2), 1, jacobi_cluster_size(1, N2), st); ++nl;
+  k_recover_v<L, NL><<<dim3(std::max(1, std::min(64, (N2 * N2 + 127) / 128)), 1), 128, 0, st>>>(
+      (const SvdItem<NL>*)(base + d_svd2)); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N2, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;
   dim3 gs(std::max(1, std::min(64, (2 * std::max(a.chiL, k1) * N2 + 255) / 256)), 1);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin2), RBr, p); ++nl;

@@ -202,7 +202,10 @@ def test_error_contract():
         st.apply(bad, [1])
     assert e.value.rc == -2
     with pytest.raises(m.MpsError) as e:
-        st.apply(gen.const_gate(p, "CNOT"), [0, 3])
+        st.apply(gen.const_gate(p, "CNOT"), [2, 2])  # repeated qubit
+    assert e.value.rc == -1
+    with pytest.raises(m.MpsError) as e:
+        st.apply(gen.const_gate(p, "CNOT"), [0, 4])  # out of range
     assert e.value.rc == -1
     with pytest.raises(m.MpsError) as e:
         st.apply_layer([(gen.const_gate(p, "CNOT"), (0, 1)), (gen.const_gate(p, "CNOT"), (1, 2))])
@@ -245,3 +248,29 @@ def test_rdo_vs_dense_partial_trace():
             tr = mpmath.fsum(want[i][i] for i in range(1 << len(keep)))
             err = max(abs(got[r][c] - want[r][c] / tr) for r in range(1 << len(keep)) for c in range(1 << len(keep)))
         assert err <= tau(p), (keep, err)
+
+
+@pytest.mark.parametrize("p", [280, 512])
+def test_general_placement_vs_oracle_and_dense(p):
+    """Gates on chosen qubits in any order / at any distance (R18: reordering + exact SWAP
+    routing) on the GPU MPS: equal to the dense simulator and to the oracle MPS, whose
+    routing is implemented independently."""
+    from tests.test_oracle_tebd import routed_circuit
+    n = 7
+    gates = routed_circuit(p, n, 95)
+    st = M().MPS(n, p, 128, 2.0 ** -(p // 2))
+    om = oracle.OracleMPS(n, p, 128, 2.0 ** -(p // 2))
+    for U, s in gates:
+        st.apply(U, s)
+        om.apply(U, s)
+    assert st.bond_dims() == om.bond_dims()
+    want = dense_of(gates, n, p)
+    assert normwise_err(cplx(st.to_dense()), want) <= tau(p)
+    assert normwise_err(cplx(st.to_dense()), cplx(om.to_dense())) <= tau(p)
+    # the same gates as disjoint layers (routed gates run one by one inside the layer)
+    st2 = M().MPS(n, p, 128, 2.0 ** -(p // 2))
+    layers = [[g] for g in gates[n:]]
+    st2.apply_layer(gates[:n])
+    for l in layers:
+        st2.apply_layer(l)
+    assert normwise_err(cplx(st2.to_dense()), want) <= tau(p)

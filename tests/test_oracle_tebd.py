@@ -236,7 +236,54 @@ def test_errors():
         m.apply(bad, [1])
     assert e.value.rc == -2
     with pytest.raises(oracle.OracleError) as e:
-        m.apply(gen.const_gate(p, "CNOT"), [0, 3])  # span 4 rejected
+        m.apply(gen.const_gate(p, "CNOT"), [2, 2])  # repeated qubit
+    assert e.value.rc == -1
+    with pytest.raises(oracle.OracleError) as e:
+        m.apply(gen.const_gate(p, "CNOT"), [0, 4])  # out of range
     assert e.value.rc == -1
     with pytest.raises(oracle.OracleError):
         oracle.OracleMPS(0, p, 4, 1e-10)
+
+
+# ---------------------------------------------------------------- general placement (R18)
+def routed_circuit(p, n, seed):
+    """Gates on chosen qubits in any order and at any distance (P:331-333 applyU on chosen
+    qubits; the n factor of O(g n m^3)): reversed pairs, spans 3..n, U(8) on
+    scattered and permuted triples, mixed with local gates."""
+    g = []
+    g += [(gen.haar_unitary(p, 2, seed, 0, q), (q,)) for q in range(n)]
+    g += [(gen.haar_unitary(p, 4, seed, 1, 0), (3, 0))]          # reversed, span 4
+    g += [(gen.haar_unitary(p, 4, seed, 2, 0), (1, n - 1))]      # long range
+    g += [(gen.haar_unitary(p, 4, seed, 3, 0), (5, 4))]          # reversed adjacent
+    g += [(gen.haar_unitary(p, 4, seed, 4, 0), (4, 2))]          # reversed span 3 (U(8) embedding)
+    g += [(gen.haar_unitary(p, 8, seed, 5, 0), (0, 3, n - 1))]   # scattered triple
+    g += [(gen.haar_unitary(p, 8, seed, 6, 0), (4, 1, 2))]       # permuted, not consecutive
+    g += [(gen.haar_unitary(p, 8, seed, 7, 0), (3, 2, 4))]       # permuted consecutive
+    g += [(gen.const_gate(p, "CNOT"), (n - 1, 1))]
+    return g
+
+
+@pytest.mark.parametrize("p", [256, 512])
+def test_general_placement_vs_dense(p):
+    """Routed / reordered gates on the oracle MPS (no truncation) equal the dense simulator,
+    which applies every gate directly on its qubits (a different code path)."""
+    n = 7
+    gates = routed_circuit(p, n, 93)
+    m = mps_of(gates, n, p, 128, 2.0 ** -(p // 2))
+    assert normwise_err(cplx(m.to_dense()), dense_of(gates, n, p)) <= tau(p)
+
+
+def test_general_placement_reversed_equals_permuted():
+    """U on (b, a) equals (SWAP U SWAP) on (a, b), up to rounding."""
+    p, n = 256, 4
+    U = gen.haar_unitary(p, 4, 94, 0, 0)
+    perm = [0, 2, 1, 3]  # W = SWAP U SWAP (exact entry permutation)
+    W = np.empty_like(U)
+    for x in range(4):
+        for y in range(4):
+            W[2 * (4 * x + y)] = U[2 * (4 * perm[x] + perm[y])]
+            W[2 * (4 * x + y) + 1] = U[2 * (4 * perm[x] + perm[y]) + 1]
+    pre = [(gen.haar_unitary(p, 2, 94, 1, q), (q,)) for q in range(n)]
+    a = mps_of(pre + [(U, (2, 0))], n, p, 16, 2.0 ** -64)
+    b = mps_of(pre + [(W, (0, 2))], n, p, 16, 2.0 ** -64)
+    assert normwise_err(cplx(a.to_dense()), cplx(b.to_dense())) <= tau(p)
