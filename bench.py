@@ -164,12 +164,20 @@ def run_reference(args, rank, world):
               f"{args.oracle_pairs} Jacobi pair evaluations, extrapolated to {S} sweeps x N(N-1)/2 pairs")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gate_updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32-limb fixed/float p=280",
-            "data": "synthetic", "config": {"workload": f"configs[1] chi={args.chi} {args.prec}-bit (bounded oracle sample)",
-                                          "chi": args.chi, "prec_bits": args.prec},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": f"u64-limb bignum (oracle), p={args.prec}",
+            "data": "synthetic", "config": workload_config(args.batch, args.chi, args.prec, args.distinct, world),
             "cpu_baseline": {"value": value, "unit": "gate_updates/s", "cores": nthreads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "gate_updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(batch, chi, p, nd, world):
+    """The config both arms report (the reference arm times a bounded sample of it)."""
+    return {"workload": f"configs[1]: batch of {batch} Theta (2chi x 2chi), chi={chi}, {p}-bit, "
+                        f"contraction+Jacobi SVD+truncate+split; {nd} distinct seeded items tiled",
+            "chi": chi, "prec_bits": p, "batch_per_gpu": batch,
+            "l2": "inputs+workspace >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world}"}
 
 
 def main():
@@ -303,10 +311,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p=280",
             "data": "synthetic",
-            "config": {"workload": f"configs[1]: batch of {batch} Theta (2chi x 2chi), chi={chi}, {p}-bit, "
-                                   f"contraction+Jacobi SVD+truncate+split; {nd} distinct seeded items tiled",
-                       "chi": chi, "prec_bits": p, "batch_per_gpu": batch, "sweeps_mean": float(np.mean(sweeps)),
-                       "l2": "inputs+workspace >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world}"},
+            "config": dict(workload_config(batch, chi, p, nd, world), sweeps_mean=float(np.mean(sweeps))),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "IMAD.WIDE/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_jacobi", "peak_source": "MEASURED_INT_PEAKS.json imad_wide_s32_per_s (IMAD.WIDE)",
