@@ -22,6 +22,12 @@ namespace mpsb {
 constexpr int NTHR = 256;  // threads per CTA of the per-item kernels
 constexpr int NWARP = NTHR / 32;
 constexpr int MAX_SWEEPS = JACOBI_MAX_SWEEPS;
+#ifndef JACOBI_STAGES_280
+#define JACOBI_STAGES_280 2
+#endif
+#ifndef JACOBI_CTAS_280
+#define JACOBI_CTAS_280 2
+#endif
 
 // ----------------------------------------------------------------------------
 // item descriptors
@@ -606,12 +612,22 @@ __constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {0, 1, 2}, {1, 0, 3}};
 __constant__ int8_t c_coefsrc[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 3, 4 | 16, 5, 3, 4, 5,
                                      6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 7, 8 | 16, 6, 7, 8, 6};
 
+// Staging buffers per warp and resident CTAs per SM of k_jacobi.  280 bits: double
+// buffering, 2 CTAs (16 warps, 128 registers).  The alternative of one buffer and 3 CTAs
+// (24 warps, 80 registers with spills; -DJACOBI_STAGES_280=1 -DJACOBI_CTAS_280=3) measured
+// 33.9 vs 34.3 updates/s per full wave and fits 1024 items worse (2.3 waves).  512 bits:
+// double buffering, 1 CTA.
+template <int L>
+__host__ __device__ constexpr int jacobi_stages() { return L <= 10 ? JACOBI_STAGES_280 : 2; }
+template <int L>
+__host__ __device__ constexpr int jacobi_min_ctas() { return L <= 10 ? JACOBI_CTAS_280 : 1; }
+
 // C CTAs (a thread-block cluster when C > 1) cooperate on one matrix: pairs, columns and
 // rows are distributed over all C*NWARP warps, column state lives in global memory, and
 // the phases are separated by cluster barriers.  The arithmetic of every pair is the same
 // whatever C is, so results are bitwise independent of C.
 template <int L, int NL>
-__global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdItem<NL>* items, int C) {
+__global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const SvdItem<NL>* items, int C) {
   namespace cg = cooperative_groups;
   const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
   const SvdItem<NL> it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
@@ -626,9 +642,11 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
   const int W = 28 * L;
   constexpr int CW = L + 1;              // words per coefficient vector
   constexpr int STAGE = 4 * L * 32;      // words per staging buffer
+  constexpr int JST = jacobi_stages<L>();
   extern __shared__ int32_t jsm[];
-  int32_t* wbuf = jsm + warp * (2 * STAGE + 24 * CW);  // per-warp: 2 stage buffers + 24 coefficients
-  int32_t* wcoef = wbuf + 2 * STAGE;
+  int32_t* wbuf = jsm + warp * (JST * STAGE + 24 * CW);  // per warp: JST stage buffers + 24 coefficients
+  int32_t* wcoef = wbuf + JST * STAGE;
+  static_assert(2 * (L + 2) * 32 * 8 <= (JST * STAGE + 24 * CW) * 4, "phase-D column sums must fit the warp's buffers");
   __shared__ mpf<NL> s_red[1];
 
   if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; }
@@ -704,7 +722,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
         stage_rows<L>(wbuf, it.A, M, p, q, 0, M, lane);
         cp_commit();
         for (int ch = 0; ch < nchA; ++ch) {
-          if (ch + 1 < nchA) {
+          if (JST == 2 && ch + 1 < nchA) {
             stage_rows<L>(wbuf + ((ch + 1) & 1) * STAGE, it.A, M, p, q, (ch + 1) * 32, M, lane);
             cp_commit();
             cp_wait<1>();
@@ -712,7 +730,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
             cp_wait<0>();
           }
           __syncwarp();
-          const int32_t* b = wbuf + (ch & 1) * STAGE;
+          const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
           int32_t xa[L], xb[L];
           // rows past M were zero-filled: their products vanish
 #pragma unroll
@@ -729,6 +747,10 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
           tmul_sub2<L>(gi, xa, xb);  // - xip xrq
           if ((ch & 7) == 7) { tnorm2<L>(gr); tnorm2<L>(gi); }
           __syncwarp();
+          if (JST == 1 && ch + 1 < nchA) {
+            stage_rows<L>(wbuf, it.A, M, p, q, (ch + 1) * 32, M, lane);
+            cp_commit();
+          }
         }
         tnorm2<L>(gr);
         tnorm2<L>(gi);
@@ -899,7 +921,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
           stage_rows<L>(wbuf, F, rows, p, q, 0, rows, lane);
           cp_commit();
           for (int ch = 0; ch < nch; ++ch) {
-            if (ch + 1 < nch) {
+            if (JST == 2 && ch + 1 < nch) {
               stage_rows<L>(wbuf + ((ch + 1) & 1) * STAGE, F, rows, p, q, (ch + 1) * 32, rows, lane);
               cp_commit();
               cp_wait<1>();
@@ -907,7 +929,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
               cp_wait<0>();
             }
             __syncwarp();
-            const int32_t* b = wbuf + (ch & 1) * STAGE;
+            const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
             const int r = ch * 32 + lane;
 #pragma unroll 1
             for (int o = 0; o < 4; ++o) {
@@ -931,6 +953,10 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
               if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
             }
             __syncwarp();
+            if (JST == 1 && ch + 1 < nch) {
+              stage_rows<L>(wbuf, F, rows, p, q, (ch + 1) * 32, rows, lane);
+              cp_commit();
+            }
           }
         }
       }
@@ -958,7 +984,7 @@ __global__ void __launch_bounds__(NTHR, (L <= 10 ? 2 : 1)) k_jacobi(const SvdIte
 }
 
 template <int L>
-constexpr size_t jacobi_smem_bytes() { return (size_t)NWARP * (2 * 4 * L * 32 + 24 * (L + 1)) * 4; }
+constexpr size_t jacobi_smem_bytes() { return (size_t)NWARP * (jacobi_stages<L>() * 4 * L * 32 + 24 * (L + 1)) * 4; }
 
 // Launch n items with C CTAs each (a cluster of C when C > 1).
 template <int L, int NL>
