@@ -84,7 +84,8 @@ struct SvdItem {
                             // block exponent eA0) and V is recovered after convergence (k_recover_v)
   int64_t* eA0;             // [1]
   int64_t* eV;              // [N] exponents of the recovered V columns
-  int a0_ready;             // 1: A0 / eA0 were written by the producer (k_build_m2), not copied here
+  int a0_ready;             // 1: A0 / eA0 were written by the producer (k_build_m2, k_mix), not copied here
+  int v_preset;             // accumulating: V already holds the starting basis (preconditioner X), not I
   long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
 };
 
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
     if (gt == 0) *it.eA0 = it.eA[0];
   }
   // V = I (exponent 1: 1 = 2^27 * 2^(28(L-1)) * 2^(1 - 28L))
-  for (int t = gt; accV && t < N * N; t += GT) {
+  for (int t = gt; accV && !it.v_preset && t < N * N; t += GT) {
     const int r = t % N, c = t / N;
     int32_t x[L], z0[L];
 #pragma unroll

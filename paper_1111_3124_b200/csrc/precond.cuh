@@ -1,0 +1,319 @@
+// Mixed-precision preconditioning of the one-sided Jacobi SVD (R19).
+//
+//   Theta' (fixed point, p bits)  --k_fx_to_d-->  Theta_d (binary64, scaled by 2^-e)
+//   one-sided Jacobi in binary64 on Theta_d     -->  V_d  (unitary to ~1e-14)
+//   X_0 = V_d (exact digits), Newton-Schulz in fixed point:
+//       D_k = I - X_k^H X_k,   X_{k+1} = X_k + X_k D_k / 2        (quadratic: 2^-45 -> 2^-90 -> ...)
+//   A_1 = Theta' X   (exactly unitary X to the working precision)
+//   the p-bit Jacobi (k_jacobi) then starts from columns orthogonal to ~1e-14 and needs
+//   ~4 sweeps instead of ~16.  V is recovered from Theta' as before (R16), or accumulated
+//   starting from X (V = X W).
+// The binary64 stage only chooses the starting basis; every p-bit quantity comes from exact
+// fixed-point arithmetic, so the result is the p-bit SVD of Theta' (the oracle's, to tau).
+#pragma once
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace mpsb {
+
+struct PreItem {
+  int M, N;
+  const int32_t* A0; const int64_t* eA0;  // Theta' (M x N, block exponent)
+  double2* Ad;                            // [N][M] column-major complex binary64
+  double2* Vd;                            // [N][N]
+  unsigned long long* rowmax;             // max_r sum_c |Ad(r,c)|^2 as ordered bits (1)
+  int* sweeps_d;                          // binary64 sweeps (1)
+  int32_t* X;                             // N x N fixed, exponent 1 (output of k_d_to_fx)
+  int64_t* eOne;                          // [2] = {1, 0}: exponents of X and of D/2
+  int64_t* eA1;                           // exponent chosen for A_1 = Theta' X (1)
+};
+
+static __global__ void k_pre_init(const PreItem* items, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < n) *items[b].rowmax = 0ull;
+}
+
+// binary64 value of an L-digit fixed number times 2^-e (its top three digits)
+template <int L>
+__device__ __forceinline__ double fx_top_double(const int32_t* p, size_t ld) {
+  const double t = (double)p[(size_t)(L - 1) * ld] * 72057594037927936.0 +  // 2^56
+                   (double)p[(size_t)(L - 2) * ld] * 268435456.0 + (double)p[(size_t)(L - 3) * ld];
+  return ldexp(t, -84);  // value * 2^-e = sum d_k 2^(28k - 28L)
+}
+
+template <int L>
+__global__ void k_fx_to_d(const PreItem* items) {
+  const PreItem it = items[blockIdx.y];
+  const int M = it.M, N = it.N;
+  double rmax = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < N; ++c) {
+      const int32_t* pr = it.A0 + ((size_t)(c * 2 + 0) * L) * M + r;
+      const int32_t* pi = it.A0 + ((size_t)(c * 2 + 1) * L) * M + r;
+      const double2 v = make_double2(fx_top_double<L>(pr, M), fx_top_double<L>(pi, M));
+      it.Ad[(size_t)c * M + r] = v;
+      s += v.x * v.x + v.y * v.y;
+    }
+    rmax = fmax(rmax, s);
+  }
+  atomicMax(it.rowmax, (unsigned long long)__double_as_longlong(rmax));
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// One-sided Jacobi in binary64 (round-robin pairs, warp per pair, V_d accumulated).
+// Stops when no pair has |gamma| > tol sqrt(alpha_p alpha_q), tol = 4 M 2^-53.
+static __global__ void __launch_bounds__(256) k_jacobi_d(const PreItem* items) {
+  const PreItem it = items[blockIdx.x];
+  const int M = it.M, N = it.N, NP = N / 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* A = it.Ad;
+  double2* V = it.Vd;
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x)
+    V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
+  __shared__ int s_any;
+  const double tol = 4.0 * M * 1.1102230246251565e-16;
+  int sweep = 0;
+  for (sweep = 1; sweep <= 40; ++sweep) {
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    for (int step = 0; step < N - 1; ++step) {
+      for (int i = warp; i < NP; i += 8) {
+        int p, q;
+        rr_pair(N, step, i, p, q);
+        double2* ap = A + (size_t)p * M;
+        double2* aq = A + (size_t)q * M;
+        double sp = 0, sq = 0, gr = 0, gi = 0;
+        for (int r = lane; r < M; r += 32) {
+          const double2 x = ap[r], y = aq[r];
+          sp += x.x * x.x + x.y * x.y;
+          sq += y.x * y.x + y.y * y.y;
+          gr += x.x * y.x + x.y * y.y;  // conj(x) y
+          gi += x.x * y.y - x.y * y.x;
+        }
+        sp = warp_sum_d(sp); sq = warp_sum_d(sq); gr = warp_sum_d(gr); gi = warp_sum_d(gi);
+        const double g2 = gr * gr + gi * gi;
+        if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
+        if (lane == 0) s_any = 1;
+        // same rotation as the p-bit kernel (R17): d = a_q - a_p, r = sqrt(d^2 + 4|g|^2),
+        // c^2 = (|d| + r)/(2r), s = sgn(d) g/(r c); y_p = c x_p - conj(s) x_q, y_q = s x_p + c x_q
+        const double d = sq - sp;
+        const double rr = sqrt(d * d + 4.0 * g2);
+        const double c = sqrt((fabs(d) + rr) / (2.0 * rr));
+        const double sc = (d < 0 ? -1.0 : 1.0) / (rr * c);
+        const double sr = gr * sc, si = gi * sc;
+        for (int r = lane; r < M; r += 32) {
+          const double2 x = ap[r], y = aq[r];
+          ap[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+          aq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+        }
+        double2* vp = V + (size_t)p * N;
+        double2* vq = V + (size_t)q * N;
+        for (int r = lane; r < N; r += 32) {
+          const double2 x = vp[r], y = vq[r];
+          vp[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+          vq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+        }
+      }
+      __syncthreads();
+    }
+    const int any = s_any;
+    __syncthreads();
+    if (!any) break;
+  }
+  if (threadIdx.x == 0) *it.sweeps_d = sweep;
+}
+
+// binary64 v (|v| <= 1) -> L balanced digits at exponent 1 (value = sum d_k 2^(28k) 2^(1-28L)), exact
+template <int L>
+__device__ __forceinline__ void double_to_fx(double v, int32_t (&d)[L]) {
+#pragma unroll
+  for (int k = 0; k < L; ++k) d[k] = 0;
+  if (v == 0.0) return;
+  const bool neg = v < 0;
+  int ex;
+  const double m = frexp(fabs(v), &ex);  // |v| = m 2^ex, m in [0.5, 1)
+  const uint64_t M53 = (uint64_t)ldexp(m, 53);
+  // integer I = |v| 2^(28L - 1) = M53 2^(ex - 53 + 28L - 1); s = bit position of M53's bit 0
+  const int s = ex - 54 + 28 * L;
+  if (s < -53) return;
+  uint64_t lo = M53;
+  int base = s;
+  if (s < 0) { lo = M53 >> (-s); base = 0; }
+  const int q = base / 28, r = base % 28;
+  // lo << r spread over digits q, q+1, q+2 (53 + 27 bits at most)
+  const unsigned __int128 w = (unsigned __int128)lo << r;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const int j = k - q;
+    if (j >= 0 && j < 3) d[k] = (int32_t)((w >> (28 * j)) & 0x0FFFFFFFu);
+  }
+  int32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) {
+    const int32_t x = d[k] + c;
+    c = (x + (1 << 27)) >> 28;
+    d[k] = x - (c << 28);
+  }
+  d[L - 1] += c << 28;
+  if (neg) {
+#pragma unroll
+    for (int k = 0; k < L; ++k) d[k] = -d[k];
+  }
+}
+
+template <int L>
+__global__ void k_d_to_fx(const PreItem* items) {
+  const PreItem it = items[blockIdx.y];
+  const int N = it.N;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { it.eOne[0] = 1; it.eOne[1] = 0; }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * N; t += gridDim.x * blockDim.x) {
+    const int r = t % N, c = t / N;
+    const double2 v = it.Vd[(size_t)c * N + r];
+    int32_t d[L];
+    double_to_fx<L>(v.x, d);
+    stfx<L>(it.X, N, c, 0, r, d);
+    double_to_fx<L>(v.y, d);
+    stfx<L>(it.X, N, c, 1, r, d);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // |A_1(r, c)| <= ||Theta'(r, :)|| ||x_c|| <= sqrt(rowmax) 2^e (1 + 2^-40): exponent
+    // ceil(log2 sqrt(rowmax)) + 1 above e, so that |A_1| < 2^(eA1 - 1)
+    const double rm = __longlong_as_double((long long)*it.rowmax);
+    int64_t ea = *it.eA0;
+    if (rm > 0) ea += (int64_t)ceil(0.5 * log2(rm) * (1 + 1e-12) + 1e-9) + 1;
+    *it.eA1 = ea;
+  }
+}
+
+// ---------------------------------------------------------------------------- GEMM
+// C (rows x cols) = sgn * op(A) B (+ Cadd) (+ I), fixed-point complex with block exponents:
+// op(A) = A (stored rows x K, column-major, ld lda) or A^H (A stored K x rows).  C is written
+// at exponent *eCout (given); the digit sum is shifted by g = eC - eA - eB bits (-27..27).
+struct GemmT {
+  const int32_t* A; int lda; const int64_t* eA;
+  const int32_t* B; int ldb; const int64_t* eB;
+  int32_t* C; int ldc; const int64_t* eCout;
+  const int32_t* Cadd;  // same shape / exponent as C, or null
+  int64_t* eCcols;      // if non-null: eCcols[c] = *eCout for every column (Jacobi layout)
+  int rows, cols, K, conjA, neg, addI;
+};
+
+// round V 2^-g / 2^(28L) for any -27 <= g <= 27
+template <int L>
+__device__ __forceinline__ void tround_any(int64_t (&acc)[L + 2], int g, int32_t (&out)[L]) {
+  if (g >= 0) {
+    tround_sr<L>(acc, g, out);
+    return;
+  }
+  tnorm2<L>(acc);
+#pragma unroll
+  for (int c = 0; c < L + 2; ++c) acc[c] *= ((int64_t)1 << (-g));
+  tround2<L>(acc, out);
+}
+
+template <int L>
+__device__ __forceinline__ void fx_balance(int32_t (&x)[L]) {
+  int32_t c = 0;
+#pragma unroll
+  for (int k = 0; k < L - 1; ++k) {
+    const int32_t v = x[k] + c;
+    c = (v + (1 << 27)) >> 28;
+    x[k] = v - (c << 28);
+  }
+  x[L - 1] += c;
+}
+
+constexpr int GT_TILE = 16, GT_KB = 8;
+
+template <int L>
+__global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
+  const GemmT it = items[blockIdx.y];
+  const int tilesR = (it.rows + GT_TILE - 1) / GT_TILE, tilesC = (it.cols + GT_TILE - 1) / GT_TILE;
+  const int tx = threadIdx.x % GT_TILE, ty = threadIdx.x / GT_TILE;
+  __shared__ int32_t As[GT_KB][2][L][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
+  __shared__ int32_t Bs[GT_KB][2][L][GT_TILE + 1];
+  const int64_t eC = *it.eCout;
+  const int g = (int)(eC - (*it.eA + *it.eB));
+  for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
+    const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;
+    const int r = r0 + tx, c = c0 + ty;
+    int64_t ar[L + 2], ai[L + 2];
+#pragma unroll
+    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    for (int k0 = 0; k0 < it.K; k0 += GT_KB) {
+      __syncthreads();
+      // stage GT_KB x 2 x L x 16 words of each operand; the index order follows the
+      // contiguous direction in global memory (rows of A, k of A^H and of B)
+      for (int w = threadIdx.x; w < GT_KB * 2 * L * GT_TILE; w += 256) {
+        int32_t va = 0;
+        if (!it.conjA) {
+          const int e = w % GT_TILE, dg = (w / GT_TILE) % L, ri = (w / (GT_TILE * L)) % 2, kk = w / (GT_TILE * L * 2);
+          const int k = k0 + kk, rr = r0 + e;
+          if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + dg) * it.lda + rr];
+          As[kk][ri][dg][e] = va;
+        } else {
+          const int kk = w % GT_KB, dg = (w / GT_KB) % L, ri = (w / (GT_KB * L)) % 2, e = w / (GT_KB * L * 2);
+          const int k = k0 + kk, rr = r0 + e;
+          if (k < it.K && rr < it.rows) {
+            va = it.A[((size_t)(rr * 2 + ri) * L + dg) * it.lda + k];
+            if (ri) va = -va;
+          }
+          As[kk][ri][dg][e] = va;
+        }
+        {
+          const int kk = w % GT_KB, dg = (w / GT_KB) % L, ri = (w / (GT_KB * L)) % 2, e = w / (GT_KB * L * 2);
+          const int k = k0 + kk, cc = c0 + e;
+          int32_t vb = 0;
+          if (k < it.K && cc < it.cols) vb = it.B[((size_t)(cc * 2 + ri) * L + dg) * it.ldb + k];
+          Bs[kk][ri][dg][e] = vb;
+        }
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int kk = 0; kk < GT_KB; ++kk) {
+        int32_t xr[L], xi[L], yr[L], yi[L];
+#pragma unroll
+        for (int j = 0; j < L; ++j) {
+          xr[j] = As[kk][0][j][tx]; xi[j] = As[kk][1][j][tx];
+          yr[j] = Bs[kk][0][j][ty]; yi[j] = Bs[kk][1][j][ty];
+        }
+        tmul_acc2<L>(ar, xr, yr);
+        tmul_sub2<L>(ar, xi, yi);
+        tmul_acc2<L>(ai, xr, yi);
+        tmul_acc2<L>(ai, xi, yr);
+      }
+      tnorm2<L>(ar);
+      tnorm2<L>(ai);
+    }
+    if (r < it.rows && c < it.cols) {
+      int32_t o[L];
+#pragma unroll
+      for (int ri = 0; ri < 2; ++ri) {
+        tround_any<L>(ri ? ai : ar, g, o);
+        if (it.neg) {
+#pragma unroll
+          for (int j = 0; j < L; ++j) o[j] = -o[j];
+        }
+        if (it.addI && ri == 0 && r == c) o[L - 1] += 1 << (28 - (int)eC);  // + 1 at exponent eC (1)
+        if (it.Cadd) {
+          int32_t x[L];
+          ldfx<L>(it.Cadd, it.ldc, c, ri, r, x);
+#pragma unroll
+          for (int j = 0; j < L; ++j) o[j] += x[j];
+        }
+        fx_balance<L>(o);
+        stfx<L>(it.C, it.ldc, c, ri, r, o);
+      }
+      if (it.eCcols && r == 0) it.eCcols[c] = eC;
+    }
+  }
+}
+
+}  // namespace mpsb

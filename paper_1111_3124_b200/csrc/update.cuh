@@ -13,6 +13,7 @@
 
 #include "common.h"
 #include "kernels.cuh"
+#include "precond.cuh"
 
 namespace mpsb {
 
@@ -119,20 +120,47 @@ struct Upd2Args {
 template <int L>
 constexpr int redo_bits() { return L <= 10 ? 4 : 16; }
 
+// MPS_NO_PRECOND=1 (debug / A-B): run the p-bit Jacobi on Theta' itself (no binary64
+// preconditioning, R19).
+inline bool use_precond() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_NO_PRECOND");
+    on = (e && atoi(e)) ? 0 : 1;
+  }
+  return on != 0;
+}
+template <int L>
+constexpr int ns_iters() { return L <= 10 ? 3 : 4; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
+
+// preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N), eMix[N], scalars
+template <int L>
+inline size_t pre_bytes(int M, int N) {
+  return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
+         256;
+}
+
 template <int L, int NL>
 inline size_t upd2_item_bytes(const Upd2Args& a) {
   const int M = 2 * std::max(a.chiL, a.chiR), N = 2 * std::min(a.chiL, a.chiR);
   size_t lr = mat_bytes(2 * a.chiL, a.chiM, L) + mat_bytes(a.chiM, 2 * a.chiR, L);
   size_t r1 = std::max(lr, mat_bytes(M, N, L));
   return r1 + mat_bytes(2 * a.chiL, 2 * a.chiR, L) + mat_bytes(N, N, L) + mat_bytes(M, N, L) +
-         SvdScratch<L, NL>::bytes(N) + 8 * (size_t)N + 512;
+         SvdScratch<L, NL>::bytes(N) + 8 * (size_t)N + 512 + pre_bytes<L>(M, N) + 256;
+}
+
+// descriptor region of launch_update2 (the redo flags follow it)
+template <int L, int NL>
+inline size_t upd2_desc_bytes(int n) {
+  return align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
+         align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(sizeof(PreItem) * n) +
+         align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n);
 }
 
 template <class T>
 size_t upd2_workspace(const Upd2Args* a, int n) {
   constexpr int L = T::L, NL = T::NL;
-  size_t s = align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
-             align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(4 * (size_t)n) + 4096;
+  size_t s = upd2_desc_bytes<L, NL>(n) + align_up(4 * (size_t)n) + 4096;
   for (int i = 0; i < n; ++i) s += align_up(upd2_item_bytes<L, NL>(a[i]));
   return s;
 }
@@ -147,9 +175,14 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   char* base = (char*)ws;
   const size_t d_prep = 0, d_gemm = align_up(sizeof(PrepItem) * 2 * n),
                d_mix = d_gemm + align_up(sizeof(GemmItem) * n), d_svd = d_mix + align_up(sizeof(MixItem) * n),
-               d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_end = d_fin + align_up(sizeof(FinItem<NL>) * n);
+               d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_pre = d_fin + align_up(sizeof(FinItem<NL>) * n),
+               d_gt = d_pre + align_up(sizeof(PreItem) * n), d_end = upd2_desc_bytes<L, NL>(n);
+  constexpr int NSIT = ns_iters<L>();
+  const bool pre = use_precond();
   int* redo = (int*)(base + d_end);  // [n] flags (run_update2)
   hd.assign(d_end, 0);
+  PreItem* hpre = (PreItem*)(hd.data() + d_pre);
+  GemmT* hgt = (GemmT*)(hd.data() + d_gt);  // [2 NSIT + 1][n]: D_k, X_k+1 per iteration, then A_1
   PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
   GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
@@ -179,6 +212,18 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     char* sp = (char*)A0f + mat_bytes(M, N, L);
     auto S = SvdScratch<L, NL>::carve(sp, N);
     int64_t* eV = (int64_t*)align_up((size_t)sp + SvdScratch<L, NL>::bytes(N), 16);
+    char* pq = (char*)align_up((size_t)eV + 8 * (size_t)N, 256);
+    double2* Ad = (double2*)pq; pq += align_up(16 * (size_t)M * N);
+    double2* Vd = (double2*)pq; pq += align_up(16 * (size_t)N * N);
+    int32_t* Xa = (int32_t*)pq; pq += mat_bytes(N, N, L);
+    int32_t* Xb = (int32_t*)pq; pq += mat_bytes(N, N, L);
+    int32_t* Dm = (int32_t*)pq; pq += mat_bytes(N, N, L);
+    int64_t* eMix = (int64_t*)pq; pq += align_up(8 * (size_t)N);
+    unsigned long long* rowmax = (unsigned long long*)pq;
+    int* sweeps_d = (int*)(pq + 8);
+    int64_t* eOne = (int64_t*)(pq + 16);
+    int64_t* eA1 = (int64_t*)(pq + 32);
+    int32_t* Xfin = (NSIT % 2) ? Xb : Xa;
     int64_t* eL = S.e_misc;
     int64_t* eR = S.e_misc + 1;
     int64_t* eT = S.e_misc + 2;
@@ -187,18 +232,32 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     hp[2 * b] = PrepItem{g.GL, g.lamL, g.lamM, chiL, chiM, 0, Lf, eL};
     hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
     hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
-    hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, Af, S.eA, M, N};
+    hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pre ? A0f : Af, pre ? eMix : S.eA, M, N};
+    if (pre) {
+      hpre[b] = PreItem{M, N, A0f, eMix, Ad, Vd, rowmax, sweeps_d, Xa, eOne, eA1};
+      for (int k = 0; k < NSIT; ++k) {
+        int32_t* Xc = (k % 2) ? Xb : Xa;
+        int32_t* Xn = (k % 2) ? Xa : Xb;
+        // D = I - X^H X (exponent 1);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
+        hgt[(2 * k) * n + b] = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1};
+        hgt[(2 * k + 1) * n + b] = GemmT{Xc, N, eOne, Dm, N, eOne + 1, Xn, N, eOne, Xc, nullptr, N, N, N, 0, 0, 0};
+      }
+      // A_1 = Theta' X at the exponent bounded by Theta's largest row norm; Jacobi column exponents
+      hgt[(2 * NSIT) * n + b] = GemmT{A0f, M, eMix, Xfin, N, eOne, Af, M, eA1, nullptr, S.eA, M, N, N, 0, 0, 0};
+    }
     SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
     const bool recover = !force_accumulate_v() && !g.accumulate_v;
-    si.A0 = recover ? A0f : nullptr; si.eA0 = S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
+    si.A0 = recover ? A0f : nullptr; si.eA0 = pre ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
+    si.a0_ready = pre ? 1 : 0;
+    if (pre && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
-    fi.M = M; fi.N = N; fi.trans = trans ? 1 : 0; fi.A = Af; fi.eA = S.eA; fi.V = Vf; fi.alpha = S.alpha;
+    fi.M = M; fi.N = N; fi.trans = trans ? 1 : 0; fi.A = Af; fi.eA = S.eA; fi.V = si.V; fi.alpha = S.alpha;
     fi.chi_max = g.chi_max; fi.thr = thr_m; fi.ord = S.ord; fi.inv_sig = S.inv_sig; fi.lam = S.lam;
     fi.k_out = g.k_out ? g.k_out : S.k; fi.status = g.status_out ? g.status_out : S.fstatus;
     fi.svd_status = S.status;
@@ -225,6 +284,24 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
   k_mix<L, NL><<<gg, 128, 16 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
   prof_mark(PROF_CONTRACT, 0, st);
+  if (pre && !any_dbg) {
+    prof_mark(PROF_PRECOND, 1, st);
+    int maxM = 0, maxN = 0;
+    for (int b = 0; b < n; ++b) { maxM = std::max(maxM, hs[b].M); maxN = std::max(maxN, hs[b].N); }
+    const PreItem* dpre = (const PreItem*)(base + d_pre);
+    const GemmT* dgt = (const GemmT*)(base + d_gt);
+    k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
+    k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
+    k_jacobi_d<<<n, 256, 0, st>>>(dpre); ++nl;
+    k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
+    const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
+    const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
+    for (int k = 0; k < 2 * NSIT; ++k) {
+      k_gemm_t<L><<<dim3(std::min(tNN, 1024), n), 256, 0, st>>>(dgt + (size_t)k * n); ++nl;
+    }
+    k_gemm_t<L><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+    prof_mark(PROF_PRECOND, 0, st);
+  }
   if (any_dbg) {
     for (int b = 0; b < n; ++b) {
       if (!a[b].theta_dbg) continue;
@@ -286,9 +363,7 @@ int run_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaStrea
   constexpr int NL = T::NL;
   int nl = launch_update2<T>(p, thr, a, n, ws, st, hd);
   if (force_accumulate_v()) return nl;
-  const size_t d_end = align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) +
-                       align_up(sizeof(MixItem) * n) + align_up(sizeof(SvdItem<NL>) * n) +
-                       align_up(sizeof(FinItem<NL>) * n);
+  const size_t d_end = upd2_desc_bytes<T::L, NL>(n);
   std::vector<int> redo(n, 0);
   cudaMemcpyAsync(redo.data(), (char*)ws + d_end, 4 * (size_t)n, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
