@@ -292,7 +292,14 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     const GemmT* dgt = (const GemmT*)(base + d_gt);
     k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
     k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
-    k_jacobi_d<<<n, 256, 0, st>>>(dpre); ++nl;
+    {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      k_jacobi_db<<<n, 256, jd_smem(maxM), st>>>(dpre); ++nl;
+    }
     k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
     const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
     const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
