@@ -1167,7 +1167,7 @@ __global__ void __launch_bounds__(NTHR) k_finalize(const FinItem<NL>* items, int
     if (it.redo && it.eV && k > 0) {
       const mpf<NL>& smax = sig[it.ord[0]];
       const mpf<NL>& smin = sig[it.ord[k - 1]];
-      if (!mpf_is_zero(smin) && smax.e - smin.e > it.redo_bits) *it.redo = 1;
+      if (!mpf_is_zero(smin) && smax.e - smin.e > it.redo_bits) atomicOr(it.redo, 1);  // 1: accumulate V
     }
     const int js = it.svd_status ? *it.svd_status : 0;
     *it.status = js ? js : (k == 0 ? -4 : 0);

@@ -46,6 +46,7 @@ template <int L>
 __global__ void k_fx_to_d(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
   const int M = it.M, N = it.N;
+  if (N == 0) return;
   double rmax = 0.0;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < M; r += gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -145,6 +146,7 @@ inline size_t jd_smem(int M) {
 static __global__ void __launch_bounds__(256) k_jacobi_db(const PreItem* items) {
   const PreItem it = items[blockIdx.x];
   const int M = it.M, N = it.N;
+  if (N == 0) return;
   const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ double2 jds[];
@@ -300,6 +302,7 @@ template <int L>
 __global__ void k_d_to_fx(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
   const int N = it.N;
+  if (N == 0) return;  // item without preconditioning
   if (blockIdx.x == 0 && threadIdx.x == 0) { it.eOne[0] = 1; it.eOne[1] = 0; }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * N; t += gridDim.x * blockDim.x) {
     const int r = t % N, c = t / N;
@@ -324,6 +327,10 @@ __global__ void k_d_to_fx(const PreItem* items) {
 // C (rows x cols) = sgn * op(A) B (+ Cadd) (+ I), fixed-point complex with block exponents:
 // op(A) = A (stored rows x K, column-major, ld lda) or A^H (A stored K x rows).  C is written
 // at exponent *eCout (given); the digit sum is shifted by g = eC - eA - eB bits (-27..27).
+// Precision schedule (template): only the top LG of the L stored digits of A and B take
+// part (an LG-digit product, rounded to LG digits and stored as the top LG digits of C, the
+// lower ones 0 (+ Cadd's)); the top Z of those digits of B are known to be 0 and skipped —
+// zerr (if set) receives 1 when one is not (the caller then re-runs without the shortcut).
 struct GemmT {
   const int32_t* A; int lda; const int64_t* eA;
   const int32_t* B; int ldb; const int64_t* eB;
@@ -331,6 +338,7 @@ struct GemmT {
   const int32_t* Cadd;  // same shape / exponent as C, or null
   int64_t* eCcols;      // if non-null: eCcols[c] = *eCout for every column (Jacobi layout)
   int rows, cols, K, conjA, neg, addI;
+  int* zerr;
 };
 
 // round V 2^-g / 2^(28L) for any -27 <= g <= 27
@@ -358,73 +366,89 @@ __device__ __forceinline__ void fx_balance(int32_t (&x)[L]) {
   x[L - 1] += c;
 }
 
+// acc (LG+2 columns: LG-2 .. 2LG-1) += / -= x y, the top Z digits of y being zero
+template <int LG, int Z, bool SUB>
+__device__ __forceinline__ void tmul_z(int64_t (&acc)[LG + 2], const int32_t (&x)[LG], const int32_t (&y)[LG]) {
+#pragma unroll
+  for (int i = 0; i < LG; ++i)
+#pragma unroll
+    for (int j = 0; j < LG - Z; ++j)
+      if (i + j >= LG - 2) acc[i + j - (LG - 2)] = madw(SUB ? -x[i] : x[i], y[j], acc[i + j - (LG - 2)]);
+}
+
 constexpr int GT_TILE = 16, GT_KB = 8;
 
-template <int L>
+template <int L, int LG, int Z>
 __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
+  static_assert(LG <= L && Z < LG, "precision schedule");
+  constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
   const int tilesR = (it.rows + GT_TILE - 1) / GT_TILE, tilesC = (it.cols + GT_TILE - 1) / GT_TILE;
   const int tx = threadIdx.x % GT_TILE, ty = threadIdx.x / GT_TILE;
-  __shared__ int32_t As[GT_KB][2][L][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
-  __shared__ int32_t Bs[GT_KB][2][L][GT_TILE + 1];
+  __shared__ int32_t As[GT_KB][2][LG][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
+  __shared__ int32_t Bs[GT_KB][2][LG][GT_TILE + 1];
   const int64_t eC = *it.eCout;
   const int g = (int)(eC - (*it.eA + *it.eB));
+  int zbad = 0;
   for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
     const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;
     const int r = r0 + tx, c = c0 + ty;
-    int64_t ar[L + 2], ai[L + 2];
+    int64_t ar[LG + 2], ai[LG + 2];
 #pragma unroll
-    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    for (int j = 0; j < LG + 2; ++j) ar[j] = ai[j] = 0;
     for (int k0 = 0; k0 < it.K; k0 += GT_KB) {
       __syncthreads();
-      // stage GT_KB x 2 x L x 16 words of each operand; the index order follows the
-      // contiguous direction in global memory (rows of A, k of A^H and of B)
-      for (int w = threadIdx.x; w < GT_KB * 2 * L * GT_TILE; w += 256) {
+      // stage the top LG digits of GT_KB x 16 elements of each operand; the index order
+      // follows the contiguous direction in global memory (rows of A, k of A^H and of B)
+      for (int w = threadIdx.x; w < GT_KB * 2 * LG * GT_TILE; w += 256) {
         int32_t va = 0;
         if (!it.conjA) {
-          const int e = w % GT_TILE, dg = (w / GT_TILE) % L, ri = (w / (GT_TILE * L)) % 2, kk = w / (GT_TILE * L * 2);
+          const int e = w % GT_TILE, dg = (w / GT_TILE) % LG, ri = (w / (GT_TILE * LG)) % 2, kk = w / (GT_TILE * LG * 2);
           const int k = k0 + kk, rr = r0 + e;
-          if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + dg) * it.lda + rr];
+          if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + D0 + dg) * it.lda + rr];
           As[kk][ri][dg][e] = va;
         } else {
-          const int kk = w % GT_KB, dg = (w / GT_KB) % L, ri = (w / (GT_KB * L)) % 2, e = w / (GT_KB * L * 2);
+          const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) {
-            va = it.A[((size_t)(rr * 2 + ri) * L + dg) * it.lda + k];
+            va = it.A[((size_t)(rr * 2 + ri) * L + D0 + dg) * it.lda + k];
             if (ri) va = -va;
           }
           As[kk][ri][dg][e] = va;
         }
         {
-          const int kk = w % GT_KB, dg = (w / GT_KB) % L, ri = (w / (GT_KB * L)) % 2, e = w / (GT_KB * L * 2);
+          const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
           const int k = k0 + kk, cc = c0 + e;
           int32_t vb = 0;
-          if (k < it.K && cc < it.cols) vb = it.B[((size_t)(cc * 2 + ri) * L + dg) * it.ldb + k];
+          if (k < it.K && cc < it.cols) vb = it.B[((size_t)(cc * 2 + ri) * L + D0 + dg) * it.ldb + k];
+          if (dg >= LG - Z && vb != 0) zbad = 1;
           Bs[kk][ri][dg][e] = vb;
         }
       }
       __syncthreads();
 #pragma unroll 1
       for (int kk = 0; kk < GT_KB; ++kk) {
-        int32_t xr[L], xi[L], yr[L], yi[L];
+        int32_t xr[LG], xi[LG], yr[LG], yi[LG];
 #pragma unroll
-        for (int j = 0; j < L; ++j) {
+        for (int j = 0; j < LG; ++j) {
           xr[j] = As[kk][0][j][tx]; xi[j] = As[kk][1][j][tx];
           yr[j] = Bs[kk][0][j][ty]; yi[j] = Bs[kk][1][j][ty];
         }
-        tmul_acc2<L>(ar, xr, yr);
-        tmul_sub2<L>(ar, xi, yi);
-        tmul_acc2<L>(ai, xr, yi);
-        tmul_acc2<L>(ai, xi, yr);
+        tmul_z<LG, Z, false>(ar, xr, yr);
+        tmul_z<LG, Z, true>(ar, xi, yi);
+        tmul_z<LG, Z, false>(ai, xr, yi);
+        tmul_z<LG, Z, false>(ai, xi, yr);
       }
-      tnorm2<L>(ar);
-      tnorm2<L>(ai);
+      tnorm2<LG>(ar);
+      tnorm2<LG>(ai);
     }
     if (r < it.rows && c < it.cols) {
-      int32_t o[L];
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
-        tround_any<L>(ri ? ai : ar, g, o);
+        int32_t t[LG], o[L];
+        tround_any<LG>(ri ? ai : ar, g, t);
+#pragma unroll
+        for (int j = 0; j < L; ++j) o[j] = j >= D0 ? t[j - D0] : 0;
         if (it.neg) {
 #pragma unroll
           for (int j = 0; j < L; ++j) o[j] = -o[j];
@@ -442,6 +466,29 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
       if (it.eCcols && r == 0) it.eCcols[c] = eC;
     }
   }
+  if (zbad && it.zerr) atomicOr(it.zerr, 2);  // 2: re-run without the preconditioner
+}
+
+// Newton-Schulz precision schedule: iteration k computes D_k with LG digits and
+// X_{k+1} = X_k + X_k D_k / 2 with LG digits skipping the Z top digits of D_k (zero since
+// |D_k| ~ 2^(-45 * 2^k)); conservative by >= 1 digit, checked at run time (zerr).
+template <int L> struct NsSched;
+template <> struct NsSched<10> {
+  static constexpr int n = 3;
+  static constexpr int lg[3] = {4, 7, 10};
+  static constexpr int z[3] = {1, 2, 5};
+};
+template <> struct NsSched<19> {
+  static constexpr int n = 4;
+  static constexpr int lg[4] = {4, 7, 14, 19};
+  static constexpr int z[4] = {1, 2, 5, 10};
+};
+
+template <int L, int K>
+inline void launch_ns_iter(const GemmT* dD, const GemmT* dX, dim3 grid, cudaStream_t st) {
+  constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K];
+  k_gemm_t<L, LG, 0><<<grid, 256, 0, st>>>(dD);
+  k_gemm_t<L, LG, Z><<<grid, 256, 0, st>>>(dX);
 }
 
 }  // namespace mpsb

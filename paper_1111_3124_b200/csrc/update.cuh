@@ -109,6 +109,7 @@ struct Upd2Args {
   int *k_out, *sweeps_out, *status_out;               // device ints (may be null)
   uint32_t* theta_dbg;                                // column-major Theta' records or null
   int accumulate_v;                                   // 1: accumulate V (else recover it, R16)
+  int no_precond;                                     // 1: no binary64 preconditioning (R19)
 };
 
 // kept-spectrum range (bits) above which a recovered V is replaced by an accumulated one:
@@ -131,7 +132,7 @@ inline bool use_precond() {
   return on != 0;
 }
 template <int L>
-constexpr int ns_iters() { return L <= 10 ? 3 : 4; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
+constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
 
 // preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N), eMix[N], scalars
 template <int L>
@@ -224,6 +225,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     int64_t* eOne = (int64_t*)(pq + 16);
     int64_t* eA1 = (int64_t*)(pq + 32);
     int32_t* Xfin = (NSIT % 2) ? Xb : Xa;
+    const bool pb = pre && !g.no_precond;
     int64_t* eL = S.e_misc;
     int64_t* eR = S.e_misc + 1;
     int64_t* eT = S.e_misc + 2;
@@ -232,18 +234,24 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     hp[2 * b] = PrepItem{g.GL, g.lamL, g.lamM, chiL, chiM, 0, Lf, eL};
     hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
     hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
-    hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pre ? A0f : Af, pre ? eMix : S.eA, M, N};
-    if (pre) {
+    hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pb ? A0f : Af, pb ? eMix : S.eA, M, N};
+    if (pre && !pb) {  // this item skips the preconditioner: empty descriptors
+      hpre[b] = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, rowmax, sweeps_d, nullptr, eOne, eA1};
+      for (int k = 0; k <= 2 * NSIT; ++k)
+        hgt[k * n + b] = GemmT{nullptr, 1, eOne, nullptr, 1, eOne, nullptr, 1, eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
+    }
+    if (pb) {
       hpre[b] = PreItem{M, N, A0f, eMix, Ad, Vd, rowmax, sweeps_d, Xa, eOne, eA1};
       for (int k = 0; k < NSIT; ++k) {
         int32_t* Xc = (k % 2) ? Xb : Xa;
         int32_t* Xn = (k % 2) ? Xa : Xb;
         // D = I - X^H X (exponent 1);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
-        hgt[(2 * k) * n + b] = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1};
-        hgt[(2 * k + 1) * n + b] = GemmT{Xc, N, eOne, Dm, N, eOne + 1, Xn, N, eOne, Xc, nullptr, N, N, N, 0, 0, 0};
+        hgt[(2 * k) * n + b] = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
+        hgt[(2 * k + 1) * n + b] =
+            GemmT{Xc, N, eOne, Dm, N, eOne + 1, Xn, N, eOne, Xc, nullptr, N, N, N, 0, 0, 0, redo + b};
       }
       // A_1 = Theta' X at the exponent bounded by Theta's largest row norm; Jacobi column exponents
-      hgt[(2 * NSIT) * n + b] = GemmT{A0f, M, eMix, Xfin, N, eOne, Af, M, eA1, nullptr, S.eA, M, N, N, 0, 0, 0};
+      hgt[(2 * NSIT) * n + b] = GemmT{A0f, M, eMix, Xfin, N, eOne, Af, M, eA1, nullptr, S.eA, M, N, N, 0, 0, 0, nullptr};
     }
     SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
@@ -251,9 +259,9 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
     const bool recover = !force_accumulate_v() && !g.accumulate_v;
-    si.A0 = recover ? A0f : nullptr; si.eA0 = pre ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
-    si.a0_ready = pre ? 1 : 0;
-    if (pre && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
+    si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
+    si.a0_ready = pb ? 1 : 0;
+    if (pb && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -303,10 +311,13 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
     const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
     const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
-    for (int k = 0; k < 2 * NSIT; ++k) {
-      k_gemm_t<L><<<dim3(std::min(tNN, 1024), n), 256, 0, st>>>(dgt + (size_t)k * n); ++nl;
-    }
-    k_gemm_t<L><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+    const dim3 gNN(std::min(tNN, 1024), n);
+    launch_ns_iter<L, 0>(dgt, dgt + (size_t)n, gNN, st);
+    launch_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, gNN, st);
+    launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
+    if constexpr (NSIT > 3) launch_ns_iter<L, 3>(dgt + (size_t)6 * n, dgt + (size_t)7 * n, gNN, st);
+    nl += 2 * NSIT;
+    k_gemm_t<L, L, 0><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
     prof_mark(PROF_PRECOND, 0, st);
   }
   if (any_dbg) {
@@ -379,6 +390,7 @@ int run_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaStrea
     if (redo[b]) {
       Upd2Args c = a[b];
       c.accumulate_v = 1;
+      if (redo[b] & 2) c.no_precond = 1;
       sub.push_back(c);
     }
   if (!sub.empty()) {
