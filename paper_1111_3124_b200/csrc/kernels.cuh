@@ -217,6 +217,27 @@ __device__ __forceinline__ void kmul_acc(int64_t (&acc)[L + 2], const int32_t (&
     for (int j = 0; j < L; ++j) acc[j + 2] = madw(K[L], x[j], acc[j + 2]);
   }
 }
+// acc += K x where the top Z fractional digits of K are known to be zero (late sweeps of a
+// preconditioned Jacobi: s ~ 2^-46, 2^-92, 2^-184 and c = 1 - O(|s|^2)); digits of x that
+// can only meet skipped digits of K are not loaded.  Same result as kmul_acc.
+template <int L, int Z>
+__device__ __forceinline__ void kmul_z(int64_t (&acc)[L + 2], const int32_t* Kp, const int32_t* xp, bool hasInt) {
+  constexpr int J0 = Z >= 1 ? Z - 1 : 0;  // x digits j < J0 only pair with skipped K digits
+  int32_t K[L + 1], x[L];
+#pragma unroll
+  for (int k = 0; k <= L; ++k) K[k] = (k < L - Z || k == L) ? Kp[k] : 0;
+#pragma unroll
+  for (int k = 0; k < L; ++k) x[k] = (k >= J0 || hasInt) ? xp[k * 32] : 0;
+#pragma unroll
+  for (int i = 0; i < L - Z; ++i)
+#pragma unroll
+    for (int j = 0; j < L; ++j)
+      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(K[i], x[j], acc[i + j - (L - 2)]);
+  if (hasInt) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) acc[j + 2] = madw(K[L], x[j], acc[j + 2]);
+  }
+}
 template <int L>
 __device__ __forceinline__ void kmul_sub(int64_t (&acc)[L + 2], const int32_t (&K)[L + 1], const int32_t (&x)[L],
                                          bool hasInt) {
@@ -604,14 +625,40 @@ __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int l
 // (0 x_p.re, 1 x_p.im, 2 x_q.re, 3 x_q.im); coefficients (sign folded) are stored as
 // [mat][o][t] in the same order:
 //   y_p.re = +Cp xrp - Psr xrq - Psi xiq     y_p.im = +Cp xip - Psr xiq + Psi xrq
-//   y_q.re = +Qsr xrp - Qsi xip + Cq xrq     y_q.im = +Qsr xip + Qsi xrp + Cq xiq
+//   y_q.re = +Cq xrq + Qsr xrp - Qsi xip     y_q.im = +Cq xiq + Qsr xip + Qsi xrp
 // with Psr+iPsi = s 2^(eq-eo_p) (conj(s) multiplies x_q), Qsr+iQsi = s 2^(ep-eo_q),
 // Cp = c 2^(ep-eo_p), Cq = c 2^(eq-eo_q); for V all scales are 1.
-__constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {0, 1, 2}, {1, 0, 3}};
+__constant__ int c_opidx[4][3] = {{0, 2, 3}, {1, 3, 2}, {2, 0, 1}, {3, 1, 0}};  // term 0: the c term
 // slot u <- (+/-) vals[src & 15] of the 9 distinct values {Cp, Psr, Psi, Qsr, Qsi, Cq, c,
 // sr, si}; bit 4 = negate
-__constant__ int8_t c_coefsrc[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 3, 4 | 16, 5, 3, 4, 5,
-                                     6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 7, 8 | 16, 6, 7, 8, 6};
+__constant__ int8_t c_coefsrc[24] = {0, 1 | 16, 2 | 16, 0, 1 | 16, 2, 5, 3, 4 | 16, 5, 3, 4,
+                                     6, 7 | 16, 8 | 16, 6, 7 | 16, 8, 6, 7, 8 | 16, 6, 7, 8};
+
+// Phase U for one 32-row chunk: the four outputs (y_p re/im, y_q re/im) of the staged rows,
+// term 0 of each output being its c term.  ZC / ZS: known-zero top fractional digits of the
+// c / s coefficients of this pair (U_VARIANTS, chosen in phase R from the actual digits).
+template <int L, int ZC, int ZS>
+__device__ __forceinline__ void u_chunk(int32_t* F, int rows, int p, int q, int r, int lane, const int32_t* b,
+                                        const int32_t* wcoef, int mat, int flag) {
+  constexpr int CW = L + 1;
+#pragma unroll 1
+  for (int o = 0; o < 4; ++o) {
+    const bool hasInt = (flag >> (8 + mat * 4 + o)) & 1;
+    int64_t acc[L + 2];
+#pragma unroll
+    for (int c = 0; c < L + 2; ++c) acc[c] = 0;
+    const int32_t* Kp = wcoef + ((mat * 4 + o) * 3) * CW;
+    kmul_z<L, ZC>(acc, Kp, b + c_opidx[o][0] * L * 32 + lane, hasInt);
+    kmul_z<L, ZS>(acc, Kp + CW, b + c_opidx[o][1] * L * 32 + lane, hasInt);
+    kmul_z<L, ZS>(acc, Kp + 2 * CW, b + c_opidx[o][2] * L * 32 + lane, hasInt);
+    int32_t out[L];
+    tround2<L>(acc, out);
+    if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
+  }
+}
+// variants (ZC, ZS): 0 = (0, 0), 1 = (3, 1), 2 = (6, 3), 3 = (10, 6)
+__host__ __device__ constexpr int u_var_zc(int v) { return v == 0 ? 0 : v == 1 ? 3 : v == 2 ? 6 : 10; }
+__host__ __device__ constexpr int u_var_zs(int v) { return v == 0 ? 0 : v == 1 ? 1 : v == 2 ? 3 : 6; }
 
 // Staging buffers per warp and resident CTAs per SM of k_jacobi.  280 bits: double
 // buffering, 2 CTAs (16 warps, 128 registers).  The alternative of one buffer and 3 CTAs
@@ -865,6 +912,22 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
             for (int u = 0; u < 24; ++u)
               if ((vint >> (c_coefsrc[u] & 15)) & 1) ints |= 1 << (u / 3);
+            // zero top fractional digits of each value -> the U variant of A (values 0..5) and V (6..8)
+            int zv[9];
+            for (int v = 0; v < 9; ++v) {
+              int z = 0;
+              while (z < L && cf[v * CW + L - 1 - z] == 0) ++z;
+              zv[v] = z;
+            }
+            int varA = 0, varV = 0;
+            {
+              const int zc = min(zv[0], zv[5]), zs = min(min(zv[1], zv[2]), min(zv[3], zv[4]));
+              const int zcv = zv[6], zsv = min(zv[7], zv[8]);
+              for (int v = 3; v >= 1; --v)
+                if (u_var_zc(v) <= zc && u_var_zs(v) <= zs) { varA = v; break; }
+              for (int v = 3; v >= 1; --v)
+                if (u_var_zc(v) <= zcv && u_var_zs(v) <= zsv) { varV = v; break; }
+            }
             if (it.phase_cycles) {  // debug: digit products a leading-zero-aware U would need
               unsigned long long full = 0, need = 0;
               for (int u = 0; u < 12; ++u) {
@@ -892,7 +955,8 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             // by cancellation has an incremental alpha with absolute error ~2^-W alpha_old,
             // which could mark a still-significant column negligible for good.  The flag is
             // only set from exact norms (jac_norms at the end of the sweep).
-            flag = 1 | (ints << 8);
+            flag = 1 | (ints << 8) | (varA << 16) | (varV << 18);
+            if (it.phase_cycles) atomicAdd(&it.phase_cycles[6 + 128 + (sweep < 15 ? sweep : 15) * 4 + varA], 1ull);
             *(volatile int*)it.sync = 1;
             ++nrot;
             if (it.dbg) atomicAdd(&it.dbg[sweep < 63 ? sweep : 63], 1);
@@ -932,27 +996,11 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             __syncwarp();
             const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
             const int r = ch * 32 + lane;
-#pragma unroll 1
-            for (int o = 0; o < 4; ++o) {
-              const bool hasInt = (flag >> (8 + mat * 4 + o)) & 1;
-              int64_t acc[L + 2];
-#pragma unroll
-              for (int c = 0; c < L + 2; ++c) acc[c] = 0;
-#pragma unroll
-              for (int t = 0; t < 3; ++t) {
-                const int32_t* Kp = wcoef + ((mat * 4 + o) * 3 + t) * CW;
-                const int32_t* xp = b + c_opidx[o][t] * L * 32 + lane;
-                int32_t K[L + 1], x[L];
-#pragma unroll
-                for (int k = 0; k <= L; ++k) K[k] = Kp[k];
-#pragma unroll
-                for (int k = 0; k < L; ++k) x[k] = xp[k * 32];
-                kmul_acc<L>(acc, K, x, hasInt);
-              }
-              int32_t out[L];
-              tround2<L>(acc, out);
-              if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
-            }
+            const int var = (flag >> (16 + 2 * mat)) & 3;  // zero-digit variant (U_VARIANTS)
+            if (var == 0) u_chunk<L, 0, 0>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else if (var == 1) u_chunk<L, 3, 1>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else if (var == 2) u_chunk<L, 6, 3>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else u_chunk<L, (L < 10 ? L : 10), 6>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
             __syncwarp();
             if (JST == 1 && ch + 1 < nch) {
               stage_rows<L>(wbuf, F, rows, p, q, (ch + 1) * 32, rows, lane);

@@ -93,8 +93,8 @@ inline unsigned long long* phase_dbg() {
     const char* e = getenv("MPS_JACOBI_PHASES");
     on = e && atoi(e) ? 1 : 0;
     if (on) {
-      cudaMalloc(&d, (6 + 128) * sizeof(unsigned long long));
-      cudaMemset(d, 0, (6 + 128) * sizeof(unsigned long long));
+      cudaMalloc(&d, (6 + 128 + 64) * sizeof(unsigned long long));
+      cudaMemset(d, 0, (6 + 128 + 64) * sizeof(unsigned long long));
     }
   }
   return on ? d : nullptr;
@@ -350,7 +350,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   }
   prof_mark(PROF_JACOBI, 0, st);
   if (unsigned long long* pd = phase_dbg()) {
-    unsigned long long h[6 + 128];
+    unsigned long long h[6 + 128 + 64];
     cudaMemcpyAsync(h, pd, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "jacobi phase cycles (sum over CTAs): D %.4e R %.4e U %.4e norms %.4e init %.4e total %.4e\n",
@@ -359,6 +359,12 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
       if (h[6 + 2 * sw])
         fprintf(stderr, "  sweep %2d: U digit products per row %.4e, needed with leading-zero skipping %.4e (%.3f)\n", sw,
                 (double)h[6 + 2 * sw], (double)h[7 + 2 * sw], (double)h[7 + 2 * sw] / (double)h[6 + 2 * sw]);
+    for (int sw = 1; sw < 16; ++sw) {
+      const unsigned long long* v = h + 6 + 128 + 4 * sw;
+      if (v[0] + v[1] + v[2] + v[3])
+        fprintf(stderr, "  sweep %2d: rotations by U variant (0,0) %llu (3,1) %llu (6,3) %llu (10,6) %llu\n", sw, v[0], v[1],
+                v[2], v[3]);
+    }
     cudaMemsetAsync(pd, 0, sizeof(h), st);
   }
   prof_mark(PROF_FINALIZE, 1, st);
