@@ -339,7 +339,39 @@ struct GemmT {
   int64_t* eCcols;      // if non-null: eCcols[c] = *eCout for every column (Jacobi layout)
   int rows, cols, K, conjA, neg, addI;
   int* zerr;
+  // per-column mode (recovery of V, R16): B has column exponents eBcols[c]; column c of C is
+  // (digit sum shifted by ghead bits) x colcoef[c] ((L+1)-digit coefficient), at exponent
+  // eA + eBcols[c] + ghead + colexp[c], written to eCcols[c].  eCout is unused.
+  const int64_t* eBcols; const int32_t* colcoef; const int64_t* colexp; int ghead;
 };
+
+// per-column coefficient of the V recovery: 1/alpha_b = m 2^e, m in [0.5, 1) as L+1 digits
+template <int NL>
+struct RecItem {
+  int N;
+  const mpf<NL>* alpha;
+  int32_t* coef;  // [N][L+1]
+  int64_t* cexp;  // [N]
+};
+template <int L, int NL>
+__global__ void k_recover_coef(const RecItem<NL>* items) {
+  const RecItem<NL> it = items[blockIdx.y];
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < it.N; b += gridDim.x * blockDim.x) {
+    const mpf<NL> al = it.alpha[b];
+    int32_t kd[L + 1];
+    if (mpf_is_zero(al)) {
+#pragma unroll
+      for (int k = 0; k <= L; ++k) kd[k] = 0;
+      it.cexp[b] = INT64_MIN;  // zero column of V
+    } else {
+      const mpf<NL> inv = mpf_recip(al);
+      mpf_to_fixed<NL, L + 1>(mpf_ldexp(inv, -inv.e), 28, kd);
+      it.cexp[b] = inv.e;
+    }
+#pragma unroll
+    for (int k = 0; k <= L; ++k) it.coef[(size_t)b * (L + 1) + k] = kd[k];
+  }
+}
 
 // round V 2^-g / 2^(28L) for any -27 <= g <= 27
 template <int L>
@@ -383,12 +415,14 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG, "precision schedule");
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
+  if (it.rows <= 0 || it.cols <= 0) return;  // item without this GEMM
   const int tilesR = (it.rows + GT_TILE - 1) / GT_TILE, tilesC = (it.cols + GT_TILE - 1) / GT_TILE;
   const int tx = threadIdx.x % GT_TILE, ty = threadIdx.x / GT_TILE;
   __shared__ int32_t As[GT_KB][2][LG][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
   __shared__ int32_t Bs[GT_KB][2][LG][GT_TILE + 1];
-  const int64_t eC = *it.eCout;
-  const int g = (int)(eC - (*it.eA + *it.eB));
+  const bool percol = it.eBcols != nullptr;
+  const int64_t eC = percol ? 0 : *it.eCout;
+  const int g = percol ? it.ghead : (int)(eC - (*it.eA + *it.eB));
   int zbad = 0;
   for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
     const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;
@@ -449,6 +483,16 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
         tround_any<LG>(ri ? ai : ar, g, t);
 #pragma unroll
         for (int j = 0; j < L; ++j) o[j] = j >= D0 ? t[j - D0] : 0;
+        if (percol && it.colcoef) {  // x column coefficient (L+1 digits, fractional)
+          int32_t K[L + 1];
+#pragma unroll
+          for (int k = 0; k <= L; ++k) K[k] = it.colcoef[(size_t)c * (L + 1) + k];
+          int64_t acc2[L + 2];
+#pragma unroll
+          for (int j = 0; j < L + 2; ++j) acc2[j] = 0;
+          kmul_acc<L>(acc2, K, o, K[L] != 0);
+          tround2<L>(acc2, o);
+        }
         if (it.neg) {
 #pragma unroll
           for (int j = 0; j < L; ++j) o[j] = -o[j];
@@ -463,7 +507,11 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
         fx_balance<L>(o);
         stfx<L>(it.C, it.ldc, c, ri, r, o);
       }
-      if (it.eCcols && r == 0) it.eCcols[c] = eC;
+      if (it.eCcols && r == 0) {
+        if (!percol) it.eCcols[c] = eC;
+        else if (it.colexp && it.colexp[c] == INT64_MIN) it.eCcols[c] = 1;  // alpha_c = 0: zero column
+        else it.eCcols[c] = *it.eA + it.eBcols[c] + it.ghead + (it.colexp ? it.colexp[c] : 0);
+      }
     }
   }
   if (zbad && it.zerr) atomicOr(it.zerr, 2);  // 2: re-run without the preconditioner

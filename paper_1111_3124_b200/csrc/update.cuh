@@ -138,7 +138,7 @@ constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2
 template <int L>
 inline size_t pre_bytes(int M, int N) {
   return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
-         256;
+         256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N);  // + recovery coefficients
 }
 
 template <int L, int NL>
@@ -155,7 +155,8 @@ template <int L, int NL>
 inline size_t upd2_desc_bytes(int n) {
   return align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
          align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(sizeof(PreItem) * n) +
-         align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n);
+         align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n) + align_up(sizeof(RecItem<NL>) * n) +
+         align_up(sizeof(GemmT) * n);
 }
 
 template <class T>
@@ -177,13 +178,17 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   const size_t d_prep = 0, d_gemm = align_up(sizeof(PrepItem) * 2 * n),
                d_mix = d_gemm + align_up(sizeof(GemmItem) * n), d_svd = d_mix + align_up(sizeof(MixItem) * n),
                d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_pre = d_fin + align_up(sizeof(FinItem<NL>) * n),
-               d_gt = d_pre + align_up(sizeof(PreItem) * n), d_end = upd2_desc_bytes<L, NL>(n);
+               d_gt = d_pre + align_up(sizeof(PreItem) * n),
+               d_rec = d_gt + align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n),
+               d_rg = d_rec + align_up(sizeof(RecItem<NL>) * n), d_end = upd2_desc_bytes<L, NL>(n);
   constexpr int NSIT = ns_iters<L>();
   const bool pre = use_precond();
   int* redo = (int*)(base + d_end);  // [n] flags (run_update2)
   hd.assign(d_end, 0);
   PreItem* hpre = (PreItem*)(hd.data() + d_pre);
   GemmT* hgt = (GemmT*)(hd.data() + d_gt);  // [2 NSIT + 1][n]: D_k, X_k+1 per iteration, then A_1
+  RecItem<NL>* hrec = (RecItem<NL>*)(hd.data() + d_rec);
+  GemmT* hrg = (GemmT*)(hd.data() + d_rg);  // V = Theta'^H A_final diag(1/alpha) (tiled GEMM)
   PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
   GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
@@ -224,6 +229,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     int* sweeps_d = (int*)(pq + 8);
     int64_t* eOne = (int64_t*)(pq + 16);
     int64_t* eA1 = (int64_t*)(pq + 32);
+    int32_t* rcoef = (int32_t*)(pq + 256);
+    int64_t* rexp = (int64_t*)((char*)rcoef + align_up(4 * (size_t)N * (L + 1)));
     int32_t* Xfin = (NSIT % 2) ? Xb : Xa;
     const bool pb = pre && !g.no_precond;
     int64_t* eL = S.e_misc;
@@ -262,6 +269,16 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     si.a0_ready = pb ? 1 : 0;
     if (pb && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
+    {
+      int gh = 1;
+      while ((1 << (gh - 1)) < M) ++gh;
+      gh += 1;  // sum of M complex products, each |.| < 2^(e0 + e_b + 1)
+      hrec[b] = RecItem<NL>{recover ? N : 0, S.alpha, rcoef, rexp};
+      hrg[b] = recover ? GemmT{A0f, M, si.eA0, Af, M, nullptr, Vf, N, nullptr, nullptr, eV, N, N, M, 1, 0, 0, nullptr,
+                               S.eA, rcoef, rexp, gh}
+                       : GemmT{nullptr, 1, nullptr, nullptr, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr, 0, 0, 0,
+                               0, 0, 0, nullptr, nullptr, nullptr, nullptr, 0};
+    }
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));
@@ -340,8 +357,13 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   {
     int maxNN = 0;
     for (int b = 0; b < n; ++b) maxNN = std::max(maxNN, hs[b].N * hs[b].N);
-    dim3 gr(std::max(1, std::min(64, (maxNN + 127) / 128)), n);
-    k_recover_v<L, NL><<<gr, 128, 0, st>>>((const SvdItem<NL>*)(base + d_svd));
+    int maxNr = 0;
+    for (int b = 0; b < n; ++b) maxNr = std::max(maxNr, hs[b].N);
+    (void)maxNN;
+    k_recover_coef<L, NL><<<dim3(std::max(1, (maxNr + 127) / 128), n), 128, 0, st>>>((const RecItem<NL>*)(base + d_rec));
+    ++nl;
+    const int tR = ((maxNr + GT_TILE - 1) / GT_TILE) * ((maxNr + GT_TILE - 1) / GT_TILE);
+    k_gemm_t<L, L, 0><<<dim3(std::max(1, std::min(tR, 1024)), n), 256, 0, st>>>((const GemmT*)(base + d_rg));
     ++nl;
     if (unsigned long long* pc = prof_counts()) {
       k_accum_stats<NL><<<(n + 127) / 128, 128, 0, st>>>((const SvdItem<NL>*)(base + d_svd), n, pc);
