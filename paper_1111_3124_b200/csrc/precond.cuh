@@ -138,12 +138,16 @@ static __global__ void __launch_bounds__(256) k_jacobi_d(const PreItem* items) {
 // HBM/L2 traffic per outer sweep drops from O(N^2 M) to O(N M N/bs) (the warp-per-pair
 // kernel above was bandwidth bound at 15% of the update).
 __host__ __device__ inline int jd_bs(int M) { return M <= 320 ? 16 : 8; }
+constexpr int JD_THREADS = 512;
+#ifndef JD_TOL
+#define JD_TOL (4.0 * M * 1.1102230246251565e-16)  // 4 M 2^-53 (1e-12 costs a p-bit sweep)
+#endif  // one warp per pair of a block pair's inner step (bs <= 16)
 inline size_t jd_smem(int M) {
   const int bs = jd_bs(M);
   return (size_t)2 * bs * M * 16 + (size_t)4 * bs * bs * 16 + 64;
 }
 
-static __global__ void __launch_bounds__(256) k_jacobi_db(const PreItem* items) {
+static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* items) {
   const PreItem it = items[blockIdx.x];
   const int M = it.M, N = it.N;
   if (N == 0) return;
@@ -157,7 +161,7 @@ static __global__ void __launch_bounds__(256) k_jacobi_db(const PreItem* items) 
   double2* V = it.Vd;
   for (int t = threadIdx.x; t < N * N; t += blockDim.x)
     V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
-  const double tol = 4.0 * M * 1.1102230246251565e-16;
+  const double tol = JD_TOL;
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
     if (threadIdx.x == 0) s_any = 0;
@@ -181,7 +185,7 @@ static __global__ void __launch_bounds__(256) k_jacobi_db(const PreItem* items) 
           W[t] = make_double2((t % nc2) == (t / nc2) ? 1.0 : 0.0, 0.0);
         __syncthreads();
         for (int s2 = 0; s2 < nc2 - 1; ++s2) {
-          for (int i = warp; i < bs; i += 8) {
+          for (int i = warp; i < bs; i += JD_THREADS / 32) {
             int p, q;
             rr_pair(nc2, s2, i, p, q);
             if (s_col[p] < 0 || s_col[q] < 0) continue;

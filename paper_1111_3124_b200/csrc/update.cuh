@@ -323,7 +323,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
         cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
       }
-      k_jacobi_db<<<n, 256, jd_smem(maxM), st>>>(dpre); ++nl;
+      k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre); ++nl;
     }
     k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
     const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
