@@ -187,14 +187,20 @@ int mps_update_batch_device(int prec_bits, int chi, int chi_max, int batch, doub
 int mps_last_launch_count(void);
 
 /* ---- measurement: CUDA events around the kernel classes of the batch path, on the
- * launching stream.  which: 0 Jacobi SVD (a3), 1 contraction+gate (a1-a2), 2 truncate+split
- * (a4-a5).  enable(1) clears and starts recording; query syncs and sums the durations. */
+ * launching stream.  which: 0 p-bit Jacobi SVD kernel (a3), 1 contraction+gate (a1-a2),
+ * 2 truncate+split (a4-a5), 3 binary64 preconditioner + Newton-Schulz + A_1 = Theta' X
+ * (R19), 4 recovery of V (R16).  enable(1) clears and starts recording; query
+ * syncs and sums the durations. */
 int mps_profile_enable(int on);
 int mps_profile_query(int which, double* total_ms, int* launches);
 /* Totals over the Jacobi problems run since mps_profile_enable(1): [0] rotations applied,
  * [1] pair evaluations (gamma computed), [2] sum (sweeps+1) M N (norm passes),
- * [3] sum N N M (recovery of V).  Used to count the executed IMAD.WIDE of the kernel. */
+ * [3] sum N N M (recovery of V), [4] digit products executed by the rotation phase
+ * (zero-digit variants counted exactly).  mps_profile_counts returns [0..3],
+ * mps_profile_counts_n the first n (1..8; [5..7] reserved, 0).  Used to count the executed
+ * IMAD.WIDE of the Jacobi kernel. */
 int mps_profile_counts(long long* out4);
+int mps_profile_counts_n(long long* out, int n);
 
 /* ---- kernel test surface --------------------------------------------------------
  * One-sided Jacobi SVD (a3) of `batch` column-major M x N complex matrices (host

@@ -20,7 +20,7 @@ STATUS = {0: "MPS_OK", -1: "MPS_EINVAL", -2: "MPS_ENOTUNITARY", -3: "MPS_ENOCONV
           -10: "MPS_ETOOBIG"}
 
 # every symbol include/mps_b200.h declares
-EXPORTS = ["mps_profile_counts", "mps_rdo", "mps_init_block", "mps_block_dims", "mps_block_export_first", "mps_block_boundary_apply",
+EXPORTS = ["mps_profile_counts", "mps_profile_counts_n", "mps_rdo", "mps_init_block", "mps_block_dims", "mps_block_export_first", "mps_block_boundary_apply",
            "mps_block_import_first", "mps_amplitude_block", "mps_record_bytes", "mps_strerror", "mps_max_chi", "mps_init", "mps_free", "mps_set_stream",
            "mps_apply_gate", "mps_apply_layer", "mps_amplitude", "mps_expect", "mps_norm2", "mps_to_dense",
            "mps_sync", "mps_n_qubits", "mps_bond_dims", "mps_schmidt", "mps_get_site", "mps_set_schmidt",
@@ -161,16 +161,16 @@ def debug_mpf(p: int, op: str, a, b=None):
     return out
 
 
-PROF_JACOBI, PROF_CONTRACT, PROF_FINALIZE = 0, 1, 2
+PROF_JACOBI, PROF_CONTRACT, PROF_FINALIZE, PROF_PRECOND, PROF_RECOVER = 0, 1, 2, 3, 4
 
 
 def profile_enable(on: bool = True):
     _chk(lib().mps_profile_enable(1 if on else 0))
 
 
-def profile_counts():
-    out = (ctypes.c_longlong * 4)()
-    _chk(lib().mps_profile_counts(out))
+def profile_counts(n: int = 5):
+    out = (ctypes.c_longlong * n)()
+    _chk(lib().mps_profile_counts_n(out, n))
     return list(out)
 
 

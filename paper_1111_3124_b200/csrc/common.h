@@ -25,7 +25,7 @@ struct BatchOut {  // device pointers (records unless stated)
 };
 
 // Optional CUDA-event bracketing of individual kernels (bench.py roofline): which = kernel id.
-enum { PROF_JACOBI = 0, PROF_CONTRACT = 1, PROF_FINALIZE = 2, PROF_PRECOND = 3, PROF_N = 4 };
+enum { PROF_JACOBI = 0, PROF_CONTRACT = 1, PROF_FINALIZE = 2, PROF_PRECOND = 3, PROF_RECOVER = 4, PROF_N = 5 };
 void prof_mark(int which, int begin, cudaStream_t st);
 // device buffer of 4 running totals while profiling is on (else null), see k_accum_stats
 unsigned long long* prof_counts();

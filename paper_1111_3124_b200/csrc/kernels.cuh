@@ -86,6 +86,7 @@ struct SvdItem {
   int64_t* eV;              // [N] exponents of the recovered V columns
   int a0_ready;             // 1: A0 / eA0 were written by the producer (k_build_m2, k_mix), not copied here
   int v_preset;             // accumulating: V already holds the starting basis (preconditioner X), not I
+  long long* uprod;         // null, or out: executed phase-U digit products per row (profiling)
   long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
 };
 
@@ -697,7 +698,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
   static_assert(2 * (L + 2) * 32 * 8 <= (JST * STAGE + 24 * CW) * 4, "phase-D column sums must fit the warp's buffers");
   __shared__ mpf<NL> s_red[1];
 
-  if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; }
+  if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; if (it.uprod) *it.uprod = 0; }
   const bool accV = it.A0 == nullptr;
   if (!accV && !it.a0_ready) {  // keep the input (block exponent from k_mix) for the recovery of V
     const size_t nw = (size_t)M * N * 2 * L;
@@ -743,7 +744,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
   const int nchA = (M + 31) / 32, nchV = (N + 31) / 32;
 
   int sweep = 0, conv = 0;
-  long long nrot = 0, nev = 0;
+  long long nrot = 0, nev = 0, nup = 0;
   const bool prof = it.phase_cycles != nullptr && tid == 0;
   unsigned long long pc[6] = {0, 0, 0, 0, 0, 0};
   long long t_start = clock64(), t_mark = t_start;
@@ -956,6 +957,18 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             // which could mark a still-significant column negligible for good.  The flag is
             // only set from exact norms (jac_norms at the end of the sweep).
             flag = 1 | (ints << 8) | (varA << 16) | (varV << 18);
+            if (it.uprod) {  // digit products phase U will execute per row (kmul_z counts)
+              auto P = [](int Z) {
+                int c = 0;
+                for (int i = 0; i < L - Z; ++i) c += (i >= L - 2) ? L : i + 2;
+                return c;
+              };
+              for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
+                const int v = mat ? varV : varA;
+                for (int o = 0; o < 4; ++o)
+                  nup += P(u_var_zc(v)) + 2 * P(u_var_zs(v)) + (((ints >> (mat * 4 + o)) & 1) ? 3 * L : 0);
+              }
+            }
             if (it.phase_cycles) atomicAdd(&it.phase_cycles[6 + 128 + (sweep < 15 ? sweep : 15) * 4 + varA], 1ull);
             *(volatile int*)it.sync = 1;
             ++nrot;
@@ -1022,6 +1035,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
   }
   atomicAdd((unsigned long long*)it.rotations, (unsigned long long)nrot);
   atomicAdd((unsigned long long*)it.evals, (unsigned long long)nev);
+  if (it.uprod) atomicAdd((unsigned long long*)it.uprod, (unsigned long long)nup);
   if (prof) {
     pc[5] = (unsigned long long)(clock64() - t_start);
     for (int i = 0; i < 6; ++i) atomicAdd(&it.phase_cycles[i], pc[i]);
@@ -1097,6 +1111,7 @@ __global__ void k_accum_stats(const SvdItem<NL>* items, int n, unsigned long lon
     atomicAdd(&tot[1], (unsigned long long)*it.evals);
     atomicAdd(&tot[2], (unsigned long long)(*it.sweeps + 1) * it.M * it.N);
     if (it.A0) atomicAdd(&tot[3], (unsigned long long)it.N * it.N * it.M);
+    if (it.uprod) atomicAdd(&tot[4], (unsigned long long)*it.uprod * it.M);
   }
 }
 

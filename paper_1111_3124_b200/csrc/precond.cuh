@@ -347,6 +347,7 @@ struct GemmT {
   // (digit sum shifted by ghead bits) x colcoef[c] ((L+1)-digit coefficient), at exponent
   // eA + eBcols[c] + ghead + colexp[c], written to eCcols[c].  eCout is unused.
   const int64_t* eBcols; const int32_t* colcoef; const int64_t* colexp; int ghead;
+  int herm;  // C is Hermitian (X^H X): only tiles on/above the diagonal are computed, mirrored
 };
 
 // per-column coefficient of the V recovery: 1/alpha_b = m 2^e, m in [0.5, 1) as L+1 digits
@@ -430,6 +431,7 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
   int zbad = 0;
   for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
     const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;
+    if (it.herm && c0 < r0) continue;  // block-uniform: the mirror tile writes these
     const int r = r0 + tx, c = c0 + ty;
     int64_t ar[LG + 2], ai[LG + 2];
 #pragma unroll
@@ -510,6 +512,13 @@ __global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
         }
         fx_balance<L>(o);
         stfx<L>(it.C, it.ldc, c, ri, r, o);
+        if (it.herm && c0 != r0) {  // C(c, r) = conj C(r, c)
+          if (ri) {
+#pragma unroll
+            for (int j = 0; j < L; ++j) o[j] = -o[j];
+          }
+          stfx<L>(it.C, it.ldc, r, ri, c, o);
+        }
       }
       if (it.eCcols && r == 0) {
         if (!percol) it.eCcols[c] = eC;

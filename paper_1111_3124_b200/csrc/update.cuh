@@ -39,6 +39,7 @@ struct SvdScratch {
   int64_t* eA; mpf<NL>* alpha; mpf<NL>* gam; mpf<NL>* inv_sig; mpf<NL>* lam; int32_t* coef;
   int* rot; int* negl; int* ord; int* status; int* sweeps; int* fstatus; int* k; long long* rots;
   int64_t* e_misc;  // 4 spare exponents
+  long long* uprod; // executed digit products of phase U per row (profiling)
   int* sync;
   mpf<NL>* zbuf;
   static size_t bytes(int N) {
@@ -67,6 +68,7 @@ struct SvdScratch {
     s.rots = (long long*)(q + 16);
     s.e_misc = (int64_t*)(q + 32);
     s.sync = (int*)(q + 64);
+    s.uprod = (long long*)(q + 72);
     s.zbuf = (mpf<NL>*)(q + 128);
     return s;
   }
@@ -253,7 +255,9 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
         int32_t* Xc = (k % 2) ? Xb : Xa;
         int32_t* Xn = (k % 2) ? Xa : Xb;
         // D = I - X^H X (exponent 1);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
-        hgt[(2 * k) * n + b] = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
+        GemmT gd = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
+        gd.herm = 1;
+        hgt[(2 * k) * n + b] = gd;
         hgt[(2 * k + 1) * n + b] =
             GemmT{Xc, N, eOne, Dm, N, eOne + 1, Xn, N, eOne, Xc, nullptr, N, N, N, 0, 0, 0, redo + b};
       }
@@ -266,6 +270,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; si.rotations = S.rots;
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
     const bool recover = !force_accumulate_v() && !g.accumulate_v;
+    si.uprod = S.uprod;
     si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     si.a0_ready = pb ? 1 : 0;
     if (pb && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
@@ -357,6 +362,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   {
     int maxNN = 0;
     for (int b = 0; b < n; ++b) maxNN = std::max(maxNN, hs[b].N * hs[b].N);
+    prof_mark(PROF_JACOBI, 0, st);
+    prof_mark(PROF_RECOVER, 1, st);
     int maxNr = 0;
     for (int b = 0; b < n; ++b) maxNr = std::max(maxNr, hs[b].N);
     (void)maxNN;
@@ -370,7 +377,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
       ++nl;
     }
   }
-  prof_mark(PROF_JACOBI, 0, st);
+  prof_mark(PROF_RECOVER, 0, st);
   if (unsigned long long* pd = phase_dbg()) {
     unsigned long long h[6 + 128 + 64];
     cudaMemcpyAsync(h, pd, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -546,6 +553,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   const Upd3Rec<L, NL> rec(base + d_end, a);
   si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr;
   const bool recover = !force_accumulate_v() && !a.accumulate_v;
+  si.uprod = S1.uprod;
   si.A0 = recover ? rec.A0a : nullptr; si.eA0 = rec.eA0a; si.eV = rec.eVa; si.evals = S1.rots + 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
@@ -636,6 +644,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   const Upd3Rec<L, NL> rec(base + d_end, a);
   si.sweeps = S2.sweeps; si.rotations = S2.rots; si.sync = S2.sync; si.zbuf = S2.zbuf; si.phase_cycles = nullptr;
   const bool recover = !force_accumulate_v() && !a.accumulate_v;
+  si.uprod = S2.uprod;
   si.A0 = recover ? rec.A0b : nullptr; si.eA0 = rec.eA0b; si.eV = rec.eVb; si.evals = S2.rots + 1; si.a0_ready = 1;
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
