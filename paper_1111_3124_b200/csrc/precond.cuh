@@ -416,7 +416,7 @@ __device__ __forceinline__ void tmul_z(int64_t (&acc)[LG + 2], const int32_t (&x
 constexpr int GT_TILE = 16, GT_KB = 8;
 
 template <int L, int LG, int Z>
-__global__ void __launch_bounds__(256) k_gemm_t(const GemmT* items) {
+__global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG, "precision schedule");
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
