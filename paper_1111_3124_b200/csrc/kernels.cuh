@@ -644,14 +644,14 @@ __device__ __forceinline__ void u_chunk(int32_t* F, int rows, int p, int q, int 
   constexpr int CW = L + 1;
 #pragma unroll 1
   for (int o = 0; o < 4; ++o) {
-    const bool hasInt = (flag >> (8 + mat * 4 + o)) & 1;
+    const int ib = 8 + (mat * 4 + o) * 3;  // integer-digit bits of this output's three slots
     int64_t acc[L + 2];
 #pragma unroll
     for (int c = 0; c < L + 2; ++c) acc[c] = 0;
     const int32_t* Kp = wcoef + ((mat * 4 + o) * 3) * CW;
-    kmul_z<L, ZC>(acc, Kp, b + c_opidx[o][0] * L * 32 + lane, hasInt);
-    kmul_z<L, ZS>(acc, Kp + CW, b + c_opidx[o][1] * L * 32 + lane, hasInt);
-    kmul_z<L, ZS>(acc, Kp + 2 * CW, b + c_opidx[o][2] * L * 32 + lane, hasInt);
+    kmul_z<L, ZC>(acc, Kp, b + c_opidx[o][0] * L * 32 + lane, (flag >> ib) & 1);
+    kmul_z<L, ZS>(acc, Kp + CW, b + c_opidx[o][1] * L * 32 + lane, (flag >> (ib + 1)) & 1);
+    kmul_z<L, ZS>(acc, Kp + 2 * CW, b + c_opidx[o][2] * L * 32 + lane, (flag >> (ib + 2)) & 1);
     int32_t out[L];
     tround2<L>(acc, out);
     if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
@@ -910,9 +910,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
               for (int k = 0; k <= L; ++k) cf[v * CW + k] = dg[k];
               if (dg[L]) vint |= 1 << v;
             }
-            int ints = 0;  // bit (mat*4 + o): some coefficient of output o has an integer digit
+            int ints = 0;  // bit u: slot u's coefficient has an integer digit
             for (int u = 0; u < 24; ++u)
-              if ((vint >> (c_coefsrc[u] & 15)) & 1) ints |= 1 << (u / 3);
+              if ((vint >> (c_coefsrc[u] & 15)) & 1) ints |= 1 << u;
             // zero top fractional digits of each value -> the U variant of A (values 0..5) and V (6..8)
             int zv[9];
             for (int v = 0; v < 9; ++v) {
@@ -956,7 +956,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             // by cancellation has an incremental alpha with absolute error ~2^-W alpha_old,
             // which could mark a still-significant column negligible for good.  The flag is
             // only set from exact norms (jac_norms at the end of the sweep).
-            flag = 1 | (ints << 8) | (varA << 16) | (varV << 18);
+            flag = 1 | (varA << 1) | (varV << 3) | (ints << 8);  // bits 8..31: slot integer digits
             if (it.uprod) {  // digit products phase U will execute per row (kmul_z counts)
               auto P = [](int Z) {
                 int c = 0;
@@ -966,7 +966,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
               for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
                 const int v = mat ? varV : varA;
                 for (int o = 0; o < 4; ++o)
-                  nup += P(u_var_zc(v)) + 2 * P(u_var_zs(v)) + (((ints >> (mat * 4 + o)) & 1) ? 3 * L : 0);
+                  nup += P(u_var_zc(v)) + 2 * P(u_var_zs(v)) + L * __popc((ints >> ((mat * 4 + o) * 3)) & 7);
               }
             }
             if (it.phase_cycles) atomicAdd(&it.phase_cycles[6 + 128 + (sweep < 15 ? sweep : 15) * 4 + varA], 1ull);
@@ -1009,7 +1009,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             __syncwarp();
             const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
             const int r = ch * 32 + lane;
-            const int var = (flag >> (16 + 2 * mat)) & 3;  // zero-digit variant (U_VARIANTS)
+            const int var = (flag >> (1 + 2 * mat)) & 3;  // zero-digit variant (U_VARIANTS)
             if (var == 0) u_chunk<L, 0, 0>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
             else if (var == 1) u_chunk<L, 3, 1>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
             else if (var == 2) u_chunk<L, 6, 3>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
