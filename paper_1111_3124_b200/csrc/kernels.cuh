@@ -12,6 +12,7 @@
 
 #include <cooperative_groups.h>
 
+#include <climits>
 #include <cstdlib>
 
 #include "common.h"
@@ -87,6 +88,8 @@ struct SvdItem {
   int a0_ready;             // 1: A0 / eA0 were written by the producer (k_build_m2, k_mix), not copied here
   int v_preset;             // accumulating: V already holds the starting basis (preconditioner X), not I
   long long* uprod;         // null, or out: executed phase-U digit products per row (profiling)
+  int* gexp;                // [2] scratch: max log2(|gamma|^2 / (alpha_p alpha_q)) of a sweep (by parity)
+  int e2_hint;              // < 0: expected log2 of that ratio before sweep 1 (preconditioned); 0: none
   long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
 };
 
@@ -592,7 +595,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
 // fixed matrix into buf[4][L][32] (one row per lane of the consumer).  When ld is a
 // multiple of 4 words each lane moves 16 bytes (4 rows of one digit plane): lanes 8o..8o+7
 // copy operand o, L copies per lane; otherwise one 4-byte copy per row and plane.
-template <int L>
+// LG (<= L): only the top LG digits of each value are staged, as buf[4][LG][32].
+template <int L, int LG = L>
 __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int ld, int p, int q, int row0, int rows,
                                           int lane) {
   if ((ld & 3) == 0) {
@@ -601,10 +605,10 @@ __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int l
     const int r = row0 + 4 * sub;
     int nv = rows - r;
     nv = nv < 0 ? 0 : (nv > 4 ? 4 : nv);
-    const int32_t* g = F + ((size_t)(col * 2 + ri) * L) * ld + (nv ? r : 0);
-    int32_t* d = buf + op * L * 32 + 4 * sub;
+    const int32_t* g = F + ((size_t)(col * 2 + ri) * L + (L - LG)) * ld + (nv ? r : 0);
+    int32_t* d = buf + op * LG * 32 + 4 * sub;
 #pragma unroll
-    for (int k = 0; k < L; ++k) {
+    for (int k = 0; k < LG; ++k) {
       cp_async16(d + k * 32, g, 4 * nv);
       g += ld;
     }
@@ -616,9 +620,9 @@ __device__ __forceinline__ void stage_rows(int32_t* buf, const int32_t* F, int l
 #pragma unroll
   for (int op = 0; op < 4; ++op) {
     const int col = op < 2 ? p : q, ri = op & 1;
-    const int32_t* g = F + ((size_t)(col * 2 + ri) * L) * ld + rr;
+    const int32_t* g = F + ((size_t)(col * 2 + ri) * L + (L - LG)) * ld + rr;
 #pragma unroll
-    for (int k = 0; k < L; ++k) cp_async4(buf + (op * L + k) * 32 + lane, g + (size_t)k * ld, ok);
+    for (int k = 0; k < LG; ++k) cp_async4(buf + (op * LG + k) * 32 + lane, g + (size_t)k * ld, ok);
   }
 }
 
@@ -657,6 +661,84 @@ __device__ __forceinline__ void u_chunk(int32_t* F, int rows, int p, int q, int 
     if (r < rows) stfx<L>(F, rows, o < 2 ? p : q, o & 1, r, out);
   }
 }
+// Phase D for one pair: gamma = sum_r conj(a_p(r)) a_q(r) from the top LG digits of the
+// columns (a truncated LG-digit product: absolute error ~2^-(28 LG - 6) ||a_p|| ||a_q||).
+// LG < L in the sweeps where the off-diagonal is still large (R20); the sweep that
+// ends the iteration always uses LG = L.
+template <int L, int NL, int LG, int JST>
+__device__ __forceinline__ void d_pair(const SvdItem<NL>& it, int32_t* wbuf, int p, int q, int i, int lane, int nchA) {
+  constexpr int STAGE = 4 * L * 32;
+  const int M = it.M;
+  int64_t gr[LG + 2], gi[LG + 2];
+#pragma unroll
+  for (int c = 0; c < LG + 2; ++c) gr[c] = gi[c] = 0;
+  stage_rows<L, LG>(wbuf, it.A, M, p, q, 0, M, lane);
+  cp_commit();
+  for (int ch = 0; ch < nchA; ++ch) {
+    if (JST == 2 && ch + 1 < nchA) {
+      stage_rows<L, LG>(wbuf + ((ch + 1) & 1) * STAGE, it.A, M, p, q, (ch + 1) * 32, M, lane);
+      cp_commit();
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncwarp();
+    const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
+    int32_t xa[LG], xb[LG];
+    // rows past M were zero-filled: their products vanish
+#pragma unroll
+    for (int k = 0; k < LG; ++k) { xa[k] = b[(0 * LG + k) * 32 + lane]; xb[k] = b[(2 * LG + k) * 32 + lane]; }
+    tmul_acc2<LG>(gr, xa, xb);  // xrp xrq
+#pragma unroll
+    for (int k = 0; k < LG; ++k) xb[k] = b[(3 * LG + k) * 32 + lane];
+    tmul_acc2<LG>(gi, xa, xb);  // xrp xiq
+#pragma unroll
+    for (int k = 0; k < LG; ++k) xa[k] = b[(1 * LG + k) * 32 + lane];
+    tmul_acc2<LG>(gr, xa, xb);  // xip xiq
+#pragma unroll
+    for (int k = 0; k < LG; ++k) xb[k] = b[(2 * LG + k) * 32 + lane];
+    tmul_sub2<LG>(gi, xa, xb);  // - xip xrq
+    if ((ch & 7) == 7) { tnorm2<LG>(gr); tnorm2<LG>(gi); }
+    __syncwarp();
+    if (JST == 1 && ch + 1 < nchA) {
+      stage_rows<L, LG>(wbuf, it.A, M, p, q, (ch + 1) * 32, M, lane);
+      cp_commit();
+    }
+  }
+  tnorm2<LG>(gr);
+  tnorm2<LG>(gi);
+  // cross-lane column sums through shared memory (the staging buffer is free now):
+  // lane l writes its 2(LG+2) columns, lanes 0..2(LG+2)-1 each sum one column over 32 lanes
+  int64_t* red = (int64_t*)wbuf;  // [2(LG+2)][32]
+  __syncwarp();
+#pragma unroll
+  for (int c = 0; c < LG + 2; ++c) { red[c * 32 + lane] = gr[c]; red[(LG + 2 + c) * 32 + lane] = gi[c]; }
+  __syncwarp();
+  int64_t sum[2] = {0, 0};  // 2(LG+2) columns over 32 lanes (two rounds when LG > 14)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < 2 * (LG + 2)) {
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) sum[h] += red[c * 32 + ((l + lane) & 31)];
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    if (lane + 32 * h < 2 * (LG + 2)) red[lane + 32 * h] = sum[h];
+  __syncwarp();
+  // lane 0 converts gamma_re, lane 1 gamma_im (in parallel)
+  if (lane < 2) {
+    int64_t cols[LG + 2];
+#pragma unroll
+    for (int c = 0; c < LG + 2; ++c) cols[c] = red[lane * (LG + 2) + c];
+    const int64_t E0 = 28 * (int64_t)(LG - 2) + it.eA[p] + it.eA[q] - 2 * 28 * (int64_t)LG;
+    it.gam[2 * i + lane] = mpf_from_cols<NL, LG + 2>(cols, E0);
+  }
+  __syncwarp();
+}
+
 // variants (ZC, ZS): 0 = (0, 0), 1 = (3, 1), 2 = (6, 3), 3 = (10, 6)
 __host__ __device__ constexpr int u_var_zc(int v) { return v == 0 ? 0 : v == 1 ? 3 : v == 2 ? 6 : 10; }
 __host__ __device__ constexpr int u_var_zs(int v) { return v == 0 ? 0 : v == 1 ? 1 : v == 2 ? 3 : 6; }
@@ -756,8 +838,23 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
     }
   };
   mark(4);
+  // digits of the dot products per sweep (R20): sweep k+1 needs gamma to ~eps_k^2 where
+  // eps_k ~ (largest |gamma|/sqrt(alpha_p alpha_q) of sweep k)^2; a reduced sweep never ends
+  // the iteration
+  int e2prev = it.e2_hint;
   for (sweep = 1; sweep <= MAX_SWEEPS; ++sweep) {
-    if (crank == 0 && tid == 0) *(volatile int*)it.sync = 0;
+    int lgd = L;
+    // only the first two sweeps of a preconditioned iteration may be reduced (bounded: the
+    // iteration then proceeds exactly as without R20)
+    if (it.gexp && it.e2_hint < 0 && sweep <= 2 && e2prev > -100000) {  // INT_MIN: no evaluated pair
+      const int64_t need = -2 * (int64_t)e2prev + 8;  // bits
+      lgd = need <= 28 * 4 ? 4 : (need <= 28 * 7 ? 7 : L);
+      if (lgd > L) lgd = L;
+    }
+    if (crank == 0 && tid == 0) {
+      *(volatile int*)it.sync = 0;
+      if (it.gexp) it.gexp[sweep & 1] = INT_MIN;
+    }
     csync();
     for (int step = 0; step < N - 1; ++step) {
       // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows, cp.async staging)
@@ -765,76 +862,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
         int p, q;
         rr_pair(N, step, i, p, q);
         if (it.negl[p] || it.negl[q]) continue;
-        int64_t gr[L + 2], gi[L + 2];
-#pragma unroll
-        for (int c = 0; c < L + 2; ++c) gr[c] = gi[c] = 0;
-        stage_rows<L>(wbuf, it.A, M, p, q, 0, M, lane);
-        cp_commit();
-        for (int ch = 0; ch < nchA; ++ch) {
-          if (JST == 2 && ch + 1 < nchA) {
-            stage_rows<L>(wbuf + ((ch + 1) & 1) * STAGE, it.A, M, p, q, (ch + 1) * 32, M, lane);
-            cp_commit();
-            cp_wait<1>();
-          } else {
-            cp_wait<0>();
-          }
-          __syncwarp();
-          const int32_t* b = wbuf + (JST == 2 ? (ch & 1) * STAGE : 0);
-          int32_t xa[L], xb[L];
-          // rows past M were zero-filled: their products vanish
-#pragma unroll
-          for (int k = 0; k < L; ++k) { xa[k] = b[(0 * L + k) * 32 + lane]; xb[k] = b[(2 * L + k) * 32 + lane]; }
-          tmul_acc2<L>(gr, xa, xb);  // xrp xrq
-#pragma unroll
-          for (int k = 0; k < L; ++k) xb[k] = b[(3 * L + k) * 32 + lane];
-          tmul_acc2<L>(gi, xa, xb);  // xrp xiq
-#pragma unroll
-          for (int k = 0; k < L; ++k) xa[k] = b[(1 * L + k) * 32 + lane];
-          tmul_acc2<L>(gr, xa, xb);  // xip xiq
-#pragma unroll
-          for (int k = 0; k < L; ++k) xb[k] = b[(2 * L + k) * 32 + lane];
-          tmul_sub2<L>(gi, xa, xb);  // - xip xrq
-          if ((ch & 7) == 7) { tnorm2<L>(gr); tnorm2<L>(gi); }
-          __syncwarp();
-          if (JST == 1 && ch + 1 < nchA) {
-            stage_rows<L>(wbuf, it.A, M, p, q, (ch + 1) * 32, M, lane);
-            cp_commit();
-          }
-        }
-        tnorm2<L>(gr);
-        tnorm2<L>(gi);
-        // cross-lane column sums through shared memory (the staging buffer is free now):
-        // lane l writes its 2(L+2) columns, lanes 0..2(L+2)-1 each sum one column over 32 lanes
-        {
-          int64_t* red = (int64_t*)wbuf;  // [2(L+2)][32]
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < L + 2; ++c) { red[c * 32 + lane] = gr[c]; red[(L + 2 + c) * 32 + lane] = gi[c]; }
-          __syncwarp();
-          int64_t sum[2] = {0, 0};  // 2(L+2) columns over 32 lanes (two rounds when L > 14)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int c = lane + 32 * h;
-            if (c < 2 * (L + 2)) {
-#pragma unroll 8
-              for (int l = 0; l < 32; ++l) sum[h] += red[c * 32 + ((l + lane) & 31)];
-            }
-          }
-          __syncwarp();
-#pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (lane + 32 * h < 2 * (L + 2)) red[lane + 32 * h] = sum[h];
-          __syncwarp();
-          // lane 0 converts gamma_re, lane 1 gamma_im (in parallel)
-          if (lane < 2) {
-            int64_t cols[L + 2];
-#pragma unroll
-            for (int c = 0; c < L + 2; ++c) cols[c] = red[lane * (L + 2) + c];
-            const int64_t E0 = 28 * (int64_t)(L - 2) + it.eA[p] + it.eA[q] - 2 * (int64_t)W;
-            it.gam[2 * i + lane] = mpf_from_cols<NL, L + 2>(cols, E0);
-          }
-          __syncwarp();
-        }
+        if (lgd == 4) d_pair<L, NL, 4, JST>(it, wbuf, p, q, i, lane, nchA);
+        else if (lgd == 7) d_pair<L, NL, (L < 7 ? L : 7), JST>(it, wbuf, p, q, i, lane, nchA);
+        else d_pair<L, NL, L, JST>(it, wbuf, p, q, i, lane, nchA);
       }
       csync();
       mark(0);
@@ -848,6 +878,10 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
           mpf<NL> ap = it.alpha[p], aq = it.alpha[q];
           const mpf<NL> gr = it.gam[2 * i], gi = it.gam[2 * i + 1];
           const mpf<NL> g2 = mpf_add(mpf_mul(gr, gr), mpf_mul(gi, gi));
+          if (it.gexp && !mpf_is_zero(g2) && !mpf_is_zero(ap) && !mpf_is_zero(aq) && !ap.neg && !aq.neg) {
+            const int64_t e2 = g2.e - ap.e - aq.e + 2;  // >= log2(g2 / (ap aq))
+            atomicMax(&it.gexp[sweep & 1], (int)(e2 < -100000 ? -100000 : (e2 > 100000 ? 100000 : e2)));
+          }
           if (!mpf_is_zero(g2) && mpf_cmp(g2, mpf_mul(tol2, mpf_mul(ap, aq))) > 0) {
             // The oracle's zeta = d/(2|g|), t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
             // c = 1/sqrt(1 + t^2), s = c t g/|g| (d = a_q - a_p, g = gamma), rewritten with
@@ -865,6 +899,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             const mpf<NL> sr = mpf_mul(sc, gr);
             const mpf<NL> si = mpf_mul(sc, gi);
             const mpf<NL> tg = mpf_mul(mpf_mul(g2, sc), ic);      // t |gamma|
+            // a reduced-precision gamma (R20) leaves the new norms uncertain by up to
+            // 2 |s| |gamma error| <= 2^-(28 lgd - 7) sqrt(alpha_p alpha_q): exponent of its square root
+            const int64_t e_slack = lgd < L ? (ap.e + aq.e) / 4 - (28 * (int64_t)lgd - 8) / 2 + 2 : INT64_MIN / 4;
             ap = mpf_sub(ap, tg);
             aq = mpf_add(aq, tg);
             const int64_t ep = it.eA[p], eq = it.eA[q];
@@ -888,6 +925,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
                 int64_t e1 = (int64_t)ceil(0.5 * mpf_log2(a) + 1e-9) + 1;
                 if (e1 > enew) enew = e1;
               }
+              if (e_slack + 1 > enew) enew = e_slack + 1;
               if (enew < tmax[u] - 26) enew = tmax[u] - 26;
               if (enew > eb) enew = eb;
               eo[u] = enew;
@@ -1026,7 +1064,8 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
       mark(2);
     }
     // refresh exact column norms (and renormalise columns) for the next sweep / the result
-    const bool any = *(volatile int*)it.sync != 0;
+    const bool any = *(volatile int*)it.sync != 0 || lgd < L;
+    if (it.gexp) e2prev = *(volatile int*)&it.gexp[sweep & 1];
     // exact norms; the negligible-column rule (R3b) is re-evaluated on them
     jac_norms<L, NL>(it, true, z, gw, GW);
     csync();

@@ -40,6 +40,7 @@ struct SvdScratch {
   int* rot; int* negl; int* ord; int* status; int* sweeps; int* fstatus; int* k; long long* rots;
   int64_t* e_misc;  // 4 spare exponents
   long long* uprod; // executed digit products of phase U per row (profiling)
+  int* gexp;        // [2] per-sweep max gamma ratio exponent (precision schedule of phase D)
   int* sync;
   mpf<NL>* zbuf;
   static size_t bytes(int N) {
@@ -69,6 +70,7 @@ struct SvdScratch {
     s.e_misc = (int64_t*)(q + 32);
     s.sync = (int*)(q + 64);
     s.uprod = (long long*)(q + 72);
+    s.gexp = (int*)(q + 80);
     s.zbuf = (mpf<NL>*)(q + 128);
     return s;
   }
@@ -125,6 +127,18 @@ constexpr int redo_bits() { return L <= 10 ? 4 : 16; }
 
 // MPS_NO_PRECOND=1 (debug / A-B): run the p-bit Jacobi on Theta' itself (no binary64
 // preconditioning, R19).
+// MPS_REDUCED_D=1 (experimental, off): the first two sweeps of a preconditioned iteration
+// compute the dot products from the top 4 / 7 digits (R20).  +3.5% at chi=128, but it failed
+// the 512-bit echo pin (2^-220 instead of 2^-465): the truncated dot is accurate relative to
+// the column exponents, not to the norms of columns collapsing inside a sweep.
+inline bool use_reduced_d() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_REDUCED_D");
+    on = (e && atoi(e)) ? 1 : 0;
+  }
+  return on != 0;
+}
 inline bool use_precond() {
   static int on = -1;
   if (on < 0) {
@@ -271,6 +285,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.sync = S.sync; si.zbuf = S.zbuf; si.phase_cycles = phase_dbg();
     const bool recover = !force_accumulate_v() && !g.accumulate_v;
     si.uprod = S.uprod;
+    si.gexp = use_reduced_d() ? S.gexp : nullptr;
+    si.e2_hint = pb ? -44 : 0;  // binary64 basis: |gamma|^2 / (alpha_p alpha_q) ~ 2^-44 at sweep 1 (1e-13)
     si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     si.a0_ready = pb ? 1 : 0;
     if (pb && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
