@@ -356,6 +356,11 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     if constexpr (NSIT > 3) launch_ns_iter<L, 3>(dgt + (size_t)6 * n, dgt + (size_t)7 * n, gNN, st);
     nl += 2 * NSIT;
     k_gemm_t<L, L, 0><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+    if (getenv("MPS_NS_FORCE_ZERR")) {  // test hook: as if every Newton-Schulz zero-digit check failed
+      std::vector<int> two(n, 2);
+      cudaMemcpyAsync(redo, two.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st);
+      cudaStreamSynchronize(st);
+    }
     prof_mark(PROF_PRECOND, 0, st);
   }
   if (any_dbg) {

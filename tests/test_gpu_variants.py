@@ -1,0 +1,26 @@
+"""The non-default paths of the GPU SVD, each checked against the oracle by re-running the
+parity tests in a subprocess with a debug switch (the switches are read once per process):
+  MPS_NO_PRECOND=1     p-bit Jacobi on Theta' itself (the paper's iteration, no binary64 basis; R19)
+  MPS_ACCUMULATE_V=1   V accumulated instead of recovered (R16)
+  MPS_NS_FORCE_ZERR=1  every item behaves as if a Newton-Schulz zero-digit check failed:
+                       the re-run without preconditioner and with accumulated V (run_update2)
+  MPS_REDUCED_D=1      is experimental and known to fail the 512-bit echo pin (R20): not tested."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+TESTS = ["tests/test_gpu_update2.py::test_update_parity", "tests/test_gpu_mps.py::test_mixed_gates_vs_dense",
+         "tests/test_gpu_mps.py::test_truncating_run_vs_oracle_mps"]
+
+
+@pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR"])
+def test_path_parity(switch):
+    env = dict(os.environ, **{switch: "1"})
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider"] + TESTS, cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
