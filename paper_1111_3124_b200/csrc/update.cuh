@@ -157,6 +157,88 @@ inline size_t pre_bytes(int M, int N) {
          256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N);  // + recovery coefficients
 }
 
+// preconditioner buffers carved from q (layout of pre_bytes)
+template <int L>
+struct PreBufs {
+  double2 *Ad, *Vd;
+  int32_t *Xa, *Xb, *Dm;
+  int64_t* eMix;
+  unsigned long long* rowmax;
+  int* sweeps_d;
+  int64_t *eOne, *eA1;
+  int32_t* rcoef;
+  int64_t* rexp;
+  int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
+};
+template <int L>
+inline PreBufs<L> carve_pre(char* q, int M, int N) {
+  PreBufs<L> b;
+  b.Ad = (double2*)q; q += align_up(16 * (size_t)M * N);
+  b.Vd = (double2*)q; q += align_up(16 * (size_t)N * N);
+  b.Xa = (int32_t*)q; q += mat_bytes(N, N, L);
+  b.Xb = (int32_t*)q; q += mat_bytes(N, N, L);
+  b.Dm = (int32_t*)q; q += mat_bytes(N, N, L);
+  b.eMix = (int64_t*)q; q += align_up(8 * (size_t)N);
+  b.rowmax = (unsigned long long*)q;
+  b.sweeps_d = (int*)(q + 8);
+  b.eOne = (int64_t*)(q + 16);
+  b.eA1 = (int64_t*)(q + 32);
+  b.rcoef = (int32_t*)(q + 256);
+  b.rexp = (int64_t*)((char*)b.rcoef + align_up(4 * (size_t)N * (L + 1)));
+  return b;
+}
+// descriptors of one item's preconditioner (gt[k * stride], k = 0 .. 2 ns_iters): the
+// input A0 (M x N, block exponent eA0) -> Af = A0 X with column exponents eAcols
+template <int L>
+inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, const int64_t* eA0, int32_t* Af,
+                      int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride) {
+  constexpr int NSIT = ns_iters<L>();
+  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1};
+  for (int k = 0; k < NSIT; ++k) {
+    int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
+    int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
+    // D = I - X^H X (exponent 1, Hermitian);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
+    GemmT gd = GemmT{Xc, N, pb.eOne, Xc, N, pb.eOne, pb.Dm, N, pb.eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
+    gd.herm = 1;
+    gt[(2 * k) * stride] = gd;
+    gt[(2 * k + 1) * stride] =
+        GemmT{Xc, N, pb.eOne, pb.Dm, N, pb.eOne + 1, Xn, N, pb.eOne, Xc, nullptr, N, N, N, 0, 0, 0, zerr};
+  }
+  // A_1 = A0 X at the exponent bounded by A0's largest row norm
+  gt[(2 * NSIT) * stride] = GemmT{A0, M, eA0, pb.Xfin(), N, pb.eOne, Af, M, pb.eA1, nullptr, eAcols, M, N, N, 0, 0, 0, nullptr};
+}
+template <int L>
+inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t stride) {
+  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1};
+  for (int k = 0; k <= 2 * ns_iters<L>(); ++k)
+    gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
+}
+// the preconditioner kernels for n items (descriptors already on the device); launch count
+template <int L>
+inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, int maxN, cudaStream_t st) {
+  constexpr int NSIT = ns_iters<L>();
+  int nl = 0;
+  k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
+  k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre); ++nl;
+  k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
+  const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
+  const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
+  const dim3 gNN(std::min(tNN, 1024), n);
+  launch_ns_iter<L, 0>(dgt, dgt + (size_t)n, gNN, st);
+  launch_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, gNN, st);
+  launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
+  if constexpr (NSIT > 3) launch_ns_iter<L, 3>(dgt + (size_t)6 * n, dgt + (size_t)7 * n, gNN, st);
+  nl += 2 * NSIT;
+  k_gemm_t<L, L, 0><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+  return nl;
+}
+
 template <int L, int NL>
 inline size_t upd2_item_bytes(const Upd2Args& a) {
   const int M = 2 * std::max(a.chiL, a.chiR), N = 2 * std::min(a.chiL, a.chiR);
@@ -234,20 +316,11 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     char* sp = (char*)A0f + mat_bytes(M, N, L);
     auto S = SvdScratch<L, NL>::carve(sp, N);
     int64_t* eV = (int64_t*)align_up((size_t)sp + SvdScratch<L, NL>::bytes(N), 16);
-    char* pq = (char*)align_up((size_t)eV + 8 * (size_t)N, 256);
-    double2* Ad = (double2*)pq; pq += align_up(16 * (size_t)M * N);
-    double2* Vd = (double2*)pq; pq += align_up(16 * (size_t)N * N);
-    int32_t* Xa = (int32_t*)pq; pq += mat_bytes(N, N, L);
-    int32_t* Xb = (int32_t*)pq; pq += mat_bytes(N, N, L);
-    int32_t* Dm = (int32_t*)pq; pq += mat_bytes(N, N, L);
-    int64_t* eMix = (int64_t*)pq; pq += align_up(8 * (size_t)N);
-    unsigned long long* rowmax = (unsigned long long*)pq;
-    int* sweeps_d = (int*)(pq + 8);
-    int64_t* eOne = (int64_t*)(pq + 16);
-    int64_t* eA1 = (int64_t*)(pq + 32);
-    int32_t* rcoef = (int32_t*)(pq + 256);
-    int64_t* rexp = (int64_t*)((char*)rcoef + align_up(4 * (size_t)N * (L + 1)));
-    int32_t* Xfin = (NSIT % 2) ? Xb : Xa;
+    const PreBufs<L> PB = carve_pre<L>((char*)align_up((size_t)eV + 8 * (size_t)N, 256), M, N);
+    int64_t* eMix = PB.eMix;
+    int32_t* Xfin = PB.Xfin();
+    int32_t* rcoef = PB.rcoef;
+    int64_t* rexp = PB.rexp;
     const bool pb = pre && !g.no_precond;
     int64_t* eL = S.e_misc;
     int64_t* eR = S.e_misc + 1;
@@ -258,26 +331,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
     hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
     hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pb ? A0f : Af, pb ? eMix : S.eA, M, N};
-    if (pre && !pb) {  // this item skips the preconditioner: empty descriptors
-      hpre[b] = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, rowmax, sweeps_d, nullptr, eOne, eA1};
-      for (int k = 0; k <= 2 * NSIT; ++k)
-        hgt[k * n + b] = GemmT{nullptr, 1, eOne, nullptr, 1, eOne, nullptr, 1, eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
-    }
-    if (pb) {
-      hpre[b] = PreItem{M, N, A0f, eMix, Ad, Vd, rowmax, sweeps_d, Xa, eOne, eA1};
-      for (int k = 0; k < NSIT; ++k) {
-        int32_t* Xc = (k % 2) ? Xb : Xa;
-        int32_t* Xn = (k % 2) ? Xa : Xb;
-        // D = I - X^H X (exponent 1);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
-        GemmT gd = GemmT{Xc, N, eOne, Xc, N, eOne, Dm, N, eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
-        gd.herm = 1;
-        hgt[(2 * k) * n + b] = gd;
-        hgt[(2 * k + 1) * n + b] =
-            GemmT{Xc, N, eOne, Dm, N, eOne + 1, Xn, N, eOne, Xc, nullptr, N, N, N, 0, 0, 0, redo + b};
-      }
-      // A_1 = Theta' X at the exponent bounded by Theta's largest row norm; Jacobi column exponents
-      hgt[(2 * NSIT) * n + b] = GemmT{A0f, M, eMix, Xfin, N, eOne, Af, M, eA1, nullptr, S.eA, M, N, N, 0, 0, 0, nullptr};
-    }
+    if (pre && !pb) pre_skip_descs<L>(PB, hpre + b, hgt + b, n);  // this item skips the preconditioner
+    if (pb) pre_descs<L>(PB, M, N, A0f, eMix, Af, S.eA, redo + b, hpre + b, hgt + b, n);
     SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
@@ -334,28 +389,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     prof_mark(PROF_PRECOND, 1, st);
     int maxM = 0, maxN = 0;
     for (int b = 0; b < n; ++b) { maxM = std::max(maxM, hs[b].M); maxN = std::max(maxN, hs[b].N); }
-    const PreItem* dpre = (const PreItem*)(base + d_pre);
-    const GemmT* dgt = (const GemmT*)(base + d_gt);
-    k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
-    k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
-    {
-      static bool attr = false;
-      if (!attr) {
-        cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-      }
-      k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre); ++nl;
-    }
-    k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
-    const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
-    const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
-    const dim3 gNN(std::min(tNN, 1024), n);
-    launch_ns_iter<L, 0>(dgt, dgt + (size_t)n, gNN, st);
-    launch_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, gNN, st);
-    launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
-    if constexpr (NSIT > 3) launch_ns_iter<L, 3>(dgt + (size_t)6 * n, dgt + (size_t)7 * n, gNN, st);
-    nl += 2 * NSIT;
-    k_gemm_t<L, L, 0><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+    nl += launch_pre<L>((const PreItem*)(base + d_pre), (const GemmT*)(base + d_gt), n, maxM, maxN, st);
     if (getenv("MPS_NS_FORCE_ZERR")) {  // test hook: as if every Newton-Schulz zero-digit check failed
       std::vector<int> two(n, 2);
       cudaMemcpyAsync(redo, two.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st);
