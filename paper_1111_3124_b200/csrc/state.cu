@@ -402,8 +402,10 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
     cudaMemcpyAsync(r1, s->dint, sizeof(r1), cudaMemcpyDeviceToHost, s->st);
     if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
     if (!r1[4] || r1[3]) break;
+    if (r1[4] & 2) a.no_precond = 1;  // a Newton-Schulz zero-digit check failed: no preconditioner
     if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 1 at %d: re-run with accumulated V\n", q);
   }
+  a.no_precond = 0;
   if (r1[3]) { s->sweeps_total += r1[2]; return s->sticky = r1[3]; }
   const int k1 = r1[0];
   a.s1_accumulated = a.accumulate_v;
@@ -416,6 +418,7 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
     cudaMemcpyAsync(r2, s->dint, sizeof(r2), cudaMemcpyDeviceToHost, s->st);
     if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
     if (!r2[4] || r2[3]) break;
+    if (r2[4] & 2) a.no_precond = 1;
     if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 2 at %d: re-run with accumulated V\n", q);
   }
   s->sweeps_total += r2[2];

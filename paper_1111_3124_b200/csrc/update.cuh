@@ -505,6 +505,7 @@ struct Upd3Args {
   int* redo;                        // device flag (one int) or null: recovered V too inaccurate
   int accumulate_v;                 // 1: accumulate V in this stage (the re-run)
   int s1_accumulated;               // stage 2: stage 1 ran with accumulated V (its V exponent is 1)
+  int no_precond;                   // 1: this stage without the binary64 preconditioner (R19)
 };
 
 // workspace of one three-site update (bounded by the capacities: k1 <= min(chi_max, 2chiR, 4chiL))
@@ -520,6 +521,7 @@ inline size_t upd3_item_bytes(const Upd3Args& a) {
   // V recovery (R16): the inputs of both SVDs and the per-column exponents of V
   s += mat_bytes(M1, N1, L) + mat_bytes(M2 + 2, N2 + 2, L) + align_up(8 * (size_t)N1) + align_up(8 * (size_t)(N2 + 2)) +
        256;
+  s += pre_bytes<L>(M1, N1) + pre_bytes<L>(M2 + 2, N2 + 2) + 512;  // preconditioners of both SVDs (R19)
   return s;
 }
 
@@ -543,7 +545,15 @@ struct Upd3Rec {
     eVb = (int64_t*)q; q += align_up(8 * (size_t)(N2 + 2));
     eA0a = (int64_t*)q;
     eA0b = eA0a + 1;
+    q += 256;
+    pre1 = (char*)align_up((size_t)q, 256);
+    pre2 = pre1 + pre_bytes<L>(M1, N1);
+    M1_ = M1; N1_ = N1; M2_ = M2 + 2; N2_ = N2 + 2;
   }
+  char *pre1, *pre2;
+  int M1_, N1_, M2_, N2_;
+  PreBufs<L> P1() const { return carve_pre<L>(pre1, M1_, N1_); }
+  PreBufs<L> P2() const { return carve_pre<L>(pre2, M2_, N2_); }
 };
 
 // T (2chiL x 2chi2) -> T' (4chiL x chi2): T'[(2i+j)chiL + a, g] = T[(i chiL + a), (j chi2 + g)]
@@ -600,16 +610,24 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   int64_t* eTh = S1.eA + N1;  // spare slot after the column exponents (64 bytes of slack)
   hg[1] = GemmItem{Tp, 4 * a.chiL, e + 3, Rf, a.chi2, e + 2, Th, 4 * a.chiL, eTh, 4 * a.chiL, 2 * a.chiR, a.chi2, 0};
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
-  hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, A1, S1.eA, M1, N1};
+  const Upd3Rec<L, NL> rec(base + d_end, a);
+  const bool pb1 = use_precond() && !a.no_precond;
+  const PreBufs<L> PB1 = rec.P1();
+  hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, pb1 ? rec.A0a : A1, pb1 ? PB1.eMix : S1.eA,
+                  M1, N1};
+  const size_t d_pre1 = 5120, d_gt1 = 5376;
+  if (pb1) pre_descs<L>(PB1, M1, N1, rec.A0a, PB1.eMix, A1, S1.eA, a.redo, (PreItem*)(hd.data() + d_pre1),
+                        (GemmT*)(hd.data() + d_gt1), 1);
   SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
   SvdItem<NL> si = {};
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
   si.coef = S1.coef; si.dbg = nullptr; si.rot = S1.rot; si.negl = S1.negl; si.status = S1.status;
-  const Upd3Rec<L, NL> rec(base + d_end, a);
   si.sweeps = S1.sweeps; si.rotations = S1.rots; si.sync = S1.sync; si.zbuf = S1.zbuf; si.phase_cycles = nullptr;
   const bool recover = !force_accumulate_v() && !a.accumulate_v;
   si.uprod = S1.uprod;
-  si.A0 = recover ? rec.A0a : nullptr; si.eA0 = rec.eA0a; si.eV = rec.eVa; si.evals = S1.rots + 1;
+  si.A0 = recover ? rec.A0a : nullptr; si.eA0 = pb1 ? PB1.eMix : rec.eA0a; si.eV = rec.eVa; si.evals = S1.rots + 1;
+  si.a0_ready = pb1 ? 1 : 0;
+  if (pb1 && !recover) { si.V = PB1.Xfin(); si.v_preset = 1; }
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin);
   FinItem<NL> fi;
@@ -638,7 +656,10 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   dim3 g2(std::max(1, std::min(128, (8 * a.chiL * a.chiR + 127) / 128)), 1);
   k_gemm<L><<<g2, 128, 0, st>>>((const GemmItem*)(base + d_gemm) + 1); ++nl;
   k_mix<L, NL><<<g2, 128, 64 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
+  if (pb1) nl += launch_pre<L>((const PreItem*)(base + d_pre1), (const GemmT*)(base + d_gt1), 1, M1, N1, st);
   launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), 1, jacobi_cluster_size(1, N1), st); ++nl;
+  if (pb1 && !recover)  // V = X W was accumulated in the preconditioner's buffer; stage 2 reads V1
+    cudaMemcpyAsync(V1, PB1.Xfin(), mat_bytes(N1, N1, L), cudaMemcpyDeviceToDevice, st);
   k_recover_v<L, NL><<<dim3(std::max(1, std::min(64, (N1 * N1 + 127) / 128)), 1), 128, 0, st>>>(
       (const SvdItem<NL>*)(base + d_svd)); ++nl;
   k_finalize<L, NL><<<1, NTHR, sizeof(mpf<NL>) * (size_t)N1, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
@@ -701,11 +722,17 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   const bool recover = !force_accumulate_v() && !a.accumulate_v;
   si.uprod = S2.uprod;
   si.A0 = recover ? rec.A0b : nullptr; si.eA0 = rec.eA0b; si.eV = rec.eVb; si.evals = S2.rots + 1; si.a0_ready = 1;
+  const bool pb2 = use_precond() && !a.no_precond;
+  const PreBufs<L> PB2 = rec.P2();
+  if (pb2 && !recover) { si.V = PB2.Xfin(); si.v_preset = 1; }
+  const size_t d_pre2 = 13312, d_gt2 = 13568;
+  if (pb2) pre_descs<L>(PB2, M2, N2, rec.A0b, rec.eA0b, A2, S2.eA, a.redo, (PreItem*)(hd.data() + d_pre2),
+                        (GemmT*)(hd.data() + d_gt2), 1);
   hs[0] = si;
   FinItem<NL>* hf = (FinItem<NL>*)(hd.data() + d_fin2);
   FinItem<NL> fi;
   std::memset(&fi, 0, sizeof(fi));
-  fi.M = M2; fi.N = N2; fi.trans = trans2 ? 1 : 0; fi.A = A2; fi.eA = S2.eA; fi.V = V2; fi.alpha = S2.alpha;
+  fi.M = M2; fi.N = N2; fi.trans = trans2 ? 1 : 0; fi.A = A2; fi.eA = S2.eA; fi.V = si.V; fi.alpha = S2.alpha;
   fi.chi_max = a.chi_max; fi.thr = mpf_host_from_double<NL>(thr); fi.ord = S2.ord; fi.inv_sig = S2.inv_sig;
   fi.lam = S2.lam; fi.k_out = a.k2; fi.status = S2.fstatus; fi.sigma_rec = nullptr; fi.nsig = 0;
   fi.svd_status = S2.status;
@@ -720,6 +747,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   k_m2_exp<L, NL><<<1, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
   dim3 gb(std::max(1, std::min(64, (rows2 * cols2 + 255) / 256)), 1);
   k_build_m2<L, NL><<<gb, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), S2.e_misc); ++nl;
+  if (pb2) nl += launch_pre<L>((const PreItem*)(base + d_pre2), (const GemmT*)(base + d_gt2), 1, M2, N2, st);
   launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd2), 1, jacobi_cluster_size(1, N2), st); ++nl;
   k_recover_v<L, NL><<<dim3(std::max(1, std::min(64, (N2 * N2 + 127) / 128)), 1), 128, 0, st>>>(
       (const SvdItem<NL>*)(base + d_svd2)); ++nl;
