@@ -348,6 +348,7 @@ struct GemmT {
   // eA + eBcols[c] + ghead + colexp[c], written to eCcols[c].  eCout is unused.
   const int64_t* eBcols; const int32_t* colcoef; const int64_t* colexp; int ghead;
   int herm;  // C is Hermitian (X^H X): only tiles on/above the diagonal are computed, mirrored
+  int64_t* eCwrite;  // if non-null (block mode, eCout null): receives eC = eA + eB + ghead
 };
 
 // per-column coefficient of the V recovery: 1/alpha_b = m 2^e, m in [0.5, 1) as L+1 digits
@@ -426,8 +427,10 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   __shared__ int32_t As[GT_KB][2][LG][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
   __shared__ int32_t Bs[GT_KB][2][LG][GT_TILE + 1];
   const bool percol = it.eBcols != nullptr;
-  const int64_t eC = percol ? 0 : *it.eCout;
+  // block exponent: given (eCout), or eA + eB + ghead (head-room for K terms, eCwrite)
+  const int64_t eC = percol ? 0 : (it.eCout ? *it.eCout : *it.eA + *it.eB + it.ghead);
   const int g = percol ? it.ghead : (int)(eC - (*it.eA + *it.eB));
+  if (!percol && it.eCwrite && blockIdx.x == 0 && threadIdx.x == 0) *it.eCwrite = eC;
   int zbad = 0;
   for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
     const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;

@@ -254,7 +254,7 @@ inline size_t upd2_desc_bytes(int n) {
   return align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
          align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(sizeof(PreItem) * n) +
          align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n) + align_up(sizeof(RecItem<NL>) * n) +
-         align_up(sizeof(GemmT) * n);
+         align_up(sizeof(GemmT) * n) + align_up(sizeof(GemmT) * n);
 }
 
 template <class T>
@@ -278,7 +278,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
                d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_pre = d_fin + align_up(sizeof(FinItem<NL>) * n),
                d_gt = d_pre + align_up(sizeof(PreItem) * n),
                d_rec = d_gt + align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n),
-               d_rg = d_rec + align_up(sizeof(RecItem<NL>) * n), d_end = upd2_desc_bytes<L, NL>(n);
+               d_rg = d_rec + align_up(sizeof(RecItem<NL>) * n), d_gc = d_rg + align_up(sizeof(GemmT) * n),
+               d_end = upd2_desc_bytes<L, NL>(n);
   constexpr int NSIT = ns_iters<L>();
   const bool pre = use_precond();
   int* redo = (int*)(base + d_end);  // [n] flags (run_update2)
@@ -287,6 +288,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   GemmT* hgt = (GemmT*)(hd.data() + d_gt);  // [2 NSIT + 1][n]: D_k, X_k+1 per iteration, then A_1
   RecItem<NL>* hrec = (RecItem<NL>*)(hd.data() + d_rec);
   GemmT* hrg = (GemmT*)(hd.data() + d_rg);  // V = Theta'^H A_final diag(1/alpha) (tiled GEMM)
+  GemmT* hgc = (GemmT*)(hd.data() + d_gc);  // a1 contraction Theta = L R (tiled GEMM)
   PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
   GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
@@ -330,6 +332,15 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     hp[2 * b] = PrepItem{g.GL, g.lamL, g.lamM, chiL, chiM, 0, Lf, eL};
     hp[2 * b + 1] = PrepItem{g.GR, nullptr, g.lamR, chiM, chiR, 1, Rf, eR};
     hg[b] = GemmItem{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, eT, 2 * chiL, 2 * chiR, chiM, 0};
+    {
+      GemmT gc = GemmT{Lf, 2 * chiL, eL, Rf, chiM, eR, Tf, 2 * chiL, nullptr, nullptr, nullptr, 2 * chiL, 2 * chiR, chiM,
+                       0, 0, 0, nullptr};
+      int gh = 1;
+      while ((1 << (gh - 1)) < chiM) ++gh;
+      gc.ghead = gh + 1;  // as k_gemm: sum of chiM complex products, each |.| < 2^(eA + eB + 1)
+      gc.eCwrite = eT;
+      hgc[b] = gc;
+    }
     hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pb ? A0f : Af, pb ? eMix : S.eA, M, N};
     if (pre && !pb) pre_skip_descs<L>(PB, hpre + b, hgt + b, n);  // this item skips the preconditioner
     if (pb) pre_descs<L>(PB, M, N, A0f, eMix, Af, S.eA, redo + b, hpre + b, hgt + b, n);
@@ -382,7 +393,12 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   k_prep_exp<<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
   k_prep_conv<L, NL><<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
   dim3 gg(std::max(1, std::min(128, (maxMN + 127) / 128)), n);
-  k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
+  {
+    int maxR = 0, maxC = 0;
+    for (int b = 0; b < n; ++b) { maxR = std::max(maxR, hgc[b].rows); maxC = std::max(maxC, hgc[b].cols); }
+    const int tC = ((maxR + GT_TILE - 1) / GT_TILE) * ((maxC + GT_TILE - 1) / GT_TILE);
+    k_gemm_t<L, L, 0><<<dim3(std::max(1, std::min(tC, 1024)), n), 256, 0, st>>>((const GemmT*)(base + d_gc)); ++nl;
+  }
   k_mix<L, NL><<<gg, 128, 16 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
   prof_mark(PROF_CONTRACT, 0, st);
   if (pre && !any_dbg) {
