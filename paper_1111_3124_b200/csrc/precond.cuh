@@ -414,11 +414,12 @@ __device__ __forceinline__ void tmul_z(int64_t (&acc)[LG + 2], const int32_t (&x
       if (i + j >= LG - 2) acc[i + j - (LG - 2)] = madw(SUB ? -x[i] : x[i], y[j], acc[i + j - (LG - 2)]);
 }
 
-constexpr int GT_TILE = 16, GT_KB = 8;
+constexpr int GT_TILE = 16;
 
 template <int L, int LG, int Z>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG, "precision schedule");
+  constexpr int GT_KB = 8;  // k per staging round (16 measured no faster)
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
   if (it.rows <= 0 || it.cols <= 0) return;  // item without this GEMM
@@ -481,6 +482,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         tmul_z<LG, Z, true>(ar, xi, yi);
         tmul_z<LG, Z, false>(ai, xr, yi);
         tmul_z<LG, Z, false>(ai, xi, yr);
+        if ((kk & 7) == 7 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); }  // <= 8 k per int64 column run
       }
       tnorm2<LG>(ar);
       tnorm2<LG>(ai);
