@@ -349,6 +349,9 @@ struct GemmT {
   const int64_t* eBcols; const int32_t* colcoef; const int64_t* colexp; int ghead;
   int herm;  // C is Hermitian (X^H X): only tiles on/above the diagonal are computed, mirrored
   int64_t* eCwrite;  // if non-null (block mode, eCout null): receives eC = eA + eB + ghead
+  // column selection: logical column b < *ncols_dev is physical column colmap[b] of B and C
+  // (the recovery of V computes only the columns kept by the truncation)
+  const int* colmap; const int* ncols_dev;
 };
 
 // per-column coefficient of the V recovery: 1/alpha_b = m 2^e, m in [0.5, 1) as L+1 digits
@@ -433,9 +436,12 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   const int g = percol ? it.ghead : (int)(eC - (*it.eA + *it.eB));
   if (!percol && it.eCwrite && blockIdx.x == 0 && threadIdx.x == 0) *it.eCwrite = eC;
   int zbad = 0;
+  const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
+  auto pcol = [&](int cc) { return it.colmap ? it.colmap[cc] : cc; };
   for (int tile = blockIdx.x; tile < tilesR * tilesC; tile += gridDim.x) {
     const int r0 = (tile % tilesR) * GT_TILE, c0 = (tile / tilesR) * GT_TILE;
     if (it.herm && c0 < r0) continue;  // block-uniform: the mirror tile writes these
+    if (c0 >= ncols) continue;          // columns not selected
     const int r = r0 + tx, c = c0 + ty;
     int64_t ar[LG + 2], ai[LG + 2];
 #pragma unroll
@@ -464,7 +470,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
           const int k = k0 + kk, cc = c0 + e;
           int32_t vb = 0;
-          if (k < it.K && cc < it.cols) vb = it.B[((size_t)(cc * 2 + ri) * L + D0 + dg) * it.ldb + k];
+          if (k < it.K && cc < ncols) vb = it.B[((size_t)(pcol(cc) * 2 + ri) * L + D0 + dg) * it.ldb + k];
           if (dg >= LG - Z && vb != 0) zbad = 1;
           Bs[kk][ri][dg][e] = vb;
         }
@@ -487,7 +493,8 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
       tnorm2<LG>(ar);
       tnorm2<LG>(ai);
     }
-    if (r < it.rows && c < it.cols) {
+    if (r < it.rows && c < ncols) {
+      const int pc = pcol(c);  // physical column
 #pragma unroll
       for (int ri = 0; ri < 2; ++ri) {
         int32_t t[LG], o[L];
@@ -497,7 +504,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         if (percol && it.colcoef) {  // x column coefficient (L+1 digits, fractional)
           int32_t K[L + 1];
 #pragma unroll
-          for (int k = 0; k <= L; ++k) K[k] = it.colcoef[(size_t)c * (L + 1) + k];
+          for (int k = 0; k <= L; ++k) K[k] = it.colcoef[(size_t)pc * (L + 1) + k];
           int64_t acc2[L + 2];
 #pragma unroll
           for (int j = 0; j < L + 2; ++j) acc2[j] = 0;
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           for (int j = 0; j < L; ++j) o[j] += x[j];
         }
         fx_balance<L>(o);
-        stfx<L>(it.C, it.ldc, c, ri, r, o);
+        stfx<L>(it.C, it.ldc, pc, ri, r, o);
         if (it.herm && c0 != r0) {  // C(c, r) = conj C(r, c)
           if (ri) {
 #pragma unroll
@@ -526,9 +533,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         }
       }
       if (it.eCcols && r == 0) {
-        if (!percol) it.eCcols[c] = eC;
-        else if (it.colexp && it.colexp[c] == INT64_MIN) it.eCcols[c] = 1;  // alpha_c = 0: zero column
-        else it.eCcols[c] = *it.eA + it.eBcols[c] + it.ghead + (it.colexp ? it.colexp[c] : 0);
+        if (!percol) it.eCcols[pc] = eC;
+        else if (it.colexp && it.colexp[pc] == INT64_MIN) it.eCcols[pc] = 1;  // alpha = 0: zero column
+        else it.eCcols[pc] = *it.eA + it.eBcols[pc] + it.ghead + (it.colexp ? it.colexp[pc] : 0);
       }
     }
   }

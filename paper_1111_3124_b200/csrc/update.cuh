@@ -362,7 +362,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
       gh += 1;  // sum of M complex products, each |.| < 2^(e0 + e_b + 1)
       hrec[b] = RecItem<NL>{recover ? N : 0, S.alpha, rcoef, rexp};
       hrg[b] = recover ? GemmT{A0f, M, si.eA0, Af, M, nullptr, Vf, N, nullptr, nullptr, eV, N, N, M, 1, 0, 0, nullptr,
-                               S.eA, rcoef, rexp, gh}
+                               S.eA, rcoef, rexp, gh, 0, nullptr, S.ord, g.k_out ? g.k_out : S.k}
                        : GemmT{nullptr, 1, nullptr, nullptr, 1, nullptr, nullptr, 1, nullptr, nullptr, nullptr, 0, 0, 0,
                                0, 0, 0, nullptr, nullptr, nullptr, nullptr, 0};
     }
@@ -430,22 +430,12 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   {
     int maxNN = 0;
     for (int b = 0; b < n; ++b) maxNN = std::max(maxNN, hs[b].N * hs[b].N);
-    prof_mark(PROF_JACOBI, 0, st);
-    prof_mark(PROF_RECOVER, 1, st);
-    int maxNr = 0;
-    for (int b = 0; b < n; ++b) maxNr = std::max(maxNr, hs[b].N);
-    (void)maxNN;
-    k_recover_coef<L, NL><<<dim3(std::max(1, (maxNr + 127) / 128), n), 128, 0, st>>>((const RecItem<NL>*)(base + d_rec));
-    ++nl;
-    const int tR = ((maxNr + GT_TILE - 1) / GT_TILE) * ((maxNr + GT_TILE - 1) / GT_TILE);
-    k_gemm_t<L, L, 0><<<dim3(std::max(1, std::min(tR, 1024)), n), 256, 0, st>>>((const GemmT*)(base + d_rg));
-    ++nl;
     if (unsigned long long* pc = prof_counts()) {
       k_accum_stats<NL><<<(n + 127) / 128, 128, 0, st>>>((const SvdItem<NL>*)(base + d_svd), n, pc);
       ++nl;
     }
   }
-  prof_mark(PROF_RECOVER, 0, st);
+  prof_mark(PROF_JACOBI, 0, st);
   if (unsigned long long* pd = phase_dbg()) {
     unsigned long long h[6 + 128 + 64];
     cudaMemcpyAsync(h, pd, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -469,6 +459,21 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   for (int b = 0; b < n; ++b) maxN = std::max(maxN, hs[b].N);
   k_finalize<L, NL><<<n, NTHR, sizeof(mpf<NL>) * (size_t)maxN, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p);
   ++nl;
+  prof_mark(PROF_FINALIZE, 0, st);
+  {
+    // V = Theta'^H A_final diag(1/alpha) for the columns the truncation keeps (ord[0..k)), after
+    // k_finalize has ordered and counted them (R16)
+    prof_mark(PROF_RECOVER, 1, st);
+    int maxNr = 0;
+    for (int b = 0; b < n; ++b) maxNr = std::max(maxNr, hs[b].N);
+    k_recover_coef<L, NL><<<dim3(std::max(1, (maxNr + 127) / 128), n), 128, 0, st>>>((const RecItem<NL>*)(base + d_rec));
+    ++nl;
+    const int tR = ((maxNr + GT_TILE - 1) / GT_TILE) * ((maxNr + GT_TILE - 1) / GT_TILE);
+    k_gemm_t<L, L, 0><<<dim3(std::max(1, std::min(tR, 1024)), n), 256, 0, st>>>((const GemmT*)(base + d_rg));
+    ++nl;
+    prof_mark(PROF_RECOVER, 0, st);
+  }
+  prof_mark(PROF_FINALIZE, 1, st);
   dim3 gs(std::max(1, std::min(64, (2 * maxOut + 255) / 256)), n);
   k_split<L, NL><<<gs, 256, 0, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p); ++nl;
   prof_mark(PROF_FINALIZE, 0, st);
