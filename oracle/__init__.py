@@ -99,6 +99,13 @@ def svd(p: int, A: np.ndarray, M: int, N: int):
     return sig, X, V, sw.value
 
 
+def theta2(p: int, chi_l: int, chi_m: int, chi_r: int, GL, GR, U):
+    """Theta' = U (G_L G_R) of one item (lambda = 1), records in update2_batch's theta layout."""
+    out = R.empty(p, 2 * 4 * chi_l * chi_r)
+    _chk(lib().orc_theta2(p, chi_l, chi_m, chi_r, _ptr(GL), _ptr(GR), _ptr(U), _ptr(out)))
+    return out
+
+
 def update2_batch(p, batch, chi_l, chi_m, chi_r, chi_max, thr, GL, GR, U, lam_l=None, lam_m=None, lam_r=None,
                   want_theta=False, nthreads=None):
     nsig = min(2 * chi_l, 2 * chi_r)

@@ -102,6 +102,22 @@ int orc_svd(int p, int M, int N, const uchar* A, uchar* sigma, uchar* X, uchar* 
 // Outputs per item: sigma_out (min(2chi_l,2chi_r) sorted), k_out, GL_out [2][chi_l][chi_max]
 // (first k columns valid, stride chi_max), GR_out [2][chi_max][chi_r], lam_out [chi_max],
 // theta_out (NULL or column-major (2chi_l) x (2chi_r)), sweeps_out.
+// Theta' = U (lam_l G_L lam_m G_R lam_r) only (contract_two_site, lambda = 1 when null), for
+// full-size samples where the SVD would take minutes.  Layout as orc_update2_batch's theta_out.
+int orc_theta2(int p, int chi_l, int chi_m, int chi_r, const uchar* GL, const uchar* GR, const uchar* U,
+               uchar* theta_out) {
+  GUARD_BEGIN
+  set_prec(p);
+  CVec gl = read_c(GL, (size_t)2 * chi_l * chi_m);
+  CVec gr = read_c(GR, (size_t)2 * chi_m * chi_r);
+  CVec u = read_c(U, 16);
+  RVec ll(chi_l, from_int(1)), lm(chi_m, from_int(1)), lr(chi_r, from_int(1));
+  CMat T = contract_two_site(gl, gr, ll, lm, lr, chi_l, chi_m, chi_r, u);
+  write_c(T.a, theta_out);
+  return ORC_OK;
+  GUARD_END
+}
+
 int orc_update2_batch(int p, int batch, int chi_l, int chi_m, int chi_r, int chi_max, double thr,
                       const uchar* GL, const uchar* GR, const uchar* lam_l, const uchar* lam_m,
                       const uchar* lam_r, const uchar* U, uchar* sigma_out, int* k_out,

@@ -287,3 +287,13 @@ def test_general_placement_reversed_equals_permuted():
     a = mps_of(pre + [(U, (2, 0))], n, p, 16, 2.0 ** -64)
     b = mps_of(pre + [(W, (0, 2))], n, p, 16, 2.0 ** -64)
     assert normwise_err(cplx(a.to_dense()), cplx(b.to_dense())) <= tau(p)
+
+
+def test_theta2_is_the_updates_contraction():
+    """orc_theta2 (contraction + gate only, used for full-size samples) equals the Theta' the
+    oracle's full update computes."""
+    p, chi = 256, 3
+    A, B, U = gen.update_batch_inputs(p, chi, 1)
+    want = oracle.update2_batch(p, 1, chi, chi, chi, chi, 2.0 ** -128, A, B, U, want_theta=True)["theta"]
+    got = oracle.theta2(p, chi, chi, chi, A, B, U)
+    assert got.tobytes() == want.tobytes()
