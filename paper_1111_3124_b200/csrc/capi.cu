@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "../../include/mps_b200.h"
@@ -167,8 +168,20 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
          olr = slot(lam_r ? nLam : 0), oU = slot(nU), oS = slot(nSig), oK = slot(4 * (size_t)batch),
          oAo = slot(nAo), oBo = slot(nAo), oLo = slot(nLo), oSw = slot(4 * (size_t)batch),
          oTh = slot(theta_debug ? nTh : 0), oWs = slot(ws);
-  char* d = nullptr;
-  if (cudaMalloc(&d, tot) != cudaSuccess) return MPS_ENOMEM;
+  // one grow-only device arena reused across calls (a cudaMalloc / cudaFree of tens of GB per
+  // call cost ~1 s of the end-to-end time); calls are serialised by the mutex
+  static std::mutex arena_mu;
+  static char* arena = nullptr;
+  static size_t arena_sz = 0;
+  std::lock_guard<std::mutex> lock(arena_mu);
+  if (arena_sz < tot) {
+    if (arena) cudaFree(arena);
+    arena = nullptr;
+    arena_sz = 0;
+    if (cudaMalloc(&arena, tot) != cudaSuccess) return MPS_ENOMEM;
+    arena_sz = tot;
+  }
+  char* d = arena;
   cudaMemcpyAsync(d + oA, A, nA, cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(d + oB, B, nA, cudaMemcpyHostToDevice, st);
   if (lam_l) cudaMemcpyAsync(d + oll, lam_l, nLam, cudaMemcpyHostToDevice, st);
@@ -201,7 +214,6 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   if (lam_out) cudaMemcpyAsync(lam_out, d + oLo, nLo, cudaMemcpyDeviceToHost, st);
   if (sweeps) cudaMemcpyAsync(sweeps, d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(d);
   if (e != cudaSuccess) {
     fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
     return MPS_ECUDA;
@@ -245,7 +257,6 @@ int mps_svd_batch(int p, int M, int N, int batch, const void* A, void* sigma, in
   cudaMemcpyAsync(sw.data(), d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
   if (rot_per_sweep) cudaMemcpyAsync(rot_per_sweep, d + oD, 256 * (size_t)batch, cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaStreamSynchronize(st);
-  cudaFree(d);
   if (e != cudaSuccess) {
     fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
     return MPS_ECUDA;
