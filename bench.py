@@ -63,6 +63,29 @@ def jacobi_limb_macs(chi: int, p: int, sweeps) -> float:
     return tot
 
 
+def trunc_products(LG: int, Z: int = 0) -> int:
+    """IMAD.WIDE of one truncated LG-digit product whose second operand has Z known-zero top
+    digits (columns >= LG-2 formed; the same count the kernels' tmul loops issue)."""
+    return sum(1 for i in range(LG) for j in range(LG - Z) if i + j >= LG - 2)
+
+
+def gemm_imad_wide_per_item(chi: int, p: int) -> float:
+    """IMAD.WIDE of the GEMM kernels of one two-site update: the a1
+    contraction, the Newton-Schulz iterations (Hermitian D_k: half the tiles), A_1 = Theta' X
+    and the recovery of the chi kept columns of V; 4 real products per complex MAC."""
+    L = 10 if p <= 280 else 19
+    sched = [(4, 1), (7, 2), (10, 5)] if L == 10 else [(4, 1), (7, 2), (14, 5), (19, 10)]
+    M = N = 2 * chi
+    t = 16
+    herm_out = (N // t) * (N // t + 1) // 2 * t * t  # tiles on / above the diagonal
+    w = (2 * chi) * (2 * chi) * chi * 4 * trunc_products(L)  # contraction (K = chi)
+    for LG, Z in sched:
+        w += herm_out * N * 4 * trunc_products(LG) + N * N * N * 4 * trunc_products(LG, Z)
+    w += M * N * N * 4 * trunc_products(L)  # A_1
+    w += N * chi * M * 4 * trunc_products(L)  # recovery of the kept columns
+    return float(w)
+
+
 def executed_imad_wide(counts, chi: int, p: int) -> float:
     """IMAD.WIDE the p-bit Jacobi kernel executes: every evaluated pair
     computes gamma (4 truncated real products per row, (L-1) + L(L+1)/2 IMAD.WIDE each: 64
@@ -273,6 +296,10 @@ def main():
     credited = jacobi_limb_macs(chi, p, sweeps) * args.steps  # SURVEY §8(d) count, all timed launches
     executed = executed_imad_wide(counts, chi, p)
     achieved = executed / (jac_ms / 1e3) if jac_ms else None
+    # the whole step: Jacobi + every GEMM kernel over the step time (the binary64 Jacobi and
+    # the O(chi^2) kernels execute no IMAD.WIDE of this kind)
+    step_imad = executed + gemm_imad_wide_per_item(chi, p) * batch * args.steps
+    step_frac = step_imad / (ms / 1e3) / peaks["imad_wide_s32_per_s"] if ms else None
     credited_rate = credited / (jac_ms / 1e3) if jac_ms else None
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
@@ -337,7 +364,8 @@ def main():
                          "kernel_ms_per_launch": jac_ms / jac_n if jac_n else None,
                          "share_of_step": jac_ms / ms if ms else None,
                          "step_ms": {"contraction": con_ms, "precondition": pre_ms, "jacobi": jac_ms,
-                                     "recover_v": rec_ms, "truncate_split": fin_ms}},
+                                     "recover_v": rec_ms, "truncate_split": fin_ms},
+                         "step_executed_imad_wide_frac": step_frac},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }
