@@ -13,6 +13,8 @@
 #pragma once
 #include <cstdint>
 
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
 
 namespace mpsb {
@@ -27,6 +29,7 @@ struct PreItem {
   int32_t* X;                             // N x N fixed, exponent 1 (output of k_d_to_fx)
   int64_t* eOne;                          // [2] = {1, 0}: exponents of X and of D/2
   int64_t* eA1;                           // exponent chosen for A_1 = Theta' X (1)
+  int* anyflag;                           // [2] "some block pair rotated" per sweep parity (cluster mode)
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -147,8 +150,17 @@ inline size_t jd_smem(int M) {
   return (size_t)2 * bs * M * 16 + (size_t)4 * bs * bs * 16 + 64;
 }
 
-static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* items) {
-  const PreItem it = items[blockIdx.x];
+// C CTAs (a thread-block cluster when C > 1) share one item: the block pairs of a step are
+// dealt round-robin to the CTAs and the steps are separated by cluster barriers (few items in
+// flight: an MPS layer).  The rotation sequence does not depend on C.
+static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* items, int C) {
+  namespace cg = cooperative_groups;
+  const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
+  const PreItem it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
+  auto csync = [&]() {
+    if (C > 1) cg::this_cluster().sync();
+    else __syncthreads();
+  };
   const int M = it.M, N = it.N;
   if (N == 0) return;
   const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs;
@@ -159,15 +171,16 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
   __shared__ int s_any, s_rot, s_col[32];
   double2* A = it.Ad;
   double2* V = it.Vd;
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x)
+  for (int t = crank * blockDim.x + threadIdx.x; t < N * N; t += C * blockDim.x)
     V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
   const double tol = JD_TOL;
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
     if (threadIdx.x == 0) s_any = 0;
-    __syncthreads();
+    if (crank == 0 && threadIdx.x == 0) *(volatile int*)&it.anyflag[sweep & 1] = 0;
+    csync();
     for (int step = 0; step < nbe - 1; ++step) {
-      for (int bp = 0; bp < nbe / 2; ++bp) {
+      for (int bp = crank; bp < nbe / 2; bp += C) {
         int I, J;
         rr_pair(nbe, step, bp, I, J);
         // local column l < bs: block I, l >= bs: block J; -1 = absent (ragged / dummy block)
@@ -256,12 +269,14 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
         }
         __syncthreads();
       }
+      csync();  // the next step's block pairs read columns this step wrote
     }
-    const int any = s_any;
-    __syncthreads();
+    if (threadIdx.x == 0 && s_any) atomicOr(&it.anyflag[sweep & 1], 1);
+    csync();
+    const int any = *(volatile int*)&it.anyflag[sweep & 1];
     if (!any) break;
   }
-  if (threadIdx.x == 0) *it.sweeps_d = sweep;
+  if (crank == 0 && threadIdx.x == 0) *it.sweeps_d = sweep;
 }
 
 // binary64 v (|v| <= 1) -> L balanced digits at exponent 1 (value = sum d_k 2^(28k) 2^(1-28L)), exact

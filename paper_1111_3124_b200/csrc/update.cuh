@@ -166,6 +166,7 @@ struct PreBufs {
   unsigned long long* rowmax;
   int* sweeps_d;
   int64_t *eOne, *eA1;
+  int* anyflag;
   int32_t* rcoef;
   int64_t* rexp;
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
@@ -183,6 +184,7 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.sweeps_d = (int*)(q + 8);
   b.eOne = (int64_t*)(q + 16);
   b.eA1 = (int64_t*)(q + 32);
+  b.anyflag = (int*)(q + 40);
   b.rcoef = (int32_t*)(q + 256);
   b.rexp = (int64_t*)((char*)b.rcoef + align_up(4 * (size_t)N * (L + 1)));
   return b;
@@ -193,7 +195,7 @@ template <int L>
 inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, const int64_t* eA0, int32_t* Af,
                       int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride) {
   constexpr int NSIT = ns_iters<L>();
-  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1};
+  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag};
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -209,7 +211,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
 }
 template <int L>
 inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t stride) {
-  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1};
+  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag};
   for (int k = 0; k <= 2 * ns_iters<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
@@ -225,7 +227,30 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
     cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre); ++nl;
+  {
+    // few items (an MPS layer): C CTAs per item share its block pairs (cluster barriers per step)
+    int C = 1;
+    const int bpairs = ((maxN + jd_bs(maxM) - 1) / jd_bs(maxM) + 1) / 2;
+    while (C < 8 && n * C * 2 <= 148 && C * 2 <= bpairs) C *= 2;
+    if (C == 1) {
+      k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre, 1);
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(n * C, 1, 1);
+      cfg.blockDim = dim3(JD_THREADS, 1, 1);
+      cfg.dynamicSmemBytes = jd_smem(maxM);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = C;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_jacobi_db, dpre, C);
+    }
+    ++nl;
+  }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
   const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
   const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
