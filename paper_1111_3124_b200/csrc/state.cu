@@ -43,6 +43,7 @@ struct mps_state {
   char* tmp = nullptr;
   size_t tmp_sz = 0;
   int* dint = nullptr;  // 256 device ints
+  std::vector<cudaStream_t> sub;  // side streams of batched three-site layers (created lazily)
   long long gates = 0, sweeps_total = 0;
   int last_sweeps = 0;
   int dl(int s) const { return s == 0 ? (has_l ? m_el : 1) : m[s - 1]; }
@@ -277,6 +278,7 @@ void mps_free(mps_state* s) {
   if (s->ws) cudaFree(s->ws);
   if (s->tmp) cudaFree(s->tmp);
   if (s->dint) cudaFree(s->dint);
+  for (auto st : s->sub) cudaStreamDestroy(st);
   delete s;
 }
 
@@ -436,6 +438,159 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
   return cuda_ok(s, cudaStreamSynchronize(s->st));
 }
 
+// Disjoint three-site gates of a layer (U8 host records, sites qs[g]..qs[g]+2): the updates run
+// concurrently on side streams (each stage is a chain of one-item kernels), with one host
+// synchronisation per stage for all gates.  Arithmetic per gate = apply_three_site.
+static int apply_three_site_batch(mps_state* s, const std::vector<int>& qs, const std::vector<const void*>& Us) {
+  const int n = (int)qs.size();
+  if (n == 0) return MPS_OK;
+  if (n == 1) return apply_three_site(s, qs[0], Us[0]);
+  constexpr int NS = 8, DI = 8;  // side streams; device ints per gate
+  if (n * DI > 256) {            // chunk
+    const int h = n / 2;
+    if (int rc = apply_three_site_batch(s, std::vector<int>(qs.begin(), qs.begin() + h),
+                                        std::vector<const void*>(Us.begin(), Us.begin() + h)))
+      return rc;
+    return apply_three_site_batch(s, std::vector<int>(qs.begin() + h, qs.end()),
+                                  std::vector<const void*>(Us.begin() + h, Us.end()));
+  }
+  while ((int)s->sub.size() < NS) {
+    cudaStream_t st;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return s->sticky = MPS_ECUDA;
+    s->sub.push_back(st);
+  }
+  std::vector<Upd3Args> A(n);
+  std::vector<size_t> off(n + 1, 0), woff(n + 1, 0);
+  std::vector<int> ldv(n);
+  for (int g = 0; g < n; ++g) {
+    const int q = qs[g];
+    const int dl = s->dl(q), dr = s->dr(q + 2), ld = std::max(s->cap[q], s->cap[q + 1]);
+    ldv[g] = ld;
+    off[g + 1] = off[g] + align_up(64 * s->cb) + align_up((size_t)2 * dl * ld * s->cb) +
+                 align_up((size_t)2 * ld * ld * s->cb) + align_up((size_t)2 * ld * dr * s->cb) +
+                 2 * align_up((size_t)ld * s->rb);
+  }
+  if (!grow((void**)&s->tmp, &s->tmp_sz, off[n] + 4096)) return s->sticky = MPS_ENOMEM;
+  for (int g = 0; g < n; ++g) {
+    const int q = qs[g];
+    const int dl = s->dl(q), d1 = s->m[q], d2 = s->m[q + 1], dr = s->dr(q + 2), ld = ldv[g];
+    char* b = s->tmp + off[g];
+    uint32_t* dU = (uint32_t*)b;
+    if (int rc = upload_gate(s, Us[g], 8, dU)) return rc;
+    Upd3Args& a = A[g];
+    std::memset(&a, 0, sizeof(a));
+    a.chiL = dl; a.chi1 = d1; a.chi2 = d2; a.chiR = dr; a.chi_max = s->chi_max;
+    a.G0 = s->G[q]; a.G1 = s->G[q + 1]; a.G2 = s->G[q + 2];
+    a.lamL = s->lamL(q); a.lam1 = s->lam[q]; a.lam2 = s->lam[q + 1]; a.lamR = s->lamR(q + 2);
+    a.U = dU;
+    b += align_up(64 * s->cb);
+    a.G0_out = (uint32_t*)b; b += align_up((size_t)2 * dl * ld * s->cb);
+    a.G1_out = (uint32_t*)b; b += align_up((size_t)2 * ld * ld * s->cb);
+    a.G2_out = (uint32_t*)b; b += align_up((size_t)2 * ld * dr * s->cb);
+    a.lam1_out = (uint32_t*)b; b += align_up((size_t)ld * s->rb);
+    a.lam2_out = (uint32_t*)b;
+    a.ld = ld;
+    int* di = s->dint + DI * g;
+    a.k1 = di; a.k2 = di + 1; a.sweeps = di + 2; a.status = di + 3; a.redo = di + 4;
+    woff[g + 1] = woff[g] + align_up(s->ops->upd3_ws(a));
+  }
+  if (!grow(&s->ws, &s->ws_sz, woff[n])) return s->sticky = MPS_ENOMEM;
+  // side streams start after everything queued on the handle's stream
+  cudaEvent_t ev0;
+  cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+  cudaEventRecord(ev0, s->st);
+  for (int i = 0; i < NS; ++i) cudaStreamWaitEvent(s->sub[i], ev0, 0);
+  auto stream_of = [&](int g) { return s->sub[g % NS]; };
+  auto sync_all = [&]() -> int {
+    for (int i = 0; i < NS; ++i)
+      if (cudaStreamSynchronize(s->sub[i]) != cudaSuccess) return cuda_ok(s, cudaGetLastError());
+    return MPS_OK;
+  };
+  std::vector<std::vector<unsigned char>> hd(2 * n);
+  std::vector<int> r(DI * n, 0), k1(n, 0);
+  // stage 1 (first pass with the predicted mode, at most one re-run per gate)
+  std::vector<char> todo(n, 1);
+  for (int g = 0; g < n; ++g) {
+    const int q = qs[g];
+    A[g].accumulate_v = lam_range_bits(s, s->lam[q + 1], s->m[q + 1]) > recover_bits(s) ? 1 : 0;
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int g = 0; g < n; ++g) {
+      if (!todo[g]) continue;
+      cudaMemsetAsync(s->dint + DI * g, 0, 5 * sizeof(int), stream_of(g));
+      s->ops->upd3_s1(s->p, s->thr, A[g], (char*)s->ws + woff[g], stream_of(g), hd[2 * g]);
+    }
+    if (int rc = sync_all()) return rc;
+    cudaMemcpy(r.data(), s->dint, sizeof(int) * DI * n, cudaMemcpyDeviceToHost);
+    bool again = false;
+    for (int g = 0; g < n; ++g) {
+      todo[g] = 0;
+      const int* rg = r.data() + DI * g;
+      if (pass == 0 && rg[4] && !rg[3] && !A[g].accumulate_v) {
+        A[g].accumulate_v = 1;
+        if (rg[4] & 2) A[g].no_precond = 1;
+        todo[g] = 1;
+        again = true;
+      }
+    }
+    if (!again) break;
+  }
+  for (int g = 0; g < n; ++g) {
+    const int* rg = r.data() + DI * g;
+    if (rg[3]) { s->sweeps_total += rg[2]; return s->sticky = rg[3]; }
+    k1[g] = rg[0];
+    A[g].s1_accumulated = A[g].accumulate_v;
+    A[g].no_precond = 0;
+    const int q = qs[g];
+    A[g].accumulate_v = lam_range_bits(s, s->lam[q], s->m[q]) > recover_bits(s) ? 1 : 0;
+    todo[g] = 1;
+  }
+  std::vector<int> r1 = r;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int g = 0; g < n; ++g) {
+      if (!todo[g]) continue;
+      cudaMemcpyAsync(s->dint + DI * g + 2, &r1[DI * g + 2], sizeof(int), cudaMemcpyHostToDevice, stream_of(g));
+      cudaMemsetAsync(s->dint + DI * g + 4, 0, sizeof(int), stream_of(g));
+      s->ops->upd3_s2(s->p, s->thr, A[g], k1[g], (char*)s->ws + woff[g], stream_of(g), hd[2 * g + 1]);
+    }
+    if (int rc = sync_all()) return rc;
+    cudaMemcpy(r.data(), s->dint, sizeof(int) * DI * n, cudaMemcpyDeviceToHost);
+    bool again = false;
+    for (int g = 0; g < n; ++g) {
+      todo[g] = 0;
+      const int* rg = r.data() + DI * g;
+      if (pass == 0 && rg[4] && !rg[3] && !A[g].accumulate_v) {
+        A[g].accumulate_v = 1;
+        if (rg[4] & 2) A[g].no_precond = 1;
+        todo[g] = 1;
+        again = true;
+      }
+    }
+    if (!again) break;
+  }
+  cudaEventDestroy(ev0);
+  for (int g = 0; g < n; ++g) {
+    const int* rg = r.data() + DI * g;
+    s->sweeps_total += rg[2];
+    s->last_sweeps = rg[2];
+    s->gates++;
+    if (rg[3]) return s->sticky = rg[3];
+  }
+  for (int g = 0; g < n; ++g) {
+    const int q = qs[g], dl = s->dl(q), dr = s->dr(q + 2), ld = ldv[g];
+    const int k2 = r[DI * g + 1];
+    const Upd3Args& a = A[g];
+    repack_rows(s, s->G[q], a.G0_out, 2 * dl, k2, ld);
+    repack_blocks(s, s->G[q + 1], a.G1_out, k2, ld, k1[g]);
+    repack_blocks(s, s->G[q + 2], a.G2_out, k1[g], ld, dr);
+    cudaMemcpyAsync(s->lam[q], a.lam1_out, (size_t)k2 * s->rb, cudaMemcpyDeviceToDevice, s->st);
+    cudaMemcpyAsync(s->lam[q + 1], a.lam2_out, (size_t)k1[g] * s->rb, cudaMemcpyDeviceToDevice, s->st);
+    s->m[q] = k2;
+    s->m[q + 1] = k1[g];
+  }
+  return cuda_ok(s, cudaStreamSynchronize(s->st));
+}
+
 static int apply_one(mps_state* s, const void* U, const int* sites, int k) {
   const int q = sites[0];
   if (k == 1) {
@@ -533,9 +688,33 @@ int mps_apply_layer(mps_state* s, int ng, const void* const* U, const int* sites
     std::vector<const void*> u(us.begin() + i, us.begin() + std::min(us.size(), i + 64));
     if (int rc = apply_two_site_batch(s, f, u)) return rc;
   }
+  // three-site gates (ascending consecutive triples, and two-site gates on (s, s+2) embedded
+  // into U(8)) run as one concurrent batch; the rest one by one
+  std::vector<int> tq;
+  std::vector<const void*> tu;
+  std::vector<std::vector<unsigned char>> emb;
+  emb.reserve(ng);
   o = 0;
   for (int g = 0; g < ng; ++g) {
-    if (!(k[g] == 2 && sites_flat[o + 1] == sites_flat[o] + 1))
+    const int* st_ = sites_flat + o;
+    if (k[g] == 3 && st_[1] == st_[0] + 1 && st_[2] == st_[0] + 2) {
+      tq.push_back(st_[0]);
+      tu.push_back(U[g]);
+    } else if (k[g] == 2 && st_[1] == st_[0] + 2) {
+      emb.emplace_back();
+      embed_u8((const unsigned char*)U[g], s->cb, emb.back(), s->p);
+      tq.push_back(st_[0]);
+      tu.push_back(emb.back().data());
+    }
+    o += k[g];
+  }
+  if (int rc = apply_three_site_batch(s, tq, tu)) return rc;
+  o = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int* st_ = sites_flat + o;
+    const bool adj2 = k[g] == 2 && st_[1] == st_[0] + 1;
+    const bool tri = (k[g] == 3 && st_[1] == st_[0] + 1 && st_[2] == st_[0] + 2) || (k[g] == 2 && st_[1] == st_[0] + 2);
+    if (!adj2 && !tri)
       if (int rc = apply_general(s, U[g], sites_flat + o, k[g])) return rc;
     o += k[g];
   }
