@@ -229,16 +229,19 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   }
   {
     // few items (an MPS layer): C CTAs per item share its block pairs (cluster barriers per step)
+    // shared memory for the largest staging of any item: the block size depends on M, and
+    // jd_smem is not monotone in M (bs halves above M = 320)
+    const size_t smem = std::max(jd_smem(std::min(maxM, 320)), jd_smem(maxM));
     int C = 1;
     const int bpairs = ((maxN + jd_bs(maxM) - 1) / jd_bs(maxM) + 1) / 2;
     while (C < 8 && n * C * 2 <= 148 && C * 2 <= bpairs) C *= 2;
     if (C == 1) {
-      k_jacobi_db<<<n, JD_THREADS, jd_smem(maxM), st>>>(dpre, 1);
+      k_jacobi_db<<<n, JD_THREADS, smem, st>>>(dpre, 1);
     } else {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(n * C, 1, 1);
       cfg.blockDim = dim3(JD_THREADS, 1, 1);
-      cfg.dynamicSmemBytes = jd_smem(maxM);
+      cfg.dynamicSmemBytes = smem;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
