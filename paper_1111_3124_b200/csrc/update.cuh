@@ -529,6 +529,11 @@ int run_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaStrea
       if (redo[b] & 2) c.no_precond = 1;
       sub.push_back(c);
     }
+  if (getenv("MPS_DEBUG_REDO")) {
+    int acc = 0;
+    for (int b = 0; b < n; ++b) acc += a[b].accumulate_v;
+    fprintf(stderr, "two-site batch of %d: %d accumulate V (predicted), %d re-run\n", n, acc, (int)sub.size());
+  }
   if (!sub.empty()) {
     std::vector<unsigned char> hd2;
     nl += launch_update2<T>(p, thr, sub.data(), (int)sub.size(), ws, st, hd2);

@@ -29,7 +29,7 @@ if len(sys.argv) > 2 and sys.argv[1] == "--config":
         per.append(round(time.perf_counter() - t1, 3))
     print(json.dumps({"config": cfg, "depth": depth, "n": n, "prec": p, "chi_max": chi, "gates": len(gates),
                       "layers": len(layers), "gpu_seconds": round(time.perf_counter() - t0, 3), "max_bond": max(st.bond_dims()),
-                      "seconds_per_layer": per}), flush=True)
+                      "seconds_per_layer": per, "stats": st.stats()}), flush=True)
     sys.exit(0)
 files = sys.argv[1:] or sorted(glob.glob(os.path.join("tests", "golden", "cfg*_oracle*.json")))
 for f in files:
