@@ -242,19 +242,6 @@ __device__ __forceinline__ void kmul_z(int64_t (&acc)[L + 2], const int32_t* Kp,
     for (int j = 0; j < L; ++j) acc[j + 2] = madw(K[L], x[j], acc[j + 2]);
   }
 }
-template <int L>
-__device__ __forceinline__ void kmul_sub(int64_t (&acc)[L + 2], const int32_t (&K)[L + 1], const int32_t (&x)[L],
-                                         bool hasInt) {
-#pragma unroll
-  for (int i = 0; i < L; ++i)
-#pragma unroll
-    for (int j = 0; j < L; ++j)
-      if (i + j >= L - 2) acc[i + j - (L - 2)] = madw(-K[i], x[j], acc[i + j - (L - 2)]);
-  if (hasInt) {
-#pragma unroll
-    for (int j = 0; j < L; ++j) acc[j + 2] = madw(-K[L], x[j], acc[j + 2]);
-  }
-}
 // round(V / 2^(28L)) of the L+2 accumulator columns (L-2 .. 2L-1) to L digits
 template <int L>
 __device__ __forceinline__ void tround2(int64_t (&acc)[L + 2], int32_t (&out)[L]) {

@@ -71,75 +71,14 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// One-sided Jacobi in binary64 (round-robin pairs, warp per pair, V_d accumulated).
-// Stops when no pair has |gamma| > tol sqrt(alpha_p alpha_q), tol = 4 M 2^-53.
-static __global__ void __launch_bounds__(256) k_jacobi_d(const PreItem* items) {
-  const PreItem it = items[blockIdx.x];
-  const int M = it.M, N = it.N, NP = N / 2;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* A = it.Ad;
-  double2* V = it.Vd;
-  for (int t = threadIdx.x; t < N * N; t += blockDim.x)
-    V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
-  __shared__ int s_any;
-  const double tol = 4.0 * M * 1.1102230246251565e-16;
-  int sweep = 0;
-  for (sweep = 1; sweep <= 40; ++sweep) {
-    if (threadIdx.x == 0) s_any = 0;
-    __syncthreads();
-    for (int step = 0; step < N - 1; ++step) {
-      for (int i = warp; i < NP; i += 8) {
-        int p, q;
-        rr_pair(N, step, i, p, q);
-        double2* ap = A + (size_t)p * M;
-        double2* aq = A + (size_t)q * M;
-        double sp = 0, sq = 0, gr = 0, gi = 0;
-        for (int r = lane; r < M; r += 32) {
-          const double2 x = ap[r], y = aq[r];
-          sp += x.x * x.x + x.y * x.y;
-          sq += y.x * y.x + y.y * y.y;
-          gr += x.x * y.x + x.y * y.y;  // conj(x) y
-          gi += x.x * y.y - x.y * y.x;
-        }
-        sp = warp_sum_d(sp); sq = warp_sum_d(sq); gr = warp_sum_d(gr); gi = warp_sum_d(gi);
-        const double g2 = gr * gr + gi * gi;
-        if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
-        if (lane == 0) s_any = 1;
-        // same rotation as the p-bit kernel (R17): d = a_q - a_p, r = sqrt(d^2 + 4|g|^2),
-        // c^2 = (|d| + r)/(2r), s = sgn(d) g/(r c); y_p = c x_p - conj(s) x_q, y_q = s x_p + c x_q
-        const double d = sq - sp;
-        const double rr = sqrt(d * d + 4.0 * g2);
-        const double c = sqrt((fabs(d) + rr) / (2.0 * rr));
-        const double sc = (d < 0 ? -1.0 : 1.0) / (rr * c);
-        const double sr = gr * sc, si = gi * sc;
-        for (int r = lane; r < M; r += 32) {
-          const double2 x = ap[r], y = aq[r];
-          ap[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-          aq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
-        }
-        double2* vp = V + (size_t)p * N;
-        double2* vq = V + (size_t)q * N;
-        for (int r = lane; r < N; r += 32) {
-          const double2 x = vp[r], y = vq[r];
-          vp[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-          vq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
-        }
-      }
-      __syncthreads();
-    }
-    const int any = s_any;
-    __syncthreads();
-    if (!any) break;
-  }
-  if (threadIdx.x == 0) *it.sweeps_d = sweep;
-}
-
-// Block variant (the one used): one CTA per item; the columns are split into blocks of bs
+// One-sided Jacobi in binary64 (V_d accumulated), blocked: one CTA (or cluster) per item;
+// the columns are split into blocks of bs
 // (16, or 8 when M > 320) and block pairs are visited round-robin; each block pair's 2bs
 // columns are staged in shared memory, given one inner round-robin sweep of pair rotations
 // (accumulated in a 2bs x 2bs W), written back, and V[:, block pair] <- V[:, block pair] W.
-// HBM/L2 traffic per outer sweep drops from O(N^2 M) to O(N M N/bs) (the warp-per-pair
-// kernel above was bandwidth bound at 15% of the update).
+// HBM/L2 traffic per outer sweep is O(N M N/bs) instead of O(N^2 M) for a warp-per-pair
+// kernel on global memory (which measured bandwidth bound at 15% of the update).  Stops when
+// no pair has |gamma| > tol sqrt(alpha_p alpha_q), tol = 4 M 2^-53.
 __host__ __device__ inline int jd_bs(int M) { return M <= 320 ? 16 : 8; }
 constexpr int JD_THREADS = 512;
 #ifndef JD_TOL
