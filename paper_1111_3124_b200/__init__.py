@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libmps_b200.so")
+_SO = os.environ.get("MPS_B200_SO") or os.path.join(_HERE, "libmps_b200.so")  # env: dev A/B builds
 
 STATUS = {0: "MPS_OK", -1: "MPS_EINVAL", -2: "MPS_ENOTUNITARY", -3: "MPS_ENOCONV", -4: "MPS_EZEROBOND",
           -5: "MPS_EOVERLAP", -6: "MPS_EUNSUPPORTED", -7: "MPS_ENOMEM", -8: "MPS_ECUDA", -9: "MPS_ENCCL",

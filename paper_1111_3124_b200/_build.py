@@ -30,16 +30,19 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """out / defines: development A/B builds (e.g. out=libmps_b200_x.so, defines=["JACOBI_GAUSS_D=0"])
+    loaded with MPS_B200_SO=<path>; the default build is the product library."""
+    if out is None and not force and up_to_date():
         return OUT
-    objdir = os.path.join(HERE, "build")
+    target = out or OUT
+    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(out).split(".")[0])
     os.makedirs(objdir, exist_ok=True)
 
     def compile_unit(u):
         src = os.path.join(CSRC, u)
         obj = os.path.join(objdir, u.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,9 +57,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for _, err in res:
             sys.stderr.write(err)
     objs = [o for o, _ in res]
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", OUT] + objs + ["-cudart", "static"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target] + objs + ["-cudart", "static"]
     subprocess.check_call(cmd)
-    return OUT
+    return target
 
 
 if __name__ == "__main__":

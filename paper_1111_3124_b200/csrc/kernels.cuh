@@ -1114,7 +1114,12 @@ inline void launch_jacobi(const SvdItem<NL>* d_items, int n, int C, cudaStream_t
 // CTAs per matrix: fill ~2 CTAs per SM when few matrices are in flight, at least one pair
 // per warp, power of two, at most 8 (portable cluster size).
 // MPS_JACOBI_MAX_CLUSTER (env, default 8) caps C; tests use it to compare C = 1 and C > 1.
-inline int jacobi_cluster_size(int n_items, int min_N) {
+// Many matrices (more than one wave of `slots` resident CTAs): one CTA per matrix leaves the
+// last wave partly empty (1024 items at chi = 128: 3.46 waves of 296 -> 4); C = 2 halves the
+// quantum at a measured per-matrix overhead of ~4.5% (cluster barriers; C = 4: 18%), so C is
+// chosen by waves(C) * overhead(C) / C (measured at N = 256, 280 bits: C = 2 gives 113.6 vs
+// 108.3 updates/s; profiles/r01_cluster_ab_v24.jsonl).
+inline int jacobi_cluster_size(int n_items, int min_N, int slots = 2 * 148) {
   static int cap = -1;
   if (cap < 0) {
     const char* e = getenv("MPS_JACOBI_MAX_CLUSTER");
@@ -1122,8 +1127,25 @@ inline int jacobi_cluster_size(int n_items, int min_N) {
     if (cap < 1) cap = 1;
     if (cap > 8) cap = 8;
   }
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("MPS_JACOBI_CLUSTER");  // A/B: force C (power of two <= 8)
+    force = e ? atoi(e) : 0;
+  }
   int C = 1;
+  if (force > 1) {
+    while (C < force && C < 8 && (C * 2) * NWARP <= min_N / 2) C *= 2;
+    return C;
+  }
   while (C < cap && n_items * C * 2 <= 2 * 148 && (C * 2) * NWARP <= min_N / 2) C *= 2;
+  if (C == 1 && n_items > slots && min_N >= 256 && cap >= 2) {
+    const double over[3] = {1.0, 1.045, 1.18};
+    double best = 1e300;
+    for (int c = 1, i = 0; c <= 4 && c <= cap && c * NWARP <= min_N / 2; c *= 2, ++i) {
+      const double cost = (double)((n_items * c + slots - 1) / slots) * over[i] / c;
+      if (cost < best - 1e-9) { best = cost; C = c; }
+    }
+  }
   return C;
 }
 

@@ -65,6 +65,29 @@ __global__ void k_fx_to_d(const PreItem* items) {
   atomicMax(it.rowmax, (unsigned long long)__double_as_longlong(rmax));
 }
 
+// all-reduce of four sums in 6 shuffles instead of 20: the first two levels exchange half of
+// the values (each lane keeps the pair / the value its lane bits select), then a plain
+// butterfly; finally every lane fetches the four totals from lanes 0..3
+__device__ __forceinline__ void warp_sum4_d(double& a, double& b, double& c, double& d) {
+  const int lane = threadIdx.x & 31;
+  const bool h16 = lane & 16, h8 = lane & 8;
+  // level 16: keep (a, b) if bit 4 clear else (c, d)
+  double x0 = h16 ? c : a, x1 = h16 ? d : b;
+  const double y0 = h16 ? a : c, y1 = h16 ? b : d;
+  x0 += __shfl_xor_sync(0xffffffffu, y0, 16);
+  x1 += __shfl_xor_sync(0xffffffffu, y1, 16);
+  // level 8: keep x0 if bit 3 clear else x1
+  double z = h8 ? x1 : x0;
+  z += __shfl_xor_sync(0xffffffffu, h8 ? x0 : x1, 8);
+#pragma unroll
+  for (int off = 4; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+  // lane with bits (4, 3) = (i1, i0) holds total number 2 i1 + i0: a = 0, b = 1, c = 2, d = 3
+  a = __shfl_sync(0xffffffffu, z, 0);
+  b = __shfl_sync(0xffffffffu, z, 8);
+  c = __shfl_sync(0xffffffffu, z, 16);
+  d = __shfl_sync(0xffffffffu, z, 24);
+}
+
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
@@ -88,6 +111,11 @@ inline size_t jd_smem(int M) {
   const int bs = jd_bs(M);
   return (size_t)2 * bs * M * 16 + (size_t)4 * bs * bs * 16 + 64;
 }
+
+// MPS_JD_PROF=1 (debug): clock64 cycles of thread 0 per phase, summed over CTAs:
+// [0] staging, [1] inner rotations, [2] A write-back, [3] V update, [4] block pairs, [5] sweeps
+static __device__ unsigned long long jd_prof[8];
+static __device__ int jd_prof_on;
 
 // C CTAs (a thread-block cluster when C > 1) share one item: the block pairs of a step are
 // dealt round-robin to the CTAs and the steps are separated by cluster barriers (few items in
@@ -113,6 +141,15 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
   for (int t = crank * blockDim.x + threadIdx.x; t < N * N; t += C * blockDim.x)
     V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
   const double tol = JD_TOL;
+  const bool prof = jd_prof_on && threadIdx.x == 0;
+  long long tm = prof ? clock64() : 0;
+  auto mark = [&](int k) {
+    if (prof) {
+      const long long t = clock64();
+      atomicAdd(&jd_prof[k], (unsigned long long)(t - tm));
+      tm = t;
+    }
+  };
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
     if (threadIdx.x == 0) s_any = 0;
@@ -136,6 +173,8 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
           W[t] = make_double2((t % nc2) == (t / nc2) ? 1.0 : 0.0, 0.0);
         __syncthreads();
+        mark(0);
+        if (prof) atomicAdd(&jd_prof[4], 1ull);
         for (int s2 = 0; s2 < nc2 - 1; ++s2) {
           for (int i = warp; i < bs; i += JD_THREADS / 32) {
             int p, q;
@@ -151,7 +190,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
               gr += x.x * y.x + x.y * y.y;
               gi += x.x * y.y - x.y * y.x;
             }
-            sp = warp_sum_d(sp); sq = warp_sum_d(sq); gr = warp_sum_d(gr); gi = warp_sum_d(gi);
+            warp_sum4_d(sp, sq, gr, gi);
             const double g2 = gr * gr + gi * gi;
             if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
             if (lane == 0) s_rot = 1;
@@ -175,38 +214,51 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
           }
           __syncthreads();
         }
+        mark(1);
         if (s_rot) {  // block-uniform
           if (threadIdx.x == 0) s_any = 1;
           for (int t = threadIdx.x; t < nc2 * M; t += blockDim.x) {
             const int l = t / M, r = t % M, c = s_col[l];
             if (c >= 0) A[(size_t)c * M + r] = Ab[t];
           }
-          // V[:, cols] <- V[:, cols] W: thread per row, its 2bs entries in registers
-          for (int r = threadIdx.x; r < N; r += blockDim.x) {
-            double2 v[32];
+          __syncthreads();  // Ab is free now
+          mark(2);
+          // stage V[:, cols] (N <= M rows) in its place
+          double2* Vb = Ab;  // [2bs][N]
+          for (int t = threadIdx.x; t < nc2 * N; t += blockDim.x) {
+            const int l = t / N, r = t % N, c = s_col[l];
+            Vb[t] = c >= 0 ? V[(size_t)c * N + r] : make_double2(0.0, 0.0);
+          }
+          __syncthreads();
+          // V[:, cols] <- V[:, cols] W: thread (row r, half h) forms bs of the 2bs outputs
+          for (int t = threadIdx.x; t < 2 * N; t += blockDim.x) {
+            const int r = t % N, h = t / N;
+            double2 acc[16];
 #pragma unroll
-            for (int l = 0; l < 32; ++l) {
-              const int c = l < nc2 ? s_col[l] : -1;
-              v[l] = c >= 0 ? V[(size_t)c * N + r] : make_double2(0.0, 0.0);
-            }
-#pragma unroll 1
-            for (int j = 0; j < nc2; ++j) {
-              const int cj = s_col[j];
-              if (cj < 0) continue;
-              double re = 0, im = 0;
+            for (int j = 0; j < 16; ++j) acc[j] = make_double2(0.0, 0.0);
+#pragma unroll 2
+            for (int l = 0; l < nc2; ++l) {
+              const double2 v = Vb[(size_t)l * N + r];
 #pragma unroll
-              for (int l = 0; l < 32; ++l) {
-                if (l < nc2) {
-                  const double2 w = W[(size_t)j * nc2 + l];
-                  re += v[l].x * w.x - v[l].y * w.y;
-                  im += v[l].x * w.y + v[l].y * w.x;
+              for (int j = 0; j < 16; ++j) {
+                if (j < bs) {
+                  const double2 w = W[(size_t)(h * bs + j) * nc2 + l];
+                  acc[j].x = fma(v.x, w.x, fma(-v.y, w.y, acc[j].x));
+                  acc[j].y = fma(v.x, w.y, fma(v.y, w.x, acc[j].y));
                 }
               }
-              V[(size_t)cj * N + r] = make_double2(re, im);
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j < bs) {
+                const int cj = s_col[h * bs + j];
+                if (cj >= 0) V[(size_t)cj * N + r] = acc[j];
+              }
             }
           }
         }
         __syncthreads();
+        mark(3);
       }
       csync();  // the next step's block pairs read columns this step wrote
     }
@@ -216,6 +268,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
     if (!any) break;
   }
   if (crank == 0 && threadIdx.x == 0) *it.sweeps_d = sweep;
+  if (prof) atomicAdd(&jd_prof[5], (unsigned long long)sweep);
 }
 
 // binary64 v (|v| <= 1) -> L balanced digits at exponent 1 (value = sum d_k 2^(28k) 2^(1-28L)), exact

@@ -159,7 +159,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
   dim3 g(std::max(1, std::min(64, (M * N + 255) / 256)), batch);
   k_mat_exp<<<g, 256, 0, st>>>((const MatItem*)(base + d_mat), RBr); ++nl;
   k_mat_conv<L, NL><<<g, 256, 0, st>>>((const MatItem*)(base + d_mat), RBr); ++nl;
-  launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), batch, jacobi_cluster_size(batch, Nj), st); ++nl;
+  launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), batch, jacobi_cluster_size(batch, Nj, jacobi_min_ctas<L>() * 148), st); ++nl;
   // the sigma records of the padded zero column are not part of the output
   k_finalize<L, NL><<<batch, NTHR, sizeof(mpf<NL>) * (size_t)Nj, st>>>((const FinItem<NL>*)(base + d_fin), RBr, p);
   ++nl;

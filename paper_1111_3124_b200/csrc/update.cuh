@@ -232,6 +232,19 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
     // shared memory for the largest staging of any item: the block size depends on M, and
     // jd_smem is not monotone in M (bs halves above M = 320)
     const size_t smem = std::max(jd_smem(std::min(maxM, 320)), jd_smem(maxM));
+    static int jprof = -1;
+    if (jprof < 0) {
+      const char* e = getenv("MPS_JD_PROF");
+      jprof = e && atoi(e) ? 1 : 0;
+      if (jprof) {
+        const int one = 1;
+        cudaMemcpyToSymbol(jd_prof_on, &one, sizeof(int));
+      }
+    }
+    if (jprof) {
+      const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      cudaMemcpyToSymbolAsync(jd_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+    }
     int C = 1;
     const int bpairs = ((maxN + jd_bs(maxM) - 1) / jd_bs(maxM) + 1) / 2;
     while (C < 8 && n * C * 2 <= 148 && C * 2 <= bpairs) C *= 2;
@@ -253,6 +266,13 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       cudaLaunchKernelEx(&cfg, k_jacobi_db, dpre, C);
     }
     ++nl;
+    if (jprof) {
+      unsigned long long h[8];
+      cudaMemcpyFromSymbolAsync(h, jd_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu sweeps %llu (items %d)\n",
+              (double)h[0], (double)h[1], (double)h[2], (double)h[3], h[4], h[5], n);
+    }
   }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
   const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
@@ -452,7 +472,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   {
     int minN = 1 << 30;
     for (int b = 0; b < n; ++b) minN = std::min(minN, hs[b].N);
-    launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n, minN), st);
+    launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n, minN, jacobi_min_ctas<L>() * 148), st);
     ++nl;
   }
   {
