@@ -425,18 +425,24 @@ __device__ __forceinline__ void tmul_z(int64_t (&acc)[LG + 2], const int32_t (&x
 }
 
 constexpr int GT_TILE = 16;
+#ifndef GEMM_3M  // complex products of k_gemm_t in three real products
+#define GEMM_3M 1
+#endif
+constexpr int GEMM_PLANES = GEMM_3M ? 3 : 2;
 
 template <int L, int LG, int Z>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG, "precision schedule");
-  constexpr int GT_KB = 8;  // k per staging round (16 measured no faster)
+  // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
+  constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
   if (it.rows <= 0 || it.cols <= 0) return;  // item without this GEMM
   const int tilesR = (it.rows + GT_TILE - 1) / GT_TILE, tilesC = (it.cols + GT_TILE - 1) / GT_TILE;
   const int tx = threadIdx.x % GT_TILE, ty = threadIdx.x / GT_TILE;
-  __shared__ int32_t As[GT_KB][2][LG][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
-  __shared__ int32_t Bs[GT_KB][2][LG][GT_TILE + 1];
+  // planes: re, im, re + im (the last for the three-product complex multiply)
+  __shared__ int32_t As[GT_KB][GEMM_PLANES][LG][GT_TILE + 1];  // +1: conflict-free k-fastest staging writes
+  __shared__ int32_t Bs[GT_KB][GEMM_PLANES][LG][GT_TILE + 1];
   const bool percol = it.eBcols != nullptr;
   // block exponent: given (eCout), or eA + eB + ghead (head-room for K terms, eCwrite)
   const int64_t eC = percol ? 0 : (it.eCout ? *it.eCout : *it.eA + *it.eB + it.ghead);
@@ -453,6 +459,11 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
     int64_t ar[LG + 2], ai[LG + 2];
 #pragma unroll
     for (int j = 0; j < LG + 2; ++j) ar[j] = ai[j] = 0;
+#if GEMM_3M
+    int64_t as[LG + 2];  // sum (xr + xi)(yr + yi)
+#pragma unroll
+    for (int j = 0; j < LG + 2; ++j) as[j] = 0;
+#endif
     for (int k0 = 0; k0 < it.K; k0 += GT_KB) {
       __syncthreads();
       // stage the top LG digits of GT_KB x 16 elements of each operand; the index order
@@ -483,6 +494,34 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         }
       }
       __syncthreads();
+#if GEMM_3M
+      // (xr + i xi)(yr + i yi) = xr yr - xi yi + i [(xr + xi)(yr + yi) - xr yr - xi yi]: three
+      // LG-digit products instead of four (digit sums |d| <= 2^29: products < 2^58, normalised
+      // every 4 k so that no int64 column exceeds 2^62)
+      for (int w = threadIdx.x; w < GT_KB * LG * GT_TILE; w += 256) {
+        const int e = w % GT_TILE, dg = (w / GT_TILE) % LG, kk = w / (GT_TILE * LG);
+        As[kk][2][dg][e] = As[kk][0][dg][e] + As[kk][1][dg][e];
+        Bs[kk][2][dg][e] = Bs[kk][0][dg][e] + Bs[kk][1][dg][e];
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int kk = 0; kk < GT_KB; ++kk) {
+        int32_t x[LG], y[LG];
+#pragma unroll
+        for (int j = 0; j < LG; ++j) { x[j] = As[kk][0][j][tx]; y[j] = Bs[kk][0][j][ty]; }
+        tmul_z<LG, Z, false>(ar, x, y);
+#pragma unroll
+        for (int j = 0; j < LG; ++j) { x[j] = As[kk][1][j][tx]; y[j] = Bs[kk][1][j][ty]; }
+        tmul_z<LG, Z, false>(ai, x, y);
+#pragma unroll
+        for (int j = 0; j < LG; ++j) { x[j] = As[kk][2][j][tx]; y[j] = Bs[kk][2][j][ty]; }
+        tmul_z<LG, Z, false>(as, x, y);
+        if ((kk & 3) == 3 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); tnorm2<LG>(as); }
+      }
+      tnorm2<LG>(ar);
+      tnorm2<LG>(ai);
+      tnorm2<LG>(as);
+#else
 #pragma unroll 1
       for (int kk = 0; kk < GT_KB; ++kk) {
         int32_t xr[LG], xi[LG], yr[LG], yi[LG];
@@ -499,7 +538,17 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
       }
       tnorm2<LG>(ar);
       tnorm2<LG>(ai);
+#endif
     }
+#if GEMM_3M
+    // ar = sum xr yr, ai = sum xi yi, as = sum (xr + xi)(yr + yi) -> re = ar - ai, im = as - ar - ai
+#pragma unroll
+    for (int j = 0; j < LG + 2; ++j) {
+      const int64_t t1 = ar[j], t2 = ai[j];
+      ar[j] = t1 - t2;
+      ai[j] = as[j] - t1 - t2;
+    }
+#endif
     if (r < it.rows && c < ncols) {
       const int pc = pcol(c);  // physical column
 #pragma unroll
