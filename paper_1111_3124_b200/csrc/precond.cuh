@@ -30,6 +30,7 @@ struct PreItem {
   int64_t* eOne;                          // [2] = {1, 0}: exponents of X and of D/2
   int64_t* eA1;                           // exponent chosen for A_1 = Theta' X (1)
   int* anyflag;                           // [2] "some block pair rotated" per sweep parity (cluster mode)
+  unsigned long long* offmax;             // [2] largest |gamma|^2 / (alpha_p alpha_q) per sweep parity (bits)
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -95,27 +96,88 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 // One-sided Jacobi in binary64 (V_d accumulated), blocked: one CTA (or cluster) per item;
-// the columns are split into blocks of bs
-// (16, or 8 when M > 320) and block pairs are visited round-robin; each block pair's 2bs
-// columns are staged in shared memory, given one inner round-robin sweep of pair rotations
-// (accumulated in a 2bs x 2bs W), written back, and V[:, block pair] <- V[:, block pair] W.
-// HBM/L2 traffic per outer sweep is O(N M N/bs) instead of O(N^2 M) for a warp-per-pair
-// kernel on global memory (which measured bandwidth bound at 15% of the update).  Stops when
-// no pair has |gamma| > tol sqrt(alpha_p alpha_q), tol = 4 M 2^-53.
-__host__ __device__ inline int jd_bs(int M) { return M <= 320 ? 16 : 8; }
+// the columns are split into blocks of bs (16; 8 when M > 320; 4 when M > 640) and block pairs
+// are visited round-robin; each block pair's 2bs columns are staged in shared memory and given
+// one inner round-robin sweep of pair rotations accumulated in a 2bs x 2bs W, then
+// A[:, block pair] and V[:, block pair] are multiplied by W.  HBM/L2 traffic per outer sweep is
+// O(N M N/bs) instead of O(N^2 M) for a warp-per-pair kernel on global memory.
+// Inner sweep, two forms (the rotation formula and the pair order are the same):
+//  * Gram form (while the previous sweep still had a relative off-diagonal above JD_GRAM_OFF
+//    and the block pair's column norms^2 are within 2^20 of each other): G = Ab^H Ab is formed
+//    once (a 2bs x 2bs x M product) and the rotations are computed from and applied to G
+//    (two-sided, G <- J^H G J) and W only; A's block columns are then Ab W.  The arithmetic
+//    per pair drops from O(M) to O(bs), but G's rounding is relative to the largest column,
+//    so the late sweeps (small off-diagonals) use
+//  * the column form: every pair's dots are taken from the (rotated) columns in shared memory.
+// Stops when a sweep rotates no pair (|gamma| > tol sqrt(alpha_p alpha_q), tol = 4 M 2^-53) —
+// always decided on dots of the current columns (a Gram-form sweep that rotates nothing has
+// not changed G, which equals those dots).  The binary64 stage only chooses the starting basis
+// of the p-bit iteration (R19): no p-bit result depends on its rounding or on the form used.
+__host__ __device__ inline int jd_bs(int M) { return M <= 320 ? 16 : (M <= 640 ? 8 : 4); }
 constexpr int JD_THREADS = 512;
 #ifndef JD_TOL
 #define JD_TOL (4.0 * M * 1.1102230246251565e-16)  // 4 M 2^-53 (1e-12 costs a p-bit sweep)
 #endif  // one warp per pair of a block pair's inner step (bs <= 16)
+#ifndef JD_GRAM_OFF
+#define JD_GRAM_OFF 1e-6  // Gram-form inner sweeps while max |gamma| / sqrt(alpha_p alpha_q) exceeds this
+#endif
+__host__ __device__ inline int jd_mp(int M) { return M | 1; }  // odd column stride: conflict-free Gram loads
 inline size_t jd_smem(int M) {
-  const int bs = jd_bs(M);
-  return (size_t)2 * bs * M * 16 + (size_t)4 * bs * bs * 16 + 64;
+  const int nc2 = 2 * jd_bs(M);
+  return (size_t)nc2 * jd_mp(M) * 16 + (size_t)nc2 * nc2 * 16 + (size_t)nc2 * (nc2 + 1) * 16 + 64;
 }
 
 // MPS_JD_PROF=1 (debug): clock64 cycles of thread 0 per phase, summed over CTAs:
-// [0] staging, [1] inner rotations, [2] A write-back, [3] V update, [4] block pairs, [5] sweeps
+// [0] staging, [1] inner rotations, [2] A write-back, [3] V update, [4] block pairs, [5] sweeps,
+// [6] block pairs in Gram form
 static __device__ unsigned long long jd_prof[8];
 static __device__ int jd_prof_on;
+
+// dst[:, s_col[j]] = src (R rows, column stride ld, 2bs columns) x W  (thread: row r, half h)
+__device__ __forceinline__ void jd_apply_w(const double2* src, int ld, double2* dst, int R, const double2* W, int bs,
+                                           const int* s_col) {
+  const int nc2 = 2 * bs;
+  for (int t = threadIdx.x; t < 2 * R; t += blockDim.x) {
+    const int r = t % R, h = t / R;
+    double2 acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = make_double2(0.0, 0.0);
+#pragma unroll 2
+    for (int l = 0; l < nc2; ++l) {
+      const double2 v = src[(size_t)l * ld + r];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < bs) {
+          const double2 w = W[(size_t)(h * bs + j) * nc2 + l];
+          acc[j].x = fma(v.x, w.x, fma(-v.y, w.y, acc[j].x));
+          acc[j].y = fma(v.x, w.y, fma(v.y, w.x, acc[j].y));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j < bs) {
+        const int cj = s_col[h * bs + j];
+        if (cj >= 0) dst[(size_t)cj * R + r] = acc[j];
+      }
+    }
+  }
+}
+
+// rotation parameters of the oracle's formula (R17 form): d = alpha_q - alpha_p,
+// r = sqrt(d^2 + 4|g|^2), c = sqrt((|d| + r) / 2r), s = sgn(d) g / (r c)
+// (two reciprocal square roots, no division: 1/r, c^2 = (|d|/r + 1)/2, 1/c, s = sgn(d) g (1/r)(1/c))
+__device__ __forceinline__ void jd_rot(double sp, double sq, double gr, double gi, double g2, double& c, double& sr,
+                                       double& si) {
+  const double d = sq - sp;
+  const double ir = rsqrt(d * d + 4.0 * g2);
+  const double c2 = 0.5 * fma(fabs(d), ir, 1.0);
+  const double ic = rsqrt(c2);
+  c = c2 * ic;
+  const double sc = (d < 0 ? -ir : ir) * ic;
+  sr = gr * sc;
+  si = gi * sc;
+}
 
 // C CTAs (a thread-block cluster when C > 1) share one item: the block pairs of a step are
 // dealt round-robin to the CTAs and the steps are separated by cluster barriers (few items in
@@ -130,12 +192,18 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
   };
   const int M = it.M, N = it.N;
   if (N == 0) return;
-  const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs;
+  const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs, MP = jd_mp(M);
+  const int nh = bs, T = nh * nh;  // Gram: 2x2 tiles of entries (i, j), (i, j+bs), (i+bs, j), (i+bs, j+bs)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ double2 jds[];
-  double2* Ab = jds;                    // [2bs][M]
-  double2* W = jds + (size_t)nc2 * M;   // [2bs][2bs] column-major
-  __shared__ int s_any, s_rot, s_col[32];
+  double2* Ab = jds;                       // [2bs][MP] block columns
+  double2* W = jds + (size_t)nc2 * MP;     // [2bs][2bs] column-major
+  double2* G = W + (size_t)nc2 * nc2;      // [2bs][2bs + 1] row-major (Gram form)
+  const int GL = nc2 + 1, lgc = __ffs(nc2) - 1;  // nc2 = 2^lgc
+  __shared__ int s_any, s_rot, s_gram, s_col[32];
+  __shared__ double s_c[16], s_sr[16], s_si[16];
+  __shared__ int s_on[16], s_p[16], s_q[16];
+  __shared__ unsigned long long s_off;  // max rel^2 = |g|^2 / (alpha_p alpha_q) of this CTA's sweep (bits)
   double2* A = it.Ad;
   double2* V = it.Vd;
   for (int t = crank * blockDim.x + threadIdx.x; t < N * N; t += C * blockDim.x)
@@ -150,11 +218,21 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
       tm = t;
     }
   };
+  auto note_off = [&](double g2, double sp, double sq) {
+    if (sp > 0 && sq > 0) atomicMax(&s_off, (unsigned long long)__double_as_longlong(g2 / (sp * sq)));
+  };
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
-    if (threadIdx.x == 0) s_any = 0;
-    if (crank == 0 && threadIdx.x == 0) *(volatile int*)&it.anyflag[sweep & 1] = 0;
+    if (threadIdx.x == 0) { s_any = 0; s_off = 0ull; }
+    if (crank == 0 && threadIdx.x == 0) {
+      *(volatile int*)&it.anyflag[sweep & 1] = 0;
+      *(volatile unsigned long long*)&it.offmax[sweep & 1] = 0ull;
+    }
     csync();
+    // Gram-form sweep while the previous sweep's largest relative off-diagonal was big
+    const bool gram_sweep =
+        sweep == 1 || __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[(sweep - 1) & 1]) >
+                          JD_GRAM_OFF * JD_GRAM_OFF;
     for (int step = 0; step < nbe - 1; ++step) {
       for (int bp = crank; bp < nbe / 2; bp += C) {
         int I, J;
@@ -164,105 +242,202 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
           const int l = threadIdx.x, blk = l < bs ? I : J, c = blk * bs + (l % bs);
           s_col[l] = (blk < nb && c < N) ? c : -1;
         }
-        if (threadIdx.x == 0) s_rot = 0;
+        if (threadIdx.x == 0) { s_rot = 0; s_gram = 0; }
         __syncthreads();
-        for (int t = threadIdx.x; t < nc2 * M; t += blockDim.x) {
-          const int l = t / M, r = t % M, c = s_col[l];
-          Ab[t] = c >= 0 ? A[(size_t)c * M + r] : make_double2(0.0, 0.0);
+        for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {  // (l, r) advance by blockDim
+          const int c = s_col[l];
+          Ab[(size_t)l * MP + r] = c >= 0 ? A[(size_t)c * M + r] : make_double2(0.0, 0.0);
+          r += blockDim.x;
+          while (r >= M) { r -= M; ++l; }
+        }
+        __syncthreads();
+        mark(0);
+        if (prof) atomicAdd(&jd_prof[4], 1ull);
+        if (gram_sweep) {
+          // G = Ab^H Ab: thread (tile, half of the rows); half 1's partial sums go through W
+          const int t = threadIdx.x;
+          double2 g[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+          const int tile = t % T, half = t / T;
+          const int ti = tile / nh, tj = tile % nh;
+          if (t < 2 * T) {
+            const int rh = (M + 1) / 2, r0 = half ? rh : 0, r1 = half ? M : rh;
+            const double2* a0 = Ab + (size_t)ti * MP;
+            const double2* a1 = Ab + (size_t)(ti + bs) * MP;
+            const double2* b0 = Ab + (size_t)tj * MP;
+            const double2* b1 = Ab + (size_t)(tj + bs) * MP;
+            for (int r = r0; r < r1; ++r) {
+              const double2 x0 = a0[r], x1 = a1[r], y0 = b0[r], y1 = b1[r];
+              // conj(x) y
+              g[0].x = fma(x0.x, y0.x, fma(x0.y, y0.y, g[0].x)); g[0].y = fma(x0.x, y0.y, fma(-x0.y, y0.x, g[0].y));
+              g[1].x = fma(x0.x, y1.x, fma(x0.y, y1.y, g[1].x)); g[1].y = fma(x0.x, y1.y, fma(-x0.y, y1.x, g[1].y));
+              g[2].x = fma(x1.x, y0.x, fma(x1.y, y0.y, g[2].x)); g[2].y = fma(x1.x, y0.y, fma(-x1.y, y0.x, g[2].y));
+              g[3].x = fma(x1.x, y1.x, fma(x1.y, y1.y, g[3].x)); g[3].y = fma(x1.x, y1.y, fma(-x1.y, y1.x, g[3].y));
+            }
+            if (half) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k) W[(size_t)tile * 4 + k] = g[k];
+            }
+          }
+          __syncthreads();
+          if (t < T) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const double2 o = W[(size_t)tile * 4 + k];
+              g[k].x += o.x;
+              g[k].y += o.y;
+            }
+            G[(size_t)ti * GL + tj] = g[0];
+            G[(size_t)ti * GL + tj + bs] = g[1];
+            G[(size_t)(ti + bs) * GL + tj] = g[2];
+            G[(size_t)(ti + bs) * GL + tj + bs] = g[3];
+          }
+          __syncthreads();
+          if (threadIdx.x == 0) {  // column norms^2 within 2^20: Gram form for this block pair
+            double mx = 0, mn = 0;
+            for (int l = 0; l < nc2; ++l) {
+              const double a = G[(size_t)l * GL + l].x;
+              if (s_col[l] < 0 || !(a > 0)) continue;
+              mx = fmax(mx, a);
+              mn = mn == 0 ? a : fmin(mn, a);
+            }
+            s_gram = mx <= mn * 1048576.0;
+          }
         }
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
           W[t] = make_double2((t % nc2) == (t / nc2) ? 1.0 : 0.0, 0.0);
         __syncthreads();
-        mark(0);
-        if (prof) atomicAdd(&jd_prof[4], 1ull);
-        for (int s2 = 0; s2 < nc2 - 1; ++s2) {
-          for (int i = warp; i < bs; i += JD_THREADS / 32) {
-            int p, q;
-            rr_pair(nc2, s2, i, p, q);
-            if (s_col[p] < 0 || s_col[q] < 0) continue;
-            double2* ap = Ab + (size_t)p * M;
-            double2* aq = Ab + (size_t)q * M;
-            double sp = 0, sq = 0, gr = 0, gi = 0;
-            for (int r = lane; r < M; r += 32) {
-              const double2 x = ap[r], y = aq[r];
-              sp += x.x * x.x + x.y * x.y;
-              sq += y.x * y.x + y.y * y.y;
-              gr += x.x * y.x + x.y * y.y;
-              gi += x.x * y.y - x.y * y.x;
+        if (s_gram) {
+          if (prof) atomicAdd(&jd_prof[6], 1ull);
+          for (int s2 = 0; s2 < nc2 - 1; ++s2) {
+            if (threadIdx.x < bs) {
+              const int i = threadIdx.x;
+              int p, q;
+              rr_pair(nc2, s2, i, p, q);
+              int on = 0;
+              if (s_col[p] >= 0 && s_col[q] >= 0) {
+                const double sp = G[(size_t)p * GL + p].x, sq = G[(size_t)q * GL + q].x;
+                const double2 gg = G[(size_t)p * GL + q];
+                const double g2 = gg.x * gg.x + gg.y * gg.y;
+                note_off(g2, sp, sq);
+                if (g2 > tol * tol * sp * sq && g2 != 0.0) {
+                  double c, sr, si;
+                  jd_rot(sp, sq, gg.x, gg.y, g2, c, sr, si);
+                  s_c[i] = c; s_sr[i] = sr; s_si[i] = si;
+                  on = 1;
+                  s_rot = 1;
+                }
+              }
+              s_on[i] = on;
+              s_p[i] = p;
+              s_q[i] = q;
             }
-            warp_sum4_d(sp, sq, gr, gi);
-            const double g2 = gr * gr + gi * gi;
-            if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
-            if (lane == 0) s_rot = 1;
-            const double d = sq - sp;
-            const double rr = sqrt(d * d + 4.0 * g2);
-            const double c = sqrt((fabs(d) + rr) / (2.0 * rr));
-            const double sc = (d < 0 ? -1.0 : 1.0) / (rr * c);
-            const double sr = gr * sc, si = gi * sc;
-            for (int r = lane; r < M; r += 32) {
-              const double2 x = ap[r], y = aq[r];
-              ap[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-              aq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+            __syncthreads();
+            // columns of G and W:  x' = c x - conj(s) y,  y' = s x + c y
+            for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
+              const int i = t >> lgc, k = t & (nc2 - 1);
+              if (!s_on[i]) continue;
+              const int p = s_p[i], q = s_q[i];
+              const double c = s_c[i], sr = s_sr[i], si = s_si[i];
+              double2* gp = G + (size_t)k * GL + p;
+              double2* gq = G + (size_t)k * GL + q;
+              double2 x = *gp, y = *gq;
+              *gp = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+              *gq = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+              double2* wp = W + (size_t)p * nc2 + k;
+              double2* wq = W + (size_t)q * nc2 + k;
+              x = *wp; y = *wq;
+              *wp = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+              *wq = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
             }
-            double2* wp = W + (size_t)p * nc2;
-            double2* wq = W + (size_t)q * nc2;
-            for (int r = lane; r < nc2; r += 32) {
-              const double2 x = wp[r], y = wq[r];
-              wp[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-              wq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+            __syncthreads();
+            // rows of G (J^H from the left):  x' = c x - s y,  y' = conj(s) x + c y
+            for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
+              const int i = t >> lgc, k = t & (nc2 - 1);
+              if (!s_on[i]) continue;
+              const int p = s_p[i], q = s_q[i];
+              const double c = s_c[i], sr = s_sr[i], si = s_si[i];
+              double2* gp = G + (size_t)p * GL + k;
+              double2* gq = G + (size_t)q * GL + k;
+              const double2 x = *gp, y = *gq;
+              *gp = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
+              *gq = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
             }
+            __syncthreads();
           }
-          __syncthreads();
+        } else {
+          for (int s2 = 0; s2 < nc2 - 1; ++s2) {
+            for (int i = warp; i < bs; i += JD_THREADS / 32) {
+              int p, q;
+              rr_pair(nc2, s2, i, p, q);
+              if (s_col[p] < 0 || s_col[q] < 0) continue;
+              double2* ap = Ab + (size_t)p * MP;
+              double2* aq = Ab + (size_t)q * MP;
+              double sp = 0, sq = 0, gr = 0, gi = 0;
+              for (int r = lane; r < M; r += 32) {
+                const double2 x = ap[r], y = aq[r];
+                sp += x.x * x.x + x.y * x.y;
+                sq += y.x * y.x + y.y * y.y;
+                gr += x.x * y.x + x.y * y.y;
+                gi += x.x * y.y - x.y * y.x;
+              }
+              warp_sum4_d(sp, sq, gr, gi);
+              const double g2 = gr * gr + gi * gi;
+              if (lane == 0) note_off(g2, sp, sq);
+              if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
+              if (lane == 0) s_rot = 1;
+              double c, sr, si;
+              jd_rot(sp, sq, gr, gi, g2, c, sr, si);
+              for (int r = lane; r < M; r += 32) {
+                const double2 x = ap[r], y = aq[r];
+                ap[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                aq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+              }
+              double2* wp = W + (size_t)p * nc2;
+              double2* wq = W + (size_t)q * nc2;
+              for (int r = lane; r < nc2; r += 32) {
+                const double2 x = wp[r], y = wq[r];
+                wp[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                wq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+              }
+            }
+            __syncthreads();
+          }
         }
         mark(1);
         if (s_rot) {  // block-uniform
           if (threadIdx.x == 0) s_any = 1;
-          for (int t = threadIdx.x; t < nc2 * M; t += blockDim.x) {
-            const int l = t / M, r = t % M, c = s_col[l];
-            if (c >= 0) A[(size_t)c * M + r] = Ab[t];
+          if (s_gram) {
+            jd_apply_w(Ab, MP, A, M, W, bs, s_col);  // A[:, cols] = Ab W
+          } else {
+            for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {
+              const int c = s_col[l];
+              if (c >= 0) A[(size_t)c * M + r] = Ab[(size_t)l * MP + r];
+              r += blockDim.x;
+              while (r >= M) { r -= M; ++l; }
+            }
           }
           __syncthreads();  // Ab is free now
           mark(2);
-          // stage V[:, cols] (N <= M rows) in its place
+          // stage V[:, cols] (N <= M rows) in its place, then V[:, cols] = Vb W
           double2* Vb = Ab;  // [2bs][N]
-          for (int t = threadIdx.x; t < nc2 * N; t += blockDim.x) {
-            const int l = t / N, r = t % N, c = s_col[l];
-            Vb[t] = c >= 0 ? V[(size_t)c * N + r] : make_double2(0.0, 0.0);
+          for (int l = threadIdx.x / N, r = threadIdx.x % N; l < nc2;) {
+            const int c = s_col[l];
+            Vb[(size_t)l * N + r] = c >= 0 ? V[(size_t)c * N + r] : make_double2(0.0, 0.0);
+            r += blockDim.x;
+            while (r >= N) { r -= N; ++l; }
           }
           __syncthreads();
-          // V[:, cols] <- V[:, cols] W: thread (row r, half h) forms bs of the 2bs outputs
-          for (int t = threadIdx.x; t < 2 * N; t += blockDim.x) {
-            const int r = t % N, h = t / N;
-            double2 acc[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[j] = make_double2(0.0, 0.0);
-#pragma unroll 2
-            for (int l = 0; l < nc2; ++l) {
-              const double2 v = Vb[(size_t)l * N + r];
-#pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                if (j < bs) {
-                  const double2 w = W[(size_t)(h * bs + j) * nc2 + l];
-                  acc[j].x = fma(v.x, w.x, fma(-v.y, w.y, acc[j].x));
-                  acc[j].y = fma(v.x, w.y, fma(v.y, w.x, acc[j].y));
-                }
-              }
-            }
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              if (j < bs) {
-                const int cj = s_col[h * bs + j];
-                if (cj >= 0) V[(size_t)cj * N + r] = acc[j];
-              }
-            }
-          }
+          jd_apply_w(Vb, N, V, N, W, bs, s_col);
         }
         __syncthreads();
         mark(3);
       }
       csync();  // the next step's block pairs read columns this step wrote
     }
-    if (threadIdx.x == 0 && s_any) atomicOr(&it.anyflag[sweep & 1], 1);
+    if (threadIdx.x == 0) {
+      if (s_any) atomicOr(&it.anyflag[sweep & 1], 1);
+      atomicMax(&it.offmax[sweep & 1], s_off);
+    }
     csync();
     const int any = *(volatile int*)&it.anyflag[sweep & 1];
     if (!any) break;

@@ -167,6 +167,7 @@ struct PreBufs {
   int* sweeps_d;
   int64_t *eOne, *eA1;
   int* anyflag;
+  unsigned long long* offmax;
   int32_t* rcoef;
   int64_t* rexp;
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
@@ -185,6 +186,7 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.eOne = (int64_t*)(q + 16);
   b.eA1 = (int64_t*)(q + 32);
   b.anyflag = (int*)(q + 40);
+  b.offmax = (unsigned long long*)(q + 64);
   b.rcoef = (int32_t*)(q + 256);
   b.rexp = (int64_t*)((char*)b.rcoef + align_up(4 * (size_t)N * (L + 1)));
   return b;
@@ -195,7 +197,7 @@ template <int L>
 inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, const int64_t* eA0, int32_t* Af,
                       int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride) {
   constexpr int NSIT = ns_iters<L>();
-  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag};
+  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -211,7 +213,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
 }
 template <int L>
 inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t stride) {
-  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag};
+  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
   for (int k = 0; k <= 2 * ns_iters<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
@@ -224,14 +226,14 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);  // + static
     attr = true;
   }
   {
     // few items (an MPS layer): C CTAs per item share its block pairs (cluster barriers per step)
     // shared memory for the largest staging of any item: the block size depends on M, and
-    // jd_smem is not monotone in M (bs halves above M = 320)
-    const size_t smem = std::max(jd_smem(std::min(maxM, 320)), jd_smem(maxM));
+    // jd_smem is not monotone in M (bs halves above M = 320 and M = 640)
+    const size_t smem = std::max(std::max(jd_smem(std::min(maxM, 320)), jd_smem(std::min(maxM, 640))), jd_smem(maxM));
     static int jprof = -1;
     if (jprof < 0) {
       const char* e = getenv("MPS_JD_PROF");
@@ -270,8 +272,8 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       unsigned long long h[8];
       cudaMemcpyFromSymbolAsync(h, jd_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu sweeps %llu (items %d)\n",
-              (double)h[0], (double)h[1], (double)h[2], (double)h[3], h[4], h[5], n);
+      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu (Gram form %llu) sweeps %llu (items %d)\n",
+              (double)h[0], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
     }
   }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
