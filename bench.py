@@ -72,7 +72,8 @@ def trunc_products(LG: int, Z: int = 0) -> int:
 def gemm_imad_wide_per_item(chi: int, p: int) -> float:
     """IMAD.WIDE of the GEMM kernels of one two-site update: the a1
     contraction, the Newton-Schulz iterations (Hermitian D_k: half the tiles), A_1 = Theta' X
-    and the recovery of the chi kept columns of V; 4 real products per complex MAC."""
+    and the recovery of the chi kept columns of V; 4 real products per complex MAC in the
+    contraction (k_gemm), 3 in the tiled k_gemm_t (three-product complex multiply)."""
     L = 10 if p <= 280 else 19
     sched = [(4, 1), (7, 2), (10, 5)] if L == 10 else [(4, 1), (7, 2), (14, 5), (19, 10)]
     M = N = 2 * chi
@@ -80,9 +81,9 @@ def gemm_imad_wide_per_item(chi: int, p: int) -> float:
     herm_out = (N // t) * (N // t + 1) // 2 * t * t  # tiles on / above the diagonal
     w = (2 * chi) * (2 * chi) * chi * 4 * trunc_products(L)  # contraction (K = chi)
     for LG, Z in sched:
-        w += herm_out * N * 4 * trunc_products(LG) + N * N * N * 4 * trunc_products(LG, Z)
-    w += M * N * N * 4 * trunc_products(L)  # A_1
-    w += N * chi * M * 4 * trunc_products(L)  # recovery of the kept columns
+        w += herm_out * N * 3 * trunc_products(LG) + N * N * N * 3 * trunc_products(LG, Z)
+    w += M * N * N * 3 * trunc_products(L)  # A_1
+    w += N * chi * M * 3 * trunc_products(L)  # recovery of the kept columns
     return float(w)
 
 

@@ -444,7 +444,8 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   k_prep_conv<L, NL><<<gp, 256, 0, st>>>((const PrepItem*)(base + d_prep), RBr); ++nl;
   dim3 gg(std::max(1, std::min(128, (maxMN + 127) / 128)), n);
   // a1 contraction: the thread-per-element k_gemm measured 10% faster than the tiled
-  // k_gemm_t at K = chi (92.7 vs 102.5 ms for 296 chi=128 items); hgc stays as the tiled form
+  // k_gemm_t at K = chi (92.7 vs 102.5 ms for 296 chi=128 items; with the three-product
+  // k_gemm_t still 1.5% slower per bench step, v26); hgc stays as the tiled form
   k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
   k_mix<L, NL><<<gg, 128, 16 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
   prof_mark(PROF_CONTRACT, 0, st);

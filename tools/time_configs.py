@@ -8,7 +8,7 @@ import os
 import sys
 import time
 
-sys.path.append('.')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # repo root before site-packages
 import paper_1111_3124_b200 as m  # noqa: E402
 from synth import gen  # noqa: E402
 from tests.test_gpu_configs import layers_of  # noqa: E402
