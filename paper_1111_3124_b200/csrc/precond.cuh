@@ -129,7 +129,7 @@ inline size_t jd_smem(int M) {
 
 // MPS_JD_PROF=1 (debug): clock64 cycles of thread 0 per phase, summed over CTAs:
 // [0] staging, [1] inner rotations, [2] A write-back, [3] V update, [4] block pairs, [5] sweeps,
-// [6] block pairs in Gram form
+// [6] block pairs in Gram form, [7] Gram products (cycles)
 static __device__ unsigned long long jd_prof[8];
 static __device__ int jd_prof_on;
 
@@ -218,8 +218,9 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
       tm = t;
     }
   };
+  double off_t = 0.0;  // this thread's largest |g|^2 / (alpha_p alpha_q) of the sweep (one atomic per sweep)
   auto note_off = [&](double g2, double sp, double sq) {
-    if (sp > 0 && sq > 0) atomicMax(&s_off, (unsigned long long)__double_as_longlong(g2 / (sp * sq)));
+    if (sp > 0 && sq > 0) off_t = fmax(off_t, g2 / (sp * sq));
   };
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
@@ -306,6 +307,11 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
           W[t] = make_double2((t % nc2) == (t / nc2) ? 1.0 : 0.0, 0.0);
         __syncthreads();
+        if (prof && gram_sweep) {  // [7]: Gram products + mode decision (moved out of "inner")
+          const long long t = clock64();
+          atomicAdd(&jd_prof[7], (unsigned long long)(t - tm));
+          tm = t;
+        }
         if (s_gram) {
           if (prof) atomicAdd(&jd_prof[6], 1ull);
           for (int s2 = 0; s2 < nc2 - 1; ++s2) {
@@ -332,35 +338,46 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
               s_q[i] = q;
             }
             __syncthreads();
-            // columns of G and W:  x' = c x - conj(s) y,  y' = s x + c y
+            // one pass: every 2x2 block (pairs a, b) of G becomes J_a^H G_ab J_b, and the
+            // columns p, q of W of every rotating pair are rotated
             for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
+              if (t < bs * bs) {
+                const int a = t / bs, b = t % bs;
+                const int pa = s_p[a], qa = s_q[a], pb = s_p[b], qb = s_q[b];
+                double2 b00 = G[(size_t)pa * GL + pb], b01 = G[(size_t)pa * GL + qb];
+                double2 b10 = G[(size_t)qa * GL + pb], b11 = G[(size_t)qa * GL + qb];
+                if (s_on[b]) {  // columns:  x' = c x - conj(s) y,  y' = s x + c y
+                  const double c = s_c[b], sr = s_sr[b], si = s_si[b];
+                  double2 x = b00, y = b01;
+                  b00 = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                  b01 = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                  x = b10; y = b11;
+                  b10 = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                  b11 = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                }
+                if (s_on[a]) {  // rows:  x' = c x - s y,  y' = conj(s) x + c y
+                  const double c = s_c[a], sr = s_sr[a], si = s_si[a];
+                  double2 x = b00, y = b10;
+                  b00 = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
+                  b10 = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
+                  x = b01; y = b11;
+                  b01 = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
+                  b11 = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
+                }
+                if (s_on[a] | s_on[b]) {
+                  G[(size_t)pa * GL + pb] = b00; G[(size_t)pa * GL + qb] = b01;
+                  G[(size_t)qa * GL + pb] = b10; G[(size_t)qa * GL + qb] = b11;
+                }
+              }
               const int i = t >> lgc, k = t & (nc2 - 1);
               if (!s_on[i]) continue;
               const int p = s_p[i], q = s_q[i];
               const double c = s_c[i], sr = s_sr[i], si = s_si[i];
-              double2* gp = G + (size_t)k * GL + p;
-              double2* gq = G + (size_t)k * GL + q;
-              double2 x = *gp, y = *gq;
-              *gp = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-              *gq = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
               double2* wp = W + (size_t)p * nc2 + k;
               double2* wq = W + (size_t)q * nc2 + k;
-              x = *wp; y = *wq;
+              const double2 x = *wp, y = *wq;
               *wp = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
               *wq = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
-            }
-            __syncthreads();
-            // rows of G (J^H from the left):  x' = c x - s y,  y' = conj(s) x + c y
-            for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
-              const int i = t >> lgc, k = t & (nc2 - 1);
-              if (!s_on[i]) continue;
-              const int p = s_p[i], q = s_q[i];
-              const double c = s_c[i], sr = s_sr[i], si = s_si[i];
-              double2* gp = G + (size_t)p * GL + k;
-              double2* gq = G + (size_t)q * GL + k;
-              const double2 x = *gp, y = *gq;
-              *gp = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
-              *gq = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
             }
             __syncthreads();
           }
@@ -434,6 +451,9 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
       }
       csync();  // the next step's block pairs read columns this step wrote
     }
+    if (off_t > 0) atomicMax(&s_off, (unsigned long long)__double_as_longlong(off_t));
+    off_t = 0.0;
+    __syncthreads();
     if (threadIdx.x == 0) {
       if (s_any) atomicOr(&it.anyflag[sweep & 1], 1);
       atomicMax(&it.offmax[sweep & 1], s_off);

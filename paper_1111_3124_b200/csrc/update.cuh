@@ -272,8 +272,8 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       unsigned long long h[8];
       cudaMemcpyFromSymbolAsync(h, jd_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu (Gram form %llu) sweeps %llu (items %d)\n",
-              (double)h[0], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
+      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e gram %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu (Gram form %llu) sweeps %llu (items %d)\n",
+              (double)h[0], (double)h[7], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
     }
   }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
