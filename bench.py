@@ -277,7 +277,7 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
     ms = e0.elapsed_time(e1)
-    counts = mps.profile_counts()
+    counts = mps.profile_counts(6)
     jac_ms, jac_n = mps.profile_query(mps.PROF_JACOBI)
     con_ms, _ = mps.profile_query(mps.PROF_CONTRACT)
     fin_ms, _ = mps.profile_query(mps.PROF_FINALIZE)
@@ -295,6 +295,10 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_INT_PEAKS.json")))
     peak = peaks["imad_wide_s32_per_s"]
     credited = jacobi_limb_macs(chi, p, sweeps) * args.steps  # SURVEY §8(d) count, all timed launches
+    # an item that ended on the certified stop (R21) ran S rotating sweeps; the
+    # textbook iteration credits S + 1 sweeps, the last one rotation-free (8M per pair)
+    M_, L_ = 2 * chi, (p + 31) // 32
+    credited += counts[5] * (M_ * (M_ - 1) / 2) * (20 * M_ + 12 * M_) * L_ * L_
     executed = executed_imad_wide(counts, chi, p)
     achieved = executed / (jac_ms / 1e3) if jac_ms else None
     # the whole step: Jacobi + every GEMM kernel over the step time (the binary64 Jacobi and
@@ -361,7 +365,8 @@ def main():
                          "achieved_counts": "executed IMAD.WIDE of the implemented algorithm (DESIGN.md §4)",
                          "credited_limb_mac_per_s": credited_rate,
                          "credited_frac": (credited_rate / peak) if credited_rate else None,
-                         "counters": {"rotations": counts[0], "pair_evals": counts[1], "u_digit_products": counts[4]},
+                         "counters": {"rotations": counts[0], "pair_evals": counts[1], "u_digit_products": counts[4],
+                                      "certified_stops": counts[5]},
                          "kernel_ms_per_launch": jac_ms / jac_n if jac_n else None,
                          "share_of_step": jac_ms / ms if ms else None,
                          "step_ms": {"contraction": con_ms, "precondition": pre_ms, "jacobi": jac_ms,

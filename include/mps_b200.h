@@ -197,8 +197,9 @@ int mps_profile_query(int which, double* total_ms, int* launches);
 /* Totals over the Jacobi problems run since mps_profile_enable(1): [0] rotations applied,
  * [1] pair evaluations (gamma computed), [2] sum (sweeps+1) M N (norm passes),
  * [3] sum N N M (recovery of V), [4] digit products executed by the rotation phase
- * (zero-digit variants counted exactly).  mps_profile_counts returns [0..3],
- * mps_profile_counts_n the first n (1..8; [5..7] reserved, 0).  Used to count the executed
+ * (zero-digit variants counted exactly), [5] Jacobi problems that ended on the certified
+ * stop instead of a rotation-free sweep (R21).  mps_profile_counts returns [0..3],
+ * mps_profile_counts_n the first n (1..8; [6..7] reserved, 0).  Used to count the executed
  * IMAD.WIDE of the Jacobi kernel. */
 int mps_profile_counts(long long* out4);
 int mps_profile_counts_n(long long* out, int n);

@@ -91,6 +91,9 @@ struct SvdItem {
   int* gexp;                // [2] scratch: max log2(|gamma|^2 / (alpha_p alpha_q)) of a sweep (by parity)
   int e2_hint;              // < 0: expected log2 of that ratio before sweep 1 (preconditioned); 0: none
   long long* evals;         // out: pair evaluations (gamma computed) over all sweeps
+  int* cexp;                // null (MPS_NO_CERT=1: the paper's rotation-free stopping sweep), or [6]
+                            // scratch of the certified stop (R21): by sweep parity [2k]
+                            // max log2 bound of mu^2, [2k+1] of rho^2; [4] out: 1 = ended on it
 };
 
 // Sort / truncate / renormalise one SVD result and produce the split outputs.
@@ -767,7 +770,11 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
   static_assert(2 * (L + 2) * 32 * 8 <= (JST * STAGE + 24 * CW) * 4, "phase-D column sums must fit the warp's buffers");
   __shared__ mpf<NL> s_red[1];
 
-  if (crank == 0 && tid == 0) { *it.rotations = 0; *it.evals = 0; if (it.uprod) *it.uprod = 0; }
+  if (crank == 0 && tid == 0) {
+    *it.rotations = 0; *it.evals = 0;
+    if (it.uprod) *it.uprod = 0;
+    if (it.cexp) it.cexp[4] = 0;
+  }
   const bool accV = it.A0 == nullptr;
   if (!accV && !it.a0_ready) {  // keep the input (block exponent from k_mix) for the recovery of V
     const size_t nw = (size_t)M * N * 2 * L;
@@ -841,7 +848,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
     if (crank == 0 && tid == 0) {
       *(volatile int*)it.sync = 0;
       if (it.gexp) it.gexp[sweep & 1] = INT_MIN;
+      if (it.cexp) { it.cexp[2 * (sweep & 1)] = INT_MIN; it.cexp[2 * (sweep & 1) + 1] = INT_MIN; }
     }
+    int lmu = INT_MIN, lrho = INT_MIN;  // this thread's bounds for the certified stop (R21)
     csync();
     for (int step = 0; step < N - 1; ++step) {
       // ---- phase D: gamma = sum conj(a_p) a_q (warp per pair, lanes over rows, cp.async staging)
@@ -869,6 +878,11 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             const int64_t e2 = g2.e - ap.e - aq.e + 2;  // >= log2(g2 / (ap aq))
             atomicMax(&it.gexp[sweep & 1], (int)(e2 < -100000 ? -100000 : (e2 > 100000 ? 100000 : e2)));
           }
+          if (it.cexp && !mpf_is_zero(g2)) {  // rho^2 = |g|^2 / (alpha_p alpha_q) < 2^e2 (values in [2^(e-1), 2^e))
+            const int64_t e2 = (mpf_is_zero(ap) || mpf_is_zero(aq) || ap.neg || aq.neg) ? 1000000
+                               : g2.e - ap.e - aq.e + 2;
+            lrho = max(lrho, (int)(e2 < -1000000 ? -1000000 : (e2 > 1000000 ? 1000000 : e2)));
+          }
           if (!mpf_is_zero(g2) && mpf_cmp(g2, mpf_mul(tol2, mpf_mul(ap, aq))) > 0) {
             // The oracle's zeta = d/(2|g|), t = sgn(zeta)/(|zeta| + sqrt(1 + zeta^2)),
             // c = 1/sqrt(1 + t^2), s = c t g/|g| (d = a_q - a_p, g = gamma), rewritten with
@@ -886,6 +900,11 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             const mpf<NL> sr = mpf_mul(sc, gr);
             const mpf<NL> si = mpf_mul(sc, gi);
             const mpf<NL> tg = mpf_mul(mpf_mul(g2, sc), ic);      // t |gamma|
+            if (it.cexp) {  // mu^2 = |s|^2 max(alpha_p, alpha_q) / min(alpha_p, alpha_q), |s| = |g| |sc|
+              const int64_t da = ap.e > aq.e ? ap.e - aq.e : aq.e - ap.e;
+              const int64_t em = g2.e + 2 * sc.e + da + 1;
+              lmu = max(lmu, (int)(em < -1000000 ? -1000000 : (em > 1000000 ? 1000000 : em)));
+            }
             // a reduced-precision gamma (R20) leaves the new norms uncertain by up to
             // 2 |s| |gamma error| <= 2^-(28 lgd - 7) sqrt(alpha_p alpha_q): exponent of its square root
             const int64_t e_slack = lgd < L ? (ap.e + aq.e) / 4 - (28 * (int64_t)lgd - 8) / 2 + 2 : INT64_MIN / 4;
@@ -1053,11 +1072,33 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
     // refresh exact column norms (and renormalise columns) for the next sweep / the result
     const bool any = *(volatile int*)it.sync != 0 || lgd < L;
     if (it.gexp) e2prev = *(volatile int*)&it.gexp[sweep & 1];
+    if (it.cexp) {
+      if (lmu > INT_MIN) atomicMax(&it.cexp[2 * (sweep & 1)], lmu);
+      if (lrho > INT_MIN) atomicMax(&it.cexp[2 * (sweep & 1) + 1], lrho);
+    }
     // exact norms; the negligible-column rule (R3b) is re-evaluated on them
     jac_norms<L, NL>(it, true, z, gw, GW);
     csync();
     mark(3);
-    if (!any) { conv = 1; break; }
+    // Certified stop (R21): a pair evaluated in this sweep ends it with
+    // rho <= max(rho at its evaluation if not rotated (<= tol), rotation residual) plus at most
+    // 2(N-2) later rotations touching p or q, each adding <= mu * (largest rho of the sweep)
+    // (x2 for off-diagonals not yet evaluated, x2 for norm drift).  When that sum is below
+    // tol / 256 the rotation-free sweep the stopping rule asks for is not run.
+    bool cert = false;
+    if (it.cexp && any && lgd == L) {
+      const int emu = *(volatile int*)&it.cexp[2 * (sweep & 1)];
+      const int erho = *(volatile int*)&it.cexp[2 * (sweep & 1) + 1];
+      const int lg2N = 32 - __clz(2 * N - 1);                 // ceil(log2 2N)
+      const int64_t etol2 = 2 * (int64_t)(31 - __clz(M)) + 4 - 2 * (int64_t)W;  // <= log2 tol^2
+      cert = emu > INT_MIN && erho > INT_MIN && emu <= -2 * (lg2N + 3) &&
+             2 * (int64_t)lg2N + emu + erho + 6 <= etol2 - 16;
+    }
+    if (!any || cert) {
+      conv = 1;
+      if (cert && crank == 0 && tid == 0) it.cexp[4] = 1;
+      break;
+    }
   }
   atomicAdd((unsigned long long*)it.rotations, (unsigned long long)nrot);
   atomicAdd((unsigned long long*)it.evals, (unsigned long long)nev);
@@ -1150,7 +1191,8 @@ inline int jacobi_cluster_size(int n_items, int min_N, int slots = 2 * 148) {
 }
 
 // per-item counters -> running totals (profiling): [0] rotations, [1] pair evaluations,
-// [2] sum over items of sweeps * M * N (norm passes), [3] sum of N*N*M (recovery GEMMs)
+// [2] sum over items of sweeps * M * N (norm passes), [3] sum of N*N*M (recovery GEMMs),
+// [4] phase-U digit products x M, [5] items that ended on the certified stop (R21)
 template <int NL>
 __global__ void k_accum_stats(const SvdItem<NL>* items, int n, unsigned long long* tot) {
   for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n; b += gridDim.x * blockDim.x) {
@@ -1160,6 +1202,7 @@ __global__ void k_accum_stats(const SvdItem<NL>* items, int n, unsigned long lon
     atomicAdd(&tot[2], (unsigned long long)(*it.sweeps + 1) * it.M * it.N);
     if (it.A0) atomicAdd(&tot[3], (unsigned long long)it.N * it.N * it.M);
     if (it.uprod) atomicAdd(&tot[4], (unsigned long long)*it.uprod * it.M);
+    if (it.cexp) atomicAdd(&tot[5], (unsigned long long)it.cexp[4]);
   }
 }
 

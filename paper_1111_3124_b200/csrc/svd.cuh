@@ -141,6 +141,7 @@ int run_svd_batch(int p, int M, int N, int batch, const uint32_t* dR, uint32_t* 
     si.dbg = ddbg ? ddbg + 64 * b : nullptr;
     si.rot = rot; si.negl = negl; si.status = ip; si.sweeps = dsweeps + b; si.rotations = rots;
     si.sync = syncp; si.zbuf = zbuf; si.phase_cycles = nullptr; si.A0 = nullptr; si.eA0 = nullptr; si.eV = nullptr; si.evals = rots + 1;
+    si.cexp = use_cert() ? syncp + 4 : nullptr;  // syncp[4..9] (zbuf at syncp + 16)
     hs[b] = si;
     FinItem<NL> fi;
     std::memset(&fi, 0, sizeof(fi));

@@ -41,6 +41,7 @@ struct SvdScratch {
   int64_t* e_misc;  // 4 spare exponents
   long long* uprod; // executed digit products of phase U per row (profiling)
   int* gexp;        // [2] per-sweep max gamma ratio exponent (precision schedule of phase D)
+  int* cexp;        // [6] certified stop of the Jacobi iteration (R21)
   int* sync;
   mpf<NL>* zbuf;
   static size_t bytes(int N) {
@@ -71,6 +72,7 @@ struct SvdScratch {
     s.sync = (int*)(q + 64);
     s.uprod = (long long*)(q + 72);
     s.gexp = (int*)(q + 80);
+    s.cexp = (int*)(q + 96);  // 6 ints, below zbuf
     s.zbuf = (mpf<NL>*)(q + 128);
     return s;
   }
@@ -136,6 +138,16 @@ inline bool use_reduced_d() {
   if (on < 0) {
     const char* e = getenv("MPS_REDUCED_D");
     on = (e && atoi(e)) ? 1 : 0;
+  }
+  return on != 0;
+}
+// MPS_NO_CERT=1 (debug): end every Jacobi iteration with the paper's rotation-free sweep
+// instead of the certified stop (R21)
+inline bool use_cert() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_NO_CERT");
+    on = (e && atoi(e)) ? 0 : 1;
   }
   return on != 0;
 }
@@ -402,6 +414,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     const bool recover = !force_accumulate_v() && !g.accumulate_v;
     si.uprod = S.uprod;
     si.gexp = use_reduced_d() ? S.gexp : nullptr;
+    si.cexp = use_cert() ? S.cexp : nullptr;
     si.e2_hint = pb ? -44 : 0;  // binary64 basis: |gamma|^2 / (alpha_p alpha_q) ~ 2^-44 at sweep 1 (1e-13)
     si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     si.a0_ready = pb ? 1 : 0;

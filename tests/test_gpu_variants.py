@@ -4,6 +4,8 @@ parity tests in a subprocess with a debug switch (the switches are read once per
   MPS_ACCUMULATE_V=1   V accumulated instead of recovered (R16)
   MPS_NS_FORCE_ZERR=1  every item behaves as if a Newton-Schulz zero-digit check failed:
                        the re-run without preconditioner and with accumulated V (run_update2)
+  MPS_NO_CERT=1        every Jacobi iteration ends with the paper's rotation-free sweep instead
+                       of the certified stop (R21)
   MPS_REDUCED_D=1      is experimental and known to fail the 512-bit echo pin (R20): not tested."""
 import os
 import subprocess
@@ -18,7 +20,7 @@ TESTS = ["tests/test_gpu_update2.py::test_update_parity", "tests/test_gpu_mps.py
          "tests/test_gpu_mps.py::test_truncating_run_vs_oracle_mps"]
 
 
-@pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR"])
+@pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR", "MPS_NO_CERT"])
 def test_path_parity(switch):
     env = dict(os.environ, **{switch: "1"})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider"] + TESTS, cwd=ROOT, env=env,
