@@ -193,7 +193,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
   const int M = it.M, N = it.N;
   if (N == 0) return;
   const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs, MP = jd_mp(M);
-  const int nh = bs, T = nh * nh;  // Gram: 2x2 tiles of entries (i, j), (i, j+bs), (i+bs, j), (i+bs, j+bs)
+  const int nh = bs;  // Gram: 2x2 tiles of entries (i, j), (i, j+bs), (i+bs, j), (i+bs, j+bs)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   extern __shared__ double2 jds[];
   double2* Ab = jds;                       // [2bs][MP] block columns
@@ -218,9 +218,11 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
       tm = t;
     }
   };
-  double off_t = 0.0;  // this thread's largest |g|^2 / (alpha_p alpha_q) of the sweep (one atomic per sweep)
+  // 1.0 once this thread saw |g|^2 / (alpha_p alpha_q) > JD_GRAM_OFF^2 in the sweep (one atomic per
+  // sweep; only that comparison is used, so no division on the rotation path)
+  double off_t = 0.0;
   auto note_off = [&](double g2, double sp, double sq) {
-    if (sp > 0 && sq > 0) off_t = fmax(off_t, g2 / (sp * sq));
+    if (sp > 0 && sq > 0 && g2 > (JD_GRAM_OFF * JD_GRAM_OFF) * (sp * sq)) off_t = 1.0;
   };
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
@@ -246,21 +248,27 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
         if (threadIdx.x == 0) { s_rot = 0; s_gram = 0; }
         __syncthreads();
         for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {  // (l, r) advance by blockDim
-          const int c = s_col[l];
-          Ab[(size_t)l * MP + r] = c >= 0 ? A[(size_t)c * M + r] : make_double2(0.0, 0.0);
+          const int c = s_col[l];  // cp.async: all loads in flight at once (absent columns zero-filled)
+          cp_async16(Ab + (size_t)l * MP + r, c >= 0 ? (const void*)(A + (size_t)c * M + r) : (const void*)A, c >= 0 ? 16 : 0);
           r += blockDim.x;
           while (r >= M) { r -= M; ++l; }
         }
+        cp_commit();
+        cp_wait<0>();
         __syncthreads();
         mark(0);
         if (prof) atomicAdd(&jd_prof[4], 1ull);
         if (gram_sweep) {
-          // G = Ab^H Ab: thread (tile, half of the rows); half 1's partial sums go through W
+          // G = Ab^H Ab, Hermitian: only the tiles ti <= tj (nh (nh + 1) / 2 of nh^2) are formed,
+          // the others mirrored; thread (tile, half of the rows), half 1's partial sums go through W
           const int t = threadIdx.x;
+          const int TU = nh * (nh + 1) / 2;
           double2 g[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-          const int tile = t % T, half = t / T;
-          const int ti = tile / nh, tj = tile % nh;
-          if (t < 2 * T) {
+          const int tile = t % TU, half = t / TU;
+          int ti = 0, tj = tile;  // tile -> (ti, tj), ti <= tj (row ti holds nh - ti tiles)
+          while (tj >= nh - ti) { tj -= nh - ti; ++ti; }
+          tj += ti;
+          if (t < 2 * TU) {
             const int rh = (M + 1) / 2, r0 = half ? rh : 0, r1 = half ? M : rh;
             const double2* a0 = Ab + (size_t)ti * MP;
             const double2* a1 = Ab + (size_t)(ti + bs) * MP;
@@ -280,7 +288,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
             }
           }
           __syncthreads();
-          if (t < T) {
+          if (t < TU) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const double2 o = W[(size_t)tile * 4 + k];
@@ -291,6 +299,12 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
             G[(size_t)ti * GL + tj + bs] = g[1];
             G[(size_t)(ti + bs) * GL + tj] = g[2];
             G[(size_t)(ti + bs) * GL + tj + bs] = g[3];
+            if (ti != tj) {  // G(b, a) = conj G(a, b)
+              G[(size_t)tj * GL + ti] = make_double2(g[0].x, -g[0].y);
+              G[(size_t)(tj + bs) * GL + ti] = make_double2(g[1].x, -g[1].y);
+              G[(size_t)tj * GL + ti + bs] = make_double2(g[2].x, -g[2].y);
+              G[(size_t)(tj + bs) * GL + ti + bs] = make_double2(g[3].x, -g[3].y);
+            }
           }
           __syncthreads();
           if (threadIdx.x == 0) {  // column norms^2 within 2^20: Gram form for this block pair
@@ -439,10 +453,12 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
           double2* Vb = Ab;  // [2bs][N]
           for (int l = threadIdx.x / N, r = threadIdx.x % N; l < nc2;) {
             const int c = s_col[l];
-            Vb[(size_t)l * N + r] = c >= 0 ? V[(size_t)c * N + r] : make_double2(0.0, 0.0);
+            cp_async16(Vb + (size_t)l * N + r, c >= 0 ? (const void*)(V + (size_t)c * N + r) : (const void*)V, c >= 0 ? 16 : 0);
             r += blockDim.x;
             while (r >= N) { r -= N; ++l; }
           }
+          cp_commit();
+          cp_wait<0>();
           __syncthreads();
           jd_apply_w(Vb, N, V, N, W, bs, s_col);
         }
@@ -504,6 +520,10 @@ __device__ __forceinline__ void double_to_fx(double v, int32_t (&d)[L]) {
   }
 }
 
+// X_0 keeps only the top NS_X0_DIGITS digits of V_d (an error < 2^-110 in a starting basis that
+// is unitary to ~2^-45 only): then every Newton-Schulz iterate X_k holds exactly lg[k-1]
+// digits and the GEMMs skip the zero ones (NsSched::nz)
+constexpr int NS_X0_DIGITS = 4;
 template <int L>
 __global__ void k_d_to_fx(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
@@ -515,8 +535,12 @@ __global__ void k_d_to_fx(const PreItem* items) {
     const double2 v = it.Vd[(size_t)c * N + r];
     int32_t d[L];
     double_to_fx<L>(v.x, d);
+#pragma unroll
+    for (int k = 0; k < L - NS_X0_DIGITS; ++k) d[k] = 0;
     stfx<L>(it.X, N, c, 0, r, d);
     double_to_fx<L>(v.y, d);
+#pragma unroll
+    for (int k = 0; k < L - NS_X0_DIGITS; ++k) d[k] = 0;
     stfx<L>(it.X, N, c, 1, r, d);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -609,13 +633,14 @@ __device__ __forceinline__ void fx_balance(int32_t (&x)[L]) {
   x[L - 1] += c;
 }
 
-// acc (LG+2 columns: LG-2 .. 2LG-1) += / -= x y, the top Z digits of y being zero
-template <int LG, int Z, bool SUB>
+// acc (LG+2 columns: LG-2 .. 2LG-1) += / -= x y, the top Z digits of y being zero and the
+// low NZA digits of x / NZB digits of y too (the products skipped are exactly zero)
+template <int LG, int Z, bool SUB, int NZA = 0, int NZB = 0>
 __device__ __forceinline__ void tmul_z(int64_t (&acc)[LG + 2], const int32_t (&x)[LG], const int32_t (&y)[LG]) {
 #pragma unroll
-  for (int i = 0; i < LG; ++i)
+  for (int i = NZA; i < LG; ++i)
 #pragma unroll
-    for (int j = 0; j < LG - Z; ++j)
+    for (int j = NZB; j < LG - Z; ++j)
       if (i + j >= LG - 2) acc[i + j - (LG - 2)] = madw(SUB ? -x[i] : x[i], y[j], acc[i + j - (LG - 2)]);
 }
 
@@ -625,9 +650,9 @@ constexpr int GT_TILE = 16;
 #endif
 constexpr int GEMM_PLANES = GEMM_3M ? 3 : 2;
 
-template <int L, int LG, int Z>
+template <int L, int LG, int Z, int NZA = 0, int NZB = 0>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
-  static_assert(LG <= L && Z < LG, "precision schedule");
+  static_assert(LG <= L && Z < LG && NZA < LG && NZB + Z < LG, "precision schedule");
   // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
   constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
   constexpr int D0 = L - LG;  // first stored digit used
@@ -669,6 +694,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           const int e = w % GT_TILE, dg = (w / GT_TILE) % LG, ri = (w / (GT_TILE * LG)) % 2, kk = w / (GT_TILE * LG * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + D0 + dg) * it.lda + rr];
+          if (dg < NZA && va != 0) zbad = 1;
           As[kk][ri][dg][e] = va;
         } else {
           const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
@@ -677,6 +703,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
             va = it.A[((size_t)(rr * 2 + ri) * L + D0 + dg) * it.lda + k];
             if (ri) va = -va;
           }
+          if (dg < NZA && va != 0) zbad = 1;
           As[kk][ri][dg][e] = va;
         }
         {
@@ -684,7 +711,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           const int k = k0 + kk, cc = c0 + e;
           int32_t vb = 0;
           if (k < it.K && cc < ncols) vb = it.B[((size_t)(pcol(cc) * 2 + ri) * L + D0 + dg) * it.ldb + k];
-          if (dg >= LG - Z && vb != 0) zbad = 1;
+          if ((dg >= LG - Z || dg < NZB) && vb != 0) zbad = 1;
           Bs[kk][ri][dg][e] = vb;
         }
       }
@@ -704,13 +731,13 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         int32_t x[LG], y[LG];
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][0][j][tx]; y[j] = Bs[kk][0][j][ty]; }
-        tmul_z<LG, Z, false>(ar, x, y);
+        tmul_z<LG, Z, false, NZA, NZB>(ar, x, y);
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][1][j][tx]; y[j] = Bs[kk][1][j][ty]; }
-        tmul_z<LG, Z, false>(ai, x, y);
+        tmul_z<LG, Z, false, NZA, NZB>(ai, x, y);
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][2][j][tx]; y[j] = Bs[kk][2][j][ty]; }
-        tmul_z<LG, Z, false>(as, x, y);
+        tmul_z<LG, Z, false, NZA, NZB>(as, x, y);
         if ((kk & 3) == 3 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); tnorm2<LG>(as); }
       }
       tnorm2<LG>(ar);
@@ -725,10 +752,10 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           xr[j] = As[kk][0][j][tx]; xi[j] = As[kk][1][j][tx];
           yr[j] = Bs[kk][0][j][ty]; yi[j] = Bs[kk][1][j][ty];
         }
-        tmul_z<LG, Z, false>(ar, xr, yr);
-        tmul_z<LG, Z, true>(ar, xi, yi);
-        tmul_z<LG, Z, false>(ai, xr, yi);
-        tmul_z<LG, Z, false>(ai, xi, yr);
+        tmul_z<LG, Z, false, NZA, NZB>(ar, xr, yr);
+        tmul_z<LG, Z, true, NZA, NZB>(ar, xi, yi);
+        tmul_z<LG, Z, false, NZA, NZB>(ai, xr, yi);
+        tmul_z<LG, Z, false, NZA, NZB>(ai, xi, yr);
         if ((kk & 7) == 7 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); }  // <= 8 k per int64 column run
       }
       tnorm2<LG>(ar);
@@ -796,23 +823,29 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
 // Newton-Schulz precision schedule: iteration k computes D_k with LG digits and
 // X_{k+1} = X_k + X_k D_k / 2 with LG digits skipping the Z top digits of D_k (zero since
 // |D_k| ~ 2^(-45 * 2^k)); conservative by >= 1 digit, checked at run time (zerr).
+// X_k (k >= 1) holds only lg[k-1] digits (the top ones: the update writes an lg[k-1]-digit
+// product onto X_{k-1}), so in iteration k's lg[k]-digit frame its low nz[k] = lg[k] - lg[k-1]
+// digits are zero: D_k skips them in both operands, the update in X_k (checked, zerr).
 template <int L> struct NsSched;
 template <> struct NsSched<10> {
+  static_assert(NS_X0_DIGITS == 4, "lg[0]");
   static constexpr int n = 3;
   static constexpr int lg[3] = {4, 7, 10};
   static constexpr int z[3] = {1, 2, 5};
+  static constexpr int nz[3] = {0, 3, 3};
 };
 template <> struct NsSched<19> {
   static constexpr int n = 4;
   static constexpr int lg[4] = {4, 7, 14, 19};
   static constexpr int z[4] = {1, 2, 5, 10};
+  static constexpr int nz[4] = {0, 3, 7, 5};
 };
 
 template <int L, int K>
 inline void launch_ns_iter(const GemmT* dD, const GemmT* dX, dim3 grid, cudaStream_t st) {
-  constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K];
-  k_gemm_t<L, LG, 0><<<grid, 256, 0, st>>>(dD);
-  k_gemm_t<L, LG, Z><<<grid, 256, 0, st>>>(dX);
+  constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K], NZ = NsSched<L>::nz[K];
+  k_gemm_t<L, LG, 0, NZ, NZ><<<grid, 256, 0, st>>>(dD);
+  k_gemm_t<L, LG, Z, NZ, 0><<<grid, 256, 0, st>>>(dX);
 }
 
 }  // namespace mpsb

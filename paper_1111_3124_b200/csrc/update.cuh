@@ -214,7 +214,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
     // D = I - X^H X (exponent 1, Hermitian);  X' = X + X (D/2)  (D read at exponent 0 = D/2)
-    GemmT gd = GemmT{Xc, N, pb.eOne, Xc, N, pb.eOne, pb.Dm, N, pb.eOne, nullptr, nullptr, N, N, N, 1, 1, 1, nullptr};
+    GemmT gd = GemmT{Xc, N, pb.eOne, Xc, N, pb.eOne, pb.Dm, N, pb.eOne, nullptr, nullptr, N, N, N, 1, 1, 1, zerr};
     gd.herm = 1;
     gt[(2 * k) * stride] = gd;
     gt[(2 * k + 1) * stride] =
