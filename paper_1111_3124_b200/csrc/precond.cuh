@@ -274,6 +274,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
             const double2* a1 = Ab + (size_t)(ti + bs) * MP;
             const double2* b0 = Ab + (size_t)tj * MP;
             const double2* b1 = Ab + (size_t)(tj + bs) * MP;
+#pragma unroll 4
             for (int r = r0; r < r1; ++r) {
               const double2 x0 = a0[r], x1 = a1[r], y0 = b0[r], y1 = b1[r];
               // conj(x) y
@@ -307,15 +308,18 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
             }
           }
           __syncthreads();
-          if (threadIdx.x == 0) {  // column norms^2 within 2^20: Gram form for this block pair
-            double mx = 0, mn = 0;
-            for (int l = 0; l < nc2; ++l) {
-              const double a = G[(size_t)l * GL + l].x;
-              if (s_col[l] < 0 || !(a > 0)) continue;
-              mx = fmax(mx, a);
-              mn = mn == 0 ? a : fmin(mn, a);
+          if (warp == 0) {  // column norms^2 within 2^20: Gram form for this block pair (lane = column)
+            double mx = 0, mn = 1.0e308;  // 1e308: no valid column
+            if (lane < nc2) {
+              const double a = G[(size_t)lane * GL + lane].x;
+              if (s_col[lane] >= 0 && a > 0) { mx = a; mn = a; }
             }
-            s_gram = mx <= mn * 1048576.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+              mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            }
+            if (lane == 0) s_gram = mn == 1.0e308 || mx <= mn * 1048576.0;
           }
         }
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
