@@ -654,9 +654,9 @@ constexpr int GT_TILE = 16;
 #endif
 constexpr int GEMM_PLANES = GEMM_3M ? 3 : 2;
 
-template <int L, int LG, int Z, int NZA = 0, int NZB = 0>
+template <int L, int LG, int Z, int NZA = 0, int NZB = 0, int ZOUT = 0>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
-  static_assert(LG <= L && Z < LG && NZA < LG && NZB + Z < LG, "precision schedule");
+  static_assert(LG <= L && Z < LG && NZA < LG && NZB + Z < LG && ZOUT < L, "precision schedule");
   // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
   constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
   constexpr int D0 = L - LG;  // first stored digit used
@@ -690,43 +690,46 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
 #endif
     for (int k0 = 0; k0 < it.K; k0 += GT_KB) {
       __syncthreads();
-      // stage the top LG digits of GT_KB x 16 elements of each operand; the index order
-      // follows the contiguous direction in global memory (rows of A, k of A^H and of B)
-      for (int w = threadIdx.x; w < GT_KB * 2 * LG * GT_TILE; w += 256) {
+      // stage the top LG digits of GT_KB x 16 elements of each operand (only the digits the
+      // products use: A's [NZA, LG), B's [NZB, LG - Z)); the index order follows the
+      // contiguous direction in global memory (rows of A, k of A^H and of B)
+      constexpr int nA = LG - NZA, nB = LG - Z - NZB;
+      for (int w = threadIdx.x; w < GT_KB * 2 * nA * GT_TILE; w += 256) {
         int32_t va = 0;
         if (!it.conjA) {
-          const int e = w % GT_TILE, dg = (w / GT_TILE) % LG, ri = (w / (GT_TILE * LG)) % 2, kk = w / (GT_TILE * LG * 2);
+          const int e = w % GT_TILE, dg = NZA + (w / GT_TILE) % nA, ri = (w / (GT_TILE * nA)) % 2,
+                    kk = w / (GT_TILE * nA * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + D0 + dg) * it.lda + rr];
-          if (dg < NZA && va != 0) zbad = 1;
           As[kk][ri][dg][e] = va;
         } else {
-          const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
+          const int kk = w % GT_KB, dg = NZA + (w / GT_KB) % nA, ri = (w / (GT_KB * nA)) % 2, e = w / (GT_KB * nA * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) {
             va = it.A[((size_t)(rr * 2 + ri) * L + D0 + dg) * it.lda + k];
             if (ri) va = -va;
           }
-          if (dg < NZA && va != 0) zbad = 1;
           As[kk][ri][dg][e] = va;
         }
-        {
-          const int kk = w % GT_KB, dg = (w / GT_KB) % LG, ri = (w / (GT_KB * LG)) % 2, e = w / (GT_KB * LG * 2);
-          const int k = k0 + kk, cc = c0 + e;
-          int32_t vb = 0;
-          if (k < it.K && cc < ncols) vb = it.B[((size_t)(pcol(cc) * 2 + ri) * L + D0 + dg) * it.ldb + k];
-          if ((dg >= LG - Z || dg < NZB) && vb != 0) zbad = 1;
-          Bs[kk][ri][dg][e] = vb;
-        }
+      }
+      for (int w = threadIdx.x; w < GT_KB * 2 * nB * GT_TILE; w += 256) {
+        const int kk = w % GT_KB, dg = NZB + (w / GT_KB) % nB, ri = (w / (GT_KB * nB)) % 2, e = w / (GT_KB * nB * 2);
+        const int k = k0 + kk, cc = c0 + e;
+        int32_t vb = 0;
+        if (k < it.K && cc < ncols) vb = it.B[((size_t)(pcol(cc) * 2 + ri) * L + D0 + dg) * it.ldb + k];
+        Bs[kk][ri][dg][e] = vb;
       }
       __syncthreads();
 #if GEMM_3M
       // (xr + i xi)(yr + i yi) = xr yr - xi yi + i [(xr + xi)(yr + yi) - xr yr - xi yi]: three
       // LG-digit products instead of four (digit sums |d| <= 2^29: products < 2^58, normalised
       // every 4 k so that no int64 column exceeds 2^62)
-      for (int w = threadIdx.x; w < GT_KB * LG * GT_TILE; w += 256) {
-        const int e = w % GT_TILE, dg = (w / GT_TILE) % LG, kk = w / (GT_TILE * LG);
+      for (int w = threadIdx.x; w < GT_KB * nA * GT_TILE; w += 256) {
+        const int e = w % GT_TILE, dg = NZA + (w / GT_TILE) % nA, kk = w / (GT_TILE * nA);
         As[kk][2][dg][e] = As[kk][0][dg][e] + As[kk][1][dg][e];
+      }
+      for (int w = threadIdx.x; w < GT_KB * nB * GT_TILE; w += 256) {
+        const int e = w % GT_TILE, dg = NZB + (w / GT_TILE) % nB, kk = w / (GT_TILE * nB);
         Bs[kk][2][dg][e] = Bs[kk][0][dg][e] + Bs[kk][1][dg][e];
       }
       __syncthreads();
@@ -805,6 +808,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           for (int j = 0; j < L; ++j) o[j] += x[j];
         }
         fx_balance<L>(o);
+#pragma unroll
+        for (int j = L - ZOUT; j < L; ++j)  // the consumer skips these digits: they must be 0
+          if (o[j] != 0) zbad = 1;
         stfx<L>(it.C, it.ldc, pc, ri, r, o);
         if (it.herm && c0 != r0) {  // C(c, r) = conj C(r, c)
           if (ri) {
@@ -828,8 +834,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
 // X_{k+1} = X_k + X_k D_k / 2 with LG digits skipping the Z top digits of D_k (zero since
 // |D_k| ~ 2^(-45 * 2^k)); conservative by >= 1 digit, checked at run time (zerr).
 // X_k (k >= 1) holds only lg[k-1] digits (the top ones: the update writes an lg[k-1]-digit
-// product onto X_{k-1}), so in iteration k's lg[k]-digit frame its low nz[k] = lg[k] - lg[k-1]
-// digits are zero: D_k skips them in both operands, the update in X_k (checked, zerr).
+// product onto X_{k-1}, X_0 is cut to NS_X0_DIGITS), so in iteration k's lg[k]-digit frame its
+// low nz[k] = lg[k] - lg[k-1] digits are zero by construction: D_k skips them in both operands,
+// the update in X_k.  The skipped top Z digits of D_k are checked where D_k is written (ZOUT).
 template <int L> struct NsSched;
 template <> struct NsSched<10> {
   static_assert(NS_X0_DIGITS == 4, "lg[0]");
@@ -848,7 +855,7 @@ template <> struct NsSched<19> {
 template <int L, int K>
 inline void launch_ns_iter(const GemmT* dD, const GemmT* dX, dim3 grid, cudaStream_t st) {
   constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K], NZ = NsSched<L>::nz[K];
-  k_gemm_t<L, LG, 0, NZ, NZ><<<grid, 256, 0, st>>>(dD);
+  k_gemm_t<L, LG, 0, NZ, NZ, Z><<<grid, 256, 0, st>>>(dD);
   k_gemm_t<L, LG, Z, NZ, 0><<<grid, 256, 0, st>>>(dX);
 }
 
