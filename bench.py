@@ -314,9 +314,12 @@ def main():
         if key in tj:
             traffic = tj[key]
 
-    # end to end through the public C API with host buffers (pinned), one step
+    # end to end through the public C API with host buffers (pinned), one step; the device
+    # buffers of the timed path are released first (at 512 bits both sets do not fit in HBM)
     e2e = None
     if not args.no_e2e:
+        del tA, tB, tU, sig, kk, Ao, Bo, lam, sw, ws
+        torch.cuda.empty_cache()
         def pinned(a):
             return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).pin_memory().numpy().view(a.dtype)
 
