@@ -161,11 +161,16 @@ inline bool use_precond() {
 }
 template <int L>
 constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
+// GEMM descriptors per item: 2 per Newton-Schulz iteration, A_1 (X route), P and A_1 (P route)
+template <int L>
+constexpr int pre_slots() { return 2 * ns_iters<L>() + 3; }
 
-// preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N), eMix[N], scalars
+// preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b (M x N: the last one also
+// holds P = A0 X_{n-1}), D (fixed N x N), eMix[N], scalars
 template <int L>
 inline size_t pre_bytes(int M, int N) {
-  return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
+  return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 2 * mat_bytes(M, N, L) + mat_bytes(N, N, L) +
+         align_up(8 * (size_t)N) +
          256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N);  // + recovery coefficients
 }
 
@@ -189,8 +194,8 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   PreBufs<L> b;
   b.Ad = (double2*)q; q += align_up(16 * (size_t)M * N);
   b.Vd = (double2*)q; q += align_up(16 * (size_t)N * N);
-  b.Xa = (int32_t*)q; q += mat_bytes(N, N, L);
-  b.Xb = (int32_t*)q; q += mat_bytes(N, N, L);
+  b.Xa = (int32_t*)q; q += mat_bytes(M, N, L);
+  b.Xb = (int32_t*)q; q += mat_bytes(M, N, L);
   b.Dm = (int32_t*)q; q += mat_bytes(N, N, L);
   b.eMix = (int64_t*)q; q += align_up(8 * (size_t)N);
   b.rowmax = (unsigned long long*)q;
@@ -204,10 +209,13 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   return b;
 }
 // descriptors of one item's preconditioner (gt[k * stride], k = 0 .. 2 ns_iters): the
-// input A0 (M x N, block exponent eA0) -> Af = A0 X with column exponents eAcols
+// input A0 (M x N, block exponent eA0) -> Af = A0 X with column exponents eAcols.
+// p_route (V is recovered, so X itself is not needed): the last Newton-Schulz update is
+// folded into A_1 = P + P D/2 with P = A0 X_{n-1} (X_{n-1} has nz zero low digits, so P costs
+// fewer digit products than A0 X_n, and the N x N update of X disappears)
 template <int L>
 inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, const int64_t* eA0, int32_t* Af,
-                      int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride) {
+                      int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride, bool p_route = false) {
   constexpr int NSIT = ns_iters<L>();
   *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
   for (int k = 0; k < NSIT; ++k) {
@@ -222,11 +230,23 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
   }
   // A_1 = A0 X at the exponent bounded by A0's largest row norm
   gt[(2 * NSIT) * stride] = GemmT{A0, M, eA0, pb.Xfin(), N, pb.eOne, Af, M, pb.eA1, nullptr, eAcols, M, N, N, 0, 0, 0, nullptr};
+  const GemmT none{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
+  gt[(2 * NSIT + 1) * stride] = none;
+  gt[(2 * NSIT + 2) * stride] = none;
+  if (p_route) {  // a per-item choice (results must not depend on how items are batched)
+    constexpr int k = NSIT - 1;
+    int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
+    int32_t* P = (k % 2) ? pb.Xa : pb.Xb;  // M x N, in place of X_n
+    gt[(2 * k + 1) * stride] = none;
+    gt[(2 * NSIT) * stride] = none;
+    gt[(2 * NSIT + 1) * stride] = GemmT{A0, M, eA0, Xc, N, pb.eOne, P, M, pb.eA1, nullptr, nullptr, M, N, N, 0, 0, 0, nullptr};
+    gt[(2 * NSIT + 2) * stride] = GemmT{P, M, pb.eA1, pb.Dm, N, pb.eOne + 1, Af, M, pb.eA1, P, eAcols, M, N, N, 0, 0, 0, zerr};
+  }
 }
 template <int L>
 inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t stride) {
   *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
-  for (int k = 0; k <= 2 * ns_iters<L>(); ++k)
+  for (int k = 0; k < pre_slots<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
 // the preconditioner kernels for n items (descriptors already on the device); launch count
@@ -292,12 +312,26 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
   const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
   const dim3 gNN(std::min(tNN, 1024), n);
+  const dim3 gMN(std::min(tMN, 1024), n);
+  constexpr int KL = NSIT - 1;  // last iteration: lg = L
+  static_assert(NsSched<L>::lg[KL] == L, "the last Newton-Schulz iteration is at full precision");
   launch_ns_iter<L, 0>(dgt, dgt + (size_t)n, gNN, st);
   launch_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, gNN, st);
-  launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
-  if constexpr (NSIT > 3) launch_ns_iter<L, 3>(dgt + (size_t)6 * n, dgt + (size_t)7 * n, gNN, st);
-  nl += 2 * NSIT;
-  k_gemm_t<L, L, 0><<<dim3(std::min(tMN, 1024), n), 256, 0, st>>>(dgt + (size_t)(2 * NSIT) * n); ++nl;
+  if constexpr (NSIT > 3) launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
+  const GemmT* dD = dgt + (size_t)(2 * KL) * n;
+  const GemmT* dX = dgt + (size_t)(2 * KL + 1) * n;
+  const GemmT* dA1 = dgt + (size_t)(2 * NSIT) * n;
+  // X route: X_n = X_{n-1} + X_{n-1} D / 2, A_1 = A0 X_n; P route (items whose V is recovered):
+  // P = A0 X_{n-1} (its nz zero low digits skipped), A_1 = P + P D / 2.  Items without a route
+  // have empty descriptors in the other route's launches.
+  launch_ns_iter<L, KL>(dD, dX, gNN, st);
+  k_gemm_t<L, L, 0><<<gMN, 256, 0, st>>>(dA1);
+  {
+    constexpr int Z = NsSched<L>::z[KL], NZ = NsSched<L>::nz[KL];
+    k_gemm_t<L, L, 0, 0, NZ><<<gMN, 256, 0, st>>>(dA1 + (size_t)n);
+    k_gemm_t<L, L, Z><<<gMN, 256, 0, st>>>(dA1 + (size_t)2 * n);
+  }
+  nl += 2 * NSIT + 3;
   return nl;
 }
 
@@ -315,7 +349,7 @@ template <int L, int NL>
 inline size_t upd2_desc_bytes(int n) {
   return align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
          align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(sizeof(PreItem) * n) +
-         align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n) + align_up(sizeof(RecItem<NL>) * n) +
+         align_up(sizeof(GemmT) * pre_slots<L>() * n) + align_up(sizeof(RecItem<NL>) * n) +
          align_up(sizeof(GemmT) * n) + align_up(sizeof(GemmT) * n);
 }
 
@@ -339,7 +373,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
                d_mix = d_gemm + align_up(sizeof(GemmItem) * n), d_svd = d_mix + align_up(sizeof(MixItem) * n),
                d_fin = d_svd + align_up(sizeof(SvdItem<NL>) * n), d_pre = d_fin + align_up(sizeof(FinItem<NL>) * n),
                d_gt = d_pre + align_up(sizeof(PreItem) * n),
-               d_rec = d_gt + align_up(sizeof(GemmT) * (2 * ns_iters<L>() + 1) * n),
+               d_rec = d_gt + align_up(sizeof(GemmT) * pre_slots<L>() * n),
                d_rg = d_rec + align_up(sizeof(RecItem<NL>) * n), d_gc = d_rg + align_up(sizeof(GemmT) * n),
                d_end = upd2_desc_bytes<L, NL>(n);
   constexpr int NSIT = ns_iters<L>();
@@ -405,7 +439,9 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     }
     hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pb ? A0f : Af, pb ? eMix : S.eA, M, N};
     if (pre && !pb) pre_skip_descs<L>(PB, hpre + b, hgt + b, n);  // this item skips the preconditioner
-    if (pb) pre_descs<L>(PB, M, N, A0f, eMix, Af, S.eA, redo + b, hpre + b, hgt + b, n);
+    if (pb)  // V recovered: the last X update is folded into A_1 (P route)
+      pre_descs<L>(PB, M, N, A0f, eMix, Af, S.eA, redo + b, hpre + b, hgt + b, n,
+                   !force_accumulate_v() && !g.accumulate_v);
     SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
@@ -703,8 +739,9 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, pb1 ? rec.A0a : A1, pb1 ? PB1.eMix : S1.eA,
                   M1, N1};
   const size_t d_pre1 = 5120, d_gt1 = 5376;
+  const bool p_route1 = !force_accumulate_v() && !a.accumulate_v;  // V recovered: fold the last X update
   if (pb1) pre_descs<L>(PB1, M1, N1, rec.A0a, PB1.eMix, A1, S1.eA, a.redo, (PreItem*)(hd.data() + d_pre1),
-                        (GemmT*)(hd.data() + d_gt1), 1);
+                        (GemmT*)(hd.data() + d_gt1), 1, p_route1);
   SvdItem<NL>* hs = (SvdItem<NL>*)(hd.data() + d_svd);
   SvdItem<NL> si = {};
   si.M = M1; si.N = N1; si.A = A1; si.eA = S1.eA; si.V = V1; si.alpha = S1.alpha; si.gam = S1.gam;
