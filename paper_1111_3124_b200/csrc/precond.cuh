@@ -657,6 +657,9 @@ constexpr int GEMM_PLANES = GEMM_3M ? 3 : 2;
 template <int L, int LG, int Z, int NZA = 0, int NZB = 0, int ZOUT = 0>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG && NZA < LG && NZB + Z < LG && ZOUT < L, "precision schedule");
+  // a truncated product forms only i + j >= LG - 2 with j < LG - Z, so digits i < Z - 1 of A
+  // never take part either: A's digits below ALO are neither staged nor multiplied
+  constexpr int ALO = NZA > Z - 1 ? NZA : (Z > 0 ? Z - 1 : 0);
   // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
   constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
   constexpr int D0 = L - LG;  // first stored digit used
@@ -691,19 +694,19 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
     for (int k0 = 0; k0 < it.K; k0 += GT_KB) {
       __syncthreads();
       // stage the top LG digits of GT_KB x 16 elements of each operand (only the digits the
-      // products use: A's [NZA, LG), B's [NZB, LG - Z)); the index order follows the
+      // products use: A's [ALO, LG), B's [NZB, LG - Z)); the index order follows the
       // contiguous direction in global memory (rows of A, k of A^H and of B)
-      constexpr int nA = LG - NZA, nB = LG - Z - NZB;
+      constexpr int nA = LG - ALO, nB = LG - Z - NZB;
       for (int w = threadIdx.x; w < GT_KB * 2 * nA * GT_TILE; w += 256) {
         int32_t va = 0;
         if (!it.conjA) {
-          const int e = w % GT_TILE, dg = NZA + (w / GT_TILE) % nA, ri = (w / (GT_TILE * nA)) % 2,
+          const int e = w % GT_TILE, dg = ALO + (w / GT_TILE) % nA, ri = (w / (GT_TILE * nA)) % 2,
                     kk = w / (GT_TILE * nA * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) va = it.A[((size_t)(k * 2 + ri) * L + D0 + dg) * it.lda + rr];
           As[kk][ri][dg][e] = va;
         } else {
-          const int kk = w % GT_KB, dg = NZA + (w / GT_KB) % nA, ri = (w / (GT_KB * nA)) % 2, e = w / (GT_KB * nA * 2);
+          const int kk = w % GT_KB, dg = ALO + (w / GT_KB) % nA, ri = (w / (GT_KB * nA)) % 2, e = w / (GT_KB * nA * 2);
           const int k = k0 + kk, rr = r0 + e;
           if (k < it.K && rr < it.rows) {
             va = it.A[((size_t)(rr * 2 + ri) * L + D0 + dg) * it.lda + k];
@@ -725,7 +728,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
       // LG-digit products instead of four (digit sums |d| <= 2^29: products < 2^58, normalised
       // every 4 k so that no int64 column exceeds 2^62)
       for (int w = threadIdx.x; w < GT_KB * nA * GT_TILE; w += 256) {
-        const int e = w % GT_TILE, dg = NZA + (w / GT_TILE) % nA, kk = w / (GT_TILE * nA);
+        const int e = w % GT_TILE, dg = ALO + (w / GT_TILE) % nA, kk = w / (GT_TILE * nA);
         As[kk][2][dg][e] = As[kk][0][dg][e] + As[kk][1][dg][e];
       }
       for (int w = threadIdx.x; w < GT_KB * nB * GT_TILE; w += 256) {
@@ -738,13 +741,13 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
         int32_t x[LG], y[LG];
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][0][j][tx]; y[j] = Bs[kk][0][j][ty]; }
-        tmul_z<LG, Z, false, NZA, NZB>(ar, x, y);
+        tmul_z<LG, Z, false, ALO, NZB>(ar, x, y);
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][1][j][tx]; y[j] = Bs[kk][1][j][ty]; }
-        tmul_z<LG, Z, false, NZA, NZB>(ai, x, y);
+        tmul_z<LG, Z, false, ALO, NZB>(ai, x, y);
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][2][j][tx]; y[j] = Bs[kk][2][j][ty]; }
-        tmul_z<LG, Z, false, NZA, NZB>(as, x, y);
+        tmul_z<LG, Z, false, ALO, NZB>(as, x, y);
         if ((kk & 3) == 3 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); tnorm2<LG>(as); }
       }
       tnorm2<LG>(ar);
@@ -759,10 +762,10 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
           xr[j] = As[kk][0][j][tx]; xi[j] = As[kk][1][j][tx];
           yr[j] = Bs[kk][0][j][ty]; yi[j] = Bs[kk][1][j][ty];
         }
-        tmul_z<LG, Z, false, NZA, NZB>(ar, xr, yr);
-        tmul_z<LG, Z, true, NZA, NZB>(ar, xi, yi);
-        tmul_z<LG, Z, false, NZA, NZB>(ai, xr, yi);
-        tmul_z<LG, Z, false, NZA, NZB>(ai, xi, yr);
+        tmul_z<LG, Z, false, ALO, NZB>(ar, xr, yr);
+        tmul_z<LG, Z, true, ALO, NZB>(ar, xi, yi);
+        tmul_z<LG, Z, false, ALO, NZB>(ai, xr, yi);
+        tmul_z<LG, Z, false, ALO, NZB>(ai, xi, yr);
         if ((kk & 7) == 7 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); }  // <= 8 k per int64 column run
       }
       tnorm2<LG>(ar);
