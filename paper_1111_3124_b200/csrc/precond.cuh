@@ -662,6 +662,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   constexpr int ALO = NZA > Z - 1 ? NZA : (Z > 0 ? Z - 1 : 0);
   // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
   constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
+  // a staging round adds <= (LG - Z - NZB) GT_KB products < 2^56 to a column: <= 2^62 -> one
+  // normalisation per round suffices
+  constexpr bool NORM_ONCE = GEMM_3M && (LG - Z - NZB) * GT_KB <= 64;
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
   if (it.rows <= 0 || it.cols <= 0) return;  // item without this GEMM
@@ -748,7 +751,9 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
 #pragma unroll
         for (int j = 0; j < LG; ++j) { x[j] = As[kk][2][j][tx]; y[j] = Bs[kk][2][j][ty]; }
         tmul_z<LG, Z, false, ALO, NZB>(as, x, y);
-        if ((kk & 3) == 3 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); tnorm2<LG>(as); }
+        // a column receives <= LG - Z - NZB products (< 2^56 each: digit sums <= 2^28) per k:
+        // normalise every 4 k unless a whole staging round cannot reach 2^62
+        if (!NORM_ONCE && (kk & 3) == 3 && kk + 1 < GT_KB) { tnorm2<LG>(ar); tnorm2<LG>(ai); tnorm2<LG>(as); }
       }
       tnorm2<LG>(ar);
       tnorm2<LG>(ai);
