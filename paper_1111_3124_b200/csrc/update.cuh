@@ -165,12 +165,11 @@ constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2
 template <int L>
 constexpr int pre_slots() { return 2 * ns_iters<L>() + 3; }
 
-// preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b (M x N: the last one also
-// holds P = A0 X_{n-1}), D (fixed N x N), eMix[N], scalars
+// preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N; for a square
+// item the last X buffer also holds P = A0 X_{n-1}), eMix[N], scalars
 template <int L>
 inline size_t pre_bytes(int M, int N) {
-  return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 2 * mat_bytes(M, N, L) + mat_bytes(N, N, L) +
-         align_up(8 * (size_t)N) +
+  return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
          256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N);  // + recovery coefficients
 }
 
@@ -194,8 +193,8 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   PreBufs<L> b;
   b.Ad = (double2*)q; q += align_up(16 * (size_t)M * N);
   b.Vd = (double2*)q; q += align_up(16 * (size_t)N * N);
-  b.Xa = (int32_t*)q; q += mat_bytes(M, N, L);
-  b.Xb = (int32_t*)q; q += mat_bytes(M, N, L);
+  b.Xa = (int32_t*)q; q += mat_bytes(N, N, L);
+  b.Xb = (int32_t*)q; q += mat_bytes(N, N, L);
   b.Dm = (int32_t*)q; q += mat_bytes(N, N, L);
   b.eMix = (int64_t*)q; q += align_up(8 * (size_t)N);
   b.rowmax = (unsigned long long*)q;
@@ -233,7 +232,8 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
   const GemmT none{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
   gt[(2 * NSIT + 1) * stride] = none;
   gt[(2 * NSIT + 2) * stride] = none;
-  if (p_route) {  // a per-item choice (results must not depend on how items are batched)
+  if (p_route && M == N) {  // a per-item choice (results must not depend on how items are batched);
+                            // square items only: P lives in the N x N buffer of X_n
     constexpr int k = NSIT - 1;
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* P = (k % 2) ? pb.Xa : pb.Xb;  // M x N, in place of X_n
