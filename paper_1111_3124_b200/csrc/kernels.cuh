@@ -387,9 +387,12 @@ __global__ void k_gemm(const GemmItem* items) {
   if (blockIdx.x == 0 && threadIdx.x == 0) *it.eC = *it.eA + *it.eB + g;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int r = t % it.rows, c = t / it.rows;
-    int64_t ar[L + 2], ai[L + 2];
+    // three real products per complex product: re = sum xr yr - sum xi yi,
+    // im = sum (xr + xi)(yr + yi) - sum xr yr - sum xi yi (digit sums |d| <= 2^29; a column
+    // gains < 2^59.6 per k, so normalising every 4 k keeps it below 2^62)
+    int64_t ar[L + 2], ai[L + 2], as[L + 2];
 #pragma unroll
-    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = 0;
+    for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = as[j] = 0;
     int cnt = 0;
     for (int k = 0; k < it.K; ++k) {
       int32_t xr[L], xi[L], yr[L], yi[L];
@@ -405,10 +408,20 @@ __global__ void k_gemm(const GemmItem* items) {
       ldfx<L>(it.B, it.ldb, c, 0, k, yr);
       ldfx<L>(it.B, it.ldb, c, 1, k, yi);
       tmul_acc2<L>(ar, xr, yr);
-      tmul_sub2<L>(ar, xi, yi);
-      tmul_acc2<L>(ai, xr, yi);
-      tmul_acc2<L>(ai, xi, yr);
-      if (++cnt == 8) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); }
+      tmul_acc2<L>(ai, xi, yi);
+#pragma unroll
+      for (int j = 0; j < L; ++j) { xr[j] += xi[j]; yr[j] += yi[j]; }
+      tmul_acc2<L>(as, xr, yr);
+      if (++cnt == 4) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); tnorm2<L>(as); }
+    }
+    tnorm2<L>(ar);
+    tnorm2<L>(ai);
+    tnorm2<L>(as);
+#pragma unroll
+    for (int j = 0; j < L + 2; ++j) {
+      const int64_t t1 = ar[j], t2 = ai[j];
+      ar[j] = t1 - t2;
+      ai[j] = as[j] - t1 - t2;
     }
     int32_t o[L];
     tround_sr<L>(ar, g, o);
