@@ -63,27 +63,32 @@ def jacobi_limb_macs(chi: int, p: int, sweeps) -> float:
     return tot
 
 
-def trunc_products(LG: int, Z: int = 0) -> int:
-    """IMAD.WIDE of one truncated LG-digit product whose second operand has Z known-zero top
-    digits (columns >= LG-2 formed; the same count the kernels' tmul loops issue)."""
-    return sum(1 for i in range(LG) for j in range(LG - Z) if i + j >= LG - 2)
+def trunc_pairs(LG: int, Z: int = 0, NZA: int = 0, NZB: int = 0) -> int:
+    """Digit products of one truncated LG-digit product in k_gemm_t (precond.cuh): digits
+    i >= NZA of A, NZB <= j < LG - Z of B, columns i + j >= LG - 2."""
+    return sum(1 for i in range(NZA, LG) for j in range(NZB, LG - Z) if i + j >= LG - 2)
 
 
 def gemm_imad_wide_per_item(chi: int, p: int) -> float:
-    """IMAD.WIDE of the GEMM kernels of one two-site update: the a1
-    contraction, the Newton-Schulz iterations (Hermitian D_k: half the tiles), A_1 = Theta' X
-    and the recovery of the chi kept columns of V; 4 real products per complex MAC in the
-    contraction (k_gemm), 3 in the tiled k_gemm_t (three-product complex multiply)."""
+    """IMAD.WIDE of the GEMM kernels of one configs[1] two-site update as they run (DESIGN.md
+    §4): the a1 contraction (k_gemm, three-product complex multiply), the Newton-Schulz
+    iterations (Hermitian D_k: half the tiles; the known-zero low digits of X_k and top digits
+    of D_k skipped), P = Theta' X_{n-1} and A_1 = P + P D/2 (square items whose V is
+    recovered), and the recovery of the chi kept columns of V; 3 real products per complex MAC."""
     L = 10 if p <= 280 else 19
-    sched = [(4, 1), (7, 2), (10, 5)] if L == 10 else [(4, 1), (7, 2), (14, 5), (19, 10)]
+    sched = ([(4, 1, 0), (7, 2, 3), (10, 5, 3)] if L == 10 else
+             [(4, 1, 0), (7, 2, 3), (14, 5, 7), (19, 10, 5)])  # (lg, z, nz): NsSched
     M = N = 2 * chi
     t = 16
     herm_out = (N // t) * (N // t + 1) // 2 * t * t  # tiles on / above the diagonal
-    w = (2 * chi) * (2 * chi) * chi * 4 * trunc_products(L)  # contraction (K = chi)
-    for LG, Z in sched:
-        w += herm_out * N * 3 * trunc_products(LG) + N * N * N * 3 * trunc_products(LG, Z)
-    w += M * N * N * 3 * trunc_products(L)  # A_1
-    w += N * chi * M * 3 * trunc_products(L)  # recovery of the kept columns
+    w = (2 * chi) * (2 * chi) * chi * 3 * trunc_pairs(L)  # contraction (K = chi)
+    for k, (LG, Z, NZ) in enumerate(sched):
+        w += herm_out * N * 3 * trunc_pairs(LG, 0, NZ, NZ)  # D_k
+        if k + 1 < len(sched):
+            w += N * N * N * 3 * trunc_pairs(LG, Z, NZ, 0)  # X_{k+1}
+        else:
+            w += M * N * N * 3 * (trunc_pairs(L, 0, 0, NZ) + trunc_pairs(L, Z))  # P, A_1 = P + P D / 2
+    w += N * chi * M * 3 * trunc_pairs(L)  # recovery of the kept columns
     return float(w)
 
 
