@@ -32,7 +32,8 @@ sys.path.insert(0, ROOT)
 from synth import gen  # noqa: E402
 from synth import records as R  # noqa: E402
 
-METRIC = "two-site gate updates/sec at chi=128, 280-bit"
+def metric_name(chi: int, p: int) -> str:
+    return f"two-site gate updates/sec at chi={chi}, {p}-bit"
 
 
 def parse():
@@ -167,10 +168,18 @@ def oracle_sample(args, nthreads: int):
     return tc, tp
 
 
-# Sweeps of the textbook one-sided Jacobi (the oracle's method) on the configs[1] chi=128
-# 280-bit workload: 15.91, measured on the GPU with the preconditioner disabled
-# (MPS_NO_PRECOND=1, same cyclic method) — the oracle's bounded sample is extrapolated with it.
-ORACLE_SWEEPS = 15.91
+def oracle_sweeps(chi: int, p: int):
+    """Sweeps of the oracle's own textbook cyclic Jacobi on this workload (final check-only sweep
+    included): the mean over the cached full oracle updates of configs[1] items
+    (tests/golden/cfg1_p{p}_chi{chi}_item*.json, written by tools/make_cfg1_golden.py, which
+    calls only oracle/).  Without such a file: 15.91, the round-robin textbook iteration's mean
+    measured on the GPU with the preconditioner off (MPS_NO_PRECOND=1), labelled as such."""
+    import glob
+    fs = sorted(glob.glob(os.path.join(ROOT, "tests", "golden", f"cfg1_p{p}_chi{chi}_item*.json")))
+    sw = [json.load(open(f))["sweeps"] for f in fs]
+    if sw:
+        return float(np.mean(sw)), f"mean of {len(sw)} complete oracle updates of this workload (tests/golden)"
+    return 15.91, "GPU-measured textbook-Jacobi sweeps (MPS_NO_PRECOND=1): no cached oracle update for this chi/p"
 
 
 def oracle_rate(args, tc, tp, sweeps_mean, nthreads):
@@ -184,7 +193,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     nthreads = os.cpu_count() or 1
-    S = ORACLE_SWEEPS
+    S, S_src = oracle_sweeps(args.chi, args.prec)
     times, vals = [], []
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -196,8 +205,8 @@ def run_reference(args, rank, world):
             vals.append(v)
     value = float(np.mean(vals))
     sample = (f"per step: {nthreads} threads, each one chi={args.chi} {args.prec}-bit item: full contraction + first "
-              f"{args.oracle_pairs} Jacobi pair evaluations, extrapolated to {S} sweeps x N(N-1)/2 pairs")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "gate_updates/s", "n_gpus": world,
+              f"{args.oracle_pairs} Jacobi pair evaluations, extrapolated to {S:.2f} sweeps ({S_src}) x N(N-1)/2 pairs")
+    line = {"impl": "reference", "metric": metric_name(args.chi, args.prec), "value": value, "unit": "gate_updates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": f"u64-limb bignum (oracle), p={args.prec}",
@@ -353,18 +362,19 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         nthreads = os.cpu_count() or 1
         tc, tp = oracle_sample(args, nthreads)
-        v, per_gate = oracle_rate(args, tc, tp, ORACLE_SWEEPS, nthreads)
+        S, S_src = oracle_sweeps(chi, p)
+        v, per_gate = oracle_rate(args, tc, tp, S, nthreads)
         cpu = {"value": v, "unit": "gate_updates/s", "cores": nthreads, "kind": "oracle",
                "sample": f"{nthreads} threads x one chi={chi} {p}-bit item each: full contraction "
                          f"({np.mean(tc):.1f}s) + first {args.oracle_pairs} Jacobi pairs ({np.mean(tp):.1f}s), "
-                         f"extrapolated to {ORACLE_SWEEPS} sweeps (the oracle's textbook Jacobi) x N(N-1)/2 pairs = "
+                         f"extrapolated to {S:.2f} sweeps ({S_src}) x N(N-1)/2 pairs = "
                          f"{per_gate:.0f} s/gate/core"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "gate_updates/s", "n_gpus": world, "steps": args.steps,
+            "metric": metric_name(chi, p), "value": value, "unit": "gate_updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p=280",
+            "vs_baseline": None, "dtype": f"int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p={p}",
             "data": "synthetic",
             "config": dict(workload_config(batch, chi, p, nd, world), sweeps_mean=float(np.mean(sweeps))),
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "IMAD.WIDE/s",

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <tuple>
 #include <mutex>
 #include <vector>
 
@@ -26,6 +27,19 @@ struct Prof {
   std::vector<cudaEvent_t> pending_begin[PROF_N];
 } g_prof;
 }  // namespace
+
+cudaError_t mpsb::smem_optin(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, int>> done;  // (kernel, device, bytes)
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& d : done)
+    if (std::get<0>(d) == kern && std::get<1>(d) == dev && std::get<2>(d) >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.emplace_back(kern, dev, bytes);
+  return e;
+}
 
 unsigned long long* mpsb::prof_counts() { return g_prof.on ? g_prof.counts : nullptr; }
 
@@ -137,9 +151,10 @@ int mps_update_batch_device(int p, int chi, int chi_max, int batch, double thr, 
                                        (const uint32_t*)dlam_l, (const uint32_t*)dlam_m, (const uint32_t*)dlam_r,
                                        (const uint32_t*)dU, o, dws, st, hd);
   // the host descriptor buffer must outlive the async copy
-  cudaStreamSynchronize(st);
+  cudaError_t e = cudaGetLastError();  // launch errors first (not sticky)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  else cudaStreamSynchronize(st);
   g_last_launches = nl;
-  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? MPS_OK : MPS_ECUDA;
 }
 
@@ -213,7 +228,8 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   if (B_out) cudaMemcpyAsync(B_out, d + oBo, nAo, cudaMemcpyDeviceToHost, st);
   if (lam_out) cudaMemcpyAsync(lam_out, d + oLo, nLo, cudaMemcpyDeviceToHost, st);
   if (sweeps) cudaMemcpyAsync(sweeps, d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
-  cudaError_t e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaGetLastError();  // launch errors first (not sticky)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
     return MPS_ECUDA;
@@ -256,7 +272,8 @@ int mps_svd_batch(int p, int M, int N, int batch, const void* A, void* sigma, in
   cudaMemcpyAsync(sigma, d + oS, nS, cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(sw.data(), d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
   if (rot_per_sweep) cudaMemcpyAsync(rot_per_sweep, d + oD, 256 * (size_t)batch, cudaMemcpyDeviceToHost, st);
-  cudaError_t e = cudaStreamSynchronize(st);
+  cudaError_t e = cudaGetLastError();  // launch errors first (not sticky)
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
     fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
     return MPS_ECUDA;

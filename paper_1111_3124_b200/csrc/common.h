@@ -16,6 +16,11 @@ constexpr int JACOBI_MAX_SWEEPS = 60;  // then MPS_ENOCONV; a failed run reports
 struct Tier280 { static constexpr int L = 10, NL = 10; };
 struct Tier512 { static constexpr int L = 19, NL = 17; };
 
+// Opt the kernel `kern` in to `bytes` of dynamic shared memory on the CURRENT device, once
+// per (kernel, device, size); thread-safe.  The attribute is per device, so a process-wide
+// "done" flag would leave a second device without it (its launches would then fail).
+cudaError_t smem_optin(const void* kern, int bytes);
+
 inline int record_words(int p) { return 4 + (p + 31) / 32; }
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

@@ -376,6 +376,37 @@ __global__ void k_prep_conv(const PrepItem* items, int RB) {
 // ----------------------------------------------------------------------------
 // a1 contraction: batched complex fixed-point GEMM (one thread per C entry)
 // ----------------------------------------------------------------------------
+// Worst-case gain of one accumulator column of the truncated product (columns i + j >= L - 2)
+// per k of the three-product contraction: the digit sums xr + xi, yr + yi are < 2^28 in
+// magnitude except the top digit (index L - 1), which may reach 2^29 (top digits of a column
+// with one integer digit of head-room reach 2^28), so a pair (i, j) adds < b(i) b(j) with
+// b = 2^28, b(L - 1) = 2^29.  Column s = i + j collects min(s, 2L - 2 - s) + 1 pairs.
+template <int L>
+__host__ __device__ constexpr double gemm3m_col_gain() {
+  double worst = 0;
+  for (int s = L - 2; s <= 2 * L - 2; ++s) {
+    double g = 0;
+    for (int i = 0; i < L; ++i) {
+      const int j = s - i;
+      if (j < 0 || j >= L) continue;
+      g += (i == L - 1 ? 536870912.0 : 268435456.0) * (j == L - 1 ? 536870912.0 : 268435456.0);
+    }
+    worst = g > worst ? g : worst;
+  }
+  return worst;
+}
+// k between normalisations: a column starts below 2^28 after tnorm2 and must stay below
+// 2^63 - 2^32 (at most 8: beyond that the saved tnorm2 calls no longer matter).  L = 10:
+// gain 12 * 2^56 per k -> 8; L = 19: 21 * 2^56 -> 6.
+template <int L>
+__host__ __device__ constexpr int gemm3m_norm_every() {
+  const int n = (int)((9223372036854775808.0 - 4294967296.0) / gemm3m_col_gain<L>());
+  return n > 8 ? 8 : n;
+}
+static_assert(gemm3m_norm_every<10>() == 8 && gemm3m_norm_every<19>() == 6, "contraction column bound");
+static_assert(gemm3m_norm_every<19>() * gemm3m_col_gain<19>() + 268435456.0 < 9223372036854775808.0,
+              "contraction columns fit int64 between normalisations");
+
 template <int L>
 __global__ void k_gemm(const GemmItem* items) {
   const GemmItem it = items[blockIdx.y];
@@ -388,8 +419,8 @@ __global__ void k_gemm(const GemmItem* items) {
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
     const int r = t % it.rows, c = t / it.rows;
     // three real products per complex product: re = sum xr yr - sum xi yi,
-    // im = sum (xr + xi)(yr + yi) - sum xr yr - sum xi yi (digit sums |d| <= 2^29; a column
-    // gains < 2^59.6 per k, so normalising every 4 k keeps it below 2^62)
+    // im = sum (xr + xi)(yr + yi) - sum xr yr - sum xi yi; the columns are normalised every
+    // gemm3m_norm_every<L>() k (worst-case column gain per k: gemm3m_col_gain, below)
     int64_t ar[L + 2], ai[L + 2], as[L + 2];
 #pragma unroll
     for (int j = 0; j < L + 2; ++j) ar[j] = ai[j] = as[j] = 0;
@@ -412,7 +443,8 @@ __global__ void k_gemm(const GemmItem* items) {
 #pragma unroll
       for (int j = 0; j < L; ++j) { xr[j] += xi[j]; yr[j] += yi[j]; }
       tmul_acc2<L>(as, xr, yr);
-      if (++cnt == 4) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); tnorm2<L>(as); }
+      constexpr int NORM_EVERY = gemm3m_norm_every<L>();
+      if (++cnt == NORM_EVERY) { cnt = 0; tnorm2<L>(ar); tnorm2<L>(ai); tnorm2<L>(as); }
     }
     tnorm2<L>(ar);
     tnorm2<L>(ai);
@@ -1136,11 +1168,7 @@ inline void launch_jacobi(const SvdItem<NL>* d_items, int n, int C, cudaStream_t
 // opt in to > 48 KB of dynamic shared memory (once per instantiation)
 template <int L, int NL>
 inline void jacobi_prepare() {
-  static bool done = false;
-  if (!done) {
-    cudaFuncSetAttribute(k_jacobi<L, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jacobi_smem_bytes<L>());
-    done = true;
-  }
+  smem_optin((const void*)k_jacobi<L, NL>, (int)jacobi_smem_bytes<L>());
 }
 
 template <int L, int NL>

@@ -662,9 +662,13 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   constexpr int ALO = NZA > Z - 1 ? NZA : (Z > 0 ? Z - 1 : 0);
   // k per staging round (16 measured no faster; 4 where 8 exceeds the 48 KB static limit)
   constexpr int GT_KB = (size_t)8 * GEMM_PLANES * LG * (GT_TILE + 1) * 4 * 2 > 48 * 1024 ? 4 : 8;
-  // a staging round adds <= (LG - Z - NZB) GT_KB products < 2^56 to a column: <= 2^62 -> one
-  // normalisation per round suffices
+  // a staging round adds, per k, <= (LG - Z - NZB) products to a column, each < 2^56 except
+  // the <= 2 that involve a top digit (digit sums up to 2^29: < 2^57 each, counted as 2 more
+  // 2^56 units): (LG - Z - NZB + 2) GT_KB 2^56 <= 80 * 2^56 = 2^62.3 -> one normalisation
+  // per round suffices
   constexpr bool NORM_ONCE = GEMM_3M && (LG - Z - NZB) * GT_KB <= 64;
+  static_assert(!NORM_ONCE || (double)(LG - Z - NZB + 2) * GT_KB * 72057594037927936.0 + 268435456.0 <
+                                  9223372036854775808.0, "k_gemm_t columns fit int64 within a staging round");
   constexpr int D0 = L - LG;  // first stored digit used
   const GemmT it = items[blockIdx.y];
   if (it.rows <= 0 || it.cols <= 0) return;  // item without this GEMM

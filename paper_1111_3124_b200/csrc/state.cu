@@ -65,6 +65,15 @@ int cuda_ok(mps_state* s, cudaError_t e) {
   return MPS_ECUDA;
 }
 
+// Launch errors (a bad configuration, a missing shared-memory opt-in, a cluster that cannot
+// be placed) are not sticky in the CUDA context and a later stream synchronisation does not
+// report them: check cudaGetLastError before synchronising, and make either error sticky.
+int sync_ok(mps_state* s, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  return cuda_ok(s, e);
+}
+
 bool grow(void** buf, size_t* sz, size_t need) {
   if (*sz >= need) return true;
   if (*buf) cudaFree(*buf);
@@ -156,7 +165,7 @@ int upload_gate(mps_state* s, const void* U, int d, uint32_t* dU) {
   s->ops->unitary(s->p, dU, d, s->dint, s->st);
   int bad = 0;
   cudaMemcpyAsync(&bad, s->dint, sizeof(int), cudaMemcpyDeviceToHost, s->st);
-  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  if (int rc = sync_ok(s, s->st)) return rc;
   return bad ? MPS_ENOTUNITARY : MPS_OK;
 }
 
@@ -291,7 +300,7 @@ int mps_set_stream(mps_state* s, void* stream) {
 int mps_sync(mps_state* s) {
   if (!s) return MPS_EINVAL;
   if (s->sticky) return s->sticky;
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_n_qubits(mps_state* s) { return s ? s->n : MPS_EINVAL; }
@@ -347,7 +356,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
   s->ops->upd2(s->p, s->thr, args.data(), ng, s->ws, s->st, hd);
   std::vector<int> res(3 * ng);
   cudaMemcpyAsync(res.data(), s->dint, sizeof(int) * 3 * ng, cudaMemcpyDeviceToHost, s->st);
-  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  if (int rc = sync_ok(s, s->st)) return rc;
   for (int g = 0; g < ng; ++g) {
     const int k = res[3 * g], sw = res[3 * g + 1], stt = res[3 * g + 2];
     s->sweeps_total += sw;
@@ -361,7 +370,7 @@ static int apply_two_site_batch(mps_state* s, const std::vector<int>& first, con
     cudaMemcpyAsync(s->lam[q], args[g].lam_out, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
     s->m[q] = k;
   }
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 static int apply_three_site(mps_state* s, int q, const void* U8) {
@@ -402,7 +411,7 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
     cudaMemsetAsync(s->dint, 0, 5 * sizeof(int), s->st);
     s->ops->upd3_s1(s->p, s->thr, a, s->ws, s->st, hd1);
     cudaMemcpyAsync(r1, s->dint, sizeof(r1), cudaMemcpyDeviceToHost, s->st);
-    if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+    if (int rc = sync_ok(s, s->st)) return rc;
     if (!r1[4] || r1[3]) break;
     if (r1[4] & 2) a.no_precond = 1;  // a Newton-Schulz zero-digit check failed: no preconditioner
     if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 1 at %d: re-run with accumulated V\n", q);
@@ -418,7 +427,7 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
     cudaMemsetAsync(s->dint + 4, 0, sizeof(int), s->st);
     s->ops->upd3_s2(s->p, s->thr, a, k1, s->ws, s->st, hd2);
     cudaMemcpyAsync(r2, s->dint, sizeof(r2), cudaMemcpyDeviceToHost, s->st);
-    if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+    if (int rc = sync_ok(s, s->st)) return rc;
     if (!r2[4] || r2[3]) break;
     if (r2[4] & 2) a.no_precond = 1;
     if (getenv("MPS_DEBUG_REDO")) fprintf(stderr, "three-site stage 2 at %d: re-run with accumulated V\n", q);
@@ -435,7 +444,7 @@ static int apply_three_site(mps_state* s, int q, const void* U8) {
   cudaMemcpyAsync(s->lam[q + 1], a.lam2_out, (size_t)k1 * s->rb, cudaMemcpyDeviceToDevice, s->st);
   s->m[q] = k2;
   s->m[q + 1] = k1;
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 // Disjoint three-site gates of a layer (U8 host records, sites qs[g]..qs[g]+2): the updates run
@@ -502,8 +511,9 @@ static int apply_three_site_batch(mps_state* s, const std::vector<int>& qs, cons
   for (int i = 0; i < NS; ++i) cudaStreamWaitEvent(s->sub[i], ev0, 0);
   auto stream_of = [&](int g) { return s->sub[g % NS]; };
   auto sync_all = [&]() -> int {
+    if (int rc = cuda_ok(s, cudaGetLastError())) return rc;  // launch errors (not sticky)
     for (int i = 0; i < NS; ++i)
-      if (cudaStreamSynchronize(s->sub[i]) != cudaSuccess) return cuda_ok(s, cudaGetLastError());
+      if (cudaError_t e = cudaStreamSynchronize(s->sub[i])) return cuda_ok(s, e);
     return MPS_OK;
   };
   std::vector<std::vector<unsigned char>> hd(2 * n);
@@ -588,7 +598,7 @@ static int apply_three_site_batch(mps_state* s, const std::vector<int>& qs, cons
     s->m[q] = k2;
     s->m[q + 1] = k1[g];
   }
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 static int apply_one(mps_state* s, const void* U, const int* sites, int k) {
@@ -603,7 +613,7 @@ static int apply_one(mps_state* s, const void* U, const int* sites, int k) {
     s->ops->onesite(s->p, s->G[q], out, dU, nab, s->st);
     cudaMemcpyAsync(s->G[q], out, (size_t)2 * nab * s->cb, cudaMemcpyDeviceToDevice, s->st);
     s->gates++;
-    return cuda_ok(s, cudaStreamSynchronize(s->st));
+    return sync_ok(s, s->st);
   }
   if (k == 2 && sites[1] == q + 1) return apply_two_site_batch(s, {q}, {U});
   if (k == 2) {
@@ -750,7 +760,7 @@ static int amplitudes(mps_state* s, const uint8_t* bits_host, long long nstates,
                      s->tmp + o_scr, nblocks, v_in ? (const uint32_t*)(s->tmp + o_vin) : nullptr,
                      (uint32_t*)(s->tmp + o_out), s->st);
   cudaMemcpyAsync(out, s->tmp + o_out, (size_t)nstates * dims[n] * s->cb, cudaMemcpyDeviceToHost, s->st);
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_amplitude(mps_state* s, const uint8_t* bits, void* out) {
@@ -795,7 +805,7 @@ static int transfer(mps_state* s, const void* O, const int* sites, int k, void* 
                    den_out ? (uint32_t*)((char*)res + s->cb) : nullptr, s->st);
   if (out) cudaMemcpyAsync(out, res, s->cb, cudaMemcpyDeviceToHost, s->st);
   if (den_out) cudaMemcpyAsync(den_out, (char*)res + s->cb, s->rb, cudaMemcpyDeviceToHost, s->st);
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 // Reduced density operator of ascending sites (P:322-341 RDO_block / RDO), normalised by its trace.
@@ -823,7 +833,7 @@ int mps_rdo(mps_state* s, const int* sites, int k, void* out) {
               (uint32_t*)(s->tmp + o_res), s->st);
   cudaMemcpyAsync(out, s->tmp + o_res, (size_t)D * D * s->cb, cudaMemcpyDeviceToHost, s->st);
   (void)X;
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_norm2(mps_state* s, void* out) {
@@ -866,7 +876,7 @@ int mps_block_export_first(mps_state* s, void* dG, void* dlam, int* m_l, int* m_
   cudaMemcpyAsync(dG, s->G[0], (size_t)2 * *m_l * *m_r * s->cb, cudaMemcpyDeviceToDevice, s->st);
   const uint32_t* lr = s->lamR(0);
   if (dlam && lr) cudaMemcpyAsync(dlam, lr, (size_t)*m_r * s->rb, cudaMemcpyDeviceToDevice, s->st);
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_block_boundary_apply(mps_state* s, const void* U, const void* dG_halo, int m_h, const void* dlam_h,
@@ -895,7 +905,7 @@ int mps_block_boundary_apply(mps_state* s, const void* U, const void* dG_halo, i
   s->ops->upd2(s->p, s->thr, &a, 1, s->ws, s->st, hd);
   int res[3];
   cudaMemcpyAsync(res, s->dint, sizeof(res), cudaMemcpyDeviceToHost, s->st);
-  if (int rc = cuda_ok(s, cudaStreamSynchronize(s->st))) return rc;
+  if (int rc = sync_ok(s, s->st)) return rc;
   s->sweeps_total += res[1];
   s->last_sweeps = res[1];
   s->gates++;
@@ -907,7 +917,7 @@ int mps_block_boundary_apply(mps_state* s, const void* U, const void* dG_halo, i
   cudaMemcpyAsync(dlam_mid_out, a.lam_out, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
   s->m_er = k;
   *k_out = k;
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_block_import_first(mps_state* s, const void* dG0, const void* dlam_mid, int k) {
@@ -916,7 +926,7 @@ int mps_block_import_first(mps_state* s, const void* dG0, const void* dlam_mid, 
   s->m_el = k;
   cudaMemcpyAsync(s->G[0], dG0, (size_t)2 * k * s->dr(0) * s->cb, cudaMemcpyDeviceToDevice, s->st);
   cudaMemcpyAsync(s->lam_el, dlam_mid, (size_t)k * s->rb, cudaMemcpyDeviceToDevice, s->st);
-  return cuda_ok(s, cudaStreamSynchronize(s->st));
+  return sync_ok(s, s->st);
 }
 
 int mps_schmidt(mps_state* s, int bond, void* out, int* m) {

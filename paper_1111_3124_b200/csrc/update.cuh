@@ -256,11 +256,7 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   int nl = 0;
   k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
   k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_jacobi_db, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024);  // + static
-    attr = true;
-  }
+  smem_optin((const void*)k_jacobi_db, 226 * 1024);  // + static
   {
     // few items (an MPS layer): C CTAs per item share its block pairs (cluster barriers per step)
     // shared memory for the largest staging of any item: the block size depends on M, and

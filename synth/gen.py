@@ -186,3 +186,90 @@ def update_batch_inputs(p: int, chi: int, batch: int, seed: int = SEED0 + 1, fir
     B = np.concatenate([gaussian_cplx(p, 2 * chi * chi, seed, b, 1, scale_exp=e) for b in range(first, first + batch)])
     U = np.concatenate([haar_unitary(p, 4, seed, b, 2) for b in range(first, first + batch)])
     return A, B, U
+
+
+# --------------------------------------------------------------------- graded spectra
+def graded_sigma(n: int, decades: float, prec: int):
+    """Nominal singular values s_b = 10^(-decades b / (n - 1)), b = 0..n-1 (mpf at prec bits)."""
+    import mpmath
+    with mpmath.workprec(prec):
+        return [mpmath.mpf(10) ** (-mpmath.mpf(decades) * b / max(n - 1, 1)) for b in range(n)]
+
+
+def householder_isometry(p: int, n: int, k: int, *key, reflections: int = 3):
+    """n x k isometry Q = H_1 ... H_r [I_k; 0] (rows of mpc at p + 64 bits), H_t = I - 2 v v^H / |v|^2
+    with complex Gaussian v: exactly unitary before rounding, dense and generic after r >= 2."""
+    import mpmath
+    prec = p + 64
+    vs = [cplx_list(gaussian_cplx(prec, n, *key, t), prec) for t in range(reflections)]
+    with mpmath.workprec(prec):
+        Q = [[mpmath.mpc(1 if r == c else 0) for c in range(k)] for r in range(n)]
+        for v in reversed(vs):  # Q <- H_t Q, last reflection first
+            nv = mpmath.fsum(abs(x) ** 2 for x in v)
+            for c in range(k):
+                h = mpmath.fsum(mpmath.conj(v[r]) * Q[r][c] for r in range(n)) * 2 / nv
+                for r in range(n):
+                    Q[r][c] -= v[r] * h
+    return Q
+
+
+def cplx_list(a: np.ndarray, prec: int):
+    import mpmath
+    with mpmath.workprec(prec):
+        vals = [R.to_mpf(a[i]) for i in range(len(a))]
+        return [mpmath.mpc(vals[2 * i], vals[2 * i + 1]) for i in range(len(vals) // 2)]
+
+
+def _round_cplx(p: int, vals) -> np.ndarray:
+    import mpmath
+    out = R.empty(p, 2 * len(vals))
+    with mpmath.workprec(p):
+        for i, z in enumerate(vals):
+            R.from_fraction(p, +mpmath.mpf(z.real), out[2 * i])
+            R.from_fraction(p, +mpmath.mpf(z.imag), out[2 * i + 1])
+    return out
+
+
+def graded_matrix(p: int, M: int, N: int, decades: float, *key, reflections: int = 3):
+    """Column-major M x N (M >= N) complex records of A = W diag(s) Z^H rounded to p bits, with
+    W an M x N Householder isometry, Z = H_1 ... H_r an N x N Householder unitary and
+    s = graded_sigma(N, decades).  Returns (A, s): the singular values of A are s up to the
+    rounding of A (normwise ~2^-p)."""
+    import mpmath
+    prec = p + 64
+    s = graded_sigma(N, decades, prec)
+    W = householder_isometry(p, M, N, *key, 0)
+    vs = [cplx_list(gaussian_cplx(prec, N, *key, 1, t), prec) for t in range(reflections)]
+    with mpmath.workprec(prec):
+        A = [[W[r][b] * s[b] for b in range(N)] for r in range(M)]
+        for v in vs:  # A <- A H_t for t = 1..r (Z^H = H_r ... H_1, each H Hermitian)
+            nv = mpmath.fsum(abs(x) ** 2 for x in v)
+            for r in range(M):
+                h = mpmath.fsum(A[r][c] * v[c] for c in range(N)) * 2 / nv
+                for c in range(N):
+                    A[r][c] -= h * mpmath.conj(v[c])
+        cm = [A[r][c] for c in range(N) for r in range(M)]
+    return _round_cplx(p, cm), s
+
+
+def graded_update_inputs(p: int, chi: int, decades: float, *key, in_lambda: bool = True):
+    """A two-site update input (BASELINE configs[1] layout, [2][chi][chi] complex records) whose
+    Theta = Gamma_A diag(lambda_m) Gamma_B is W diag(s) Z^H: W, Z 2chi x chi Householder isometries,
+    s = graded_sigma(chi, decades); Gamma_A^i(a, b) = W[i chi + a][b], Gamma_B^j(b, c) =
+    conj(Z[j chi + c][b]).  in_lambda: s is the middle Schmidt vector lambda_m (returned as
+    records); else s is folded into Gamma_A and lambda_m is None (all ones).
+    Returns (A, B, lam_m or None, s)."""
+    import mpmath
+    s = graded_sigma(chi, decades, p + 64)
+    W = householder_isometry(p, 2 * chi, chi, *key, 0)
+    Z = householder_isometry(p, 2 * chi, chi, *key, 1)
+    with mpmath.workprec(p + 64):
+        GA = [W[i * chi + a][b] * (1 if in_lambda else s[b]) for i in range(2) for a in range(chi) for b in range(chi)]
+        GB = [mpmath.conj(Z[j * chi + c][b]) for j in range(2) for b in range(chi) for c in range(chi)]
+    lam = None
+    if in_lambda:
+        lam = R.empty(p, chi)
+        with mpmath.workprec(p):
+            for b in range(chi):
+                R.from_fraction(p, +s[b], lam[b])
+    return _round_cplx(p, GA), _round_cplx(p, GB), lam, s

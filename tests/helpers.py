@@ -102,3 +102,27 @@ def _ptrace(psi, n, keep):
 
 def frac(x) -> Fraction:
     return Fraction(x)
+
+
+def p_sample(p: int, chi: int, k: int, GL, GR, lam, rows, cols):
+    """Entries (rows x cols) of the gauge-invariant local check P = X_k diag(lambda') V_k^H
+    (SURVEY §8(c) "Comparison metrics") of a configs[1] item with lambda_l = lambda_r = 1:
+    P[(i,a),(j,c)] = sum_{b<k} GL[i][a][b] lambda'_b GR[j][b][c], row r = i chi + a,
+    column j chi + c (GL [2][chi][chi_max], GR [2][chi_max][chi] complex records,
+    chi_max = chi).  Each entry summed in mpmath at p + 64 bits, rounded to p bits."""
+    from synth import records as R
+    gl = cplx(GL)
+    gr = cplx(GR)
+    lm = reals(lam)
+    out = R.empty(p, 2 * len(rows) * len(cols))
+    with mpmath.workprec(p + 64):
+        for ri, r in enumerate(rows):
+            i, a = divmod(r, chi)
+            xl = [gl[(i * chi + a) * chi + b] * lm[b] for b in range(k)]
+            for ci, c in enumerate(cols):
+                j, cc = divmod(c, chi)
+                v = mpmath.fsum(xl[b] * gr[(j * chi + b) * chi + cc] for b in range(k))
+                with mpmath.workprec(p):
+                    R.from_fraction(p, +v.real, out[2 * (ri * len(cols) + ci)])
+                    R.from_fraction(p, +v.imag, out[2 * (ri * len(cols) + ci) + 1])
+    return out

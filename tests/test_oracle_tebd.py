@@ -205,6 +205,27 @@ def test_truncation_eckart_young_and_renorm():
     with mpmath.workprec(p + 32):
         f2 = mpmath.fsum(abs(z) ** 2 for z in th)
         assert abs(mpmath.fsum(s ** 2 for s in sig) - f2) / f2 <= mpmath.mpf(2) ** (-p + 16)
+    # Eckart-Young: the kept factors are the best rank-k approximation, so the residual of
+    # X_k S_k V_k^H = nu Gamma_A' diag(lambda') Gamma_B' (lambda_l = lambda_r = 1) carries
+    # exactly the dropped weight; keeping any other k columns would leave more.  Theta' is
+    # column-major 2chi x 2chi (rows (i, a), columns (j, c)).
+    N = 2 * chi
+    GL = cplx(out["GL"])  # [2][chi][chi_max]
+    GR = cplx(out["GR"])  # [2][chi_max][chi]
+    with mpmath.workprec(2 * p):
+        res2 = mpmath.mpf(0)
+        for c in range(N):
+            j, g = divmod(c, chi)
+            for r in range(N):
+                i, a = divmod(r, chi)
+                approx = nu * mpmath.fsum(GL[(i * chi + a) * chi + b] * lam[b] * GR[(j * chi + b) * chi + g]
+                                          for b in range(k))
+                res2 += abs(th[c * N + r] - approx) ** 2
+        dropped = mpmath.fsum(s ** 2 for s in sig[k:])
+        assert dropped > mpmath.mpf(2) ** -20 * f2  # the cut removes real weight
+        assert abs(res2 - dropped) <= mpmath.mpf(2) ** (-p + 16) * f2, (res2, dropped)
+        # and it is the SMALLEST possible residual: the dropped sigma are the N - k smallest
+        assert min(sig[:k]) >= max(sig[k:])
 
 
 def test_expectation_vs_dense():
