@@ -49,6 +49,11 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--oracle-pairs", type=int, default=1500)
+    ap.add_argument("--workload", default="cfg1", choices=["cfg1", "cfg4"],
+                    help="cfg1: the configs[1] batch (default, BASELINE metric); cfg4: the configs[4] circuit "
+                         "(n=64, chi_max=256, 512 bits) sharded over the ranks (strong scaling)")
+    ap.add_argument("--depth", type=int, default=12, help="cfg4: circuit depth (configs[4] is 40)")
+    ap.add_argument("--no-lpt", action="store_true", help="cfg4: owner-computes placement")
     return ap.parse_args()
 
 
@@ -224,6 +229,85 @@ def workload_config(batch, chi, p, nd, world):
             "l2": "inputs+workspace >> 126 MB L2 (no flush needed)", "parallelism": f"replicas x{world}"}
 
 
+def run_cfg4(args, rank, world, local):
+    """configs[4] (BASELINE: 64 qubits, brick-wall Haar U(4), chi_max = 256, 512 bits) sharded
+    over the ranks by paper_1111_3124_b200.dist.ShardedMPS: sites in contiguous
+    blocks, LPT placement per layer, NCCL send/recv of migrated site tensors, one all-reduce of
+    the new Schmidt vectors per layer.  One timed run of the depth --depth prefix of the
+    circuit through the public API (gates uploaded from host records every layer; the
+    amplitude of |0...0> read back at the end), CUDA events on each rank's stream, max over
+    ranks.  Warm-up: the first two layers on a throw-away state."""
+    import torch
+
+    from paper_1111_3124_b200.dist import ShardedMPS
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    n, p, chi, thr, gates = gen.config_circuit(4, depth=args.depth)
+    layers, i = [], 0
+    for t in range(args.depth):  # brickwall() lists layer t's gates (s = t % 2, t % 2 + 2, ...) in order
+        k = len(range(t % 2, n - 1, 2))
+        layers.append(gates[i:i + k])
+        i += k
+    assert i == len(gates)
+    for _ in range(max(1, min(args.warmup, 1))):
+        W = ShardedMPS(n, p, chi, thr, lpt=not args.no_lpt)
+        for layer in layers[:2]:
+            W.apply_layer(layer)
+        del W
+    S = ShardedMPS(n, p, chi, thr, lpt=not args.no_lpt)
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        t0 = time.perf_counter()
+        per_layer = []
+        for layer in layers:
+            tl = time.perf_counter()
+            S.apply_layer(layer)
+            per_layer.append(time.perf_counter() - tl)
+        amp = S.amplitude([0] * n)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t0
+        if dist is not None:
+            dist.barrier()
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms, wall * 1e3], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, wall = float(t[0].item()), float(t[1].item()) / 1e3
+    ng = len(gates)
+    if rank == 0:
+        loads = S.stats["loads"]
+        line = {
+            "metric": f"configs[4] gate updates/sec (n=64, chi_max={chi}, {p}-bit, depth {args.depth})",
+            "value": ng / (ms / 1e3), "unit": "gate_updates/s", "n_gpus": world, "steps": 1, "warmup": 1,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": f"int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p={p}", "data": "synthetic",
+            "config": {"workload": f"configs[4] prefix: {args.depth} brick-wall layers of seeded Haar U(4) on 64 qubits, "
+                                   f"chi_max={chi}, thr=2^-256, {p}-bit; sites in contiguous blocks of "
+                                   f"{n // world} per GPU, {'owner-computes' if args.no_lpt else 'LPT'} placement",
+                       "gates": ng, "final_bond_dims_max": max(S.dims), "parallelism": f"site-sharded x{world}"},
+            "e2e": {"value": ng / wall, "unit": "gate_updates/s",
+                    "h2d_bytes_per_step": int(sum(U.nbytes for U, _ in gates)), "d2h_bytes_per_step": int(amp.nbytes)},
+            "sharding": {"predicted_efficiency": sum(loads) / (world * max(loads)) if max(loads) > 0 else 1.0,
+                         "gates_moved": S.stats["moved_gates"], "migrated_bytes": S.stats["migrated_bytes"]},
+            "per_layer_s": [round(x, 3) for x in per_layer],
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -231,6 +315,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.workload == "cfg4":
+        run_cfg4(args, rank, world, local)
         return
     import torch
     import paper_1111_3124_b200 as mps

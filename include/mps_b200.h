@@ -145,6 +145,12 @@ int mps_amplitude_block(mps_state* st, const uint8_t* bits, const void* v_in, vo
 /* ---- diagnostics / test surface ----------------------------------------------- */
 int mps_n_qubits(mps_state* st);
 int mps_bond_dims(mps_state* st, int* out /* n-1 ints */);
+/* Site tensor Gamma_site ([2][m_l][m_r] complex records) and Schmidt vector of a bond
+ * (m reals).  The buffers may be HOST or DEVICE memory (unified addressing picks the
+ * copy direction); the copy is ordered on the state's stream and complete on return.  The
+ * site-sharded SPMD driver (paper_1111_3124_b200/dist.py) moves tensors between
+ * ranks through device buffers with these four calls.  EINVAL: bad index, dims that differ
+ * from the current bond dims (set_site), m outside [1, capacity of the bond] (set_schmidt). */
 int mps_schmidt(mps_state* st, int bond, void* out /* m reals, may be NULL */, int* m);
 int mps_get_site(mps_state* st, int site, void* out /* 2*m_l*m_r complex, may be NULL */, int* m_l, int* m_r);
 /* set_schmidt may change the bond dimension; the caller then sets both neighbouring sites. */

@@ -929,11 +929,17 @@ int mps_block_import_first(mps_state* s, const void* dG0, const void* dlam_mid, 
   return sync_ok(s, s->st);
 }
 
+// Site / Schmidt-vector transfer: `out` / `in` may be host or device memory (unified
+// addressing decides the copy direction); copies are ordered on the state's stream and
+// complete when the call returns.  The SPMD driver (dist.py) moves site tensors between
+// ranks through device buffers with these calls.
 int mps_schmidt(mps_state* s, int bond, void* out, int* m) {
   if (!s || !m || bond < 0 || bond >= s->n - 1) return MPS_EINVAL;
   *m = s->m[bond];
-  if (out && cudaMemcpy(out, s->lam[bond], (size_t)s->m[bond] * s->rb, cudaMemcpyDeviceToHost) != cudaSuccess)
-    return MPS_ECUDA;
+  if (out) {
+    cudaMemcpyAsync(out, s->lam[bond], (size_t)s->m[bond] * s->rb, cudaMemcpyDefault, s->st);
+    if (int rc = sync_ok(s, s->st)) return rc;
+  }
   return s->sticky;
 }
 
@@ -941,22 +947,25 @@ int mps_get_site(mps_state* s, int site, void* out, int* ml, int* mr) {
   if (!s || !ml || !mr || site < 0 || site >= s->n) return MPS_EINVAL;
   *ml = s->dl(site);
   *mr = s->dr(site);
-  if (out && cudaMemcpy(out, s->G[site], (size_t)2 * *ml * *mr * s->cb, cudaMemcpyDeviceToHost) != cudaSuccess)
-    return MPS_ECUDA;
+  if (out) {
+    cudaMemcpyAsync(out, s->G[site], (size_t)2 * *ml * *mr * s->cb, cudaMemcpyDefault, s->st);
+    if (int rc = sync_ok(s, s->st)) return rc;
+  }
   return s->sticky;
 }
 
 int mps_set_schmidt(mps_state* s, int bond, const void* in, int m) {
   if (!s || !in || bond < 0 || bond >= s->n - 1 || m < 1 || m > s->cap[bond]) return MPS_EINVAL;
   s->m[bond] = m;
-  return cudaMemcpy(s->lam[bond], in, (size_t)m * s->rb, cudaMemcpyHostToDevice) == cudaSuccess ? MPS_OK : MPS_ECUDA;
+  cudaMemcpyAsync(s->lam[bond], in, (size_t)m * s->rb, cudaMemcpyDefault, s->st);
+  return sync_ok(s, s->st);
 }
 
 int mps_set_site(mps_state* s, int site, const void* in, int ml, int mr) {
   if (!s || !in || site < 0 || site >= s->n) return MPS_EINVAL;
   if (ml != s->dl(site) || mr != s->dr(site)) return MPS_EINVAL;
-  return cudaMemcpy(s->G[site], in, (size_t)2 * ml * mr * s->cb, cudaMemcpyHostToDevice) == cudaSuccess ? MPS_OK
-                                                                                                       : MPS_ECUDA;
+  cudaMemcpyAsync(s->G[site], in, (size_t)2 * ml * mr * s->cb, cudaMemcpyDefault, s->st);
+  return sync_ok(s, s->st);
 }
 
 int mps_stats(mps_state* s, char* json, size_t cap) {

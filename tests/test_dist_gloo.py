@@ -1,32 +1,46 @@
-"""Multi-rank path of the site-sharded MPS on CPU: world_size 2 over gloo.
-The sharded driver (paper_1111_3124_b200/dist.py) exchanges block-edge halos by
-torch.distributed point-to-point; the local arithmetic is the test-only oracle engine.
-Result: equal to the single-process oracle MPS (bond updates are the same oracle update
-on the same tensors, so Schmidt vectors agree bitwise; amplitudes within tau)."""
+"""Multi-rank path of the site-sharded MPS on CPU ranks over gloo.
+
+The sharded driver (paper_1111_3124_b200/dist.py: LPT placement, batched point-to-point
+migration of site tensors, one all-reduce of the new Schmidt vectors per layer) runs with
+the test-only oracle engine (tests/dist_oracle_engine.py) as its arithmetic.  Every gate
+is the same oracle update on the same tensors wherever it runs, so the result must be
+BITWISE equal to a single-process oracle MPS: every Schmidt vector, every site tensor
+(gathered on rank 0) and the amplitudes.  The circuits put two-site gates, three-site U(8)
+gates and span-3 two-qubit gates across the block edges, with
+world sizes 2 and 3 (uneven blocks, so LPT moves gates off their owners).
+
+plan_layer itself is pinned on configs[4]'s saturated bond profile against SURVEY §8(e):
+owner-computes gives E(8) ~ 0.74, LPT ~ 0.98."""
 import os
 import socket
 
-import mpmath
+import numpy as np
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
 from synth import gen
-from tests.helpers import cplx, tau
 
-N, P, CHI, THR, DEPTH = 8, 256, 8, 2.0 ** -128, 5
+N, P, CHI, THR = 9, 256, 8, 2.0 ** -128
 
 
 def layers():
     out = []
-    for t in range(DEPTH):
+    for t in range(4):  # brick-wall U(4)
         out.append([(gen.haar_unitary(P, 4, 4242, t, s), (s, s + 1)) for s in range(t % 2, N - 1, 2)])
+    for t in range(4, 7):  # U(8) triples at offsets 0, 1, 2 (every block edge is crossed)
+        o = t % 3
+        out.append([(gen.haar_unitary(P, 8, 4242, t, s), (s, s + 1, s + 2)) for s in range(o, N - 2, 3)])
+    # span-3 two-qubit gates (embedded into U(8)) and one-qubit gates
+    out.append([(gen.haar_unitary(P, 4, 4242, 7, s), (s, s + 2)) for s in (0, 3, 6)])
+    out.append([(gen.haar_unitary(P, 2, 4242, 8, s), (s,)) for s in range(N)])
+    out.append([(gen.haar_unitary(P, 4, 4242, 9, s), (s, s + 1)) for s in range(0, N - 1, 2)])
     return out
 
 
 def bitlist():
-    return [[0] * N, [1] * N, [0, 1] * (N // 2), [1, 1, 0, 1, 0, 0, 1, 0]]
+    return [[0] * N, [1] * N, [0, 1] * (N // 2) + [0], [1, 1, 0, 1, 0, 0, 1, 0, 1]]
 
 
 def _worker(rank, world, port, q):
@@ -34,13 +48,14 @@ def _worker(rank, world, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1111_3124_b200.dist import ShardedMPS
-    from tests.dist_oracle_engine import OracleBlockEngine
-    S = ShardedMPS(N, P, CHI, THR, engine_factory=OracleBlockEngine)
+    from tests.dist_oracle_engine import OracleEngine
+    S = ShardedMPS(N, P, CHI, THR, engine_factory=OracleEngine)
     for layer in layers():
         S.apply_layer(layer)
-    amps = [S.amplitude(b).tobytes().hex() for b in bitlist()]
-    lam_edge = S.engine.lam_er.tobytes().hex() if rank == 0 else S.engine.lam_el.tobytes().hex()
-    q.put((rank, amps, lam_edge))
+    lam = [S.schmidt(b).tobytes().hex() for b in range(N - 1)]
+    amps = [S.amplitude(b).tobytes().hex() for b in bitlist()]  # gathers every site on rank 0
+    sites = [S.engine.m.get_site(s)[0].tobytes().hex() for s in range(N)] if rank == 0 else None
+    q.put((rank, lam, amps, sites, S.dims, S.stats["moved_gates"]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -53,8 +68,8 @@ def free_port():
     return port
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_two_ranks_gloo(world):
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gloo_bitwise_equals_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
@@ -63,23 +78,40 @@ def test_sharded_two_ranks_gloo(world):
         p.start()
     res = {}
     for _ in range(world):
-        r, amps, lam = q.get(timeout=600)
-        res[r] = (amps, lam)
+        r, lam, amps, sites, dims, moved = q.get(timeout=900)
+        res[r] = (lam, amps, sites, dims, moved)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    # reference: single-process oracle MPS
     ref = oracle.OracleMPS(N, P, CHI, THR)
     for layer in layers():
-        for U, s in layer:
-            ref.apply(U, s)
-    import numpy as np
-    from synth import records as R
-    # the mirrored edge Schmidt vector is identical on both ranks and equals the oracle's
-    assert res[0][1] == res[1][1] == ref.schmidt(N // 2 - 1).tobytes().hex()
-    for i, bits in enumerate(bitlist()):
-        want = cplx(ref.amplitude(bits))[0]
-        for r in range(world):
-            got = cplx(np.frombuffer(bytes.fromhex(res[r][0][i]), dtype=R.record_dtype(P)))[0]
-            with mpmath.workprec(2 * P):
-                assert abs(got - want) <= tau(P), (r, bits, got, want)
+        ref.apply_layer(layer, nthreads=1)
+    want_lam = [ref.schmidt(b).tobytes().hex() for b in range(N - 1)]
+    want_amp = [ref.amplitude(b).tobytes().hex() for b in bitlist()]
+    want_sites = [ref.get_site(s)[0].tobytes().hex() for s in range(N)]
+    for r in range(world):
+        assert res[r][0] == want_lam, r          # Schmidt vectors replicated, bitwise
+        assert res[r][1] == want_amp, r          # amplitudes on every rank, bitwise
+        assert res[r][3] == ref.bond_dims(), r
+    assert res[0][2] == want_sites               # every site tensor, bitwise
+    if world == 3:
+        assert res[0][4] > 0                     # LPT ran some gates away from their owners
+
+
+def test_plan_layer_configs4_efficiency():
+    """configs[4] (n = 64, chi_max = 256) at saturation, 8 ranks of 8 sites (SURVEY §8(e)
+    efficiency analysis): per two layers, owner-computes E(8) ~ 0.74; LPT >= 0.95."""
+    from paper_1111_3124_b200.dist import block_range, plan_layer
+    n, chi, world = 64, 256, 8
+    dims = [min(chi, 2 ** min(b + 1, n - b - 1)) for b in range(n - 1)]
+    bounds = [block_range(n, world, r) for r in range(world)]
+    E = {}
+    for lpt in (False, True):
+        tot = [0.0] * world
+        for off in (0, 1):
+            gates = [(None, (s, s + 1)) for s in range(off, n - 1, 2)]
+            _, loads = plan_layer(gates, dims, n, chi, bounds, lpt=lpt)
+            E[(lpt, off)] = sum(loads) / (world * max(loads))
+            tot = [a + b for a, b in zip(tot, loads)]
+    assert 0.70 <= E[(False, 0)] <= 0.78 and 0.70 <= E[(False, 1)] <= 0.78, E
+    assert E[(True, 0)] >= 0.95 and E[(True, 1)] >= 0.95, E

@@ -31,7 +31,7 @@ from tests.helpers import p_sample  # noqa: E402
 from tools.make_cfg1_golden import grid, pmax  # noqa: E402
 
 KEY = 0x6AADED
-SVD_CASES = [(280, 64, 60), (280, 128, 60), (512, 64, 120), (512, 128, 120)]
+SVD_CASES = [(280, 64, 60), (280, 128, 40), (512, 64, 120), (512, 128, 80)]
 UPD_CASES = [(280, 32, 60, True), (280, 64, 60, True), (280, 64, 60, False),
              (512, 32, 120, True), (512, 64, 120, True), (512, 64, 120, False)]
 
@@ -45,7 +45,11 @@ def main():
         for p, N, dec in SVD_CASES:
             A, s = gen.graded_matrix(p, N, N, dec, KEY, N, p)
             t0 = time.time()
-            sig, X, V, sw = oracle.svd(p, A, N, N)
+            try:
+                sig, X, V, sw = oracle.svd(p, A, N, N)
+            except oracle.OracleError as e:  # the textbook iteration's 60-sweep cap
+                print(f"p={p} N={N} decades={dec}: oracle {e} after {time.time() - t0:.0f}s", flush=True)
+                continue
             res = {"what": "oracle SVD of gen.graded_matrix(p, N, N, decades, KEY, N, p)", "prec": p, "N": N,
                    "decades": dec, "key": [KEY, N, p], "sigma": sig.tobytes().hex(), "sweeps": sw,
                    "seconds": time.time() - t0}
