@@ -1002,6 +1002,16 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             int ints = 0;  // bit u: slot u's coefficient has an integer digit
             for (int u = 0; u < 24; ++u)
               if ((vint >> (c_coefsrc[u] & 15)) & 1) ints |= 1 << u;
+            // the signed slots [mat][o][t] in the order phase U reads them (slots 9.. of the
+            // pair's area): phase U then copies them without index arithmetic or negation
+#pragma unroll 1
+            for (int u = 0; u < (accV ? 24 : 12); ++u) {
+              const int src = c_coefsrc[u];
+              const int32_t* from = cf + (src & 15) * CW;
+              int32_t* to = cf + (9 + u) * CW;
+#pragma unroll
+              for (int k = 0; k <= L; ++k) to[k] = (src & 16) ? -from[k] : from[k];
+            }
             // zero top fractional digits of each value -> the U variant of A (values 0..5) and V (6..8)
             int zv[9];
             for (int v = 0; v < 9; ++v) {
@@ -1074,12 +1084,8 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
         if (!(flag & 1)) continue;
         int p, q;
         rr_pair(N, step, i, p, q);
-        const int32_t* cfg = it.coef + (size_t)i * 33 * CW;
-        for (int w = lane; w < 24 * CW; w += 32) {
-          const int src = c_coefsrc[w / CW];
-          const int32_t v = cfg[(src & 15) * CW + w % CW];
-          wcoef[w] = (src & 16) ? -v : v;
-        }
+        const int32_t* cfg = it.coef + (size_t)i * 33 * CW + 9 * CW;  // signed slots (phase R)
+        for (int w = lane; w < (accV ? 24 : 12) * CW; w += 32) wcoef[w] = cfg[w];
         __syncwarp();
         for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
           int32_t* F = mat ? it.V : it.A;

@@ -113,8 +113,21 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // always decided on dots of the current columns (a Gram-form sweep that rotates nothing has
 // not changed G, which equals those dots).  The binary64 stage only chooses the starting basis
 // of the p-bit iteration (R19): no p-bit result depends on its rounding or on the form used.
-__host__ __device__ inline int jd_bs(int M) { return M <= 320 ? 16 : (M <= 640 ? 8 : 4); }
-constexpr int JD_THREADS = 512;
+// JD_BS_MAX caps the block size.  16 (default): 165 KB of shared memory, one CTA of 512 threads
+// per SM.  8 keeps a CTA at 74 KB for M <= 320 (3 CTAs of 256 threads per SM overlap each other's
+// barrier-bound inner steps) but doubles the inner steps: measured slower (configs[1] chi = 128:
+// 132.7 vs 137.2 updates/s, preconditioner 2.78 vs 2.52 s per step; profiles/r02_jdb_bs8_ab.jsonl).
+// The block size depends on M only, never on the batch, so a gate's result does not depend on
+// which gates share its launch.
+#ifndef JD_BS_MAX
+#define JD_BS_MAX 16
+#endif
+__host__ __device__ inline int jd_bs(int M) {
+  const int b = M <= 320 ? 16 : (M <= 640 ? 8 : 4);
+  return b < JD_BS_MAX ? b : JD_BS_MAX;
+}
+constexpr int JD_THREADS = JD_BS_MAX >= 16 ? 512 : 256;  // the Gram phase needs bs (bs + 1) threads
+constexpr int JD_MINB = JD_BS_MAX >= 16 ? 1 : 3;
 #ifndef JD_TOL
 #define JD_TOL (4.0 * M * 1.1102230246251565e-16)  // 4 M 2^-53 (1e-12 costs a p-bit sweep)
 #endif  // one warp per pair of a block pair's inner step (bs <= 16)
@@ -122,9 +135,16 @@ constexpr int JD_THREADS = 512;
 #define JD_GRAM_OFF 1e-6  // Gram-form inner sweeps while max |gamma| / sqrt(alpha_p alpha_q) exceeds this
 #endif
 __host__ __device__ inline int jd_mp(int M) { return M | 1; }  // odd column stride: conflict-free Gram loads
+// Gram phase: thread (tile, part) sums rows [part M / P, (part + 1) M / P) of one 2x2 tile of
+// the bs (bs + 1) / 2 upper tiles; parts 1.. leave their partial sums in a scratch area
+__host__ __device__ inline int jd_gram_parts(int bs) {
+  const int TU = bs * (bs + 1) / 2, P = JD_THREADS / TU;
+  return P < 1 ? 1 : (P > 4 ? 4 : P);
+}
 inline size_t jd_smem(int M) {
-  const int nc2 = 2 * jd_bs(M);
-  return (size_t)nc2 * jd_mp(M) * 16 + (size_t)nc2 * nc2 * 16 + (size_t)nc2 * (nc2 + 1) * 16 + 64;
+  const int bs = jd_bs(M), nc2 = 2 * bs;
+  const size_t scr = (size_t)(jd_gram_parts(bs) - 1) * (bs * (bs + 1) / 2) * 4 * 16;
+  return (size_t)nc2 * jd_mp(M) * 16 + (size_t)nc2 * nc2 * 16 + (size_t)nc2 * (nc2 + 1) * 16 + scr + 64;
 }
 
 // MPS_JD_PROF=1 (debug): clock64 cycles of thread 0 per phase, summed over CTAs:
@@ -139,14 +159,14 @@ __device__ __forceinline__ void jd_apply_w(const double2* src, int ld, double2* 
   const int nc2 = 2 * bs;
   for (int t = threadIdx.x; t < 2 * R; t += blockDim.x) {
     const int r = t % R, h = t / R;
-    double2 acc[16];
+    double2 acc[JD_BS_MAX];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] = make_double2(0.0, 0.0);
+    for (int j = 0; j < JD_BS_MAX; ++j) acc[j] = make_double2(0.0, 0.0);
 #pragma unroll 2
     for (int l = 0; l < nc2; ++l) {
       const double2 v = src[(size_t)l * ld + r];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
+      for (int j = 0; j < JD_BS_MAX; ++j) {
         if (j < bs) {
           const double2 w = W[(size_t)(h * bs + j) * nc2 + l];
           acc[j].x = fma(v.x, w.x, fma(-v.y, w.y, acc[j].x));
@@ -155,7 +175,7 @@ __device__ __forceinline__ void jd_apply_w(const double2* src, int ld, double2* 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < JD_BS_MAX; ++j) {
       if (j < bs) {
         const int cj = s_col[h * bs + j];
         if (cj >= 0) dst[(size_t)cj * R + r] = acc[j];
@@ -182,7 +202,7 @@ __device__ __forceinline__ void jd_rot(double sp, double sq, double gr, double g
 // C CTAs (a thread-block cluster when C > 1) share one item: the block pairs of a step are
 // dealt round-robin to the CTAs and the steps are separated by cluster barriers (few items in
 // flight: an MPS layer).  The rotation sequence does not depend on C.
-static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* items, int C) {
+static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const PreItem* items, int C) {
   namespace cg = cooperative_groups;
   const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
   const PreItem it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
@@ -199,6 +219,7 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
   double2* Ab = jds;                       // [2bs][MP] block columns
   double2* W = jds + (size_t)nc2 * MP;     // [2bs][2bs] column-major
   double2* G = W + (size_t)nc2 * nc2;      // [2bs][2bs + 1] row-major (Gram form)
+  double2* Gs = G + (size_t)nc2 * (nc2 + 1);  // Gram partial sums of parts 1..P-1
   const int GL = nc2 + 1, lgc = __ffs(nc2) - 1;  // nc2 = 2^lgc
   __shared__ int s_any, s_rot, s_gram, s_col[32];
   __shared__ double s_c[16], s_sr[16], s_si[16];
@@ -260,16 +281,16 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
         if (prof) atomicAdd(&jd_prof[4], 1ull);
         if (gram_sweep) {
           // G = Ab^H Ab, Hermitian: only the tiles ti <= tj (nh (nh + 1) / 2 of nh^2) are formed,
-          // the others mirrored; thread (tile, half of the rows), half 1's partial sums go through W
+          // the others mirrored; thread (tile, part of the rows), parts 1.. sum through Gs
           const int t = threadIdx.x;
-          const int TU = nh * (nh + 1) / 2;
+          const int TU = nh * (nh + 1) / 2, NP = jd_gram_parts(bs);
           double2 g[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
-          const int tile = t % TU, half = t / TU;
+          const int tile = t % TU, part = t / TU;
           int ti = 0, tj = tile;  // tile -> (ti, tj), ti <= tj (row ti holds nh - ti tiles)
           while (tj >= nh - ti) { tj -= nh - ti; ++ti; }
           tj += ti;
-          if (t < 2 * TU) {
-            const int rh = (M + 1) / 2, r0 = half ? rh : 0, r1 = half ? M : rh;
+          if (t < NP * TU) {
+            const int r0 = part * M / NP, r1 = (part + 1) * M / NP;
             const double2* a0 = Ab + (size_t)ti * MP;
             const double2* a1 = Ab + (size_t)(ti + bs) * MP;
             const double2* b0 = Ab + (size_t)tj * MP;
@@ -283,18 +304,20 @@ static __global__ void __launch_bounds__(JD_THREADS) k_jacobi_db(const PreItem* 
               g[2].x = fma(x1.x, y0.x, fma(x1.y, y0.y, g[2].x)); g[2].y = fma(x1.x, y0.y, fma(-x1.y, y0.x, g[2].y));
               g[3].x = fma(x1.x, y1.x, fma(x1.y, y1.y, g[3].x)); g[3].y = fma(x1.x, y1.y, fma(-x1.y, y1.x, g[3].y));
             }
-            if (half) {
+            if (part) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) W[(size_t)tile * 4 + k] = g[k];
+              for (int k = 0; k < 4; ++k) Gs[((size_t)(part - 1) * TU + tile) * 4 + k] = g[k];
             }
           }
           __syncthreads();
           if (t < TU) {
+            for (int pp = 1; pp < NP; ++pp) {  // parts in order: the sum does not depend on timing
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const double2 o = W[(size_t)tile * 4 + k];
-              g[k].x += o.x;
-              g[k].y += o.y;
+              for (int k = 0; k < 4; ++k) {
+                const double2 o = Gs[((size_t)(pp - 1) * TU + tile) * 4 + k];
+                g[k].x += o.x;
+                g[k].y += o.y;
+              }
             }
             G[(size_t)ti * GL + tj] = g[0];
             G[(size_t)ti * GL + tj + bs] = g[1];
