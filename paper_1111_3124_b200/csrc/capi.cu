@@ -41,6 +41,39 @@ cudaError_t mpsb::smem_optin(const void* kern, int bytes) {
   return e;
 }
 
+void* mpsb::tc_scratch(size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  struct Buf { int dev; cudaStream_t st; void* p; size_t n; };
+  static std::vector<Buf> bufs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  for (auto& b : bufs) {
+    if (b.dev != dev || b.st != st) continue;
+    if (b.n >= bytes) return b.p;
+    cudaStreamSynchronize(st);  // the previous buffer may still be in use on this stream
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.n = 0;
+    if (cudaMalloc(&b.p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    b.n = bytes;
+    return b.p;
+  }
+  void* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  bufs.push_back({dev, st, p, bytes});
+  return p;
+}
+
+bool mpsb::tc_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_TC");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
+
 unsigned long long* mpsb::prof_counts() { return g_prof.on ? g_prof.counts : nullptr; }
 
 void mpsb::prof_mark(int which, int begin, cudaStream_t st) {

@@ -23,6 +23,11 @@ struct Tier512 { static constexpr int L = 19, NL = 17; };
 // per (kernel, device, size); thread-safe.  The attribute is per device, so a process-wide
 // "done" flag would leave a second device without it (its launches would then fail).
 cudaError_t smem_optin(const void* kern, int bytes);
+// Grow-only device scratch of the tensor-core GEMM path per (device, stream): GEMMs on
+// different streams (the three-site side streams) never share it; null if cudaMalloc fails.
+void* tc_scratch(size_t bytes, cudaStream_t st);
+// the tensor-core GEMM path (tcgemm.cuh) is on unless MPS_TC=0 (A/B measurements)
+bool tc_enabled();
 
 inline int record_words(int p) { return 4 + (p + 31) / 32; }
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }

@@ -677,6 +677,64 @@ constexpr int GT_TILE = 16;
 #endif
 constexpr int GEMM_PLANES = GEMM_3M ? 3 : 2;
 
+// Epilogue of one output entry (r, c) of a k_gemm_t-style GEMM: ar / ai are the exact sums of
+// the real / imaginary parts as LG + 2 int64 digit columns (columns LG - 2 .. 2LG - 1 of the
+// LG-digit frame); round by the head-room shift g, then the per-column coefficient, negation,
+// + I, + Cadd, balancing, the known-zero top digit check (ZOUT), the store (mirrored for a
+// Hermitian off-diagonal tile) and the column exponents.  Shared by k_gemm_t and the
+// tensor-core path (tcgemm.cuh), so both write identical formats.
+template <int L, int LG, int ZOUT>
+__device__ __forceinline__ void gemm_t_store(const GemmT& it, int r, int c, int pc, int64_t (&ar)[LG + 2],
+                                             int64_t (&ai)[LG + 2], int g, int64_t eC, bool percol, bool mirror,
+                                             int& zbad) {
+  constexpr int D0 = L - LG;
+#pragma unroll
+  for (int ri = 0; ri < 2; ++ri) {
+    int32_t t[LG], o[L];
+    tround_any<LG>(ri ? ai : ar, g, t);
+#pragma unroll
+    for (int j = 0; j < L; ++j) o[j] = j >= D0 ? t[j - D0] : 0;
+    if (percol && it.colcoef) {  // x column coefficient (L+1 digits, fractional)
+      int32_t K[L + 1];
+#pragma unroll
+      for (int k = 0; k <= L; ++k) K[k] = it.colcoef[(size_t)pc * (L + 1) + k];
+      int64_t acc2[L + 2];
+#pragma unroll
+      for (int j = 0; j < L + 2; ++j) acc2[j] = 0;
+      kmul_acc<L>(acc2, K, o, K[L] != 0);
+      tround2<L>(acc2, o);
+    }
+    if (it.neg) {
+#pragma unroll
+      for (int j = 0; j < L; ++j) o[j] = -o[j];
+    }
+    if (it.addI && ri == 0 && r == c) o[L - 1] += 1 << (28 - (int)eC);  // + 1 at exponent eC (1)
+    if (it.Cadd) {
+      int32_t x[L];
+      ldfx<L>(it.Cadd, it.ldc, c, ri, r, x);
+#pragma unroll
+      for (int j = 0; j < L; ++j) o[j] += x[j];
+    }
+    fx_balance<L>(o);
+#pragma unroll
+    for (int j = L - ZOUT; j < L; ++j)  // the consumer skips these digits: they must be 0
+      if (o[j] != 0) zbad = 1;
+    stfx<L>(it.C, it.ldc, pc, ri, r, o);
+    if (mirror) {  // C(c, r) = conj C(r, c)
+      if (ri) {
+#pragma unroll
+        for (int j = 0; j < L; ++j) o[j] = -o[j];
+      }
+      stfx<L>(it.C, it.ldc, r, ri, c, o);
+    }
+  }
+  if (it.eCcols && r == 0) {
+    if (!percol) it.eCcols[pc] = eC;
+    else if (it.colexp && it.colexp[pc] == INT64_MIN) it.eCcols[pc] = 1;  // alpha = 0: zero column
+    else it.eCcols[pc] = *it.eA + it.eBcols[pc] + it.ghead + (it.colexp ? it.colexp[pc] : 0);
+  }
+}
+
 template <int L, int LG, int Z, int NZA = 0, int NZB = 0, int ZOUT = 0>
 __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
   static_assert(LG <= L && Z < LG && NZA < LG && NZB + Z < LG && ZOUT < L, "precision schedule");
@@ -813,54 +871,7 @@ __global__ void __launch_bounds__(256, 2) k_gemm_t(const GemmT* items) {
       ai[j] = as[j] - t1 - t2;
     }
 #endif
-    if (r < it.rows && c < ncols) {
-      const int pc = pcol(c);  // physical column
-#pragma unroll
-      for (int ri = 0; ri < 2; ++ri) {
-        int32_t t[LG], o[L];
-        tround_any<LG>(ri ? ai : ar, g, t);
-#pragma unroll
-        for (int j = 0; j < L; ++j) o[j] = j >= D0 ? t[j - D0] : 0;
-        if (percol && it.colcoef) {  // x column coefficient (L+1 digits, fractional)
-          int32_t K[L + 1];
-#pragma unroll
-          for (int k = 0; k <= L; ++k) K[k] = it.colcoef[(size_t)pc * (L + 1) + k];
-          int64_t acc2[L + 2];
-#pragma unroll
-          for (int j = 0; j < L + 2; ++j) acc2[j] = 0;
-          kmul_acc<L>(acc2, K, o, K[L] != 0);
-          tround2<L>(acc2, o);
-        }
-        if (it.neg) {
-#pragma unroll
-          for (int j = 0; j < L; ++j) o[j] = -o[j];
-        }
-        if (it.addI && ri == 0 && r == c) o[L - 1] += 1 << (28 - (int)eC);  // + 1 at exponent eC (1)
-        if (it.Cadd) {
-          int32_t x[L];
-          ldfx<L>(it.Cadd, it.ldc, c, ri, r, x);
-#pragma unroll
-          for (int j = 0; j < L; ++j) o[j] += x[j];
-        }
-        fx_balance<L>(o);
-#pragma unroll
-        for (int j = L - ZOUT; j < L; ++j)  // the consumer skips these digits: they must be 0
-          if (o[j] != 0) zbad = 1;
-        stfx<L>(it.C, it.ldc, pc, ri, r, o);
-        if (it.herm && c0 != r0) {  // C(c, r) = conj C(r, c)
-          if (ri) {
-#pragma unroll
-            for (int j = 0; j < L; ++j) o[j] = -o[j];
-          }
-          stfx<L>(it.C, it.ldc, r, ri, c, o);
-        }
-      }
-      if (it.eCcols && r == 0) {
-        if (!percol) it.eCcols[pc] = eC;
-        else if (it.colexp && it.colexp[pc] == INT64_MIN) it.eCcols[pc] = 1;  // alpha = 0: zero column
-        else it.eCcols[pc] = *it.eA + it.eBcols[pc] + it.ghead + (it.colexp ? it.colexp[pc] : 0);
-      }
-    }
+    if (r < it.rows && c < ncols) gemm_t_store<L, LG, ZOUT>(it, r, c, pcol(c), ar, ai, g, eC, percol, it.herm && c0 != r0, zbad);
   }
   if (zbad && it.zerr) atomicOr(it.zerr, 2);  // 2: re-run without the preconditioner
 }

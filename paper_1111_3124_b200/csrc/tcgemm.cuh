@@ -1,0 +1,396 @@
+// Tensor-core multiprecision GEMM: the GemmT products of the preconditioner (A_1 = Theta' X,
+// P = Theta' X_{n-1}, A_1 = P + P D/2) and of the recovery of V (V = Theta'^H A Sigma^-2), on
+// the 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM) instead of the
+// IMAD.WIDE pipe (DESIGN.md §4 "Tensor cores").
+//
+// Every p-bit operand value of the LG-digit frame (balanced radix-2^28 int32 digits) is
+// re-sliced EXACTLY into S = 4 LG + 1 signed slices, x = sum_s u_s 2^(7s): three balanced 7-bit
+// slices and a fourth (|u| <= 128) per digit, the last slice the carry out of the top digit.  A real product of two values is then
+// sum_{s,t} u_s v_t 2^(7(s+t)), and a real GEMM C = A B is, per slice-weight group d = s + t,
+// the int8 GEMM sum_{s+t=d} A_s B_t with exact int32 accumulation (each term <= 2^14, K <= 512,
+// <= 41 pairs per group, 2 real GEMMs per complex plane: < 2^30).  Groups d >= 4 (LG - 2) are
+// formed (a superset of the digit pairs i + j >= LG - 2 the IMAD path keeps, so the truncated
+// product is at least as accurate); the epilogue combines the groups into the int64 digit
+// columns of the IMAD path and runs the same rounding / store code (gemm_t_store).  Complex:
+// Re C = Ar Br + Ai (-Bi), Im C = Ar Bi + Ai Br (4 real products, accumulated in TMEM).
+//
+// Kernels per chunk of items: k_tc_slice_a / k_tc_slice_b (digits -> int8 slice tiles in the
+// UMMA K-major no-swizzle layout, so that staging is a straight copy), k_tc_mma (one CTA per
+// 128 x 32 output tile and plane: 16 groups at a time in TMEM (16 x 32 of its 512 columns),
+// for each group chunk, term and k block the needed slice tiles of A (4 KB) and B (1 KB) are
+// staged by cp.async and one thread issues the pair MMAs; the group sums are drained by
+// tcgen05.ld to global memory), k_tc_epi (one thread per output entry).
+#pragma once
+#include <mutex>
+#include <tuple>
+
+#include "precond.cuh"
+
+namespace mpsb {
+
+constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
+constexpr int TC_N = 32;   // output columns per CTA = MMA N
+constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
+constexpr int TC_GCH = 16;  // slice-weight groups per chunk: 16 accumulators x 32 columns = 512 TMEM columns
+constexpr int TC_ATILE = TC_M * TC_K;  // bytes of one A slice tile
+constexpr int TC_BTILE = TC_N * TC_K;  // bytes of one B slice tile
+
+template <int LG> __host__ __device__ constexpr int tc_ns() { return 4 * LG + 1; }
+template <int LG> __host__ __device__ constexpr int tc_dlo() { return 4 * (LG - 2); }
+template <int LG> __host__ __device__ constexpr int tc_ng() { return 8 * LG - tc_dlo<LG>() + 1; }
+
+struct TcDims {
+  int tilesR, tilesC, kb;  // output row tiles (128), column tiles (32), k blocks (32), max over items
+  size_t a_item, b_item, g_item;  // scratch bytes per item
+  int8_t* A;                     // [item][plane 2][S][tilesR][kb][4096]
+  int8_t* B;                     // [item][plane 3: re, im, -im][S][tilesC][kb][1024]
+  int32_t* G;                    // [item][plane 2][NG][tilesC * 32][tilesR * 128]
+};
+
+// byte offset of element (x, k) inside a K-major no-swizzle UMMA tile: core matrices of 8 rows
+// x 16 bytes, [x / 8][k / 16][x % 8][k % 16] (32 k per tile)
+__device__ __forceinline__ int tc_off(int x, int k) { return (((x >> 3) * 2 + (k >> 4)) << 7) + ((x & 7) << 4) + (k & 15); }
+
+// next balanced 7-bit slice of v (v <- (v - u) / 128)
+__device__ __forceinline__ int tc_bal7(int32_t& v) {
+  const int32_t u = ((v + 64) & 127) - 64;
+  v = (v - u) >> 7;
+  return u;
+}
+
+// the four slices of digit v (+ the carry from the digit below): three balanced 7-bit slices and
+// a fourth that keeps the rest when it fits int8 (always for balanced digits, so a zero digit
+// gives zero slices and no carry), else balanced with a carry into the next digit
+__device__ __forceinline__ void tc_digit(int32_t v, int32_t& carry, int (&u)[4]) {
+  v += carry;
+  u[0] = tc_bal7(v);
+  u[1] = tc_bal7(v);
+  u[2] = tc_bal7(v);
+  if (v >= -128 && v <= 127) {
+    u[3] = v;
+    carry = 0;
+  } else {
+    u[3] = tc_bal7(v);
+    carry = v;
+  }
+}
+
+__device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// descriptor of a K-major no-swizzle tile: LBO = 128 B (k-adjacent core matrices), SBO = 256 B
+// (8-row groups), sm100 descriptor version 1
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+// instruction descriptor: dense, s32 accumulator, signed int8 A and B, K-major, M x N
+__host__ __device__ constexpr uint32_t tc_idesc(int M, int N) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ---------------------------------------------------------------------------- slicing
+// Operand A of the item (rows x K): plane ri of op(A)(r, k) in the LG-digit frame (digits
+// D0 .. L-1 of the stored value).  conjA: A is stored K x rows, op(A) = A^H.
+// Block (tile r, k block) of 128 x 32 entries; 256 threads.
+template <int L, int LG>
+__global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int first, TcDims dm) {
+  constexpr int S = tc_ns<LG>(), D0 = L - LG;
+  const int item = first + blockIdx.z;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const int ri = blockIdx.y, rt = blockIdx.x % dm.tilesR, kbk = blockIdx.x / dm.tilesR;
+  if (rt * TC_M >= it.rows || kbk * TC_K >= it.K) return;  // tiles no MMA reads
+  int8_t* out = dm.A + blockIdx.z * dm.a_item + (size_t)ri * S * dm.tilesR * dm.kb * TC_ATILE +
+                ((size_t)rt * dm.kb + kbk) * TC_ATILE;
+  const size_t sstride = (size_t)dm.tilesR * dm.kb * TC_ATILE;  // between slices
+  __shared__ int32_t T[TC_K][TC_M + 1];
+  // element e = t + 256 i: k = e % 32 (fastest: coalesced tile bytes), x = e / 32
+  int32_t carry[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) carry[i] = 0;
+  for (int j = 0; j < LG; ++j) {
+    if (!it.conjA) {  // digits contiguous along rows: stage [k][x] through shared memory
+      __syncthreads();
+      for (int e = threadIdx.x; e < TC_M * TC_K; e += 256) {
+        const int x = e % TC_M, k = e / TC_M;
+        const int r = rt * TC_M + x, kk = kbk * TC_K + k;
+        T[k][x] = (r < it.rows && kk < it.K) ? it.A[((size_t)(kk * 2 + ri) * L + D0 + j) * it.lda + r] : 0;
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int e = threadIdx.x + 256 * i, k = e & 31, x = e >> 5;
+      int32_t v;
+      if (!it.conjA) {
+        v = T[k][x];
+      } else {  // A stored K x rows, digits contiguous along k: op(A)(r, k) = conj A(k, r)
+        const int r = rt * TC_M + x, kk = kbk * TC_K + k;
+        v = (r < it.rows && kk < it.K) ? it.A[((size_t)(r * 2 + ri) * L + D0 + j) * it.lda + kk] : 0;
+        if (ri) v = -v;
+      }
+      int uu[4];
+      tc_digit(v, carry[i], uu);
+      const int o = tc_off(x, k);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int e = threadIdx.x + 256 * i, k = e & 31, x = e >> 5;
+    out[(size_t)(S - 1) * sstride + tc_off(x, k)] = (int8_t)carry[i];
+  }
+}
+
+// Operand B (K x cols), logical column c = physical column colmap[c] (c < ncols): planes
+// 0 re, 1 im, 2 -im.  Block (tile c, k block) of 32 x 32 entries; 256 threads, 4 entries each.
+template <int L, int LG>
+__global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int first, TcDims dm) {
+  constexpr int S = tc_ns<LG>(), D0 = L - LG;
+  const int item = first + blockIdx.z;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const int ri = blockIdx.y, ct = blockIdx.x % dm.tilesC, kbk = blockIdx.x / dm.tilesC;
+  const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
+  if (ct * TC_N >= ncols || kbk * TC_K >= it.K) return;  // tiles no MMA reads
+  const size_t sstride = (size_t)dm.tilesC * dm.kb * TC_BTILE;
+  const size_t pstride = (size_t)S * sstride;
+  int8_t* out = dm.B + blockIdx.z * dm.b_item + (size_t)ri * pstride + ((size_t)ct * dm.kb + kbk) * TC_BTILE;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int e = threadIdx.x + 256 * i, k = e & 31, x = e >> 5;
+    const int c = ct * TC_N + x, kk = kbk * TC_K + k;
+    const bool ok = c < ncols && kk < it.K;
+    const int pc = ok ? (it.colmap ? it.colmap[c] : c) : 0;
+    const int o = tc_off(x, k);
+    int32_t carry = 0;
+#pragma unroll
+    for (int j = 0; j < LG; ++j) {
+      const int32_t v = ok ? it.B[((size_t)(pc * 2 + ri) * L + D0 + j) * it.ldb + kk] : 0;
+      int uu[4];
+      tc_digit(v, carry, uu);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
+        if (ri) out[pstride + (size_t)(4 * j + u) * sstride + o] = (int8_t)(-uu[u]);  // plane 2: -im
+      }
+    }
+    out[(size_t)(S - 1) * sstride + o] = (int8_t)carry;
+    if (ri) out[pstride + (size_t)(S - 1) * sstride + o] = (int8_t)(-carry);
+  }
+}
+
+// ---------------------------------------------------------------------------- MMA
+// Slice ranges: A s in [SA0, S), B t in [SB0, SB1); groups d = s + t in [DLO, 8 LG].
+template <int LG, int SA0, int SB0, int SB1>
+__global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
+  constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = 8 * LG;
+  constexpr int NCH = (NG + TC_GCH - 1) / TC_GCH;
+  constexpr uint32_t IDESC = tc_idesc(TC_M, TC_N);
+  const int item = first + blockIdx.y;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const int plane = blockIdx.x & 1, rest = blockIdx.x >> 1;
+  const int rt = rest % dm.tilesR, ct = rest / dm.tilesR;
+  const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
+  if (rt * TC_M >= it.rows || ct * TC_N >= ncols) return;  // CTA-uniform
+  const int nkb = (it.K + TC_K - 1) / TC_K;
+  extern __shared__ __align__(1024) int8_t tcs[];
+  int8_t* sA = tcs;                              // [S][4096]
+  int8_t* sB = tcs + (size_t)S * TC_ATILE;       // [S][1024]
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t started;  // bit j: group d0 + j of the chunk received an MMA
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(&tmem_base)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = tmem_base;
+  uint32_t phase = 0;
+  const size_t a_s = (size_t)dm.tilesR * dm.kb * TC_ATILE, b_s = (size_t)dm.tilesC * dm.kb * TC_BTILE;
+  const int8_t* Ab = dm.A + blockIdx.y * dm.a_item;
+  const int8_t* Bb = dm.B + blockIdx.y * dm.b_item;
+  int32_t* Gb = dm.G + blockIdx.y * dm.g_item;
+  const int RRr = dm.tilesR * TC_M, RCc = dm.tilesC * TC_N;
+  for (int ch = 0; ch < NCH; ++ch) {
+    const int d0 = DLO + ch * TC_GCH, d1 = min(d0 + TC_GCH - 1, DHI);
+    // slices any pair of this chunk uses
+    const int sa_lo = max(SA0, d0 - (SB1 - 1)), sb_lo = max(SB0, d0 - (S - 1));
+    if (tid == 0) started = 0u;
+    for (int term = 0; term < 2; ++term) {
+      // Re: Ar Br + Ai (-Bi); Im: Ar Bi + Ai Br
+      const int ap = term, bp = plane == 0 ? (term == 0 ? 0 : 2) : (term == 0 ? 1 : 0);
+      const int8_t* Ap = Ab + (size_t)ap * S * a_s + (size_t)rt * dm.kb * TC_ATILE;
+      const int8_t* Bp = Bb + (size_t)bp * S * b_s + (size_t)ct * dm.kb * TC_BTILE;
+      for (int kbk = 0; kbk < nkb; ++kbk) {
+        // stage the slice tiles (straight 16-byte copies: the global layout is the tile layout)
+        const int na = (S - sa_lo) * (TC_ATILE / 16), nb = (SB1 - sb_lo) * (TC_BTILE / 16);
+        for (int w = tid; w < na; w += 128) {
+          const int s = sa_lo + w / (TC_ATILE / 16), o = (w % (TC_ATILE / 16)) * 16;
+          cp_async16(sA + (size_t)s * TC_ATILE + o, Ap + (size_t)s * a_s + (size_t)kbk * TC_ATILE + o, 16);
+        }
+        for (int w = tid; w < nb; w += 128) {
+          const int t = sb_lo + w / (TC_BTILE / 16), o = (w % (TC_BTILE / 16)) * 16;
+          cp_async16(sB + (size_t)t * TC_BTILE + o, Bp + (size_t)t * b_s + (size_t)kbk * TC_BTILE + o, 16);
+        }
+        cp_commit();
+        cp_wait<0>();
+        asm volatile("fence.proxy.async.shared::cta;\n");
+        __syncthreads();
+        if (tid == 0) {
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          uint32_t st = started;
+          // A slice outer, group inner: consecutive MMAs go to different accumulators
+          for (int s = sa_lo; s < S; ++s) {
+            const uint64_t da = tc_desc(tc_smem(sA + (size_t)s * TC_ATILE));
+            const int dlo = max(d0, s + sb_lo), dhi = min(d1, s + SB1 - 1);
+            for (int d = dlo; d <= dhi; ++d) {
+              const int t = d - s;
+              const uint32_t acc_addr = tmem + (uint32_t)((d - d0) * TC_N);
+              const uint64_t db = tc_desc(tc_smem(sB + (size_t)t * TC_BTILE));
+              const uint32_t acc = (st >> (d - d0)) & 1u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
+                  "l"(da), "l"(db), "r"(IDESC), "r"(acc));
+              st |= 1u << (d - d0);
+            }
+          }
+          started = st;
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tc_smem(&bar)));
+        }
+        // the MMAs read the staged tiles: wait before they are overwritten (and before the drain)
+        asm volatile(
+            "{\n\t.reg .pred done;\n\tTCW_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+            "@!done bra TCW_%=;\n\t}\n" ::"r"(tc_smem(&bar)), "r"(phase));
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        __syncthreads();
+      }
+    }
+    // drain: warp w reads TMEM lanes 32w .. 32w + 31 (rows), 32 columns per group
+    const uint32_t st = started;
+    const int row = rt * TC_M + 32 * warp + lane;
+    for (int d = d0; d <= d1; ++d) {
+      uint32_t v[32];
+      if ((st >> (d - d0)) & 1u) {
+        const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0;
+      }
+      int32_t* g = Gb + (((size_t)plane * NG + (d - DLO)) * RCc + (size_t)ct * TC_N) * RRr + row;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[(size_t)j * RRr] = (int32_t)v[j];
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();  // the next chunk's MMAs overwrite the accumulators
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+  }
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
+}
+
+// ---------------------------------------------------------------------------- epilogue
+// One thread per output entry: group sums -> LG + 2 int64 digit columns (column d / 4 of the
+// product, shifted by 7 (d % 4) bits) -> gemm_t_store (the IMAD path's rounding and store).
+template <int L, int LG, int ZOUT>
+__global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, TcDims dm) {
+  constexpr int DLO = tc_dlo<LG>(), NG = tc_ng<LG>();
+  const int item = first + blockIdx.y;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const bool percol = it.eBcols != nullptr;
+  const int64_t eC = percol ? 0 : (it.eCout ? *it.eCout : *it.eA + *it.eB + it.ghead);
+  const int g = percol ? it.ghead : (int)(eC - (*it.eA + *it.eB));
+  if (!percol && it.eCwrite && blockIdx.x == 0 && threadIdx.x == 0) *it.eCwrite = eC;
+  const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
+  const int RRr = dm.tilesR * TC_M, RCc = dm.tilesC * TC_N;
+  const int32_t* Gb = dm.G + blockIdx.y * dm.g_item;
+  int zbad = 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < it.rows * ncols; t += gridDim.x * blockDim.x) {
+    const int r = t % it.rows, c = t / it.rows;
+    int64_t acc[2][LG + 3];
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri) {
+#pragma unroll
+      for (int j = 0; j < LG + 3; ++j) acc[ri][j] = 0;
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        const int d = DLO + q;
+        const int64_t v = Gb[(((size_t)ri * NG + q) * RCc + c) * RRr + r];
+        acc[ri][d / 4 - (LG - 2)] += v * ((int64_t)1 << (7 * (d % 4)));
+      }
+      acc[ri][LG + 1] += acc[ri][LG + 2] * ((int64_t)1 << 28);  // column 2LG (the top slices' carry)
+    }
+    int64_t ar[LG + 2], ai[LG + 2];
+#pragma unroll
+    for (int j = 0; j < LG + 2; ++j) { ar[j] = acc[0][j]; ai[j] = acc[1][j]; }
+    gemm_t_store<L, LG, ZOUT>(it, r, c, it.colmap ? it.colmap[c] : c, ar, ai, g, eC, percol, false, zbad);
+  }
+  if (zbad && it.zerr) atomicOr(it.zerr, 2);
+}
+
+// ---------------------------------------------------------------------------- launch
+
+template <int LG, int SA0, int SB0, int SB1>
+constexpr size_t tc_mma_smem() { return (size_t)tc_ns<LG>() * (TC_ATILE + TC_BTILE); }
+
+// C = op(A) B for n items (GemmT on the device) on the tensor cores.  Z / NZA / NZB: known-zero
+// top digits of B / low digits of A / low digits of B (their slices are not multiplied).
+// Returns the number of kernel launches, or -1 when the scratch cannot be allocated (the
+// caller then runs the IMAD kernel).
+template <int L, int LG, int Z, int NZA, int NZB, int ZOUT>
+inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int maxK, cudaStream_t st) {
+  constexpr int S = tc_ns<LG>(), NG = tc_ng<LG>();
+  constexpr int SA0 = 4 * NZA, SB0 = 4 * NZB, SB1 = Z > 0 ? 4 * (LG - Z) : S;
+  TcDims dm;
+  dm.tilesR = (maxR + TC_M - 1) / TC_M;
+  dm.tilesC = (maxC + TC_N - 1) / TC_N;
+  dm.kb = (maxK + TC_K - 1) / TC_K;
+  dm.a_item = align_up((size_t)2 * S * dm.tilesR * dm.kb * TC_ATILE);
+  dm.b_item = align_up((size_t)3 * S * dm.tilesC * dm.kb * TC_BTILE);
+  dm.g_item = align_up((size_t)2 * NG * dm.tilesC * TC_N * dm.tilesR * TC_M * 4);
+  const size_t per = dm.a_item + dm.b_item + dm.g_item;
+  const size_t budget = (size_t)3 << 30;
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>(n, budget / per));
+  char* scr = (char*)tc_scratch(per * chunk, st);
+  if (!scr) return -1;
+  dm.A = (int8_t*)scr;
+  dm.B = (int8_t*)(scr + dm.a_item * chunk);
+  dm.G = (int32_t*)(scr + (dm.a_item + dm.b_item) * chunk);
+  constexpr size_t smem = tc_mma_smem<LG, SA0, SB0, SB1>();
+  smem_optin((const void*)k_tc_mma<LG, SA0, SB0, SB1>, (int)smem);
+  int nl = 0;
+  for (int f = 0; f < n; f += chunk) {
+    const int cnt = std::min(chunk, n - f);
+    k_tc_slice_a<L, LG><<<dim3(dm.tilesR * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
+    k_tc_slice_b<L, LG><<<dim3(dm.tilesC * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
+    k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), 128, smem, st>>>(d_items, f, dm);
+    const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
+    k_tc_epi<L, LG, ZOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);
+    nl += 4;
+  }
+  return nl;
+}
+
+}  // namespace mpsb

@@ -14,6 +14,7 @@
 #include "common.h"
 #include "kernels.cuh"
 #include "precond.cuh"
+#include "tcgemm.cuh"
 
 namespace mpsb {
 
@@ -249,6 +250,31 @@ inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t 
   for (int k = 0; k < pre_slots<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
+// One GemmT launch over n items: the tensor-core path (tcgemm.cuh) for the 280-bit tier (its
+// 41 slice tiles of A and B fit shared memory; the 512-bit tier's 77 do not) unless
+// MPS_TC=0, else (or when its scratch cannot be allocated) the IMAD.WIDE kernel.  Launch count.
+template <int L, int LG, int Z, int NZA = 0, int NZB = 0, int ZOUT = 0>
+inline int run_gemm(const GemmT* d, int n, int maxR, int maxC, int maxK, dim3 grid, cudaStream_t st) {
+  if constexpr (LG <= 10) {
+    if (tc_enabled() && maxR > 0 && maxC > 0 && maxK > 0) {
+      const int nl = launch_gemm_tc<L, LG, Z, NZA, NZB, ZOUT>(d, n, maxR, maxC, maxK, st);
+      if (nl >= 0) return nl;
+    }
+  }
+  k_gemm_t<L, LG, Z, NZA, NZB, ZOUT><<<grid, 256, 0, st>>>(d);
+  return 1;
+}
+
+// Newton-Schulz iteration K (precond.cuh NsSched): D_k = I - X_k^H X_k, X_{k+1} = X_k + X_k D_k / 2.
+// On the tensor cores D_k is formed in full (no mirrored half: its two triangles are exact
+// conjugates before the identical rounding).  Launch count.
+template <int L, int K>
+inline int run_ns_iter(const GemmT* dD, const GemmT* dX, int n, int maxN, dim3 grid, cudaStream_t st) {
+  constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K], NZ = NsSched<L>::nz[K];
+  return run_gemm<L, LG, 0, NZ, NZ, Z>(dD, n, maxN, maxN, maxN, grid, st) +
+         run_gemm<L, LG, Z, NZ, 0>(dX, n, maxN, maxN, maxN, grid, st);
+}
+
 // the preconditioner kernels for n items (descriptors already on the device); launch count
 template <int L>
 inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, int maxN, cudaStream_t st) {
@@ -311,23 +337,22 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   const dim3 gMN(std::min(tMN, 1024), n);
   constexpr int KL = NSIT - 1;  // last iteration: lg = L
   static_assert(NsSched<L>::lg[KL] == L, "the last Newton-Schulz iteration is at full precision");
-  launch_ns_iter<L, 0>(dgt, dgt + (size_t)n, gNN, st);
-  launch_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, gNN, st);
-  if constexpr (NSIT > 3) launch_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, gNN, st);
+  nl += run_ns_iter<L, 0>(dgt, dgt + (size_t)n, n, maxN, gNN, st);
+  nl += run_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, n, maxN, gNN, st);
+  if constexpr (NSIT > 3) nl += run_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, n, maxN, gNN, st);
   const GemmT* dD = dgt + (size_t)(2 * KL) * n;
   const GemmT* dX = dgt + (size_t)(2 * KL + 1) * n;
   const GemmT* dA1 = dgt + (size_t)(2 * NSIT) * n;
   // X route: X_n = X_{n-1} + X_{n-1} D / 2, A_1 = A0 X_n; P route (items whose V is recovered):
   // P = A0 X_{n-1} (its nz zero low digits skipped), A_1 = P + P D / 2.  Items without a route
   // have empty descriptors in the other route's launches.
-  launch_ns_iter<L, KL>(dD, dX, gNN, st);
-  k_gemm_t<L, L, 0><<<gMN, 256, 0, st>>>(dA1);
+  nl += run_ns_iter<L, KL>(dD, dX, n, maxN, gNN, st);
+  nl += run_gemm<L, L, 0>(dA1, n, maxM, maxN, maxN, gMN, st);
   {
     constexpr int Z = NsSched<L>::z[KL], NZ = NsSched<L>::nz[KL];
-    k_gemm_t<L, L, 0, 0, NZ><<<gMN, 256, 0, st>>>(dA1 + (size_t)n);
-    k_gemm_t<L, L, Z><<<gMN, 256, 0, st>>>(dA1 + (size_t)2 * n);
+    nl += run_gemm<L, L, 0, 0, NZ>(dA1 + (size_t)n, n, maxM, maxN, maxN, gMN, st);
+    nl += run_gemm<L, L, Z>(dA1 + (size_t)2 * n, n, maxM, maxN, maxN, gMN, st);
   }
-  nl += 2 * NSIT + 3;
   return nl;
 }
 
@@ -491,7 +516,18 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   // a1 contraction: the thread-per-element k_gemm measured 10% faster than the tiled
   // k_gemm_t at K = chi (92.7 vs 102.5 ms for 296 chi=128 items; with the three-product
   // k_gemm_t still 1.5% slower per bench step, v26); hgc stays as the tiled form
-  k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
+  if (L <= 10 && tc_enabled()) {  // on the tensor cores (tcgemm.cuh), as the GemmT form hgc
+    int mr = 0, mc = 0, mk = 0;
+    for (int b = 0; b < n; ++b) {
+      mr = std::max(mr, hgc[b].rows);
+      mc = std::max(mc, hgc[b].cols);
+      mk = std::max(mk, hgc[b].K);
+    }
+    const int tC = ((mr + GT_TILE - 1) / GT_TILE) * ((mc + GT_TILE - 1) / GT_TILE);
+    nl += run_gemm<L, L, 0>((const GemmT*)(base + d_gc), n, mr, mc, mk, dim3(std::max(1, std::min(tC, 1024)), n), st);
+  } else {
+    k_gemm<L><<<gg, 128, 0, st>>>((const GemmItem*)(base + d_gemm)); ++nl;
+  }
   k_mix<L, NL><<<gg, 128, 16 * 2 * L * 4, st>>>((const MixItem*)(base + d_mix), RBr); ++nl;
   prof_mark(PROF_CONTRACT, 0, st);
   if (pre && !any_dbg) {
@@ -564,9 +600,11 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     for (int b = 0; b < n; ++b) maxNr = std::max(maxNr, hs[b].N);
     k_recover_coef<L, NL><<<dim3(std::max(1, (maxNr + 127) / 128), n), 128, 0, st>>>((const RecItem<NL>*)(base + d_rec));
     ++nl;
+    int maxMr = 0;
+    for (int b = 0; b < n; ++b) maxMr = std::max(maxMr, hs[b].M);
     const int tR = ((maxNr + GT_TILE - 1) / GT_TILE) * ((maxNr + GT_TILE - 1) / GT_TILE);
-    k_gemm_t<L, L, 0><<<dim3(std::max(1, std::min(tR, 1024)), n), 256, 0, st>>>((const GemmT*)(base + d_rg));
-    ++nl;
+    nl += run_gemm<L, L, 0>((const GemmT*)(base + d_rg), n, maxNr, maxNr, maxMr,
+                            dim3(std::max(1, std::min(tR, 1024)), n), st);
     prof_mark(PROF_RECOVER, 0, st);
   }
   prof_mark(PROF_FINALIZE, 1, st);
