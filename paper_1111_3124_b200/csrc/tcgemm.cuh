@@ -21,6 +21,8 @@
 // staged by cp.async and one thread issues the pair MMAs; the group sums are drained by
 // tcgen05.ld to global memory), k_tc_epi (one thread per output entry).
 #pragma once
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <tuple>
 
@@ -45,6 +47,7 @@ struct TcDims {
   int8_t* A;                     // [item][plane 2][S][tilesR][kb][4096]
   int8_t* B;                     // [item][plane 3: re, im, -im][S][tilesC][kb][1024]
   int32_t* G;                    // [item][plane 2][NG][tilesC * 32][tilesR * 128]
+  int bisect;                    // debug (MPS_TC_BISECT): bit 0 no MMA, bit 1 no drain, bit 2 no staging
 };
 
 // byte offset of element (x, k) inside a K-major no-swizzle UMMA tile: core matrices of 8 rows
@@ -219,7 +222,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   const size_t a_s = (size_t)dm.tilesR * dm.kb * TC_ATILE, b_s = (size_t)dm.tilesC * dm.kb * TC_BTILE;
   const int8_t* Ab = dm.A + blockIdx.y * dm.a_item;
   const int8_t* Bb = dm.B + blockIdx.y * dm.b_item;
-  int32_t* Gb = dm.G + blockIdx.y * dm.g_item;
+  int32_t* Gb = (int32_t*)((char*)dm.G + blockIdx.y * dm.g_item);
   const int RRr = dm.tilesR * TC_M, RCc = dm.tilesC * TC_N;
   for (int ch = 0; ch < NCH; ++ch) {
     const int d0 = DLO + ch * TC_GCH, d1 = min(d0 + TC_GCH - 1, DHI);
@@ -234,11 +237,11 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
       for (int kbk = 0; kbk < nkb; ++kbk) {
         // stage the slice tiles (straight 16-byte copies: the global layout is the tile layout)
         const int na = (S - sa_lo) * (TC_ATILE / 16), nb = (SB1 - sb_lo) * (TC_BTILE / 16);
-        for (int w = tid; w < na; w += 128) {
+        for (int w = tid; w < na && !(dm.bisect & 4); w += 128) {
           const int s = sa_lo + w / (TC_ATILE / 16), o = (w % (TC_ATILE / 16)) * 16;
           cp_async16(sA + (size_t)s * TC_ATILE + o, Ap + (size_t)s * a_s + (size_t)kbk * TC_ATILE + o, 16);
         }
-        for (int w = tid; w < nb; w += 128) {
+        for (int w = tid; w < nb && !(dm.bisect & 4); w += 128) {
           const int t = sb_lo + w / (TC_BTILE / 16), o = (w % (TC_BTILE / 16)) * 16;
           cp_async16(sB + (size_t)t * TC_BTILE + o, Bp + (size_t)t * b_s + (size_t)kbk * TC_BTILE + o, 16);
         }
@@ -246,7 +249,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
         cp_wait<0>();
         asm volatile("fence.proxy.async.shared::cta;\n");
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && !(dm.bisect & 1)) {
           asm volatile("tcgen05.fence::after_thread_sync;\n");
           uint32_t st = started;
           // A slice outer, group inner: consecutive MMAs go to different accumulators
@@ -263,17 +266,19 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
                   "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
                   "l"(da), "l"(db), "r"(IDESC), "r"(acc));
               st |= 1u << (d - d0);
+              if (dm.bisect & 8) break;
             }
+            if (dm.bisect & 8) break;
           }
           started = st;
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tc_smem(&bar)));
         }
         // the MMAs read the staged tiles: wait before they are overwritten (and before the drain)
-        asm volatile(
+        if (!(dm.bisect & 1)) asm volatile(
             "{\n\t.reg .pred done;\n\tTCW_%=:\n\t"
             "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
             "@!done bra TCW_%=;\n\t}\n" ::"r"(tc_smem(&bar)), "r"(phase));
-        phase ^= 1;
+        if (!(dm.bisect & 1)) phase ^= 1;
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         __syncthreads();
       }
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
     const int row = rt * TC_M + 32 * warp + lane;
     for (int d = d0; d <= d1; ++d) {
       uint32_t v[32];
-      if ((st >> (d - d0)) & 1u) {
+      if (((st >> (d - d0)) & 1u) && !(dm.bisect & 2)) {
         const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
   if (!percol && it.eCwrite && blockIdx.x == 0 && threadIdx.x == 0) *it.eCwrite = eC;
   const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
   const int RRr = dm.tilesR * TC_M, RCc = dm.tilesC * TC_N;
-  const int32_t* Gb = dm.G + blockIdx.y * dm.g_item;
+  const int32_t* Gb = (int32_t*)((char*)dm.G + blockIdx.y * dm.g_item);
   int zbad = 0;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < it.rows * ncols; t += gridDim.x * blockDim.x) {
     const int r = t % it.rows, c = t / it.rows;
@@ -364,6 +369,8 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
   constexpr int S = tc_ns<LG>(), NG = tc_ng<LG>();
   constexpr int SA0 = 4 * NZA, SB0 = 4 * NZB, SB1 = Z > 0 ? 4 * (LG - Z) : S;
   TcDims dm;
+  static const int bis = getenv("MPS_TC_BISECT") ? atoi(getenv("MPS_TC_BISECT")) : 0;
+  dm.bisect = bis;
   dm.tilesR = (maxR + TC_M - 1) / TC_M;
   dm.tilesC = (maxC + TC_N - 1) / TC_N;
   dm.kb = (maxK + TC_K - 1) / TC_K;
@@ -380,14 +387,25 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
   dm.G = (int32_t*)(scr + (dm.a_item + dm.b_item) * chunk);
   constexpr size_t smem = tc_mma_smem<LG, SA0, SB0, SB1>();
   smem_optin((const void*)k_tc_mma<LG, SA0, SB0, SB1>, (int)smem);
+  static const bool dbg = getenv("MPS_TC_DEBUG") != nullptr;  // sync + check after every launch
+  auto check = [&](const char* what) {
+    if (!dbg) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    fprintf(stderr, "tc L=%d LG=%d Z=%d NZA=%d NZB=%d: %s n=%d chunk=%d R=%d C=%d K=%d: %s\n", L, LG, Z, NZA, NZB, what, n,
+            chunk, maxR, maxC, maxK, cudaGetErrorString(e));
+  };
   int nl = 0;
   for (int f = 0; f < n; f += chunk) {
     const int cnt = std::min(chunk, n - f);
     k_tc_slice_a<L, LG><<<dim3(dm.tilesR * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
+    check("slice_a");
     k_tc_slice_b<L, LG><<<dim3(dm.tilesC * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
+    check("slice_b");
     k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), 128, smem, st>>>(d_items, f, dm);
+    check("mma");
     const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
     k_tc_epi<L, LG, ZOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);
+    check("epi");
     nl += 4;
   }
   return nl;
