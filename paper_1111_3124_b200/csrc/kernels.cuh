@@ -13,6 +13,7 @@
 #include <cooperative_groups.h>
 
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.h"
@@ -792,6 +793,10 @@ __host__ __device__ constexpr int jacobi_min_ctas() { return L <= 10 ? JACOBI_CT
 // rows are distributed over all C*NWARP warps, column state lives in global memory, and
 // the phases are separated by cluster barriers.  The arithmetic of every pair is the same
 // whatever C is, so results are bitwise independent of C.
+// debug (MPS_JACOBI_TRACE=k): the first k matrices of a launch print, per sweep, the bounds of
+// the certified stop (R21): log2 rho^2_max, log2 mu^2_max, rotations seen, certified
+static __device__ int jac_trace_items;
+
 template <int L, int NL>
 __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const SvdItem<NL>* items, int C) {
   namespace cg = cooperative_groups;
@@ -1145,6 +1150,10 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
       cert = emu > INT_MIN && erho > INT_MIN && emu <= -2 * (lg2N + 3) &&
              2 * (int64_t)lg2N + emu + erho + 6 <= etol2 - 16;
     }
+    if (jac_trace_items && crank == 0 && tid == 0 && (int)(C > 1 ? blockIdx.x / C : blockIdx.x) < jac_trace_items)
+      printf("jacobi item %d N %d sweep %d lgd %d erho2 %d emu2 %d any %d cert %d\n", (int)(C > 1 ? blockIdx.x / C : blockIdx.x),
+             N, sweep, lgd, it.cexp ? *(volatile int*)&it.cexp[2 * (sweep & 1) + 1] : 0,
+             it.cexp ? *(volatile int*)&it.cexp[2 * (sweep & 1)] : 0, (int)any, (int)cert);
     if (!any || cert) {
       conv = 1;
       if (cert && crank == 0 && tid == 0) it.cexp[4] = 1;
@@ -1172,9 +1181,18 @@ template <int L, int NL>
 inline void launch_jacobi(const SvdItem<NL>* d_items, int n, int C, cudaStream_t st);
 
 // opt in to > 48 KB of dynamic shared memory (once per instantiation)
+inline void jacobi_trace_init() {
+  static int tr = -1;
+  if (tr < 0) {
+    const char* e = getenv("MPS_JACOBI_TRACE");
+    tr = e ? atoi(e) : 0;
+    if (tr > 0) cudaMemcpyToSymbol(jac_trace_items, &tr, sizeof(int));
+  }
+}
 template <int L, int NL>
 inline void jacobi_prepare() {
   smem_optin((const void*)k_jacobi<L, NL>, (int)jacobi_smem_bytes<L>());
+  jacobi_trace_init();
 }
 
 template <int L, int NL>

@@ -31,6 +31,9 @@ struct PreItem {
   int64_t* eA1;                           // exponent chosen for A_1 = Theta' X (1)
   int* anyflag;                           // [2] "some block pair rotated" per sweep parity (cluster mode)
   unsigned long long* offmax;             // [2] largest |gamma|^2 / (alpha_p alpha_q) per sweep parity (bits)
+  // refinement sweep (xsweep.cuh, R22): X_1 (rotated in place), G = A_t^H A_t and its
+  // exponent, the rotation records; X1 == nullptr: no refinement sweep for this item
+  int32_t* X1; const int32_t* G; const int64_t* eG; int4* xs_rec;
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {

@@ -15,6 +15,7 @@
 #include "kernels.cuh"
 #include "precond.cuh"
 #include "tcgemm.cuh"
+#include "xsweep.cuh"
 
 namespace mpsb {
 
@@ -162,16 +163,28 @@ inline bool use_precond() {
 }
 template <int L>
 constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
-// GEMM descriptors per item: 2 per Newton-Schulz iteration, A_1 (X route), P and A_1 (P route)
+// GEMM descriptors per item: 2 per Newton-Schulz iteration, A_1 (X route), P and A_1 (P route),
+// A_t = Theta' X and G = A_t^H A_t of the two refinement sweeps (R22)
 template <int L>
-constexpr int pre_slots() { return 2 * ns_iters<L>() + 3; }
+constexpr int pre_slots() { return 2 * ns_iters<L>() + 7; }
+// the refinement sweep (xsweep.cuh, R22) is on unless MPS_XSWEEP=0
+inline bool use_xsweep() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_XSWEEP");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
+constexpr int XS_MIN_N = 16;  // smaller items: no refinement sweep
 
 // preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N; for a square
 // item the last X buffer also holds P = A0 X_{n-1}), eMix[N], scalars
 template <int L>
 inline size_t pre_bytes(int M, int N) {
   return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
-         256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N);  // + recovery coefficients
+         256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N) +  // + recovery coefficients
+         xs_rec_bytes(N);                                                      // + refinement sweep records
 }
 
 // preconditioner buffers carved from q (layout of pre_bytes)
@@ -187,6 +200,8 @@ struct PreBufs {
   unsigned long long* offmax;
   int32_t* rcoef;
   int64_t* rexp;
+  int64_t* eG;   // exponent of G (refinement sweep)
+  int4* xs_rec;  // refinement sweep records
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
 };
 template <int L>
@@ -206,6 +221,8 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.offmax = (unsigned long long*)(q + 64);
   b.rcoef = (int32_t*)(q + 256);
   b.rexp = (int64_t*)((char*)b.rcoef + align_up(4 * (size_t)N * (L + 1)));
+  b.eG = (int64_t*)(q + 96);
+  b.xs_rec = (int4*)((char*)b.rexp + align_up(8 * (size_t)N));
   return b;
 }
 // descriptors of one item's preconditioner (gt[k * stride], k = 0 .. 2 ns_iters): the
@@ -217,7 +234,8 @@ template <int L>
 inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, const int64_t* eA0, int32_t* Af,
                       int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride, bool p_route = false) {
   constexpr int NSIT = ns_iters<L>();
-  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
+  *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax,
+                nullptr, nullptr, nullptr, nullptr};
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -243,10 +261,33 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
     gt[(2 * NSIT + 1) * stride] = GemmT{A0, M, eA0, Xc, N, pb.eOne, P, M, pb.eA1, nullptr, nullptr, M, N, N, 0, 0, 0, nullptr};
     gt[(2 * NSIT + 2) * stride] = GemmT{P, M, pb.eA1, pb.Dm, N, pb.eOne + 1, Af, M, pb.eA1, P, eAcols, M, N, N, 0, 0, 0, zerr};
   }
+  // refinement sweeps (R22): at 4 digits between Newton-Schulz iterations 0 and 1 on X_1 (the
+  // output of iteration 0, in Xn = Xb), at 7 digits between iterations 1 and 2 on X_2 (in Xa):
+  // A_t = Theta' X into Af at A_1's exponent, G = A_t^H A_t into D's buffer (free between the
+  // iterations); each sweep rotates its X in place
+  for (int k = 3; k < 7; ++k) gt[(2 * NSIT + k) * stride] = none;
+  if (use_xsweep() && N >= XS_MIN_N) {
+    int32_t* X1 = pb.Xb;
+    int gh = 1;
+    while ((1 << (gh - 1)) < M) ++gh;
+    for (int w = 0; w < 2; ++w) {
+      gt[(2 * NSIT + 3 + 2 * w) * stride] =
+          GemmT{A0, M, eA0, w ? pb.Xa : X1, N, pb.eOne, Af, M, pb.eA1, nullptr, nullptr, M, N, N, 0, 0, 0, nullptr};
+      GemmT g{Af, M, pb.eA1, Af, M, pb.eA1, pb.Dm, N, nullptr, nullptr, nullptr, N, N, M, 1, 0, 0, nullptr};
+      g.ghead = gh + 1;  // sum of M products, each |.| < 2^(2 eA1 - 2)
+      g.eCwrite = pb.eG;
+      gt[(2 * NSIT + 4 + 2 * w) * stride] = g;
+    }
+    pi->X1 = X1;
+    pi->G = pb.Dm;
+    pi->eG = pb.eG;
+    pi->xs_rec = pb.xs_rec;
+  }
 }
 template <int L>
 inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t stride) {
-  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag, pb.offmax};
+  *pi = PreItem{0, 0, nullptr, nullptr, nullptr, nullptr, pb.rowmax, pb.sweeps_d, nullptr, pb.eOne, pb.eA1, pb.anyflag, pb.offmax,
+                nullptr, nullptr, nullptr, nullptr};
   for (int k = 0; k < pre_slots<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
@@ -338,7 +379,20 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   constexpr int KL = NSIT - 1;  // last iteration: lg = L
   static_assert(NsSched<L>::lg[KL] == L, "the last Newton-Schulz iteration is at full precision");
   nl += run_ns_iter<L, 0>(dgt, dgt + (size_t)n, n, maxN, gNN, st);
+  const bool xs = use_xsweep() && maxN >= XS_MIN_N;  // refinement sweeps (R22); items without them
+                                                       // have empty descriptors
+  if (xs) {
+    nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 3) * n, n, maxM, maxN, maxN, gMN, st);
+    nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 4) * n, n, maxN, maxN, maxM, gNN, st);
+    nl += launch_xsweep<L, 4>(dpre, n, maxN, 0, st);
+  }
   nl += run_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, n, maxN, gNN, st);
+  if (xs) {
+    static_assert(NsSched<L>::lg[1] == 7, "X_2 holds 7 digits");
+    nl += run_gemm<L, 7, 0>(dgt + (size_t)(2 * NSIT + 5) * n, n, maxM, maxN, maxN, gMN, st);
+    nl += run_gemm<L, 7, 0>(dgt + (size_t)(2 * NSIT + 6) * n, n, maxN, maxN, maxM, gNN, st);
+    nl += launch_xsweep<L, 7>(dpre, n, maxN, 1, st);
+  }
   if constexpr (NSIT > 3) nl += run_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, n, maxN, gNN, st);
   const GemmT* dD = dgt + (size_t)(2 * KL) * n;
   const GemmT* dX = dgt + (size_t)(2 * KL + 1) * n;
@@ -773,6 +827,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, pb1 ? rec.A0a : A1, pb1 ? PB1.eMix : S1.eA,
                   M1, N1};
   const size_t d_pre1 = 5120, d_gt1 = 5376;
+  static_assert(5120 + sizeof(PreItem) <= 5376 && 5376 + sizeof(GemmT) * pre_slots<L>() <= 8192, "stage-1 descriptors");
   const bool p_route1 = !force_accumulate_v() && !a.accumulate_v;  // V recovered: fold the last X update
   if (pb1) pre_descs<L>(PB1, M1, N1, rec.A0a, PB1.eMix, A1, S1.eA, a.redo, (PreItem*)(hd.data() + d_pre1),
                         (GemmT*)(hd.data() + d_gt1), 1, p_route1);
@@ -884,6 +939,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   const PreBufs<L> PB2 = rec.P2();
   if (pb2 && !recover) { si.V = PB2.Xfin(); si.v_preset = 1; }
   const size_t d_pre2 = 13312, d_gt2 = 13568;
+  static_assert(13312 + sizeof(PreItem) <= 13568 && 13568 + sizeof(GemmT) * pre_slots<L>() <= 16384, "stage-2 descriptors");
   if (pb2) pre_descs<L>(PB2, M2, N2, rec.A0b, rec.eA0b, A2, S2.eA, a.redo, (PreItem*)(hd.data() + d_pre2),
                         (GemmT*)(hd.data() + d_gt2), 1);
   hs[0] = si;

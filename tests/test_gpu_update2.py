@@ -109,4 +109,4 @@ def test_update_parity(p, chi, chi_max):
             d = max(abs(Pg[r][c] - Pw[r][c]) for r in range(N) for c in range(N))
             s = max(abs(Pw[r][c]) for r in range(N) for c in range(N))
             assert d / s <= tau(p), (b, d / s)
-        assert 3 <= got["sweeps"][b] <= 40
+        assert 1 <= got["sweeps"][b] <= 40  # R22: the refined basis leaves 1-2 p-bit sweeps

@@ -8,6 +8,8 @@ parity tests in a subprocess with a debug switch (the switches are read once per
                        of the certified stop (R21)
   MPS_TC=0             the 280-bit GemmT products on the IMAD.WIDE kernel k_gemm_t instead of the
                        tensor cores (tcgemm.cuh; the 512-bit tier always uses k_gemm_t)
+  MPS_XSWEEP=0         no 112-bit refinement sweep of the preconditioner's basis between the first
+                       two Newton-Schulz iterations (R22)
   MPS_REDUCED_D=1      is experimental and known to fail the 512-bit echo pin (R20): not tested."""
 import os
 import subprocess
@@ -22,9 +24,10 @@ TESTS = ["tests/test_gpu_update2.py::test_update_parity", "tests/test_gpu_mps.py
          "tests/test_gpu_mps.py::test_truncating_run_vs_oracle_mps"]
 
 
-@pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR", "MPS_NO_CERT", "MPS_TC"])
+@pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR", "MPS_NO_CERT", "MPS_TC",
+                                    "MPS_XSWEEP"])
 def test_path_parity(switch):
-    env = dict(os.environ, **{switch: "0" if switch == "MPS_TC" else "1"})
+    env = dict(os.environ, **{switch: "0" if switch in ("MPS_TC", "MPS_XSWEEP") else "1"})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider"] + TESTS, cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
