@@ -775,9 +775,13 @@ __device__ __forceinline__ void d_pair(const SvdItem<NL>& it, int32_t* wbuf, int
   __syncwarp();
 }
 
-// variants (ZC, ZS): 0 = (0, 0), 1 = (3, 1), 2 = (6, 3), 3 = (10, 6)
-__host__ __device__ constexpr int u_var_zc(int v) { return v == 0 ? 0 : v == 1 ? 3 : v == 2 ? 6 : 10; }
-__host__ __device__ constexpr int u_var_zs(int v) { return v == 0 ? 0 : v == 1 ? 1 : v == 2 ? 3 : 6; }
+// variants (ZC, ZS), 280 bits: 0 = (0, 0), 1 = (3, 1), 2 = (6, 3), 3 = (10, 5); 512 bits: (0, 0),
+// (3, 1), (10, 5), (19, 10).  After the refinement sweeps (R22) the p-bit sweeps rotate by
+// |s| ~ 2^-155 (c = 1 - O(2^-310): no fractional digit) and, at 512 bits, then ~2^-310.
+template <int L>
+__host__ __device__ constexpr int u_var_zc(int v) { return v == 0 ? 0 : v == 1 ? 3 : v == 2 ? (L < 19 ? 6 : 10) : (L < 19 ? L : 19); }
+template <int L>
+__host__ __device__ constexpr int u_var_zs(int v) { return v == 0 ? 0 : v == 1 ? 1 : v == 2 ? (L < 19 ? 3 : 5) : (L < 19 ? 5 : 10); }
 
 // Staging buffers per warp and resident CTAs per SM of k_jacobi.  280 bits: double
 // buffering, 2 CTAs (16 warps, 128 registers).  The alternative of one buffer and 3 CTAs
@@ -1029,9 +1033,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
               const int zc = min(zv[0], zv[5]), zs = min(min(zv[1], zv[2]), min(zv[3], zv[4]));
               const int zcv = zv[6], zsv = min(zv[7], zv[8]);
               for (int v = 3; v >= 1; --v)
-                if (u_var_zc(v) <= zc && u_var_zs(v) <= zs) { varA = v; break; }
+                if (u_var_zc<L>(v) <= zc && u_var_zs<L>(v) <= zs) { varA = v; break; }
               for (int v = 3; v >= 1; --v)
-                if (u_var_zc(v) <= zcv && u_var_zs(v) <= zsv) { varV = v; break; }
+                if (u_var_zc<L>(v) <= zcv && u_var_zs<L>(v) <= zsv) { varV = v; break; }
             }
             if (it.phase_cycles) {  // debug: digit products a leading-zero-aware U would need
               unsigned long long full = 0, need = 0;
@@ -1070,7 +1074,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
               for (int mat = 0; mat < (accV ? 2 : 1); ++mat) {
                 const int v = mat ? varV : varA;
                 for (int o = 0; o < 4; ++o)
-                  nup += P(u_var_zc(v)) + 2 * P(u_var_zs(v)) + L * __popc((ints >> ((mat * 4 + o) * 3)) & 7);
+                  nup += P(u_var_zc<L>(v)) + 2 * P(u_var_zs<L>(v)) + L * __popc((ints >> ((mat * 4 + o) * 3)) & 7);
               }
             }
             if (it.phase_cycles) atomicAdd(&it.phase_cycles[6 + 128 + (sweep < 15 ? sweep : 15) * 4 + varA], 1ull);
@@ -1111,9 +1115,9 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
             const int r = ch * 32 + lane;
             const int var = (flag >> (1 + 2 * mat)) & 3;  // zero-digit variant (U_VARIANTS)
             if (var == 0) u_chunk<L, 0, 0>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
-            else if (var == 1) u_chunk<L, 3, 1>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
-            else if (var == 2) u_chunk<L, 6, 3>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
-            else u_chunk<L, (L < 10 ? L : 10), 6>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else if (var == 1) u_chunk<L, u_var_zc<L>(1), u_var_zs<L>(1)>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else if (var == 2) u_chunk<L, u_var_zc<L>(2), u_var_zs<L>(2)>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
+            else u_chunk<L, u_var_zc<L>(3), u_var_zs<L>(3)>(F, rows, p, q, r, lane, b, wcoef, mat, flag);
             __syncwarp();
             if (JST == 1 && ch + 1 < nch) {
               stage_rows<L>(wbuf, F, rows, p, q, (ch + 1) * 32, rows, lane);
