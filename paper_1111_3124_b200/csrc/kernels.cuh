@@ -95,6 +95,7 @@ struct SvdItem {
   int* cexp;                // null (MPS_NO_CERT=1: the paper's rotation-free stopping sweep), or [6]
                             // scratch of the certified stop (R21): by sweep parity [2k]
                             // max log2 bound of mu^2, [2k+1] of rho^2; [4] out: 1 = ended on it
+  const int* done;          // null, or [1]: 1 = converged by the first-order finish (fo.cuh, R23)
 };
 
 // Sort / truncate / renormalise one SVD result and produce the split outputs.
@@ -806,6 +807,7 @@ __global__ void __launch_bounds__(NTHR, jacobi_min_ctas<L>()) k_jacobi(const Svd
   namespace cg = cooperative_groups;
   const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
   const SvdItem<NL> it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
+  if (it.done && *it.done) return;  // converged by the first-order finish (R23): outputs written
   auto csync = [&]() {
     if (C > 1) cg::this_cluster().sync();
     else __syncthreads();

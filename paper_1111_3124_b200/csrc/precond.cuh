@@ -608,6 +608,7 @@ struct GemmT {
   // column selection: logical column b < *ncols_dev is physical column colmap[b] of B and C
   // (the recovery of V computes only the columns kept by the truncation)
   const int* colmap; const int* ncols_dev;
+  int upper;  // only entries r <= c are needed (tensor-core path: tiles below the diagonal skipped)
 };
 
 // per-column coefficient of the V recovery: 1/alpha_b = m 2^e, m in [0.5, 1) as L+1 digits

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int firs
       for (int e = threadIdx.x; e < TC_M * TC_K; e += 256) {
         const int x = e % TC_M, k = e / TC_M;
         const int r = rt * TC_M + x, kk = kbk * TC_K + k;
-        T[k][x] = (r < it.rows && kk < it.K) ? it.A[((size_t)(kk * 2 + ri) * L + D0 + j) * it.lda + r] : 0;
+        T[k][x] = (r < it.rows && kk < it.K && D0 + j >= 0) ? it.A[((size_t)(kk * 2 + ri) * L + D0 + j) * it.lda + r] : 0;
       }
       __syncthreads();
     }
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int firs
         v = T[k][x];
       } else {  // A stored K x rows, digits contiguous along k: op(A)(r, k) = conj A(k, r)
         const int r = rt * TC_M + x, kk = kbk * TC_K + k;
-        v = (r < it.rows && kk < it.K) ? it.A[((size_t)(r * 2 + ri) * L + D0 + j) * it.lda + kk] : 0;
+        v = (r < it.rows && kk < it.K && D0 + j >= 0) ? it.A[((size_t)(r * 2 + ri) * L + D0 + j) * it.lda + kk] : 0;
         if (ri) v = -v;
       }
       int uu[4];
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
     int32_t carry = 0;
 #pragma unroll
     for (int j = 0; j < LG; ++j) {
-      const int32_t v = ok ? it.B[((size_t)(pc * 2 + ri) * L + D0 + j) * it.ldb + kk] : 0;
+      const int32_t v = (ok && D0 + j >= 0) ? it.B[((size_t)(pc * 2 + ri) * L + D0 + j) * it.ldb + kk] : 0;
       int uu[4];
       tc_digit(v, carry, uu);
 #pragma unroll
@@ -198,10 +198,11 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   const int rt = rest % dm.tilesR, ct = rest / dm.tilesR;
   const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
   if (rt * TC_M >= it.rows || ct * TC_N >= ncols) return;  // CTA-uniform
+  if (it.upper && ct * TC_N + TC_N <= rt * TC_M) return;      // entirely below the diagonal
   const int nkb = (it.K + TC_K - 1) / TC_K;
   extern __shared__ __align__(1024) int8_t tcs[];
-  int8_t* sA = tcs;                              // [S][4096]
-  int8_t* sB = tcs + (size_t)S * TC_ATILE;       // [S][1024]
+  int8_t* sA = tcs - (size_t)SA0 * TC_ATILE;                          // slices [SA0, S), 4096 bytes each
+  int8_t* sB = tcs + (size_t)(S - SA0) * TC_ATILE - (size_t)SB0 * TC_BTILE;  // slices [SB0, SB1), 1024 each
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t started;  // bit j: group d0 + j of the chunk received an MMA
@@ -318,7 +319,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
 // ---------------------------------------------------------------------------- epilogue
 // One thread per output entry: group sums -> LG + 2 int64 digit columns (column d / 4 of the
 // product, shifted by 7 (d % 4) bits) -> gemm_t_store (the IMAD path's rounding and store).
-template <int L, int LG, int ZOUT>
+template <int L, int LG, int ZOUT, int LOUT>
 __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, TcDims dm) {
   constexpr int DLO = tc_dlo<LG>(), NG = tc_ng<LG>();
   const int item = first + blockIdx.y;
@@ -334,6 +335,7 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
   int zbad = 0;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < it.rows * ncols; t += gridDim.x * blockDim.x) {
     const int r = t % it.rows, c = t / it.rows;
+    if (it.upper && r > c) continue;
     int64_t acc[2][LG + 3];
 #pragma unroll
     for (int ri = 0; ri < 2; ++ri) {
@@ -350,7 +352,7 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
     int64_t ar[LG + 2], ai[LG + 2];
 #pragma unroll
     for (int j = 0; j < LG + 2; ++j) { ar[j] = acc[0][j]; ai[j] = acc[1][j]; }
-    gemm_t_store<L, LG, ZOUT>(it, r, c, it.colmap ? it.colmap[c] : c, ar, ai, g, eC, percol, false, zbad);
+    gemm_t_store<LOUT, LG, ZOUT>(it, r, c, it.colmap ? it.colmap[c] : c, ar, ai, g, eC, percol, false, zbad);
   }
   if (zbad && it.zerr) atomicOr(it.zerr, 2);
 }
@@ -358,14 +360,18 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
 // ---------------------------------------------------------------------------- launch
 
 template <int LG, int SA0, int SB0, int SB1>
-constexpr size_t tc_mma_smem() { return (size_t)tc_ns<LG>() * (TC_ATILE + TC_BTILE); }
+constexpr size_t tc_mma_smem() { return (size_t)(tc_ns<LG>() - SA0) * TC_ATILE + (size_t)(SB1 - SB0) * TC_BTILE; }
 
 // C = op(A) B for n items (GemmT on the device) on the tensor cores.  Z / NZA / NZB: known-zero
 // top digits of B / low digits of A / low digits of B (their slices are not multiplied).
 // Returns the number of kernel launches, or -1 when the scratch cannot be allocated (the
 // caller then runs the IMAD kernel).
-template <int L, int LG, int Z, int NZA, int NZB, int ZOUT>
+// LG > L: the operands' LG - L digits below the stored ones are zero (then NZA, NZB >= LG - L);
+// LOUT: digits of C (default L; LOUT = LG keeps the product's full LG-digit rounding).
+template <int L, int LG, int Z, int NZA, int NZB, int ZOUT, int LOUT = L>
 inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int maxK, cudaStream_t st) {
+  static_assert(LG <= L || (NZA >= LG - L && NZB >= LG - L), "zero-padded digits must be skipped");
+  static_assert(LOUT >= LG || LOUT == L, "output digits");
   constexpr int S = tc_ns<LG>(), NG = tc_ng<LG>();
   constexpr int SA0 = 4 * NZA, SB0 = 4 * NZB, SB1 = Z > 0 ? 4 * (LG - Z) : S;
   TcDims dm;
@@ -404,7 +410,7 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
     k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), 128, smem, st>>>(d_items, f, dm);
     check("mma");
     const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
-    k_tc_epi<L, LG, ZOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);
+    k_tc_epi<L, LG, ZOUT, LOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);
     check("epi");
     nl += 4;
   }

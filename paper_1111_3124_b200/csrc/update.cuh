@@ -16,6 +16,7 @@
 #include "precond.cuh"
 #include "tcgemm.cuh"
 #include "xsweep.cuh"
+#include "fo.cuh"
 
 namespace mpsb {
 
@@ -177,6 +178,36 @@ inline bool use_xsweep() {
   return on != 0;
 }
 constexpr int XS_MIN_N = 16;  // smaller items: no refinement sweep
+// the first-order finish (fo.cuh, R23) is on unless MPS_FO=0; it needs the refinement
+// sweeps and the tensor-core GEMMs (its Gram matrices are (L+1)-digit products), 280-bit tier
+inline bool use_fo() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_FO");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0 && use_xsweep() && tc_enabled();
+}
+// per-item buffers of the first-order finish: A_1 (M x N), G (N x N, L + 1 digits), flags
+template <int L>
+inline size_t fo_bytes(int M, int N) {
+  return mat_bytes(M, N, L) + align_up((size_t)N * N * 2 * (L + 1) * 4) + 256;
+}
+// Gram matrix of the first-order finish: (L+1)-digit product of the zero-padded operands,
+// upper triangle (tensor cores only; -1 if their scratch cannot be allocated)
+template <int L>
+inline int run_gram_ext(const GemmT* d, int n, int maxM, int maxN, cudaStream_t st) {
+  return launch_gemm_tc<L, L + 1, 0, 1, 1, 0, L + 1>(d, n, maxN, maxN, maxM, st);
+}
+template <int NL>
+static __global__ void k_fo_fail(const FoItem<NL>* items, int n, int L) {
+  // the Gram GEMM could not run: E = 0 (A_2 = A_1), every item falls back to k_jacobi
+  const FoItem<NL> it = items[blockIdx.y];
+  if (it.N == 0) return;
+  const size_t nw = (size_t)it.N * it.N * 2 * L;
+  for (size_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += gridDim.x * blockDim.x) it.E[w] = 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { *it.ok = 0; *it.done = 0; }
+}
 
 // preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N; for a square
 // item the last X buffer also holds P = A0 X_{n-1}), eMix[N], scalars
@@ -416,7 +447,7 @@ inline size_t upd2_item_bytes(const Upd2Args& a) {
   size_t lr = mat_bytes(2 * a.chiL, a.chiM, L) + mat_bytes(a.chiM, 2 * a.chiR, L);
   size_t r1 = std::max(lr, mat_bytes(M, N, L));
   return r1 + mat_bytes(2 * a.chiL, 2 * a.chiR, L) + mat_bytes(N, N, L) + mat_bytes(M, N, L) +
-         SvdScratch<L, NL>::bytes(N) + 8 * (size_t)N + 512 + pre_bytes<L>(M, N) + 256;
+         SvdScratch<L, NL>::bytes(N) + 8 * (size_t)N + 512 + pre_bytes<L>(M, N) + 256 + fo_bytes<L>(M, N);
 }
 
 // descriptor region of launch_update2 (the redo flags follow it)
@@ -425,7 +456,8 @@ inline size_t upd2_desc_bytes(int n) {
   return align_up(sizeof(PrepItem) * 2 * n) + align_up(sizeof(GemmItem) * n) + align_up(sizeof(MixItem) * n) +
          align_up(sizeof(SvdItem<NL>) * n) + align_up(sizeof(FinItem<NL>) * n) + align_up(sizeof(PreItem) * n) +
          align_up(sizeof(GemmT) * pre_slots<L>() * n) + align_up(sizeof(RecItem<NL>) * n) +
-         align_up(sizeof(GemmT) * n) + align_up(sizeof(GemmT) * n);
+         align_up(sizeof(GemmT) * n) + align_up(sizeof(GemmT) * n) + align_up(sizeof(FoItem<NL>) * n) +
+         align_up(sizeof(GemmT) * 3 * n);
 }
 
 template <class T>
@@ -450,6 +482,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
                d_gt = d_pre + align_up(sizeof(PreItem) * n),
                d_rec = d_gt + align_up(sizeof(GemmT) * pre_slots<L>() * n),
                d_rg = d_rec + align_up(sizeof(RecItem<NL>) * n), d_gc = d_rg + align_up(sizeof(GemmT) * n),
+               d_fo = d_gc + align_up(sizeof(GemmT) * n), d_fogt = d_fo + align_up(sizeof(FoItem<NL>) * n),
                d_end = upd2_desc_bytes<L, NL>(n);
   constexpr int NSIT = ns_iters<L>();
   const bool pre = use_precond();
@@ -460,6 +493,9 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   RecItem<NL>* hrec = (RecItem<NL>*)(hd.data() + d_rec);
   GemmT* hrg = (GemmT*)(hd.data() + d_rg);  // V = Theta'^H A_final diag(1/alpha) (tiled GEMM)
   GemmT* hgc = (GemmT*)(hd.data() + d_gc);  // a1 contraction Theta = L R (tiled GEMM)
+  FoItem<NL>* hfo = (FoItem<NL>*)(hd.data() + d_fo);  // first-order finish (R23)
+  GemmT* hfg = (GemmT*)(hd.data() + d_fogt);          // [3][n]: G_1, A_2 = A_1 (I + E), G_2
+  int n_fo = 0;
   PrepItem* hp = (PrepItem*)(hd.data() + d_prep);
   GemmItem* hg = (GemmItem*)(hd.data() + d_gemm);
   MixItem* hm = (MixItem*)(hd.data() + d_mix);
@@ -495,6 +531,14 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     int32_t* rcoef = PB.rcoef;
     int64_t* rexp = PB.rexp;
     const bool pb = pre && !g.no_precond;
+    // first-order finish (R23): 280-bit tier, preconditioned with refinement sweeps, V recovered
+    const bool fo = L == 10 && pb && use_fo() && N >= XS_MIN_N && !force_accumulate_v() && !g.accumulate_v;
+    char* fob = (char*)PB.xs_rec + xs_rec_bytes(N);
+    fob = (char*)align_up((size_t)fob, 256);
+    int32_t* A1x = (int32_t*)fob;
+    int32_t* Gx = (int32_t*)(fob + mat_bytes(M, N, L));
+    int* foflags = (int*)(fob + mat_bytes(M, N, L) + align_up((size_t)N * N * 2 * (L + 1) * 4));  // ok, done
+    int64_t* eGx = (int64_t*)(foflags + 4);
     int64_t* eL = S.e_misc;
     int64_t* eR = S.e_misc + 1;
     int64_t* eT = S.e_misc + 2;
@@ -514,9 +558,34 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     }
     hm[b] = MixItem{Tf, 2 * chiL, eT, g.U, 2, chiL, chiR, trans ? 1 : 0, pb ? A0f : Af, pb ? eMix : S.eA, M, N};
     if (pre && !pb) pre_skip_descs<L>(PB, hpre + b, hgt + b, n);  // this item skips the preconditioner
-    if (pb)  // V recovered: the last X update is folded into A_1 (P route)
-      pre_descs<L>(PB, M, N, A0f, eMix, Af, S.eA, redo + b, hpre + b, hgt + b, n,
+    if (pb)  // V recovered: the last X update is folded into A_1 (P route); R23 items: A_1 into A1x
+      pre_descs<L>(PB, M, N, A0f, eMix, fo ? A1x : Af, fo ? nullptr : S.eA, redo + b, hpre + b, hgt + b, n,
                    !force_accumulate_v() && !g.accumulate_v);
+    {
+      const GemmT none{nullptr, 1, PB.eOne, nullptr, 1, PB.eOne, nullptr, 1, PB.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
+      FoItem<NL> fi{};
+      hfg[b] = hfg[n + b] = hfg[2 * n + b] = none;
+      if (fo) {
+        int gh = 1;
+        while ((1 << (gh - 1)) < M) ++gh;
+        for (int w = 0; w < 2; ++w) {  // G_1 = A_1^H A_1, G_2 = A_2^H A_2 (upper triangle)
+          GemmT gg{w ? Af : A1x, M, PB.eA1, w ? Af : A1x, M, PB.eA1, Gx, N, nullptr, nullptr, nullptr, N, N, M, 1, 0, 0, nullptr};
+          gg.ghead = gh + 1;
+          gg.eCwrite = eGx;
+          gg.upper = 1;
+          hfg[(2 * w) * n + b] = gg;
+        }
+        // A_2 = A_1 + A_1 E (E: the X buffer the preconditioner no longer needs, exponent 1)
+        int32_t* E = PB.Xfin() == PB.Xa ? PB.Xb : PB.Xa;
+        hfg[n + b] = GemmT{A1x, M, PB.eA1, E, N, PB.eOne, Af, M, PB.eA1, A1x, S.eA, M, N, N, 0, 0, 0, nullptr};
+        fi.M = M; fi.N = N; fi.G = Gx; fi.eG = eGx; fi.E = E; fi.ok = foflags; fi.done = foflags + 1;
+        fi.alpha = S.alpha; fi.negl = S.negl; fi.status = S.status;
+        fi.sweeps = g.sweeps_out ? g.sweeps_out : S.sweeps; fi.rots = S.rots; fi.evals = S.rots + 1;
+        fi.uprod = S.uprod; fi.cexp = use_cert() ? S.cexp : nullptr;
+        ++n_fo;
+      }
+      hfo[b] = fi;
+    }
     SvdItem<NL> si = {};
     si.M = M; si.N = N; si.A = Af; si.eA = S.eA; si.V = Vf; si.alpha = S.alpha; si.gam = S.gam; si.coef = S.coef;
     si.dbg = nullptr; si.rot = S.rot; si.negl = S.negl; si.status = S.status;
@@ -529,6 +598,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     si.e2_hint = pb ? -44 : 0;  // binary64 basis: |gamma|^2 / (alpha_p alpha_q) ~ 2^-44 at sweep 1 (1e-13)
     si.A0 = recover ? A0f : nullptr; si.eA0 = pb ? eMix : S.e_misc + 3; si.eV = eV; si.evals = S.rots + 1;
     si.a0_ready = pb ? 1 : 0;
+    si.done = fo ? foflags + 1 : nullptr;
     if (pb && !recover) { si.V = Xfin; si.v_preset = 1; }  // V = X W
     {
       int gh = 1;
@@ -589,6 +659,29 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
     int maxM = 0, maxN = 0;
     for (int b = 0; b < n; ++b) { maxM = std::max(maxM, hs[b].M); maxN = std::max(maxN, hs[b].N); }
     nl += launch_pre<L>((const PreItem*)(base + d_pre), (const GemmT*)(base + d_gt), n, maxM, maxN, st);
+    if (n_fo > 0) {  // first-order finish (R23)
+      const FoItem<NL>* dfo = (const FoItem<NL>*)(base + d_fo);
+      const GemmT* dfg = (const GemmT*)(base + d_fogt);
+      const size_t fsm = fo_smem<NL>(maxN);
+      smem_optin((const void*)k_fo_coef<L, NL>, (int)fsm);
+      smem_optin((const void*)k_fo_check<L, NL>, (int)fsm);
+      const int tMN = ((maxM + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
+      const int g1 = run_gram_ext<L>(dfg, n, maxM, maxN, st);
+      if (g1 >= 0) {
+        nl += g1;
+        k_fo_coef<L, NL><<<n, 256, fsm, st>>>(dfo); ++nl;
+      } else {
+        k_fo_fail<NL><<<dim3(64, n), 256, 0, st>>>(dfo, n, L); ++nl;
+      }
+      nl += run_gemm<L, L, 5>(dfg + n, n, maxM, maxN, maxN, dim3(std::min(tMN, 1024), n), st);
+      if (g1 >= 0) {
+        const int g2 = run_gram_ext<L>(dfg + 2 * n, n, maxM, maxN, st);
+        if (g2 >= 0) {
+          nl += g2;
+          k_fo_check<L, NL><<<n, 256, fsm, st>>>(dfo); ++nl;
+        }
+      }
+    }
     if (getenv("MPS_NS_FORCE_ZERR")) {  // test hook: as if every Newton-Schulz zero-digit check failed
       std::vector<int> two(n, 2);
       cudaMemcpyAsync(redo, two.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, st);

@@ -13,4 +13,5 @@ p = int(sys.argv[2]) if len(sys.argv) > 2 else 280
 batch = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 A, B, U = gen.update_batch_inputs(p, chi, batch)
 out = m.update_batch(p, chi, batch, A, B, U, thr=2.0 ** -140)
-print("sweeps", list(out["sweeps"]), "k", list(out["k"]), flush=True)
+import collections
+print("sweeps", dict(collections.Counter(int(x) for x in out["sweeps"])), "k", dict(collections.Counter(int(x) for x in out["k"])), flush=True)
