@@ -31,9 +31,11 @@
 namespace mpsb {
 
 constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
-constexpr int TC_N = 32;   // output columns per CTA = MMA N
+constexpr int TC_N = 64;   // output columns per CTA = MMA N
 constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
-constexpr int TC_GCH = 16;  // slice-weight groups per chunk: 16 accumulators x 32 columns = 512 TMEM columns
+constexpr int TC_GCH = 8;   // slice-weight groups per chunk: 8 accumulators x 64 columns = 512 TMEM columns
+constexpr int TC_SBK = 16;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
+constexpr int TC_STAGE = TC_SBK * 4096 + (TC_SBK + TC_GCH - 1) * TC_N * 32;  // bytes of one stage buffer
 constexpr int TC_ATILE = TC_M * TC_K;  // bytes of one A slice tile
 constexpr int TC_BTILE = TC_N * TC_K;  // bytes of one B slice tile
 
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int firs
 }
 
 // Operand B (K x cols), logical column c = physical column colmap[c] (c < ncols): planes
-// 0 re, 1 im, 2 -im.  Block (tile c, k block) of 32 x 32 entries; 256 threads, 4 entries each.
+// 0 re, 1 im, 2 -im.  Block (tile c, k block) of TC_N x 32 entries; 256 threads.
 template <int L, int LG>
 __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int first, TcDims dm) {
   constexpr int S = tc_ns<LG>(), D0 = L - LG;
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
   const size_t pstride = (size_t)S * sstride;
   int8_t* out = dm.B + blockIdx.z * dm.b_item + (size_t)ri * pstride + ((size_t)ct * dm.kb + kbk) * TC_BTILE;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < TC_N * TC_K / 256; ++i) {
     const int e = threadIdx.x + 256 * i, k = e & 31, x = e >> 5;
     const int c = ct * TC_N + x, kk = kbk * TC_K + k;
     const bool ok = c < ncols && kk < it.K;
@@ -185,7 +187,20 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
 }
 
 // ---------------------------------------------------------------------------- MMA
-// Slice ranges: A s in [SA0, S), B t in [SB0, SB1); groups d = s + t in [DLO, 8 LG].
+__device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\tTCW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra TCW_%=;\n\t}\n" ::"r"(bar), "r"(parity));
+}
+
+// One CTA per 128 x TC_N output tile and plane (re / im of C = Re / Im sum of 2 real products).
+// Slice-weight groups d = s + t in [DLO, 8 LG] are accumulated TC_GCH at a time in TMEM
+// (a chunk).  The MMAs of a chunk are cut into stages (term, k block, block of TC_SBK A slices
+// with the B slices they meet); thread 0 streams the stage tiles into two shared-memory buffers
+// with bulk copies (mbarrier transaction counts) one stage ahead and issues the stage's MMAs,
+// whose tcgen05.commit frees the buffer; after a chunk all warps drain its accumulators to the
+// group-sum scratch (tcgen05.ld).  Slice ranges: A s in [SA0, S), B t in [SB0, SB1).
 template <int LG, int SA0, int SB0, int SB1>
 __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
   constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = 8 * LG;
@@ -200,119 +215,186 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   if (rt * TC_M >= it.rows || ct * TC_N >= ncols) return;  // CTA-uniform
   if (it.upper && ct * TC_N + TC_N <= rt * TC_M) return;      // entirely below the diagonal
   const int nkb = (it.K + TC_K - 1) / TC_K;
-  extern __shared__ __align__(1024) int8_t tcs[];
-  int8_t* sA = tcs - (size_t)SA0 * TC_ATILE;                          // slices [SA0, S), 4096 bytes each
-  int8_t* sB = tcs + (size_t)(S - SA0) * TC_ATILE - (size_t)SB0 * TC_BTILE;  // slices [SB0, SB1), 1024 each
+  extern __shared__ __align__(1024) int8_t tcs[];  // [2][TC_STAGE]
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ uint32_t started;  // bit j: group d0 + j of the chunk received an MMA
+  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(&tmem_base)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar)));
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_full[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_empty[b])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = tmem_base;
-  uint32_t phase = 0;
   const size_t a_s = (size_t)dm.tilesR * dm.kb * TC_ATILE, b_s = (size_t)dm.tilesC * dm.kb * TC_BTILE;
   const int8_t* Ab = dm.A + blockIdx.y * dm.a_item;
   const int8_t* Bb = dm.B + blockIdx.y * dm.b_item;
   int32_t* Gb = (int32_t*)((char*)dm.G + blockIdx.y * dm.g_item);
   const int RRr = dm.tilesR * TC_M, RCc = dm.tilesC * TC_N;
+  // stage enumeration (thread 0): chunk ch, term, k block, A block [s0, s1], B range [t0, t1]
+  struct Stage { int ch, term, kbk, s0, s1, t0, t1; };
+  auto chunk_range = [&](int ch, int& d0, int& d1, int& slo, int& shi) {
+    d0 = DLO + ch * TC_GCH;
+    d1 = min(d0 + TC_GCH - 1, DHI);
+    slo = max(SA0, d0 - (SB1 - 1));
+    shi = min(S - 1, d1 - SB0);
+  };
+  auto chunk_empty = [&](int ch) {  // no slice pair reaches the chunk's groups
+    int d0, d1, slo, shi;
+    chunk_range(ch, d0, d1, slo, shi);
+    return slo > shi;
+  };
+  auto set_ranges = [&](Stage& g) {
+    int d0, d1, slo, shi;
+    chunk_range(g.ch, d0, d1, slo, shi);
+    g.s1 = min(g.s0 + TC_SBK - 1, shi);
+    g.t0 = max(SB0, d0 - g.s1);
+    g.t1 = min(SB1 - 1, d1 - g.s0);
+  };
+  // first stage of the first non-empty chunk at or after ch (false: none)
+  auto chunk_start = [&](Stage& g, int ch) -> bool {
+    while (ch < NCH && chunk_empty(ch)) ++ch;
+    if (ch >= NCH) return false;
+    int d0, d1, slo, shi;
+    chunk_range(ch, d0, d1, slo, shi);
+    g.ch = ch; g.term = 0; g.kbk = 0; g.s0 = slo;
+    set_ranges(g);
+    return true;
+  };
+  // advance a stage cursor; returns false past the last stage
+  auto next_stage = [&](Stage& g) -> bool {
+    int d0, d1, slo, shi;
+    chunk_range(g.ch, d0, d1, slo, shi);
+    g.s0 += TC_SBK;
+    if (g.s0 > shi) {
+      g.s0 = slo;
+      if (++g.kbk >= nkb) {
+        g.kbk = 0;
+        if (++g.term >= 2) return chunk_start(g, g.ch + 1);
+      }
+    }
+    set_ranges(g);
+    return true;
+  };
+  // bulk copies of stage g into buffer b (A tiles at [0, 64 KB), B tiles after)
+  auto load_stage = [&](const Stage& g, int b) {
+    const int ap = g.term, bp = plane == 0 ? (g.term == 0 ? 0 : 2) : (g.term == 0 ? 1 : 0);
+    const int8_t* Ap = Ab + (size_t)ap * S * a_s + ((size_t)rt * dm.kb + g.kbk) * TC_ATILE;
+    const int8_t* Bp = Bb + (size_t)bp * S * b_s + ((size_t)ct * dm.kb + g.kbk) * TC_BTILE;
+    const uint32_t bytes = (uint32_t)((g.s1 - g.s0 + 1) * TC_ATILE + (g.t1 - g.t0 + 1) * TC_BTILE);
+    const uint32_t fb = tc_smem(&bar_full[b]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(bytes));
+    int8_t* buf = tcs + (size_t)b * TC_STAGE;
+    for (int s = g.s0; s <= g.s1; ++s)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       tc_smem(buf + (size_t)(s - g.s0) * TC_ATILE)),
+                   "l"(Ap + (size_t)s * a_s), "n"(TC_ATILE), "r"(fb)
+                   : "memory");
+    int8_t* bbuf = buf + TC_SBK * TC_ATILE;
+    for (int t = g.t0; t <= g.t1; ++t)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                       tc_smem(bbuf + (size_t)(t - g.t0) * TC_BTILE)),
+                   "l"(Bp + (size_t)t * b_s), "n"(TC_BTILE), "r"(fb)
+                   : "memory");
+  };
+  Stage cur, nxt;
+  int i = 0;             // stage index (thread 0)
+  bool more = false;     // nxt valid
+  uint32_t started = 0;  // bit j: group d0 + j of the current chunk received an MMA
+  if (tid == 0 && chunk_start(cur, 0)) {
+    load_stage(cur, 0);
+    nxt = cur;
+    more = next_stage(nxt);
+  }
   for (int ch = 0; ch < NCH; ++ch) {
-    const int d0 = DLO + ch * TC_GCH, d1 = min(d0 + TC_GCH - 1, DHI);
-    // slices any pair of this chunk uses
-    const int sa_lo = max(SA0, d0 - (SB1 - 1)), sb_lo = max(SB0, d0 - (S - 1));
-    if (tid == 0) started = 0u;
-    for (int term = 0; term < 2; ++term) {
-      // Re: Ar Br + Ai (-Bi); Im: Ar Bi + Ai Br
-      const int ap = term, bp = plane == 0 ? (term == 0 ? 0 : 2) : (term == 0 ? 1 : 0);
-      const int8_t* Ap = Ab + (size_t)ap * S * a_s + (size_t)rt * dm.kb * TC_ATILE;
-      const int8_t* Bp = Bb + (size_t)bp * S * b_s + (size_t)ct * dm.kb * TC_BTILE;
-      for (int kbk = 0; kbk < nkb; ++kbk) {
-        // stage the slice tiles (straight 16-byte copies: the global layout is the tile layout)
-        const int na = (S - sa_lo) * (TC_ATILE / 16), nb = (SB1 - sb_lo) * (TC_BTILE / 16);
-        for (int w = tid; w < na && !(dm.bisect & 4); w += 128) {
-          const int s = sa_lo + w / (TC_ATILE / 16), o = (w % (TC_ATILE / 16)) * 16;
-          cp_async16(sA + (size_t)s * TC_ATILE + o, Ap + (size_t)s * a_s + (size_t)kbk * TC_ATILE + o, 16);
+    int d0, d1, slo, shi;
+    chunk_range(ch, d0, d1, slo, shi);
+    if (tid == 0) started = 0;
+    if (tid == 0 && slo <= shi) {
+      while (true) {
+        const int b = i & 1;
+        // prefetch stage i + 1 into the other buffer once the MMAs of stage i - 1 released it
+        if (more) {
+          if (i >= 1) tc_mbar_wait(tc_smem(&bar_empty[b ^ 1]), ((i - 1) >> 1) & 1);
+          load_stage(nxt, b ^ 1);
         }
-        for (int w = tid; w < nb && !(dm.bisect & 4); w += 128) {
-          const int t = sb_lo + w / (TC_BTILE / 16), o = (w % (TC_BTILE / 16)) * 16;
-          cp_async16(sB + (size_t)t * TC_BTILE + o, Bp + (size_t)t * b_s + (size_t)kbk * TC_BTILE + o, 16);
-        }
-        cp_commit();
-        cp_wait<0>();
-        asm volatile("fence.proxy.async.shared::cta;\n");
-        __syncthreads();
-        if (tid == 0 && !(dm.bisect & 1)) {
-          asm volatile("tcgen05.fence::after_thread_sync;\n");
-          uint32_t st = started;
-          // A slice outer, group inner: consecutive MMAs go to different accumulators
-          for (int s = sa_lo; s < S; ++s) {
-            const uint64_t da = tc_desc(tc_smem(sA + (size_t)s * TC_ATILE));
-            const int dlo = max(d0, s + sb_lo), dhi = min(d1, s + SB1 - 1);
-            for (int d = dlo; d <= dhi; ++d) {
-              const int t = d - s;
-              const uint32_t acc_addr = tmem + (uint32_t)((d - d0) * TC_N);
-              const uint64_t db = tc_desc(tc_smem(sB + (size_t)t * TC_BTILE));
-              const uint32_t acc = (st >> (d - d0)) & 1u;
+        tc_mbar_wait(tc_smem(&bar_full[b]), (i >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const int8_t* buf = tcs + (size_t)b * TC_STAGE;
+        const int8_t* bbuf = buf + TC_SBK * TC_ATILE;
+        for (int s = cur.s0; s <= cur.s1; ++s) {
+          const uint64_t da = tc_desc(tc_smem(buf + (size_t)(s - cur.s0) * TC_ATILE));
+          const int dlo = max(d0, s + cur.t0), dhi = min(d1, s + cur.t1);
+          for (int d = dlo; d <= dhi; ++d) {
+            const int t = d - s;
+            const uint32_t acc_addr = tmem + (uint32_t)((d - d0) * TC_N);
+            const uint64_t db = tc_desc(tc_smem(bbuf + (size_t)(t - cur.t0) * TC_BTILE));
+            const uint32_t acc = (started >> (d - d0)) & 1u;
+            if (!(dm.bisect & 1))
               asm volatile(
                   "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                   "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
                   "l"(da), "l"(db), "r"(IDESC), "r"(acc));
-              st |= 1u << (d - d0);
-              if (dm.bisect & 8) break;
-            }
-            if (dm.bisect & 8) break;
+            started |= 1u << (d - d0);
           }
-          started = st;
-          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tc_smem(&bar)));
         }
-        // the MMAs read the staged tiles: wait before they are overwritten (and before the drain)
-        if (!(dm.bisect & 1)) asm volatile(
-            "{\n\t.reg .pred done;\n\tTCW_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
-            "@!done bra TCW_%=;\n\t}\n" ::"r"(tc_smem(&bar)), "r"(phase));
-        if (!(dm.bisect & 1)) phase ^= 1;
-        asm volatile("tcgen05.fence::after_thread_sync;\n");
-        __syncthreads();
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            tc_smem(&bar_empty[b])));
+        const bool last_of_chunk = !more || nxt.ch != ch;
+        ++i;
+        if (more) {
+          cur = nxt;
+          more = next_stage(nxt);
+        }
+        if (last_of_chunk) {
+          tc_mbar_wait(tc_smem(&bar_empty[b]), ((i - 1) >> 1) & 1);  // every MMA of the chunk is done
+          break;
+        }
       }
     }
-    // drain: warp w reads TMEM lanes 32w .. 32w + 31 (rows), 32 columns per group
-    const uint32_t st = started;
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    __shared__ uint32_t s_started;
+    if (tid == 0) s_started = started;
+    __syncthreads();
+    const uint32_t stg = s_started;
+    // drain: warp w reads TMEM lanes 32w .. 32w + 31 (rows), TC_N columns per group
     const int row = rt * TC_M + 32 * warp + lane;
     for (int d = d0; d <= d1; ++d) {
-      uint32_t v[32];
-      if (((st >> (d - d0)) & 1u) && !(dm.bisect & 2)) {
-        const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-            "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(addr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0;
-      }
       int32_t* g = Gb + (((size_t)plane * NG + (d - DLO)) * RCc + (size_t)ct * TC_N) * RRr + row;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g[(size_t)j * RRr] = (int32_t)v[j];
+      for (int h = 0; h < TC_N / 32; ++h) {
+        uint32_t v[32];
+        if (((stg >> (d - d0)) & 1u) && !(dm.bisect & 2)) {
+          const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N + 32 * h);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(addr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) g[(size_t)(32 * h + j) * RRr] = (int32_t)v[j];
+      }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     __syncthreads();  // the next chunk's MMAs overwrite the accumulators
-    asm volatile("tcgen05.fence::after_thread_sync;\n");
   }
-  __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
 }
 
@@ -360,7 +442,7 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
 // ---------------------------------------------------------------------------- launch
 
 template <int LG, int SA0, int SB0, int SB1>
-constexpr size_t tc_mma_smem() { return (size_t)(tc_ns<LG>() - SA0) * TC_ATILE + (size_t)(SB1 - SB0) * TC_BTILE; }
+constexpr size_t tc_mma_smem() { return (size_t)2 * TC_STAGE; }
 
 // C = op(A) B for n items (GemmT on the device) on the tensor cores.  Z / NZA / NZB: known-zero
 // top digits of B / low digits of A / low digits of B (their slices are not multiplied).
