@@ -187,6 +187,12 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
 }
 
 // ---------------------------------------------------------------------------- MMA
+// 1 in exactly one lane of the (converged) warp
+__device__ __forceinline__ uint32_t tc_elect() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}\n" : "=r"(e));
+  return e;
+}
 __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred done;\n\tTCW_%=:\n\t"
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
     const int8_t* Bp = Bb + (size_t)bp * S * b_s + ((size_t)ct * dm.kb + g.kbk) * TC_BTILE;
     const uint32_t bytes = (uint32_t)((g.s1 - g.s0 + 1) * TC_ATILE + (g.t1 - g.t0 + 1) * TC_BTILE);
     const uint32_t fb = tc_smem(&bar_full[b]);
+    if (!tc_elect()) return;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(bytes));
     int8_t* buf = tcs + (size_t)b * TC_STAGE;
     for (int s = g.s0; s <= g.s1; ++s)
@@ -309,7 +316,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   int i = 0;             // stage index (thread 0)
   bool more = false;     // nxt valid
   uint32_t started = 0;  // bit j: group d0 + j of the current chunk received an MMA
-  if (tid == 0 && chunk_start(cur, 0)) {
+  if (warp == 0 && chunk_start(cur, 0)) {  // warp 0 runs the pipeline (uniform values, elected issue)
     load_stage(cur, 0);
     nxt = cur;
     more = next_stage(nxt);
@@ -317,8 +324,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   for (int ch = 0; ch < NCH; ++ch) {
     int d0, d1, slo, shi;
     chunk_range(ch, d0, d1, slo, shi);
-    if (tid == 0) started = 0;
-    if (tid == 0 && slo <= shi) {
+    started = 0;
+    if (warp == 0 && slo <= shi) {
       while (true) {
         const int b = i & 1;
         // prefetch stage i + 1 into the other buffer once the MMAs of stage i - 1 released it
@@ -340,14 +347,16 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
             const uint32_t acc = (started >> (d - d0)) & 1u;
             if (!(dm.bisect & 1))
               asm volatile(
-                  "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
+                  "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                  "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
                   "l"(da), "l"(db), "r"(IDESC), "r"(acc));
             started |= 1u << (d - d0);
           }
         }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            tc_smem(&bar_empty[b])));
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+                tc_smem(&bar_empty[b])));
         const bool last_of_chunk = !more || nxt.ch != ch;
         ++i;
         if (more) {
