@@ -205,7 +205,8 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
 // (a chunk).  The MMAs of a chunk are cut into stages (term, k block, block of TC_SBK A slices
 // with the B slices they meet); thread 0 streams the stage tiles into two shared-memory buffers
 // with bulk copies (mbarrier transaction counts) one stage ahead and issues the stage's MMAs,
-// whose tcgen05.commit frees the buffer; after a chunk all warps drain its accumulators to the
+// whose tcgen05.commit frees the buffer (the next stage is loaded right after a stage's MMAs are
+// issued, into the buffer the previous stage's MMAs release); after a chunk all warps drain its accumulators to the
 // group-sum scratch (tcgen05.ld).  Slice ranges: A s in [SA0, S), B t in [SB0, SB1).
 template <int LG, int SA0, int SB0, int SB1>
 __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_full[b])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_empty[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(tc_smem(&bar_empty[b])));  // one commit per warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
@@ -297,7 +298,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
     const int8_t* Bp = Bb + (size_t)bp * S * b_s + ((size_t)ct * dm.kb + g.kbk) * TC_BTILE;
     const uint32_t bytes = (uint32_t)((g.s1 - g.s0 + 1) * TC_ATILE + (g.t1 - g.t0 + 1) * TC_BTILE);
     const uint32_t fb = tc_smem(&bar_full[b]);
-    if (!tc_elect()) return;
+    if (warp != 0 || !tc_elect()) return;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(bytes));
     int8_t* buf = tcs + (size_t)b * TC_STAGE;
     for (int s = g.s0; s <= g.s1; ++s)
@@ -316,7 +317,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   int i = 0;             // stage index (thread 0)
   bool more = false;     // nxt valid
   uint32_t started = 0;  // bit j: group d0 + j of the current chunk received an MMA
-  if (warp == 0 && chunk_start(cur, 0)) {  // warp 0 runs the pipeline (uniform values, elected issue)
+  // every warp follows the stage sequence (warp-uniform values, elect.sync-predicated issue): warp 0
+  // also streams the tiles; warp w issues the MMAs of the chunk's groups d0 + 2w, d0 + 2w + 1
+  if (chunk_start(cur, 0)) {
     load_stage(cur, 0);
     nxt = cur;
     more = next_stage(nxt);
@@ -325,21 +328,18 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
     int d0, d1, slo, shi;
     chunk_range(ch, d0, d1, slo, shi);
     started = 0;
-    if (warp == 0 && slo <= shi) {
+    __shared__ uint32_t s_started;
+    if (tid == 0) s_started = 0;
+    if (slo <= shi) {
       while (true) {
         const int b = i & 1;
-        // prefetch stage i + 1 into the other buffer once the MMAs of stage i - 1 released it
-        if (more) {
-          if (i >= 1) tc_mbar_wait(tc_smem(&bar_empty[b ^ 1]), ((i - 1) >> 1) & 1);
-          load_stage(nxt, b ^ 1);
-        }
         tc_mbar_wait(tc_smem(&bar_full[b]), (i >> 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const int8_t* buf = tcs + (size_t)b * TC_STAGE;
         const int8_t* bbuf = buf + TC_SBK * TC_ATILE;
         for (int s = cur.s0; s <= cur.s1; ++s) {
           const uint64_t da = tc_desc(tc_smem(buf + (size_t)(s - cur.s0) * TC_ATILE));
-          const int dlo = max(d0, s + cur.t0), dhi = min(d1, s + cur.t1);
+          const int dlo = max(d0 + 2 * warp, s + cur.t0), dhi = min(min(d1, d0 + 2 * warp + 1), s + cur.t1);
           for (int d = dlo; d <= dhi; ++d) {
             const int t = d - s;
             const uint32_t acc_addr = tmem + (uint32_t)((d - d0) * TC_N);
@@ -357,6 +357,12 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
             "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
                 tc_smem(&bar_empty[b])));
+        // prefetch stage i + 1 into the other buffer once the MMAs of stage i - 1 released it (the
+        // MMAs of stage i are queued behind them, so the tensor pipe does not drain)
+        if (more) {
+          if (i >= 1) tc_mbar_wait(tc_smem(&bar_empty[b ^ 1]), ((i - 1) >> 1) & 1);
+          load_stage(nxt, b ^ 1);
+        }
         const bool last_of_chunk = !more || nxt.ch != ch;
         ++i;
         if (more) {
@@ -369,11 +375,9 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
         }
       }
     }
+    if (lane == 0) atomicOr(&s_started, started);
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
-    __shared__ uint32_t s_started;
-    if (tid == 0) s_started = started;
-    __syncthreads();
     const uint32_t stg = s_started;
     // drain: warp w reads TMEM lanes 32w .. 32w + 31 (rows), TC_N columns per group
     const int row = rt * TC_M + 32 * warp + lane;
