@@ -34,6 +34,7 @@ constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
 constexpr int TC_N = 64;   // output columns per CTA = MMA N
 constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
 constexpr int TC_GCH = 8;   // slice-weight groups per chunk: 8 accumulators x 64 columns = 512 TMEM columns
+constexpr int TC_WARPS = 8;  // warps of k_tc_mma: warp w issues the MMAs of group d0 + w of a chunk
 constexpr int TC_SBK = 16;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
 constexpr int TC_STAGE = TC_SBK * 4096 + (TC_SBK + TC_GCH - 1) * TC_N * 32;  // bytes of one stage buffer
 constexpr int TC_ATILE = TC_M * TC_K;  // bytes of one A slice tile
@@ -209,7 +210,7 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
 // issued, into the buffer the previous stage's MMAs release); after a chunk all warps drain its accumulators to the
 // group-sum scratch (tcgen05.ld).  Slice ranges: A s in [SA0, S), B t in [SB0, SB1).
 template <int LG, int SA0, int SB0, int SB1>
-__global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
+__global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
   constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = 8 * LG;
   constexpr int NCH = (NG + TC_GCH - 1) / TC_GCH;
   constexpr uint32_t IDESC = tc_idesc(TC_M, TC_N);
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_full[b])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;\n" ::"r"(tc_smem(&bar_empty[b])));  // one commit per warp
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tc_smem(&bar_empty[b])), "n"(TC_WARPS));  // one commit per warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n");
   }
@@ -339,7 +340,8 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
         const int8_t* bbuf = buf + TC_SBK * TC_ATILE;
         for (int s = cur.s0; s <= cur.s1; ++s) {
           const uint64_t da = tc_desc(tc_smem(buf + (size_t)(s - cur.s0) * TC_ATILE));
-          const int dlo = max(d0 + 2 * warp, s + cur.t0), dhi = min(min(d1, d0 + 2 * warp + 1), s + cur.t1);
+          const int dlo = max(d0 + warp * (TC_GCH / TC_WARPS), s + cur.t0),
+                    dhi = min(min(d1, d0 + (warp + 1) * (TC_GCH / TC_WARPS) - 1), s + cur.t1);
           for (int d = dlo; d <= dhi; ++d) {
             const int t = d - s;
             const uint32_t acc_addr = tmem + (uint32_t)((d - d0) * TC_N);
@@ -379,15 +381,15 @@ __global__ void __launch_bounds__(128, 1) k_tc_mma(const GemmT* items, int first
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t stg = s_started;
-    // drain: warp w reads TMEM lanes 32w .. 32w + 31 (rows), TC_N columns per group
-    const int row = rt * TC_M + 32 * warp + lane;
-    for (int d = d0; d <= d1; ++d) {
+    // drain: warp w reads TMEM lanes 32 (w % 4) .. + 31 (rows) of groups d0 + w / 4, + 2, ...
+    const int row = rt * TC_M + 32 * (warp & 3) + lane;
+    for (int d = d0 + (warp >> 2); d <= d1; d += TC_WARPS / 4) {
       int32_t* g = Gb + (((size_t)plane * NG + (d - DLO)) * RCc + (size_t)ct * TC_N) * RRr + row;
 #pragma unroll
       for (int h = 0; h < TC_N / 32; ++h) {
         uint32_t v[32];
         if (((stg >> (d - d0)) & 1u) && !(dm.bisect & 2)) {
-          const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N + 32 * h);
+          const uint32_t addr = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((d - d0) * TC_N + 32 * h);
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
               "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
@@ -502,7 +504,7 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
     check("slice_a");
     k_tc_slice_b<L, LG><<<dim3(dm.tilesC * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
     check("slice_b");
-    k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), 128, smem, st>>>(d_items, f, dm);
+    k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), TC_WARPS * 32, smem, st>>>(d_items, f, dm);
     check("mma");
     const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
     k_tc_epi<L, LG, ZOUT, LOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);
