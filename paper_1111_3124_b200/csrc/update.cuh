@@ -178,6 +178,10 @@ inline bool use_xsweep() {
   return on != 0;
 }
 constexpr int XS_MIN_N = 16;  // smaller items: no refinement sweep
+#ifndef XS2_D
+#define XS2_D 7  // digits of the second refinement sweep (6 measured: G resolves gamma to ~2^-156 of alpha only,
+               // the sweep then ends at rho ~ 2^-140 and the first-order finish does not apply)
+#endif
 // the first-order finish (fo.cuh, R23) is on unless MPS_FO=0; it needs the refinement
 // sweeps and the tensor-core GEMMs (its Gram matrices are (L+1)-digit products), 280-bit tier
 inline bool use_fo() {
@@ -419,10 +423,12 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   }
   nl += run_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, n, maxN, gNN, st);
   if (xs) {
-    static_assert(NsSched<L>::lg[1] == 7, "X_2 holds 7 digits");
-    nl += run_gemm<L, 7, 0>(dgt + (size_t)(2 * NSIT + 5) * n, n, maxM, maxN, maxN, gMN, st);
-    nl += run_gemm<L, 7, 0>(dgt + (size_t)(2 * NSIT + 6) * n, n, maxN, maxN, maxM, gNN, st);
-    nl += launch_xsweep<L, 7>(dpre, n, maxN, 1, st);
+    // X_2 holds 7 digits; the sweep works on its top XS2_D (its 7th is dropped: X_2 then stays
+    // unitary to 2^-168, which the last Newton-Schulz iteration squares away)
+    static_assert(NsSched<L>::lg[1] == 7 && XS2_D <= 7, "X_2 holds 7 digits");
+    nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 5) * n, n, maxM, maxN, maxN, gMN, st);
+    nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 6) * n, n, maxN, maxN, maxM, gNN, st);
+    nl += launch_xsweep<L, XS2_D>(dpre, n, maxN, 1, st);
   }
   if constexpr (NSIT > 3) nl += run_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, n, maxN, gNN, st);
   const GemmT* dD = dgt + (size_t)(2 * KL) * n;

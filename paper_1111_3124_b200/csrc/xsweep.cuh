@@ -28,7 +28,7 @@ namespace mpsb {
 // Per item (PreItem fields): X1 (= Xb) and X (= Xa) = N x N fixed (L stored digits, the top XD
 // significant), exponent 1, rotated in place; G = N x N fixed (top XD digits), Hermitian, block
 // exponent *eG; xs_rec = [N - 1][N / 2] rotation records (k_xs_params).
-// records of the widest sweep (7 digits: 112 bytes per pair)
+// records of the widest sweep (7 digits: 112 bytes per pair; 6 digits use the same padding)
 inline size_t xs_rec_bytes(int N) { return align_up((size_t)112 * (N / 2) * (N > 1 ? N - 1 : 0)); }
 
 // ---------------------------------------------------------------------------- double-double
@@ -82,8 +82,8 @@ __device__ __forceinline__ dd dd_scale(dd a, int e) { return {ldexp(a.hi, e), ld
 template <int XD> struct XsT {
   static constexpr int P = (XD + 3) / 4 * 4;
   static constexpr int REC = 3 * P + 4;
-  static constexpr int ZC = XD == 4 ? 3 : 5;
-  static constexpr int ZS = XD == 4 ? 1 : 2;
+  static constexpr int ZC = XD == 4 ? 3 : 5;  // |c - 1| ~ 2^-86 (4 digits), ~2^-141 (6, 7 digits)
+  static constexpr int ZS = XD == 4 ? 1 : 2;  // |s| ~ 2^-40, ~2^-70
 };
 
 // add the integer-valued double x (|x| < 2^(28 XD)) to the digit columns D (28-bit weights)
@@ -235,55 +235,92 @@ __device__ __forceinline__ void xs_mul(int64_t (&acc)[XD + 2], const int32_t* K,
       if (i + j >= XD - 2) acc[i + j - (XD - 2)] = madw(SUB ? -K[i] : K[i], x[j], acc[i + j - (XD - 2)]);
 }
 
-// one output: x0 + cf x0 +/- K1 x1 +/- K2 x2
-template <int XD, int ZC, int ZS, bool S1, bool S2>
-__device__ __forceinline__ void xs_out(const int32_t* cf, const int32_t* K1, const int32_t* K2, const int32_t* x0,
-                                       const int32_t* x1, const int32_t* x2, int32_t* y) {
-  int64_t acc[XD + 2];
+// Rotation of one row entry pair with Gauss's three-product complex multiplies:
+//   y_p = c x_p - conj(s) x_q:  re = x_rp + cf x_rp - T1 - si (x_rq + x_iq)
+//                               im = x_ip + cf x_ip - T1 - sr (x_iq - x_rq),   T1 = x_rq (sr - si)
+//   y_q = c x_q + s x_p:        re = x_rq + cf x_rq + T2 - si (x_rp + x_ip)
+//                               im = x_iq + cf x_iq + T2 + sr (x_ip - x_rp),   T2 = x_rp (sr + si)
+// (c = 1 + cf; rc = [cf | sr | si]).  Digit-wise sums and differences stay below 2^28 (products
+// below 2^56) and keep the known-zero top digits of s.
+template <int XD, int ZC>
+__device__ __forceinline__ void xs_out(int64_t (&acc)[XD + 2], const int64_t (&T)[XD + 2], bool Tneg,
+                                       const int32_t* cf, const int32_t* x0, int32_t* y) {
 #pragma unroll
-  for (int c = 0; c < 2; ++c) acc[c] = 0;
+  for (int c = 0; c < XD + 2; ++c) acc[c] = Tneg ? acc[c] - T[c] : acc[c] + T[c];
 #pragma unroll
-  for (int j = 0; j < XD; ++j) acc[j + 2] = x0[j];  // 1 * x0 (the integer digit of c)
+  for (int j = 0; j < XD; ++j) acc[j + 2] += x0[j];  // 1 * x0 (the integer digit of c)
   xs_mul<XD, ZC, false>(acc, cf, x0);
-  xs_mul<XD, ZS, S1>(acc, K1, x1);
-  xs_mul<XD, ZS, S2>(acc, K2, x2);
   int32_t o[XD];
   tround2<XD>(acc, o);
 #pragma unroll
   for (int j = 0; j < XD; ++j) y[j] = o[j];
 }
 
-// y_p = c x_p - conj(s) x_q, y_q = c x_q + s x_p (the V update of k_jacobi); rc = [cf | sr | si]
 template <int XD, int ZC, int ZS>
 __device__ __forceinline__ void xs_rotate(const int32_t* rc, int32_t* xrp, int32_t* xip, int32_t* xrq, int32_t* xiq) {
   constexpr int P = XsT<XD>::P;
   const int32_t *cf = rc, *sr = rc + P, *si = rc + 2 * P;
+  int32_t smi[XD], spl[XD], sq[XD], dq[XD], sp[XD], dp[XD];
+#pragma unroll
+  for (int k = 0; k < XD; ++k) {
+    smi[k] = sr[k] - si[k];
+    spl[k] = sr[k] + si[k];
+    sq[k] = xrq[k] + xiq[k];
+    dq[k] = xiq[k] - xrq[k];
+    sp[k] = xrp[k] + xip[k];
+    dp[k] = xip[k] - xrp[k];
+  }
   int32_t yrp[XD], yip[XD], yrq[XD], yiq[XD];
-  xs_out<XD, ZC, ZS, true, true>(cf, sr, si, xrp, xrq, xiq, yrp);    // c xrp - sr xrq - si xiq
-  xs_out<XD, ZC, ZS, true, false>(cf, sr, si, xip, xiq, xrq, yip);   // c xip - sr xiq + si xrq
-  xs_out<XD, ZC, ZS, false, true>(cf, sr, si, xrq, xrp, xip, yrq);   // c xrq + sr xrp - si xip
-  xs_out<XD, ZC, ZS, false, false>(cf, sr, si, xiq, xip, xrp, yiq);  // c xiq + sr xip + si xrp
+  int64_t T[XD + 2], acc[XD + 2];
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) T[c] = 0;
+  xs_mul<XD, ZS, false>(T, smi, xrq);  // T1
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) acc[c] = 0;
+  xs_mul<XD, ZS, true>(acc, si, sq);
+  xs_out<XD, ZC>(acc, T, true, cf, xrp, yrp);
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) acc[c] = 0;
+  xs_mul<XD, ZS, true>(acc, sr, dq);
+  xs_out<XD, ZC>(acc, T, true, cf, xip, yip);
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) T[c] = 0;
+  xs_mul<XD, ZS, false>(T, spl, xrp);  // T2
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) acc[c] = 0;
+  xs_mul<XD, ZS, true>(acc, si, sp);
+  xs_out<XD, ZC>(acc, T, false, cf, xrq, yrq);
+#pragma unroll
+  for (int c = 0; c < XD + 2; ++c) acc[c] = 0;
+  xs_mul<XD, ZS, false>(acc, sr, dp);
+  xs_out<XD, ZC>(acc, T, false, cf, xiq, yiq);
 #pragma unroll
   for (int j = 0; j < XD; ++j) { xrp[j] = yrp[j]; xip[j] = yip[j]; xrq[j] = yrq[j]; xiq[j] = yiq[j]; }
 }
 
 template <int P>
-__device__ __forceinline__ void xs_ld(const int4* s, int32_t* v) {
+__device__ __forceinline__ void xs_ld(const int4* s, int hs, int32_t* v) {
 #pragma unroll
   for (int k = 0; k < P / 4; ++k) {
-    const int4 t = s[k];
+    const int4 t = s[(size_t)k * hs];
     v[4 * k] = t.x; v[4 * k + 1] = t.y; v[4 * k + 2] = t.z; v[4 * k + 3] = t.w;
   }
 }
 template <int P>
-__device__ __forceinline__ void xs_st(int4* s, const int32_t* v) {
+__device__ __forceinline__ void xs_st(int4* s, int hs, const int32_t* v) {
 #pragma unroll
-  for (int k = 0; k < P / 4; ++k) s[k] = make_int4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  for (int k = 0; k < P / 4; ++k) s[(size_t)k * hs] = make_int4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
 }
+// shared-memory column stride (int4) of k_xs_apply: entry (c, re/im, row r) at c CS + ri R + r,
+// its k-th group of 4 digits at + k N CS.  With 2 groups (XD = 7, R = 4 rows) a warp's 16-byte
+// phase of 8 lanes covers two pairs of 4 rows; a column stride of 192 bytes puts consecutive
+// columns 64 bytes apart modulo 128, so the two pairs hit different banks.
+template <int XD, int R>
+__host__ __device__ constexpr int xs_cs() { return 2 * R + (XsT<XD>::P > 4 ? 4 : 0); }
 
 // Apply the sweep's rotations to rows [R blockIdx.x, + R) of X (sel: see k_xs_params): the rows
-// stay in shared memory, entry (col c, re/im, row r) as P ints (its top XD digits) at
-// int4 [((c 2 + ri) R + r) P / 4]; per step, task t = (pair t / R, row t % R).
+// stay in shared memory, entry (col c, re/im, row r) as P ints (its top XD digits, xs_cs
+// layout); per step, task t = (pair t / R, row t % R).
 template <int L, int XD, int R>
 __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel) {
   using T = XsT<XD>;
@@ -294,7 +331,9 @@ __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel)
   int32_t* X = sel ? it.X : it.X1;
   const int r0 = blockIdx.x * R;
   if (r0 >= N) return;
-  extern __shared__ int4 xs_rows[];  // [N][2][R][Q]
+  extern __shared__ int4 xs_rows[];  // [Q][N][CS]
+  constexpr int CS = xs_cs<XD, R>();
+  const int HS = N * CS;
   for (int t = threadIdx.x; t < N * 2 * R; t += blockDim.x) {
     const int r = t % R, ri = (t / R) % 2, c = t / (2 * R);
     int32_t v[P];
@@ -305,7 +344,7 @@ __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel)
 #pragma unroll
       for (int k = 0; k < XD; ++k) v[k] = g[(size_t)k * N];
     }
-    xs_st<P>(xs_rows + (size_t)t * Q, v);
+    xs_st<P>(xs_rows + (size_t)c * CS + ri * R + r, HS, v);
   }
   __syncthreads();
   for (int step = 0; step < N - 1; ++step) {
@@ -323,19 +362,19 @@ __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel)
         const int4 u = __ldg(&rr[k]);
         rc[4 * k] = u.x; rc[4 * k + 1] = u.y; rc[4 * k + 2] = u.z; rc[4 * k + 3] = u.w;
       }
-      int4* sp = xs_rows + ((size_t)p * 2 * R + r) * Q;
-      int4* sq = xs_rows + ((size_t)q * 2 * R + r) * Q;
+      int4* sp = xs_rows + (size_t)p * CS + r;
+      int4* sq = xs_rows + (size_t)q * CS + r;
       int32_t xrp[P], xip[P], xrq[P], xiq[P];
-      xs_ld<P>(sp, xrp);
-      xs_ld<P>(sp + R * Q, xip);
-      xs_ld<P>(sq, xrq);
-      xs_ld<P>(sq + R * Q, xiq);
+      xs_ld<P>(sp, HS, xrp);
+      xs_ld<P>(sp + R, HS, xip);
+      xs_ld<P>(sq, HS, xrq);
+      xs_ld<P>(sq + R, HS, xiq);
       if (flag & 2) xs_rotate<XD, T::ZC, T::ZS>(rc, xrp, xip, xrq, xiq);
       else xs_rotate<XD, 0, 0>(rc, xrp, xip, xrq, xiq);
-      xs_st<P>(sp, xrp);
-      xs_st<P>(sp + R * Q, xip);
-      xs_st<P>(sq, xrq);
-      xs_st<P>(sq + R * Q, xiq);
+      xs_st<P>(sp, HS, xrp);
+      xs_st<P>(sp + R, HS, xip);
+      xs_st<P>(sq, HS, xrq);
+      xs_st<P>(sq + R, HS, xiq);
     }
     __syncthreads();
   }
@@ -343,15 +382,16 @@ __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel)
     const int r = t % R, ri = (t / R) % 2, c = t / (2 * R);
     if (r0 + r >= N) continue;
     int32_t v[P];
-    xs_ld<P>(xs_rows + (size_t)t * Q, v);
+    xs_ld<P>(xs_rows + (size_t)c * CS + ri * R + r, HS, v);
     int32_t* g = X + ((size_t)(c * 2 + ri) * L + (L - XD)) * N + r0 + r;
 #pragma unroll
     for (int k = 0; k < XD; ++k) g[(size_t)k * N] = v[k];
+    for (int k = 1; k <= L - XD; ++k) g[-(ptrdiff_t)k * N] = 0;  // digits below the sweep's (X_2's 7th)
   }
 }
 
 template <int XD, int R>
-constexpr size_t xs_apply_smem(int N) { return (size_t)N * 2 * R * XsT<XD>::P * 4; }
+constexpr size_t xs_apply_smem(int N) { return (size_t)N * xs_cs<XD, R>() * XsT<XD>::P * 4; }
 
 // the two kernels of one refinement sweep at XD digits for n items (descriptors on the
 // device); sel: which X (see k_xs_params); launch count
