@@ -709,7 +709,11 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   {
     int minN = 1 << 30;
     for (int b = 0; b < n; ++b) minN = std::min(minN, hs[b].N);
-    launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n, minN, jacobi_min_ctas<L>() * 148), st);
+    // when most items took the first-order finish (R23) only the few that failed its check run
+    // here: size the clusters for a handful of active items (the finished ones exit at once)
+    const int n_active = n_fo * 2 >= n ? std::max(1, (n - n_fo) + n_fo / 32) : n;
+    launch_jacobi<L, NL>((const SvdItem<NL>*)(base + d_svd), n, jacobi_cluster_size(n_active, minN, jacobi_min_ctas<L>() * 148),
+                         st);
     ++nl;
   }
   {
