@@ -134,6 +134,9 @@ constexpr int JD_MINB = JD_BS_MAX >= 16 ? 1 : 3;
 #ifndef JD_TOL
 #define JD_TOL (4.0 * M * 1.1102230246251565e-16)  // 4 M 2^-53 (1e-12 costs a p-bit sweep)
 #endif  // one warp per pair of a block pair's inner step (bs <= 16)
+#ifndef JD_CROSS  // 1: block pairs after the first step of a sweep rotate only their cross pairs
+#define JD_CROSS 1
+#endif
 #ifndef JD_GRAM_OFF
 #define JD_GRAM_OFF 1e-6  // Gram-form inner sweeps while max |gamma| / sqrt(alpha_p alpha_q) exceeds this
 #endif
@@ -270,6 +273,16 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
           s_col[l] = (blk < nb && c < N) ? c : -1;
         }
         if (threadIdx.x == 0) { s_rot = 0; s_gram = 0; }
+        // inner pair order: the first step of a sweep (its block pairs cover every block once)
+        // visits all pairs of the 2bs columns (round-robin, 2bs - 1 steps), later steps only the
+        // bs^2 cross pairs (i, bs + (i + s2) % bs), bs steps: every column pair is still met once
+        // per sweep, the pairs inside a block are not re-rotated in each of its nbe - 1 visits
+        const bool cross = JD_CROSS && step > 0;
+        const int nin = cross ? bs : nc2 - 1;
+        auto inner_pair = [&](int s2, int i, int& p, int& q) {
+          if (cross) { p = i; q = bs + (i + s2) % bs; }
+          else rr_pair(nc2, s2, i, p, q);
+        };
         __syncthreads();
         for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {  // (l, r) advance by blockDim
           const int c = s_col[l];  // cp.async: all loads in flight at once (absent columns zero-filled)
@@ -358,11 +371,11 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
         }
         if (s_gram) {
           if (prof) atomicAdd(&jd_prof[6], 1ull);
-          for (int s2 = 0; s2 < nc2 - 1; ++s2) {
+          for (int s2 = 0; s2 < nin; ++s2) {
             if (threadIdx.x < bs) {
               const int i = threadIdx.x;
               int p, q;
-              rr_pair(nc2, s2, i, p, q);
+              inner_pair(s2, i, p, q);
               int on = 0;
               if (s_col[p] >= 0 && s_col[q] >= 0) {
                 const double sp = G[(size_t)p * GL + p].x, sq = G[(size_t)q * GL + q].x;
@@ -426,10 +439,10 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
             __syncthreads();
           }
         } else {
-          for (int s2 = 0; s2 < nc2 - 1; ++s2) {
+          for (int s2 = 0; s2 < nin; ++s2) {
             for (int i = warp; i < bs; i += JD_THREADS / 32) {
               int p, q;
-              rr_pair(nc2, s2, i, p, q);
+              inner_pair(s2, i, p, q);
               if (s_col[p] < 0 || s_col[q] < 0) continue;
               double2* ap = Ab + (size_t)p * MP;
               double2* aq = Ab + (size_t)q * MP;
