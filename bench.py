@@ -57,47 +57,6 @@ def parse():
     return ap.parse_args()
 
 
-def jacobi_limb_macs(chi: int, p: int, sweeps) -> float:
-    """Algorithmic limb-MACs of the Jacobi kernel: per item
-    (S-1) N(N-1)/2 (20M + 12N) + N(N-1)/2 8M real multiplies, x L^2 limb-MACs, L = ceil(p/32)."""
-    M = N = 2 * chi
-    L = (p + 31) // 32
-    pairs = N * (N - 1) / 2
-    tot = 0.0
-    for S in sweeps:
-        tot += ((S - 1) * pairs * (20 * M + 12 * N) + pairs * 8 * M) * L * L
-    return tot
-
-
-def trunc_pairs(LG: int, Z: int = 0, NZA: int = 0, NZB: int = 0) -> int:
-    """Digit products of one truncated LG-digit product in k_gemm_t (precond.cuh): digits
-    i >= NZA of A, NZB <= j < LG - Z of B, columns i + j >= LG - 2."""
-    return sum(1 for i in range(NZA, LG) for j in range(NZB, LG - Z) if i + j >= LG - 2)
-
-
-def gemm_imad_wide_per_item(chi: int, p: int) -> float:
-    """IMAD.WIDE of the GEMM kernels of one configs[1] two-site update as they run (DESIGN.md
-    §4): the a1 contraction (k_gemm, three-product complex multiply), the Newton-Schulz
-    iterations (Hermitian D_k: half the tiles; the known-zero low digits of X_k and top digits
-    of D_k skipped), P = Theta' X_{n-1} and A_1 = P + P D/2 (square items whose V is
-    recovered), and the recovery of the chi kept columns of V; 3 real products per complex MAC."""
-    L = 10 if p <= 280 else 19
-    sched = ([(4, 1, 0), (7, 2, 3), (10, 5, 3)] if L == 10 else
-             [(4, 1, 0), (7, 2, 3), (14, 5, 7), (19, 10, 5)])  # (lg, z, nz): NsSched
-    M = N = 2 * chi
-    t = 16
-    herm_out = (N // t) * (N // t + 1) // 2 * t * t  # tiles on / above the diagonal
-    w = (2 * chi) * (2 * chi) * chi * 3 * trunc_pairs(L)  # contraction (K = chi)
-    for k, (LG, Z, NZ) in enumerate(sched):
-        w += herm_out * N * 3 * trunc_pairs(LG, 0, NZ, NZ)  # D_k
-        if k + 1 < len(sched):
-            w += N * N * N * 3 * trunc_pairs(LG, Z, NZ, 0)  # X_{k+1}
-        else:
-            w += M * N * N * 3 * (trunc_pairs(L, 0, 0, NZ) + trunc_pairs(L, Z))  # P, A_1 = P + P D / 2
-    w += N * chi * M * 3 * trunc_pairs(L)  # recovery of the kept columns
-    return float(w)
-
-
 def executed_imad_wide(counts, chi: int, p: int) -> float:
     """IMAD.WIDE the p-bit Jacobi kernel executes: every evaluated pair
     computes gamma (4 truncated real products per row, (L-1) + L(L+1)/2 IMAD.WIDE each: 64
@@ -110,11 +69,6 @@ def executed_imad_wide(counts, chi: int, p: int) -> float:
     per = (L - 1) + L * (L + 1) // 2
     rot, ev, normw, recw, uprods = counts[:5]
     return float(ev * 4 * M + normw * 2) * per + float(uprods)
-
-
-def contraction_limb_macs(chi: int, p: int, n_items: int) -> float:
-    L = (p + 31) // 32
-    return n_items * (16 * chi ** 3 + 64 * chi ** 2) * L * L
 
 
 class ClockSampler:
@@ -378,12 +332,11 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
     ms = e0.elapsed_time(e1)
-    counts = mps.profile_counts(6)
-    jac_ms, jac_n = mps.profile_query(mps.PROF_JACOBI)
-    con_ms, _ = mps.profile_query(mps.PROF_CONTRACT)
-    fin_ms, _ = mps.profile_query(mps.PROF_FINALIZE)
-    pre_ms, _ = mps.profile_query(mps.PROF_PRECOND)
-    rec_ms, _ = mps.profile_query(mps.PROF_RECOVER)
+    counts = mps.profile_counts(8)
+    q = {name: mps.profile_query(k) for name, k in
+         (("jacobi", mps.PROF_JACOBI), ("contraction", mps.PROF_CONTRACT), ("truncate_split", mps.PROF_FINALIZE),
+          ("precondition", mps.PROF_PRECOND), ("recover_v", mps.PROF_RECOVER), ("binary64_jacobi", mps.PROF_JDB),
+          ("refinement_sweeps", mps.PROF_XS), ("tensor_mma", mps.PROF_TCMMA))}
     mps.profile_enable(False)
     if dist is not None:
         t = torch.tensor([ms], device=dev)
@@ -392,29 +345,31 @@ def main():
     total_items = batch * args.steps * world
     value = total_items / (ms / 1e3)
 
-    # roofline of the dominant kernel (Jacobi SVD): algorithmic limb-MACs per launch / launch time
+    # Roofline of the dominant kernel, the binary64 block Jacobi k_jacobi_db (fp64 pipe):
+    # algorithmic DFMA (counted per block-pair visit on the device) over its
+    # launch time (CUDA events on the launching stream), against the measured DFMA peak.
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_INT_PEAKS.json")))
-    peak = peaks["imad_wide_s32_per_s"]
-    credited = jacobi_limb_macs(chi, p, sweeps) * args.steps  # SURVEY §8(d) count, all timed launches
-    # an item that ended on the certified stop (R21) ran S rotating sweeps; the
-    # textbook iteration credits S + 1 sweeps, the last one rotation-free (8M per pair)
-    M_, L_ = 2 * chi, (p + 31) // 32
-    credited += counts[5] * (M_ * (M_ - 1) / 2) * (20 * M_ + 12 * M_) * L_ * L_
-    executed = executed_imad_wide(counts, chi, p)
-    achieved = executed / (jac_ms / 1e3) if jac_ms else None
-    # the whole step: Jacobi + every GEMM kernel over the step time (the binary64 Jacobi and
-    # the O(chi^2) kernels execute no IMAD.WIDE of this kind)
-    step_imad = executed + gemm_imad_wide_per_item(chi, p) * batch * args.steps
-    step_frac = step_imad / (ms / 1e3) / peaks["imad_wide_s32_per_s"] if ms else None
-    credited_rate = credited / (jac_ms / 1e3) if jac_ms else None
+    dfma_peak = peaks["dfma_per_s"]
+    jdb_ms, jdb_n = q["binary64_jacobi"]
+    achieved = counts[mps.CNT_JDB_DFMA] / (jdb_ms / 1e3) if jdb_ms else None
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
-        tj = json.load(open(tfile))
-        key = f"jacobi_chi{chi}_p{p}_batch{batch}"
-        if key in tj:
-            traffic = tj[key]
-
+        traffic = json.load(open(tfile)).get(f"jacobi_db_chi{chi}_p{p}_batch{batch}")
+    # the tensor-core GEMMs (all k_tc_mma launches): int8 MACs issued over their launch time,
+    # against the int8 dense peak = the measured bf16 peak x 2 (nominal 4.5 / 2.25 PFLOP/s) / 2
+    mp_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp_file):
+        i8_peak = json.load(open(mp_file))["bf16_tflops"] * 1e12
+        i8_src = "MEASURED_PEAKS.json bf16_tflops x 2 (int8/bf16) / 2 (MAC = 2 ops)"
+    else:
+        i8_peak = 2.25e15
+        i8_src = "nominal 4.5 POPS int8 dense (B200_PROFILING.md) / 2"
+    tc_ms, tc_n = q["tensor_mma"]
+    tc_rate = counts[mps.CNT_TC_MAC] / (tc_ms / 1e3) if tc_ms else None
+    # the p-bit Jacobi kernel (only the items the first-order finish did not close, R23)
+    jac_ms, jac_n = q["jacobi"]
+    jac_exec = executed_imad_wide(counts, chi, p)
     # end to end through the public C API with host buffers (pinned), one step; the device
     # buffers of the timed path are released first (at 512 bits both sets do not fit in HBM)
     e2e = None
@@ -464,19 +419,27 @@ def main():
             "vs_baseline": None, "dtype": f"int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p={p}",
             "data": "synthetic",
             "config": dict(workload_config(batch, chi, p, nd, world), sweeps_mean=float(np.mean(sweeps))),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "IMAD.WIDE/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_jacobi", "peak_source": "MEASURED_INT_PEAKS.json imad_wide_s32_per_s (IMAD.WIDE)",
-                         "achieved_counts": "executed IMAD.WIDE of the implemented algorithm (DESIGN.md §4)",
-                         "credited_limb_mac_per_s": credited_rate,
-                         "credited_frac": (credited_rate / peak) if credited_rate else None,
-                         "counters": {"rotations": counts[0], "pair_evals": counts[1], "u_digit_products": counts[4],
-                                      "certified_stops": counts[5]},
-                         "kernel_ms_per_launch": jac_ms / jac_n if jac_n else None,
-                         "share_of_step": jac_ms / ms if ms else None,
-                         "step_ms": {"contraction": con_ms, "precondition": pre_ms, "jacobi": jac_ms,
-                                     "recover_v": rec_ms, "truncate_split": fin_ms},
-                         "step_executed_imad_wide_frac": step_frac},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": dfma_peak, "unit": "DFMA/s",
+                         "frac": (achieved / dfma_peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_jacobi_db (binary64 block Jacobi, fp64 pipe)",
+                         "peak_source": "MEASURED_INT_PEAKS.json dfma_per_s (tools/peaks/int_peak.cu)",
+                         "achieved_counts": "algorithmic DFMA per block-pair visit: Gram 4 nc2(nc2+1)/2 M, "
+                                            "inner rotations, W applied to A and V 4 nc2^2 (M + N) (DESIGN.md §4)",
+                         "dfma_per_step": counts[mps.CNT_JDB_DFMA] / args.steps,
+                         "kernel_ms_per_launch": jdb_ms / jdb_n if jdb_n else None,
+                         "share_of_step": jdb_ms / ms if ms else None,
+                         "step_ms": {k: v[0] for k, v in q.items()},
+                         "tensor_gemm": {"bound": "tensor", "achieved": tc_rate, "peak": i8_peak,
+                                         "unit": "int8 MAC/s", "frac": (tc_rate / i8_peak) if tc_rate else None,
+                                         "peak_source": i8_src, "kernel": "k_tc_mma (all launches)",
+                                         "macs_per_step": counts[mps.CNT_TC_MAC] / args.steps,
+                                         "share_of_step": tc_ms / ms if ms else None, "launches": tc_n},
+                         "p_bit_jacobi": {"kernel": "k_jacobi (items not closed by the first-order finish)",
+                                          "executed_imad_wide_per_s": jac_exec / (jac_ms / 1e3) if jac_ms else None,
+                                          "peak": peaks["imad_wide_s32_per_s"],
+                                          "share_of_step": jac_ms / ms if ms else None,
+                                          "counters": {"rotations": counts[0], "pair_evals": counts[1],
+                                                       "u_digit_products": counts[4], "certified_stops": counts[5]}}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

@@ -121,16 +121,16 @@ int mps_profile_enable(int on) {
   }
   g_prof.on = on != 0;
   if (g_prof.on) {
-    if (!g_prof.counts && cudaMalloc(&g_prof.counts, 8 * sizeof(unsigned long long)) != cudaSuccess) return MPS_ENOMEM;
-    cudaMemset(g_prof.counts, 0, 8 * sizeof(unsigned long long));
+    if (!g_prof.counts && cudaMalloc(&g_prof.counts, CNT_N * sizeof(unsigned long long)) != cudaSuccess) return MPS_ENOMEM;
+    cudaMemset(g_prof.counts, 0, CNT_N * sizeof(unsigned long long));
   }
   return MPS_OK;
 }
 
 int mps_profile_counts_n(long long* out, int n) {
-  if (!out || n < 1 || n > 8 || !g_prof.counts) return MPS_EINVAL;
+  if (!out || n < 1 || n > CNT_N || !g_prof.counts) return MPS_EINVAL;
   cudaDeviceSynchronize();
-  unsigned long long h[8];
+  unsigned long long h[CNT_N];
   if (cudaMemcpy(h, g_prof.counts, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) return MPS_ECUDA;
   for (int i = 0; i < n; ++i) out[i] = (long long)h[i];
   return MPS_OK;

@@ -34,6 +34,7 @@ struct PreItem {
   // refinement sweep (xsweep.cuh, R22): X_1 (rotated in place), G = A_t^H A_t and its
   // exponent, the rotation records; X1 == nullptr: no refinement sweep for this item
   int32_t* X1; const int32_t* G; const int64_t* eG; int4* xs_rec;
+  unsigned long long* cnt;  // profiling counters (CNT_*), or null
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -478,6 +479,14 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
           }
         }
         mark(1);
+        if (it.cnt && threadIdx.x == 0) {  // algorithmic DFMA of this visit (bench.py roofline)
+          const unsigned long long nc2u = nc2, Mu = M, Nu = N;
+          unsigned long long f = 0;
+          if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * bs * bs + 8ull * bs * nc2u);
+          else f = (unsigned long long)nin * bs * (16ull * Mu + 8ull * nc2u);
+          if (s_rot) f += 4ull * nc2u * nc2u * (Mu + Nu);
+          atomicAdd(&it.cnt[CNT_JDB_DFMA], f);
+        }
         if (s_rot) {  // block-uniform
           if (threadIdx.x == 0) s_any = 1;
           if (s_gram) {

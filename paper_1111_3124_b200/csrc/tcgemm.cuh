@@ -51,6 +51,7 @@ struct TcDims {
   int8_t* B;                     // [item][plane 3: re, im, -im][S][tilesC][kb][1024]
   int32_t* G;                    // [item][plane 2][NG][tilesC * 32][tilesR * 128]
   int bisect;                    // debug (MPS_TC_BISECT): bit 0 no MMA, bit 1 no drain, bit 2 no staging
+  unsigned long long* cnt;       // profiling counters (CNT_TC_MAC), or null
 };
 
 // byte offset of element (x, k) inside a K-major no-swizzle UMMA tile: core matrices of 8 rows
@@ -318,6 +319,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
   int i = 0;             // stage index (thread 0)
   bool more = false;     // nxt valid
   uint32_t started = 0;  // bit j: group d0 + j of the current chunk received an MMA
+  unsigned long long nmma = 0;  // MMAs this warp issued (profiling)
   // every warp follows the stage sequence (warp-uniform values, elect.sync-predicated issue): warp 0
   // also streams the tiles; warp w issues the MMAs of the chunk's groups d0 + 2w, d0 + 2w + 1
   if (chunk_start(cur, 0)) {
@@ -353,6 +355,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
                   "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(acc_addr),
                   "l"(da), "l"(db), "r"(IDESC), "r"(acc));
             started |= 1u << (d - d0);
+            ++nmma;
           }
         }
         asm volatile(
@@ -411,6 +414,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
     __syncthreads();  // the next chunk's MMAs overwrite the accumulators
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
+  if (dm.cnt && lane == 0 && nmma) atomicAdd(&dm.cnt[CNT_TC_MAC], nmma * (unsigned long long)(TC_M * TC_N * TC_K));
 }
 
 // ---------------------------------------------------------------------------- epilogue
@@ -474,6 +478,7 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
   TcDims dm;
   static const int bis = getenv("MPS_TC_BISECT") ? atoi(getenv("MPS_TC_BISECT")) : 0;
   dm.bisect = bis;
+  dm.cnt = prof_counts();
   dm.tilesR = (maxR + TC_M - 1) / TC_M;
   dm.tilesC = (maxC + TC_N - 1) / TC_N;
   dm.kb = (maxK + TC_K - 1) / TC_K;
@@ -504,7 +509,9 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
     check("slice_a");
     k_tc_slice_b<L, LG><<<dim3(dm.tilesC * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
     check("slice_b");
+    prof_mark(PROF_TCMMA, 1, st);
     k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), TC_WARPS * 32, smem, st>>>(d_items, f, dm);
+    prof_mark(PROF_TCMMA, 0, st);
     check("mma");
     const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
     k_tc_epi<L, LG, ZOUT, LOUT><<<dim3(std::min(1024, (ne + 255) / 256), cnt), 256, 0, st>>>(d_items, f, dm);

@@ -270,7 +270,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
                       int64_t* eAcols, int* zerr, PreItem* pi, GemmT* gt, size_t stride, bool p_route = false) {
   constexpr int NSIT = ns_iters<L>();
   *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax,
-                nullptr, nullptr, nullptr, nullptr};
+                nullptr, nullptr, nullptr, nullptr, prof_counts()};
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -380,6 +380,7 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
     int C = 1;
     const int bpairs = ((maxN + jd_bs(maxM) - 1) / jd_bs(maxM) + 1) / 2;
     while (C < 8 && n * C * 2 <= 148 && C * 2 <= bpairs) C *= 2;
+    prof_mark(PROF_JDB, 1, st);
     if (C == 1) {
       k_jacobi_db<<<n, JD_THREADS, smem, st>>>(dpre, 1);
     } else {
@@ -397,6 +398,7 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       cfg.numAttrs = 1;
       cudaLaunchKernelEx(&cfg, k_jacobi_db, dpre, C);
     }
+    prof_mark(PROF_JDB, 0, st);
     ++nl;
     if (jprof) {
       unsigned long long h[8];
@@ -419,7 +421,9 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   if (xs) {
     nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 3) * n, n, maxM, maxN, maxN, gMN, st);
     nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 4) * n, n, maxN, maxN, maxM, gNN, st);
+    prof_mark(PROF_XS, 1, st);
     nl += launch_xsweep<L, 4>(dpre, n, maxN, 0, st);
+    prof_mark(PROF_XS, 0, st);
   }
   nl += run_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, n, maxN, gNN, st);
   if (xs) {
@@ -428,7 +432,9 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
     static_assert(NsSched<L>::lg[1] == 7 && XS2_D <= 7, "X_2 holds 7 digits");
     nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 5) * n, n, maxM, maxN, maxN, gMN, st);
     nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 6) * n, n, maxN, maxN, maxM, gNN, st);
+    prof_mark(PROF_XS, 1, st);
     nl += launch_xsweep<L, XS2_D>(dpre, n, maxN, 1, st);
+    prof_mark(PROF_XS, 0, st);
   }
   if constexpr (NSIT > 3) nl += run_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, n, maxN, gNN, st);
   const GemmT* dD = dgt + (size_t)(2 * KL) * n;
