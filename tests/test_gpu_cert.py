@@ -3,7 +3,10 @@ rule (a final sweep that rotates no pair, MPS_NO_CERT=1): the same configs[1]-sh
 run in two subprocesses (the switch is read once per process).  The certificate bounds every
 pair's relative off-diagonal at the end of the last rotating sweep by tol (1 + 2^-8), so both
 runs must agree to the working precision (here 2^-(p-24) relative to sigma_1, far inside the
-tau of north_star), keep the same k, and the certified run must need fewer sweeps."""
+tau of north_star), keep the same k, and the certified run must need fewer sweeps.  The
+first-order finish (R23) closes most 280-bit items without the p-bit iteration; this test pins
+the iteration's certificate, the path the items R23 does not close take, so both runs set
+MPS_FO=0 (test_gpu_fo.py compares the first-order finish with it)."""
 import json
 import os
 import subprocess
@@ -38,6 +41,7 @@ print("JSON" + json.dumps(res))
 def _run(no_cert: bool):
     env = dict(os.environ)
     env.pop("MPS_NO_CERT", None)
+    env["MPS_FO"] = "0"
     if no_cert:
         env["MPS_NO_CERT"] = "1"
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
