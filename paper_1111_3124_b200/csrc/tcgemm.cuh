@@ -30,19 +30,49 @@
 
 namespace mpsb {
 
+#ifndef TC_N_   // tile shape switches (development A/B builds)
+#define TC_N_ 64
+#endif
+#ifndef TC_GCH_
+#define TC_GCH_ (512 / TC_N_)
+#endif
+#ifndef TC_WARPS_
+#define TC_WARPS_ 8
+#endif
+#ifndef TC_SBK_
+#define TC_SBK_ 16
+#endif
 constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
-constexpr int TC_N = 64;   // output columns per CTA = MMA N
+constexpr int TC_N = TC_N_;   // output columns per CTA = MMA N
 constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
-constexpr int TC_GCH = 8;   // slice-weight groups per chunk: 8 accumulators x 64 columns = 512 TMEM columns
-constexpr int TC_WARPS = 8;  // warps of k_tc_mma: warp w issues the MMAs of group d0 + w of a chunk
-constexpr int TC_SBK = 16;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
+constexpr int TC_GCH = TC_GCH_;   // slice-weight groups per chunk: TC_GCH accumulators x TC_N columns = 512 TMEM columns
+constexpr int TC_WARPS = TC_WARPS_;  // warps of k_tc_mma: warp w issues the MMAs of groups d0 + w (TC_GCH / TC_WARPS each)
+constexpr int TC_SBK = TC_SBK_;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
+static_assert(TC_GCH * TC_N <= 512 && TC_GCH % TC_WARPS == 0 && TC_WARPS % 4 == 0, "TMEM columns / warp roles");
 constexpr int TC_STAGE = TC_SBK * 4096 + (TC_SBK + TC_GCH - 1) * TC_N * 32;  // bytes of one stage buffer
 constexpr int TC_ATILE = TC_M * TC_K;  // bytes of one A slice tile
 constexpr int TC_BTILE = TC_N * TC_K;  // bytes of one B slice tile
 
-template <int LG> __host__ __device__ constexpr int tc_ns() { return 4 * LG + 1; }
-template <int LG> __host__ __device__ constexpr int tc_dlo() { return 4 * (LG - 2); }
-template <int LG> __host__ __device__ constexpr int tc_ng() { return 8 * LG - tc_dlo<LG>() + 1; }
+// Slice width: TC_SLICE_BITS = 7 (four slices per 28-bit digit) or 8 (balanced base-256 slices of
+// the whole value: 7 slices per two digits, ~20% fewer slice pairs per product).
+#ifndef TC_SLICE_BITS
+#define TC_SLICE_BITS 7
+#endif
+constexpr int TC_SB = TC_SLICE_BITS;
+static_assert(TC_SB == 7 || TC_SB == 8, "slice width");
+// slices per LG-digit value (the last one the carry out of the top), the lowest slice-weight
+// group formed (weight 2^(TC_SB d) >= 2^(28 (LG - 2)), the lowest digit column the IMAD path keeps),
+// the highest group, the group count
+template <int LG> __host__ __device__ constexpr int tc_ns() { return TC_SB == 7 ? 4 * LG + 1 : (7 * LG + 1) / 2 + 1; }
+template <int LG> __host__ __device__ constexpr int tc_dlo() { return TC_SB == 7 ? 4 * (LG - 2) : (7 * (LG - 2) + 1) / 2; }
+template <int LG> __host__ __device__ constexpr int tc_dhi() { return 2 * (tc_ns<LG>() - 1); }
+template <int LG> __host__ __device__ constexpr int tc_ng() { return tc_dhi<LG>() - tc_dlo<LG>() + 1; }
+// first slice that can be nonzero when the nz lowest digits are zero; one past the last slice
+// that can be nonzero when the top z digits are zero
+__host__ __device__ constexpr int tc_slice_lo(int nz) { return TC_SB == 7 ? 4 * nz : (7 * nz) / 2; }
+template <int LG> __host__ __device__ constexpr int tc_slice_hi(int z) {
+  return z <= 0 ? tc_ns<LG>() : (TC_SB == 7 ? 4 * (LG - z) : ((7 * (LG - z) + 1) / 2 + 1 < tc_ns<LG>() ? (7 * (LG - z) + 1) / 2 + 1 : tc_ns<LG>()));
+}
 
 struct TcDims {
   int tilesR, tilesC, kb;  // output row tiles (128), column tiles (32), k blocks (32), max over items
@@ -82,6 +112,17 @@ __device__ __forceinline__ void tc_digit(int32_t v, int32_t& carry, int (&u)[4])
   }
 }
 
+// base-256 slicing (TC_SB = 8): acc holds (x_{<=j} - emitted slices) / 2^(8 s); digit j enters at
+// bit 28 j - 8 s in {0, 4}; slices s with 8 (s + 1) <= 28 (j + 1) are final after digit j (later
+// digits only touch higher bits); balanced slices in [-128, 127] (the unique balanced base-256
+// representation of x, so -x is sliced separately, never negated slice by slice)
+__device__ __forceinline__ int tc_bal8(int64_t& acc) {
+  const int u = (int)(((acc + 128) & 255) - 128);
+  acc = (acc - u) >> 8;
+  return u;
+}
+__device__ __forceinline__ void tc_add_digit8(int64_t& acc, int32_t d, int j) { acc += (int64_t)d << (28 * j - 8 * ((7 * j) / 2)); }
+
 __device__ __forceinline__ uint32_t tc_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // descriptor of a K-major no-swizzle tile: LBO = 128 B (k-adjacent core matrices), SBO = 256 B
@@ -113,8 +154,9 @@ __global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int firs
   __shared__ int32_t T[TC_K][TC_M + 1];
   // element e = t + 256 i: k = e % 32 (fastest: coalesced tile bytes), x = e / 32
   int32_t carry[16];
+  int64_t acc8[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) carry[i] = 0;
+  for (int i = 0; i < 16; ++i) { carry[i] = 0; acc8[i] = 0; }
   for (int j = 0; j < LG; ++j) {
     if (!it.conjA) {  // digits contiguous along rows: stage [k][x] through shared memory
       __syncthreads();
@@ -136,17 +178,27 @@ __global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int firs
         v = (r < it.rows && kk < it.K && D0 + j >= 0) ? it.A[((size_t)(r * 2 + ri) * L + D0 + j) * it.lda + kk] : 0;
         if (ri) v = -v;
       }
-      int uu[4];
-      tc_digit(v, carry[i], uu);
       const int o = tc_off(x, k);
+      if (TC_SB == 7) {
+        int uu[4];
+        tc_digit(v, carry[i], uu);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
+        for (int u = 0; u < 4; ++u) out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
+      } else {
+        tc_add_digit8(acc8[i], v, j);
+        for (int sl = (7 * j) / 2; sl < (7 * (j + 1)) / 2; ++sl) out[(size_t)sl * sstride + o] = (int8_t)tc_bal8(acc8[i]);
+      }
     }
   }
 #pragma unroll
   for (int i = 0; i < 16; ++i) {
     const int e = threadIdx.x + 256 * i, k = e & 31, x = e >> 5;
-    out[(size_t)(S - 1) * sstride + tc_off(x, k)] = (int8_t)carry[i];
+    if (TC_SB == 7) {
+      out[(size_t)(S - 1) * sstride + tc_off(x, k)] = (int8_t)carry[i];
+    } else {
+      for (int sl = (7 * LG) / 2; sl < S - 1; ++sl) out[(size_t)sl * sstride + tc_off(x, k)] = (int8_t)tc_bal8(acc8[i]);
+      out[(size_t)(S - 1) * sstride + tc_off(x, k)] = (int8_t)acc8[i];
+    }
   }
 }
 
@@ -172,19 +224,39 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
     const int pc = ok ? (it.colmap ? it.colmap[c] : c) : 0;
     const int o = tc_off(x, k);
     int32_t carry = 0;
+    int64_t ap = 0, an = 0;  // TC_SB = 8: slicing of v and of -v (plane 2)
 #pragma unroll
     for (int j = 0; j < LG; ++j) {
       const int32_t v = (ok && D0 + j >= 0) ? it.B[((size_t)(pc * 2 + ri) * L + D0 + j) * it.ldb + kk] : 0;
-      int uu[4];
-      tc_digit(v, carry, uu);
+      if (TC_SB == 7) {
+        int uu[4];
+        tc_digit(v, carry, uu);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
-        if (ri) out[pstride + (size_t)(4 * j + u) * sstride + o] = (int8_t)(-uu[u]);  // plane 2: -im
+        for (int u = 0; u < 4; ++u) {
+          out[(size_t)(4 * j + u) * sstride + o] = (int8_t)uu[u];
+          if (ri) out[pstride + (size_t)(4 * j + u) * sstride + o] = (int8_t)(-uu[u]);  // plane 2: -im
+        }
+      } else {
+        tc_add_digit8(ap, v, j);
+        if (ri) tc_add_digit8(an, -v, j);
+#pragma unroll
+        for (int sl = (7 * j) / 2; sl < (7 * (j + 1)) / 2; ++sl) {
+          out[(size_t)sl * sstride + o] = (int8_t)tc_bal8(ap);
+          if (ri) out[pstride + (size_t)sl * sstride + o] = (int8_t)tc_bal8(an);
+        }
       }
     }
-    out[(size_t)(S - 1) * sstride + o] = (int8_t)carry;
-    if (ri) out[pstride + (size_t)(S - 1) * sstride + o] = (int8_t)(-carry);
+    if (TC_SB == 7) {
+      out[(size_t)(S - 1) * sstride + o] = (int8_t)carry;
+      if (ri) out[pstride + (size_t)(S - 1) * sstride + o] = (int8_t)(-carry);
+    } else {
+      for (int sl = (7 * LG) / 2; sl < S - 1; ++sl) {
+        out[(size_t)sl * sstride + o] = (int8_t)tc_bal8(ap);
+        if (ri) out[pstride + (size_t)sl * sstride + o] = (int8_t)tc_bal8(an);
+      }
+      out[(size_t)(S - 1) * sstride + o] = (int8_t)ap;
+      if (ri) out[pstride + (size_t)(S - 1) * sstride + o] = (int8_t)an;
+    }
   }
 }
 
@@ -212,7 +284,7 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
 // group-sum scratch (tcgen05.ld).  Slice ranges: A s in [SA0, S), B t in [SB0, SB1).
 template <int LG, int SA0, int SB0, int SB1>
 __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
-  constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = 8 * LG;
+  constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = tc_dhi<LG>();
   constexpr int NCH = (NG + TC_GCH - 1) / TC_GCH;
   constexpr uint32_t IDESC = tc_idesc(TC_M, TC_N);
   const int item = first + blockIdx.y;
@@ -446,7 +518,8 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
       for (int q = 0; q < NG; ++q) {
         const int d = DLO + q;
         const int64_t v = Gb[(((size_t)ri * NG + q) * RCc + c) * RRr + r];
-        acc[ri][d / 4 - (LG - 2)] += v * ((int64_t)1 << (7 * (d % 4)));
+        if (TC_SB == 7) acc[ri][d / 4 - (LG - 2)] += v * ((int64_t)1 << (7 * (d % 4)));
+        else acc[ri][(8 * d) / 28 - (LG - 2)] += v * ((int64_t)1 << (8 * d - 28 * ((8 * d) / 28)));
       }
       acc[ri][LG + 1] += acc[ri][LG + 2] * ((int64_t)1 << 28);  // column 2LG (the top slices' carry)
     }
@@ -474,7 +547,7 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
   static_assert(LG <= L || (NZA >= LG - L && NZB >= LG - L), "zero-padded digits must be skipped");
   static_assert(LOUT >= LG || LOUT == L, "output digits");
   constexpr int S = tc_ns<LG>(), NG = tc_ng<LG>();
-  constexpr int SA0 = 4 * NZA, SB0 = 4 * NZB, SB1 = Z > 0 ? 4 * (LG - Z) : S;
+  constexpr int SA0 = tc_slice_lo(NZA), SB0 = tc_slice_lo(NZB), SB1 = tc_slice_hi<LG>(Z);
   TcDims dm;
   static const int bis = getenv("MPS_TC_BISECT") ? atoi(getenv("MPS_TC_BISECT")) : 0;
   dm.bisect = bis;

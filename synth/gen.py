@@ -273,3 +273,46 @@ def graded_update_inputs(p: int, chi: int, decades: float, *key, in_lambda: bool
             for b in range(chi):
                 R.from_fraction(p, +s[b], lam[b])
     return _round_cplx(p, GA), _round_cplx(p, GB), lam, s
+
+
+def schmidt_profile(chi: int, decades: float, prec: int):
+    """A unit-norm Schmidt vector with a graded profile: graded_sigma(chi, decades) / its 2-norm
+    (descending, sum of squares 1 to the rounding of prec bits)."""
+    import mpmath
+    s = graded_sigma(chi, decades, prec)
+    with mpmath.workprec(prec):
+        nrm = mpmath.sqrt(mpmath.fsum(x * x for x in s))
+        return [x / nrm for x in s]
+
+
+def canonical_update_inputs(p: int, chi: int, dec_l: float, dec_m: float, dec_r: float, *key):
+    """One two-site gate input as it meets a gate deep inside a saturated configs[4] circuit
+    (BASELINE configs[4]: chi_l = chi_m = chi_r = chi): a Vidal canonical window (Eq. 1,
+    P:240-247) with graded unit-norm Schmidt vectors lambda_l, lambda_m, lambda_r
+    (schmidt_profile with dec_l, dec_m, dec_r decades) and
+      Gamma_A^i(a, b) = W[i chi + a][b] / lambda_l(a)     (lambda_l Gamma_A left-normalised),
+      Gamma_B^j(b, c) = conj(Z[j chi + c][b]) / lambda_r(c) (Gamma_B lambda_r right-normalised),
+    W, Z 2chi x chi Householder isometries at p + 64 bits, so Theta = lambda_l Gamma_A lambda_m
+    Gamma_B lambda_r = W diag(lambda_m) Z^H before the gate, and a seeded Haar U(4).  The gate
+    mixes the physical indices, so Theta' = U Theta has 2chi generic graded singular values and
+    truncation to chi_max = chi drops half of them.  Nothing here computes the update.
+    Returns (A, B, lam_l, lam_m, lam_r, U) as p-bit records."""
+    import mpmath
+    prec = p + 64
+    ll = schmidt_profile(chi, dec_l, prec)
+    lm = schmidt_profile(chi, dec_m, prec)
+    lr = schmidt_profile(chi, dec_r, prec)
+    W = householder_isometry(p, 2 * chi, chi, *key, 0)
+    Z = householder_isometry(p, 2 * chi, chi, *key, 1)
+    with mpmath.workprec(prec):
+        GA = [W[i * chi + a][b] / ll[a] for i in range(2) for a in range(chi) for b in range(chi)]
+        GB = [mpmath.conj(Z[j * chi + c][b]) / lr[c] for j in range(2) for b in range(chi) for c in range(chi)]
+    lams = []
+    for v in (ll, lm, lr):
+        r = R.empty(p, chi)
+        with mpmath.workprec(p):
+            for b in range(chi):
+                R.from_fraction(p, +v[b], r[b])
+        lams.append(r)
+    U = haar_unitary(p, 4, *key, 2)
+    return (_round_cplx(p, GA), _round_cplx(p, GB), *lams, U)

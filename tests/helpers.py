@@ -104,16 +104,21 @@ def frac(x) -> Fraction:
     return Fraction(x)
 
 
-def p_sample(p: int, chi: int, k: int, GL, GR, lam, rows, cols):
+def p_sample(p: int, chi: int, k: int, GL, GR, lam, rows, cols, lam_l=None, lam_r=None):
     """Entries (rows x cols) of the gauge-invariant local check P = X_k diag(lambda') V_k^H
     (SURVEY §8(c) "Comparison metrics") of a configs[1] item with lambda_l = lambda_r = 1:
     P[(i,a),(j,c)] = sum_{b<k} GL[i][a][b] lambda'_b GR[j][b][c], row r = i chi + a,
     column j chi + c (GL [2][chi][chi_max], GR [2][chi_max][chi] complex records,
-    chi_max = chi).  Each entry summed in mpmath at p + 64 bits, rounded to p bits."""
+    chi_max = chi).  Each entry summed in mpmath at p + 64 bits, rounded to p bits.
+    With lam_l / lam_r (records) the outer Schmidt vectors are multiplied back in,
+    P[(i,a),(j,c)] = lambda_l(a) sum_b GL lambda' GR lambda_r(c): the gauge-invariant
+    X_k diag(lambda') V_k^H of a window with nontrivial outer bonds (Eq. 1)."""
     from synth import records as R
     gl = cplx(GL)
     gr = cplx(GR)
     lm = reals(lam)
+    ll = reals(lam_l) if lam_l is not None else None
+    lr = reals(lam_r) if lam_r is not None else None
     out = R.empty(p, 2 * len(rows) * len(cols))
     with mpmath.workprec(p + 64):
         for ri, r in enumerate(rows):
@@ -122,6 +127,10 @@ def p_sample(p: int, chi: int, k: int, GL, GR, lam, rows, cols):
             for ci, c in enumerate(cols):
                 j, cc = divmod(c, chi)
                 v = mpmath.fsum(xl[b] * gr[(j * chi + b) * chi + cc] for b in range(k))
+                if ll is not None:
+                    v *= ll[a]
+                if lr is not None:
+                    v *= lr[cc]
                 with mpmath.workprec(p):
                     R.from_fraction(p, +v.real, out[2 * (ri * len(cols) + ci)])
                     R.from_fraction(p, +v.imag, out[2 * (ri * len(cols) + ci) + 1])

@@ -1,0 +1,115 @@
+"""configs[4] sampled-gate parity (SURVEY §8(c) "cfg5 end-to-end"; VERDICT r01 "Next round" 1):
+configs[4]-shaped gates at chi = 256, 512 bits against cached complete ORACLE updates.
+
+The inputs are seeded synthetic windows of the shape a gate meets deep inside the saturated
+configs[4] circuit (`synth.gen.canonical_update_inputs`, R25: Vidal canonical Gamma
+tensors, graded unit-norm Schmidt vectors lambda_l, lambda_m, lambda_r over 6-16 decades, a
+Haar U(4); chi_l = chi_m = chi_r = 256, chi_max = 256, threshold 2^-256).  The goldens
+(`tests/golden/cfg5_p512_chi256_item*.json`) are written by tools/make_cfg5_golden.py, which
+calls only oracle/ (the textbook cyclic Jacobi from Theta' with accumulated V, ~2 h per item
+on one core).  Theta' has 512 generic singular values; truncation keeps 256.
+
+Two launch configurations, both through the C ABI:
+  * the MPS store as configs[4] runs it: the four windows written into a 64-site 512-bit state
+    (mps_set_schmidt / mps_set_site) at sites 15-16, 19-20, 27-28, 31-32 and applied as ONE
+    mps_apply_layer (few gates per layer: the cluster-cooperative Jacobi of DESIGN §9); windows
+    15-16 and 31-32 are the block-edge gates of the 8-sites-per-GPU sharding, whose arithmetic
+    is bitwise that of this single-state layer (test_gpu_sharded.py);
+  * mps_bench_update_batch (the batched update path) on the same four inputs.
+Compared with the oracle (Eq. 2): the kept count k exactly, all 512
+singular values normwise (batch path), lambda' normwise, and the gauge-invariant
+P = lambda_l Gamma_A' diag(lambda') Gamma_B' lambda_r = X_k diag(lambda') V_k^H on the seeded
+32 x 32 grid relative to ||P||_max — each within tau(512) = 2^-466 (~1e-140).
+"""
+import glob
+import json
+import os
+import sys
+
+import mpmath
+import numpy as np
+import pytest
+
+from synth import records as R
+from tests.helpers import p_sample, reals, tau
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+GOLDS = [json.load(open(f)) for f in sorted(glob.glob(os.path.join(GOLD, "cfg5_p512_chi256_item*.json")))]
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+
+
+def _m():
+    import paper_1111_3124_b200 as m
+    return m
+
+
+def recs(p, h):
+    return np.frombuffer(bytes.fromhex(h), dtype=R.record_dtype(p)).copy()
+
+
+@pytest.fixture(scope="module")
+def items():
+    import make_cfg5_golden as mk  # the generator recipe only (synth), no oracle call
+    return {g["item"]: mk.inputs(g["item"]) for g in GOLDS}
+
+
+def _check(g, k, lam, GL, GR, ll, lr, sigma=None, what=""):
+    p, chi = g["prec"], g["chi"]
+    assert k == g["k"]
+    with mpmath.workprec(2 * p):
+        lg, lw = reals(lam[:k]), reals(recs(p, g["lam"]))
+        e_l = max(abs(x - y) for x, y in zip(lg, lw)) / lw[0]
+        Pg = reals(p_sample(p, chi, k, GL, GR, lam, g["P_rows"], g["P_cols"], lam_l=ll, lam_r=lr))
+        Pw = reals(recs(p, g["P"]))
+        e_p = max(abs(x - y) for x, y in zip(Pg, Pw)) / mpmath.mpf(g["Pmax"])
+        e_s = mpmath.mpf(0)
+        if sigma is not None:
+            got = reals(sigma)
+            want = sorted(reals(recs(p, g["sigma"])), reverse=True)
+            e_s = max(abs(x - y) for x, y in zip(got, want)) / want[0]
+    print(f"cfg5 item {g['item']} {what}: k {k} sigma {float(e_s):.2e} lambda {float(e_l):.2e} P {float(e_p):.2e} "
+          f"(oracle sweeps {g['sweeps']})")
+    for e in (e_s, e_l, e_p):
+        assert e <= tau(p)
+
+
+@pytest.mark.skipif(not GOLDS, reason="no cached configs[4] gate goldens")
+def test_cfg5_gates_in_mps_layer(items):
+    m = _m()
+    p, chi = 512, 256
+    st = m.MPS(64, p, chi, 2.0 ** -256)
+    gates = []
+    for g in GOLDS:
+        A, B, ll, lm, lr, U = items[g["item"]]
+        s = g["spec"][1]
+        st.set_schmidt(s - 1, ll)
+        st.set_schmidt(s, lm)
+        st.set_schmidt(s + 1, lr)
+        st.set_site(s, A, chi, chi)
+        st.set_site(s + 1, B, chi, chi)
+        gates.append((U, (s, s + 1)))
+    st.apply_layer(gates)
+    st.sync()
+    for g in GOLDS:
+        A, B, ll, lm, lr, U = items[g["item"]]
+        s = g["spec"][1]
+        lam = st.schmidt(s)
+        GL, ml, mr = st.get_site(s)
+        GR, ml2, mr2 = st.get_site(s + 1)
+        assert (ml, mr, ml2, mr2) == (chi, len(lam), len(lam), chi)
+        # the store's site layout [2][ml][mr] is the oracle's [2][chi][chi_max] when k = chi_max
+        _check(g, len(lam), lam, GL, GR, ll, lr, what="mps_apply_layer")
+    st.close()
+
+
+@pytest.mark.skipif(not GOLDS, reason="no cached configs[4] gate goldens")
+def test_cfg5_gates_in_update_batch(items):
+    m = _m()
+    p, chi = 512, 256
+    for g in GOLDS:
+        A, B, ll, lm, lr, U = items[g["item"]]
+        out = m.update_batch(p, chi, 1, A, B, U, lam_l=ll, lam_m=lm, lam_r=lr, chi_max=chi, thr=2.0 ** -256)
+        k = int(out["k"][0])
+        _check(g, k, out["lam"], out["GL"], out["GR"], ll, lr, sigma=out["sigma"], what="update_batch")
