@@ -35,6 +35,9 @@ struct PreItem {
   // exponent, the rotation records; X1 == nullptr: no refinement sweep for this item
   int32_t* X1; const int32_t* G; const int64_t* eG; int4* xs_rec;
   unsigned long long* cnt;  // profiling counters (CNT_*), or null
+  // GEMM form of the refinement sweeps (R26): exponents {0, -1} of E and E/2; per sweep
+  // the number of pairs applied as sequential exact rotations (the others enter E)
+  int64_t* eXs; int* xs_big;
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -581,7 +584,10 @@ __global__ void k_d_to_fx(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
   const int N = it.N;
   if (N == 0) return;  // item without preconditioning
-  if (blockIdx.x == 0 && threadIdx.x == 0) { it.eOne[0] = 1; it.eOne[1] = 0; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    it.eOne[0] = 1; it.eOne[1] = 0;
+    if (it.eXs) { it.eXs[0] = 0; it.eXs[1] = -1; }
+  }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < N * N; t += gridDim.x * blockDim.x) {
     const int r = t % N, c = t / N;
     const double2 v = it.Vd[(size_t)c * N + r];

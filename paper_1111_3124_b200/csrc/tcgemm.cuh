@@ -56,7 +56,7 @@ constexpr int TC_BTILE = TC_N * TC_K;  // bytes of one B slice tile
 // Slice width: TC_SLICE_BITS = 7 (four slices per 28-bit digit) or 8 (balanced base-256 slices of
 // the whole value: 7 slices per two digits, ~20% fewer slice pairs per product).
 #ifndef TC_SLICE_BITS
-#define TC_SLICE_BITS 7
+#define TC_SLICE_BITS 8
 #endif
 constexpr int TC_SB = TC_SLICE_BITS;
 static_assert(TC_SB == 7 || TC_SB == 8, "slice width");

@@ -165,9 +165,10 @@ inline bool use_precond() {
 template <int L>
 constexpr int ns_iters() { return NsSched<L>::n; }  // Newton-Schulz: 2^-45 -> 2^-360 / 2^-720
 // GEMM descriptors per item: 2 per Newton-Schulz iteration, A_1 (X route), P and A_1 (P route),
-// A_t = Theta' X and G = A_t^H A_t of the two refinement sweeps (R22)
+// A_t = Theta' X and G = A_t^H A_t of the two refinement sweeps (R22), F = E + E E / 2 and
+// X + X F of their GEMM form (R26)
 template <int L>
-constexpr int pre_slots() { return 2 * ns_iters<L>() + 7; }
+constexpr int pre_slots() { return 2 * ns_iters<L>() + 11; }
 // the refinement sweep (xsweep.cuh, R22) is on unless MPS_XSWEEP=0
 inline bool use_xsweep() {
   static int on = -1;
@@ -237,6 +238,8 @@ struct PreBufs {
   int64_t* rexp;
   int64_t* eG;   // exponent of G (refinement sweep)
   int4* xs_rec;  // refinement sweep records
+  int64_t* eXs;  // [2] = {0, -1}: exponents of E and E / 2 (GEMM form of the refinement sweeps)
+  int* xs_big;   // pairs of the current refinement sweep applied as sequential rotations
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
 };
 template <int L>
@@ -257,6 +260,8 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.rcoef = (int32_t*)(q + 256);
   b.rexp = (int64_t*)((char*)b.rcoef + align_up(4 * (size_t)N * (L + 1)));
   b.eG = (int64_t*)(q + 96);
+  b.eXs = (int64_t*)(q + 112);
+  b.xs_big = (int*)(q + 128);
   b.xs_rec = (int4*)((char*)b.rexp + align_up(8 * (size_t)N));
   return b;
 }
@@ -300,7 +305,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
   // output of iteration 0, in Xn = Xb), at 7 digits between iterations 1 and 2 on X_2 (in Xa):
   // A_t = Theta' X into Af at A_1's exponent, G = A_t^H A_t into D's buffer (free between the
   // iterations); each sweep rotates its X in place
-  for (int k = 3; k < 7; ++k) gt[(2 * NSIT + k) * stride] = none;
+  for (int k = 3; k < 11; ++k) gt[(2 * NSIT + k) * stride] = none;
   if (use_xsweep() && N >= XS_MIN_N) {
     int32_t* X1 = pb.Xb;
     int gh = 1;
@@ -312,7 +317,15 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
       g.ghead = gh + 1;  // sum of M products, each |.| < 2^(2 eA1 - 2)
       g.eCwrite = pb.eG;
       gt[(2 * NSIT + 4 + 2 * w) * stride] = g;
+      // GEMM form (R26): E in the X buffer the sweep does not rotate (exponent 0),
+      // F = E + E (E / 2) into Af (A_t is dead once G is formed), X + X F into G's buffer
+      int32_t* Xr = w ? pb.Xa : X1;
+      int32_t* E = w ? X1 : pb.Xa;
+      gt[(2 * NSIT + 7 + 2 * w) * stride] = GemmT{E, N, pb.eXs, E, N, pb.eXs + 1, Af, N, pb.eXs, E, nullptr, N, N, N, 0, 0, 0, nullptr};
+      gt[(2 * NSIT + 8 + 2 * w) * stride] = GemmT{Xr, N, pb.eOne, Af, N, pb.eXs, pb.Dm, N, pb.eOne, Xr, nullptr, N, N, N, 0, 0, 0, nullptr};
     }
+    pi->eXs = pb.eXs;
+    pi->xs_big = pb.xs_big;
     pi->X1 = X1;
     pi->G = pb.Dm;
     pi->eG = pb.eG;
@@ -349,6 +362,31 @@ inline int run_ns_iter(const GemmT* dD, const GemmT* dX, int n, int maxN, dim3 g
   constexpr int LG = NsSched<L>::lg[K], Z = NsSched<L>::z[K], NZ = NsSched<L>::nz[K];
   return run_gemm<L, LG, 0, NZ, NZ, Z>(dD, n, maxN, maxN, maxN, grid, st) +
          run_gemm<L, LG, Z, NZ, 0>(dX, n, maxN, maxN, maxN, grid, st);
+}
+
+// One refinement sweep at XD digits from G (R22): sequential row rotations, or (R26, default) E,
+// F = E + E E / 2, X + X F as two GEMMs (dF: their descriptors, n apart), the copy back, and the
+// sequential rotations of the few pairs left out of E.  Launch count.
+template <int L, int XD>
+inline int run_xsweep(const PreItem* dpre, const GemmT* dF, int n, int maxN, int sel, dim3 gNN, cudaStream_t st) {
+  int nl = 0;
+  if (!xs_gemm_form()) {
+    prof_mark(PROF_XS, 1, st);
+    nl += launch_xsweep<L, XD>(dpre, n, maxN, sel, st);
+    prof_mark(PROF_XS, 0, st);
+    return nl;
+  }
+  constexpr int ZE = XsT<XD>::ZE;
+  prof_mark(PROF_XS, 1, st);
+  nl += launch_xs_emat<L, XD>(dpre, n, maxN, sel, st);
+  prof_mark(PROF_XS, 0, st);
+  nl += run_gemm<L, XD, ZE>(dF, n, maxN, maxN, maxN, gNN, st);
+  nl += run_gemm<L, XD, ZE>(dF + (size_t)n, n, maxN, maxN, maxN, gNN, st);
+  prof_mark(PROF_XS, 1, st);
+  k_xs_copy<L><<<dim3(32, n), 256, 0, st>>>(dpre, sel); ++nl;
+  nl += launch_xs_apply<L, XD>(dpre, n, maxN, sel, st);
+  prof_mark(PROF_XS, 0, st);
+  return nl;
 }
 
 // the preconditioner kernels for n items (descriptors already on the device); launch count
@@ -421,9 +459,7 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
   if (xs) {
     nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 3) * n, n, maxM, maxN, maxN, gMN, st);
     nl += run_gemm<L, 4, 0>(dgt + (size_t)(2 * NSIT + 4) * n, n, maxN, maxN, maxM, gNN, st);
-    prof_mark(PROF_XS, 1, st);
-    nl += launch_xsweep<L, 4>(dpre, n, maxN, 0, st);
-    prof_mark(PROF_XS, 0, st);
+    nl += run_xsweep<L, 4>(dpre, dgt + (size_t)(2 * NSIT + 7) * n, n, maxN, 0, gNN, st);
   }
   nl += run_ns_iter<L, 1>(dgt + (size_t)2 * n, dgt + (size_t)3 * n, n, maxN, gNN, st);
   if (xs) {
@@ -432,9 +468,7 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
     static_assert(NsSched<L>::lg[1] == 7 && XS2_D <= 7, "X_2 holds 7 digits");
     nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 5) * n, n, maxM, maxN, maxN, gMN, st);
     nl += run_gemm<L, XS2_D, 0>(dgt + (size_t)(2 * NSIT + 6) * n, n, maxN, maxN, maxM, gNN, st);
-    prof_mark(PROF_XS, 1, st);
-    nl += launch_xsweep<L, XS2_D>(dpre, n, maxN, 1, st);
-    prof_mark(PROF_XS, 0, st);
+    nl += run_xsweep<L, XS2_D>(dpre, dgt + (size_t)(2 * NSIT + 9) * n, n, maxN, 1, gNN, st);
   }
   if constexpr (NSIT > 3) nl += run_ns_iter<L, 2>(dgt + (size_t)4 * n, dgt + (size_t)5 * n, n, maxN, gNN, st);
   const GemmT* dD = dgt + (size_t)(2 * KL) * n;
@@ -893,7 +927,7 @@ __global__ void k_relayout_T(const int32_t* T, int32_t* Tp, int chiL, int chi2) 
 
 template <class T>
 size_t upd3_workspace(const Upd3Args& a) {
-  return upd3_item_bytes<T::L, T::NL>(a) + 4 * 4096;
+  return upd3_item_bytes<T::L, T::NL>(a) + 6 * 4096;
 }
 
 // Stage 1: contraction, SVD#1, truncation, Gamma_{s+2}' and lambda_{s+1}'.  k1 lands in *a.k1.
@@ -903,7 +937,7 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   constexpr int L = T::L, NL = T::NL;
   const int RBr = record_words(p);
   char* base = (char*)ws;
-  const size_t d_prep = 0, d_gemm = 1024, d_mix = 2048, d_svd = 2560, d_fin = 4096, d_end = 4 * 4096;
+  const size_t d_prep = 0, d_gemm = 1024, d_mix = 2048, d_svd = 2560, d_fin = 4096, d_end = 6 * 4096;
   hd.assign(d_end, 0);
   char* q = base + d_end;
   const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
@@ -935,8 +969,8 @@ int launch_update3_stage1(int p, double thr, const Upd3Args& a, void* ws, cudaSt
   const PreBufs<L> PB1 = rec.P1();
   hm[0] = MixItem{Th, 4 * a.chiL, eTh, a.U, 4, a.chiL, a.chiR, trans1 ? 1 : 0, pb1 ? rec.A0a : A1, pb1 ? PB1.eMix : S1.eA,
                   M1, N1};
-  const size_t d_pre1 = 5120, d_gt1 = 5376;
-  static_assert(5120 + sizeof(PreItem) <= 5376 && 5376 + sizeof(GemmT) * pre_slots<L>() <= 8192, "stage-1 descriptors");
+  const size_t d_pre1 = 16384, d_gt1 = 16640;
+  static_assert(16384 + sizeof(PreItem) <= 16640 && 16640 + sizeof(GemmT) * pre_slots<L>() <= 20480, "stage-1 descriptors");
   const bool p_route1 = !force_accumulate_v() && !a.accumulate_v;  // V recovered: fold the last X update
   if (pb1) pre_descs<L>(PB1, M1, N1, rec.A0a, PB1.eMix, A1, S1.eA, a.redo, (PreItem*)(hd.data() + d_pre1),
                         (GemmT*)(hd.data() + d_gt1), 1, p_route1);
@@ -999,7 +1033,7 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   constexpr int L = T::L, NL = T::NL;
   const int RBr = record_words(p);
   char* base = (char*)ws;
-  const size_t d_fin = 4096, d_svd2 = 8192, d_fin2 = 12288, d_end = 4 * 4096;
+  const size_t d_fin = 4096, d_svd2 = 8192, d_fin2 = 12288, d_end = 6 * 4096;
   // recover the stage-1 layout
   char* q = base + d_end;
   const int M1 = std::max(4 * a.chiL, 2 * a.chiR), N1 = std::min(4 * a.chiL, 2 * a.chiR);
@@ -1047,8 +1081,8 @@ int launch_update3_stage2(int p, double thr, const Upd3Args& a, int k1, void* ws
   const bool pb2 = use_precond() && !a.no_precond;
   const PreBufs<L> PB2 = rec.P2();
   if (pb2 && !recover) { si.V = PB2.Xfin(); si.v_preset = 1; }
-  const size_t d_pre2 = 13312, d_gt2 = 13568;
-  static_assert(13312 + sizeof(PreItem) <= 13568 && 13568 + sizeof(GemmT) * pre_slots<L>() <= 16384, "stage-2 descriptors");
+  const size_t d_pre2 = 20480, d_gt2 = 20736;
+  static_assert(20480 + sizeof(PreItem) <= 20736 && 20736 + sizeof(GemmT) * pre_slots<L>() <= 24576, "stage-2 descriptors");
   if (pb2) pre_descs<L>(PB2, M2, N2, rec.A0b, rec.eA0b, A2, S2.eA, a.redo, (PreItem*)(hd.data() + d_pre2),
                         (GemmT*)(hd.data() + d_gt2), 1);
   hs[0] = si;

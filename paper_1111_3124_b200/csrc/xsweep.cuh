@@ -15,6 +15,17 @@
 //   k_xs_apply: X <- X R_1 R_2 ... (every row of X independently: a CTA keeps R rows of X in
 //     shared memory and applies the whole sequence of rotations, one barrier per step)
 //
+// GEMM form (R26, default; MPS_XS_GEMM=0 applies every rotation sequentially as above):
+// the rotations of a refinement sweep are tiny (|s| ~ 2^-41 / 2^-78) and their parameters all
+// come from the Gram matrix at the start of the sweep, so their product is exp(E) up to
+// commutators of order |s|^2 |gamma|, E_pq = s_pq, E_qp = -conj(s_pq): k_xs_params writes E, and
+//   F = E + E E / 2,   X <- X + X F      (two XD-digit tensor-core GEMMs, k_xs_copy)
+// replaces k_xs_apply's N(N-1)/2 sequential row rotations.  I + F is unitary to |E|^3, below the
+// 2^-92 / 2^-184 the basis is unitary to; the columns of Theta' X end as orthogonal as after the
+// sequential sweep (both are first-order in the stale gamma).  Pairs with |s| >= 2^-32 (4
+// digits) / 2^-64 (7 digits) -- near-degenerate column norms -- are left out of E and applied
+// afterwards by k_xs_apply as exact rotations (items without such pairs exit at once).
+//
 // The sweeps only choose a better starting basis: X stays unitary to the level the next
 // Newton-Schulz iteration needs, and every p-bit quantity is still computed exactly from
 // Theta' by the later stages, whose stopping rule decides convergence (as for R19).
@@ -84,7 +95,21 @@ template <int XD> struct XsT {
   static constexpr int REC = 3 * P + 4;
   static constexpr int ZC = XD == 4 ? 3 : 5;  // |c - 1| ~ 2^-86 (4 digits), ~2^-141 (6, 7 digits)
   static constexpr int ZS = XD == 4 ? 1 : 2;  // |s| ~ 2^-40, ~2^-70
+  // GEMM form: E (exponent 0) and F = E + E E / 2 have ZE zero top digits; pairs with
+  // |Re s| or |Im s| >= 2^-EBIG stay sequential rotations
+  static constexpr int ZE = XD == 4 ? 1 : 2;
+  static constexpr int EBIG = XD == 4 ? 32 : 64;  // |s|^3 below 2^-92 / 2^-184
 };
+
+// the GEMM form of the refinement sweeps (R26) is on unless MPS_XS_GEMM=0
+inline bool xs_gemm_form() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_XS_GEMM");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
 
 // add the integer-valued double x (|x| < 2^(28 XD)) to the digit columns D (28-bit weights)
 template <int XD>
@@ -146,15 +171,20 @@ __device__ __forceinline__ dd xs_g_dd(const int32_t* p, size_t ld) {
 // g = G_pq); s is rounded to the XD-digit grid and c - 1 = -|s|^2 / (1 + sqrt(1 - |s|^2))
 // computed from the rounded s, so that the rotation is unitary to ~2^-(28 XD).
 // sel: 0 rotates PreItem::X1 (after Newton-Schulz iteration 0), 1 PreItem::X (iteration 1).
+// gemm: pairs with small s are written into E (the X buffer the sweep does not rotate: sel 0 ->
+// PreItem::X, 1 -> X1; zeroed by k_xs_zero) instead of being flagged for k_xs_apply; *xs_big
+// receives the number of pairs left to k_xs_apply.
 template <int L, int XD>
-__global__ void k_xs_params(const PreItem* items) {
+__global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
   using T = XsT<XD>;
   const PreItem it = items[blockIdx.x];
   const int N = it.N, NP = N / 2;
   if (N < 2 || it.X1 == nullptr) return;
+  int32_t* E = sel ? it.X1 : it.X;
   extern __shared__ dd xs_alpha[];  // [N]
   __shared__ double s_tr;
-  __shared__ int s_nrot;
+  __shared__ int s_nrot, s_nbig, s_emax;
+  if (threadIdx.x == 0) { s_nbig = 0; s_emax = -9999; }
   for (int p = threadIdx.x; p < N; p += blockDim.x) xs_alpha[p] = xs_g_dd<L, XD>(it.G + ((size_t)(p * 2) * L) * N + p, N);
   if (threadIdx.x == 0) s_nrot = 0;
   __syncthreads();
@@ -209,7 +239,27 @@ __global__ void k_xs_params(const PreItem* items) {
 #pragma unroll
           for (int k = 0; k < 3 * T::P / 4; ++k) rec[k] = make_int4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
           flag = 1 | ((zc && zs) ? 2 : 0);
-          if (jac_trace_items) atomicAdd(&s_nrot, 1);
+          if (gemm && fabs(sr.hi) < ldexp(1.0, -T::EBIG) && fabs(si.hi) < ldexp(1.0, -T::EBIG)) {
+            // E_pq = s (row p, column q), E_qp = -conj(s); top XD of the L stored digits
+            flag = 4;
+            int32_t* e1 = E + ((size_t)(q * 2) * L + (L - XD)) * N + p;
+            int32_t* e2 = E + ((size_t)(p * 2) * L + (L - XD)) * N + q;
+#pragma unroll
+            for (int k = 0; k < XD; ++k) {
+              e1[(size_t)k * N] = Kr[k];
+              e1[(size_t)(L + k) * N] = Ki[k];
+              e2[(size_t)k * N] = -Kr[k];
+              e2[(size_t)(L + k) * N] = Ki[k];
+            }
+          } else if (gemm) {
+            atomicAdd(&s_nbig, 1);
+          }
+          if (jac_trace_items) {
+            atomicAdd(&s_nrot, 1);
+            int ex;
+            frexp(fmax(fabs(sr.hi), fabs(si.hi)), &ex);
+            atomicMax(&s_emax, ex);
+          }
           const dd tg = dd_div(dd_mul(g2, sc), c);  // t |g| (signed like d)
           xs_alpha[p] = dd_add(ap, dd_neg(tg));
           xs_alpha[q] = dd_add(aq, tg);
@@ -219,9 +269,31 @@ __global__ void k_xs_params(const PreItem* items) {
     }
     __syncthreads();
   }
+  if (threadIdx.x == 0 && it.xs_big) *it.xs_big = gemm ? s_nbig : -1;
   if (jac_trace_items && threadIdx.x == 0 && (int)blockIdx.x < jac_trace_items)
-    printf("xsweep(%d digits) item %d N %d rotated %d of %d pairs, alpha0 %.6e trace %.6e\n", XD, (int)blockIdx.x, N,
-           s_nrot, NP * (N - 1), xs_alpha[0].hi, s_tr);
+    printf("xsweep(%d digits) item %d N %d rotated %d of %d pairs (%d as sequential rotations), max |s| < 2^%d, alpha0 %.6e trace %.6e\n",
+           XD, (int)blockIdx.x, N, s_nrot, NP * (N - 1), gemm ? s_nbig : s_nrot, s_emax, xs_alpha[0].hi, s_tr);
+}
+
+// GEMM form: zero E (all L digits) before k_xs_params scatters the rotation coefficients into it
+template <int L>
+__global__ void __launch_bounds__(256) k_xs_zero(const PreItem* items, int sel) {
+  const PreItem it = items[blockIdx.y];
+  if (it.N < 2 || it.X1 == nullptr) return;
+  int4* E = (int4*)(sel ? it.X1 : it.X);
+  const size_t n4 = (size_t)it.N * it.N * 2 * L / 4;  // N even: a multiple of 4 ints
+  for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < n4; w += (size_t)gridDim.x * blockDim.x)
+    E[w] = make_int4(0, 0, 0, 0);
+}
+// GEMM form: X <- X + X F was written into G's buffer; copy it back over X
+template <int L>
+__global__ void __launch_bounds__(256) k_xs_copy(const PreItem* items, int sel) {
+  const PreItem it = items[blockIdx.y];
+  if (it.N < 2 || it.X1 == nullptr) return;
+  int4* X = (int4*)(sel ? it.X : it.X1);
+  const int4* S = (const int4*)it.G;
+  const size_t n4 = (size_t)it.N * it.N * 2 * L / 4;
+  for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < n4; w += (size_t)gridDim.x * blockDim.x) X[w] = S[w];
 }
 
 // acc (XD + 2 columns: digit products XD - 2 .. 2 XD - 1) +/-= K x, truncated like tmul_acc2,
@@ -328,6 +400,7 @@ __global__ void __launch_bounds__(256) k_xs_apply(const PreItem* items, int sel)
   const PreItem it = items[blockIdx.y];
   const int N = it.N, NP = N / 2;
   if (N < 2 || it.X1 == nullptr) return;
+  if (it.xs_big && *it.xs_big == 0) return;  // GEMM form: every rotation of the sweep went into E
   int32_t* X = sel ? it.X : it.X1;
   const int r0 = blockIdx.x * R;
   if (r0 >= N) return;
@@ -396,15 +469,29 @@ constexpr size_t xs_apply_smem(int N) { return (size_t)N * xs_cs<XD, R>() * XsT<
 // the two kernels of one refinement sweep at XD digits for n items (descriptors on the
 // device); sel: which X (see k_xs_params); launch count
 template <int L, int XD>
-inline int launch_xsweep(const PreItem* d, int n, int maxN, int sel, cudaStream_t st) {
-  if (n <= 0 || maxN < 2) return 0;
-  jacobi_trace_init();
-  const int thr = std::min(1024, std::max(32, ((maxN / 2 + 31) / 32) * 32));
-  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d);
+inline int launch_xs_apply(const PreItem* d, int n, int maxN, int sel, cudaStream_t st) {
   constexpr int R = XD <= 4 ? 8 : 4;  // 64 KB of rows at N = 256
   const size_t sm = xs_apply_smem<XD, R>(maxN);
   smem_optin((const void*)k_xs_apply<L, XD, R>, (int)sm);
   k_xs_apply<L, XD, R><<<dim3((maxN + R - 1) / R, n), 256, sm, st>>>(d, sel);
+  return 1;
+}
+template <int L, int XD>
+inline int launch_xsweep(const PreItem* d, int n, int maxN, int sel, cudaStream_t st) {
+  if (n <= 0 || maxN < 2) return 0;
+  jacobi_trace_init();
+  const int thr = std::min(1024, std::max(32, ((maxN / 2 + 31) / 32) * 32));
+  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d, sel, 0);
+  return 1 + launch_xs_apply<L, XD>(d, n, maxN, sel, st);
+}
+// GEMM form, first half: E from G (the caller then runs the two GEMMs, k_xs_copy and launch_xs_apply)
+template <int L, int XD>
+inline int launch_xs_emat(const PreItem* d, int n, int maxN, int sel, cudaStream_t st) {
+  if (n <= 0 || maxN < 2) return 0;
+  jacobi_trace_init();
+  k_xs_zero<L><<<dim3(32, n), 256, 0, st>>>(d, sel);
+  const int thr = std::min(1024, std::max(32, ((maxN / 2 + 31) / 32) * 32));
+  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d, sel, 1);
   return 2;
 }
 
