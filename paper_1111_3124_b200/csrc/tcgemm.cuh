@@ -42,12 +42,16 @@ namespace mpsb {
 #ifndef TC_SBK_
 #define TC_SBK_ 16
 #endif
+#ifndef TC_NSTG_
+#define TC_NSTG_ 2
+#endif
 constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
 constexpr int TC_N = TC_N_;   // output columns per CTA = MMA N
 constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
 constexpr int TC_GCH = TC_GCH_;   // slice-weight groups per chunk: TC_GCH accumulators x TC_N columns = 512 TMEM columns
 constexpr int TC_WARPS = TC_WARPS_;  // warps of k_tc_mma: warp w issues the MMAs of groups d0 + w (TC_GCH / TC_WARPS each)
 constexpr int TC_SBK = TC_SBK_;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
+constexpr int TC_NSTG = TC_NSTG_;  // shared-memory stage buffers (bulk copies run TC_NSTG - 1 stages ahead of the MMAs)
 static_assert(TC_GCH * TC_N <= 512 && TC_GCH % TC_WARPS == 0 && TC_WARPS % 4 == 0, "TMEM columns / warp roles");
 constexpr int TC_STAGE = TC_SBK * 4096 + (TC_SBK + TC_GCH - 1) * TC_N * 32;  // bytes of one stage buffer
 constexpr int TC_ATILE = TC_M * TC_K;  // bytes of one A slice tile
@@ -296,16 +300,16 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
   if (rt * TC_M >= it.rows || ct * TC_N >= ncols) return;  // CTA-uniform
   if (it.upper && ct * TC_N + TC_N <= rt * TC_M) return;      // entirely below the diagonal
   const int nkb = (it.K + TC_K - 1) / TC_K;
-  extern __shared__ __align__(1024) int8_t tcs[];  // [2][TC_STAGE]
+  extern __shared__ __align__(1024) int8_t tcs[];  // [TC_NSTG][TC_STAGE]
   __shared__ uint32_t tmem_base;
-  __shared__ __align__(8) uint64_t bar_full[2], bar_empty[2];
+  __shared__ __align__(8) uint64_t bar_full[TC_NSTG], bar_empty[TC_NSTG];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(&tmem_base)), "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < TC_NSTG; ++b) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_full[b])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tc_smem(&bar_empty[b])), "n"(TC_WARPS));  // one commit per warp
     }
@@ -387,17 +391,22 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
                    "l"(Bp + (size_t)t * b_s), "n"(TC_BTILE), "r"(fb)
                    : "memory");
   };
-  Stage cur, nxt;
-  int i = 0;             // stage index (thread 0)
+  Stage cur, nxt;        // cur: the stage whose MMAs are issued next; nxt: the next stage to load
+  int i = 0;             // index of cur
+  int nld = 0;           // stages loaded so far (index of nxt)
   bool more = false;     // nxt valid
   uint32_t started = 0;  // bit j: group d0 + j of the current chunk received an MMA
   unsigned long long nmma = 0;  // MMAs this warp issued (profiling)
   // every warp follows the stage sequence (warp-uniform values, elect.sync-predicated issue): warp 0
-  // also streams the tiles; warp w issues the MMAs of the chunk's groups d0 + 2w, d0 + 2w + 1
+  // also streams the tiles, TC_NSTG - 1 stages ahead; warp w issues the MMAs of its groups of the chunk
   if (chunk_start(cur, 0)) {
-    load_stage(cur, 0);
     nxt = cur;
-    more = next_stage(nxt);
+    more = true;
+    for (int k = 0; k < TC_NSTG - 1 && more; ++k) {
+      load_stage(nxt, nld % TC_NSTG);
+      ++nld;
+      more = next_stage(nxt);
+    }
   }
   for (int ch = 0; ch < NCH; ++ch) {
     int d0, d1, slo, shi;
@@ -407,8 +416,8 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
     if (tid == 0) s_started = 0;
     if (slo <= shi) {
       while (true) {
-        const int b = i & 1;
-        tc_mbar_wait(tc_smem(&bar_full[b]), (i >> 1) & 1);
+        const int b = i % TC_NSTG;
+        tc_mbar_wait(tc_smem(&bar_full[b]), (i / TC_NSTG) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const int8_t* buf = tcs + (size_t)b * TC_STAGE;
         const int8_t* bbuf = buf + TC_SBK * TC_ATILE;
@@ -434,20 +443,21 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
             "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
             "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
                 tc_smem(&bar_empty[b])));
-        // prefetch stage i + 1 into the other buffer once the MMAs of stage i - 1 released it (the
-        // MMAs of stage i are queued behind them, so the tensor pipe does not drain)
+        // prefetch stage i + TC_NSTG - 1 into the buffer of stage i - 1 once that stage's MMAs released
+        // it (the MMAs of stage i are queued behind them, so the tensor pipe does not drain)
         if (more) {
-          if (i >= 1) tc_mbar_wait(tc_smem(&bar_empty[b ^ 1]), ((i - 1) >> 1) & 1);
-          load_stage(nxt, b ^ 1);
-        }
-        const bool last_of_chunk = !more || nxt.ch != ch;
-        ++i;
-        if (more) {
-          cur = nxt;
+          if (nld >= TC_NSTG) tc_mbar_wait(tc_smem(&bar_empty[nld % TC_NSTG]), ((nld - TC_NSTG) / TC_NSTG) & 1);
+          load_stage(nxt, nld % TC_NSTG);
+          ++nld;
           more = next_stage(nxt);
         }
+        Stage tmp = cur;
+        const bool has_next = next_stage(tmp);
+        const bool last_of_chunk = !has_next || tmp.ch != ch;
+        ++i;
+        if (has_next) cur = tmp;
         if (last_of_chunk) {
-          tc_mbar_wait(tc_smem(&bar_empty[b]), ((i - 1) >> 1) & 1);  // every MMA of the chunk is done
+          tc_mbar_wait(tc_smem(&bar_empty[b]), ((i - 1) / TC_NSTG) & 1);  // every MMA of the chunk is done
           break;
         }
       }
@@ -534,7 +544,7 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
 // ---------------------------------------------------------------------------- launch
 
 template <int LG, int SA0, int SB0, int SB1>
-constexpr size_t tc_mma_smem() { return (size_t)2 * TC_STAGE; }
+constexpr size_t tc_mma_smem() { return (size_t)TC_NSTG * TC_STAGE; }
 
 // C = op(A) B for n items (GemmT on the device) on the tensor cores.  Z / NZA / NZB: known-zero
 // top digits of B / low digits of A / low digits of B (their slices are not multiplied).

@@ -316,6 +316,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
       GemmT g{Af, M, pb.eA1, Af, M, pb.eA1, pb.Dm, N, nullptr, nullptr, nullptr, N, N, M, 1, 0, 0, nullptr};
       g.ghead = gh + 1;  // sum of M products, each |.| < 2^(2 eA1 - 2)
       g.eCwrite = pb.eG;
+      g.upper = 1;  // k_xs_params reads the diagonal and G(p, q), p < q
       gt[(2 * NSIT + 4 + 2 * w) * stride] = g;
       // GEMM form (R26): E in the X buffer the sweep does not rotate (exponent 0),
       // F = E + E (E / 2) into Af (A_t is dead once G is formed), X + X F into G's buffer

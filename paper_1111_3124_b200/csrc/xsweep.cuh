@@ -212,8 +212,38 @@ __global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
         const int32_t* gp = it.G + ((size_t)(q * 2) * L) * N + p;  // G(p, q), column q
         const dd gr = xs_g_dd<L, XD>(gp, N), gi = xs_g_dd<L, XD>(gp + (size_t)L * N, N);
         const dd g2 = dd_add(dd_mul(gr, gr), dd_mul(gi, gi));
-        if (g2.hi > thr2 * pa) {
-          const dd d = dd_add(aq, dd_neg(ap));
+        const dd d = dd_add(aq, dd_neg(ap));
+        // GEMM form, |gamma|^2 <= 2^-60 d^2 (every pair but the near-degenerate ones): the rotation
+        // to first order, s = gamma / d (R17's s = sgn(d) gamma / (r c) has r c = |d| (1 + O(|gamma|^2
+        // / d^2)): relative 2^-60 in a coefficient whose residual is second order anyway), c = 1
+        if (gemm && g2.hi > thr2 * pa && g2.hi <= 8.673617379884035e-19 * (d.hi * d.hi)) {
+          const dd inv = dd_div({1.0, 0.0}, d);
+          int32_t Kr[XD], Ki[XD];
+          const dd sr = xs_round_grid<XD>(dd_mul(inv, gr), Kr);
+          const dd si = xs_round_grid<XD>(dd_mul(inv, gi), Ki);
+          if (fabs(sr.hi) < ldexp(1.0, -T::EBIG) && fabs(si.hi) < ldexp(1.0, -T::EBIG)) {
+            flag = 4;
+            int32_t* e1 = E + ((size_t)(q * 2) * L + (L - XD)) * N + p;
+            int32_t* e2 = E + ((size_t)(p * 2) * L + (L - XD)) * N + q;
+#pragma unroll
+            for (int k = 0; k < XD; ++k) {
+              e1[(size_t)k * N] = Kr[k];
+              e1[(size_t)(L + k) * N] = Ki[k];
+              e2[(size_t)k * N] = -Kr[k];
+              e2[(size_t)(L + k) * N] = Ki[k];
+            }
+            if (jac_trace_items) {
+              atomicAdd(&s_nrot, 1);
+              int ex;
+              frexp(fmax(fabs(sr.hi), fabs(si.hi)), &ex);
+              atomicMax(&s_emax, ex);
+            }
+            const dd tg = dd_mul(g2, inv);  // t |g| to first order (signed like d)
+            xs_alpha[p] = dd_add(ap, dd_neg(tg));
+            xs_alpha[q] = dd_add(aq, tg);
+          }
+        }
+        if (flag == 0 && g2.hi > thr2 * pa) {
           const dd ad = d.hi < 0 ? dd_neg(d) : d;
           const dd r = dd_sqrt(dd_add(dd_mul(d, d), dd_scale(g2, 2)));
           const dd c = dd_sqrt(dd_div(dd_add(ad, r), dd_scale(r, 1)));
