@@ -332,11 +332,11 @@ def main():
         torch.cuda.synchronize(dev)
         barrier()
     ms = e0.elapsed_time(e1)
-    counts = mps.profile_counts(8)
+    counts = mps.profile_counts(9)
     q = {name: mps.profile_query(k) for name, k in
          (("jacobi", mps.PROF_JACOBI), ("contraction", mps.PROF_CONTRACT), ("truncate_split", mps.PROF_FINALIZE),
           ("precondition", mps.PROF_PRECOND), ("recover_v", mps.PROF_RECOVER), ("binary64_jacobi", mps.PROF_JDB),
-          ("refinement_sweeps", mps.PROF_XS), ("tensor_mma", mps.PROF_TCMMA))}
+          ("refinement_sweeps", mps.PROF_XS), ("tensor_mma", mps.PROF_TCMMA), ("binary32_jacobi", mps.PROF_JSP))}
     mps.profile_enable(False)
     if dist is not None:
         t = torch.tensor([ms], device=dev)
@@ -345,19 +345,21 @@ def main():
     total_items = batch * args.steps * world
     value = total_items / (ms / 1e3)
 
-    # Roofline of the dominant kernel, the binary64 block Jacobi k_jacobi_db (fp64 pipe):
-    # algorithmic DFMA (counted per block-pair visit on the device) over its
-    # launch time (CUDA events on the launching stream), against the measured DFMA peak.
+    # Rooflines of the three kernel classes that make up the step; the one with the
+    # largest share of the step is reported as `roofline`, the others under `roofline.kernels`.
+    #  * k_tc_mma (every tensor-core GEMM): int8 MACs issued (counted on the device) over the time of
+    #    all its launches (CUDA events on the launching stream), against the int8 dense peak = the
+    #    measured bf16 peak x 2 (nominal 4.5 / 2.25 PFLOP/s) / 2 (MAC = 2 ops);
+    #  * k_jacobi_blk<double> (binary64 block Jacobi, fp64 pipe): algorithmic DFMA per block-pair
+    #    visit over its launch time, against the measured DFMA peak;
+    #  * k_jacobi_blk<float> (its binary32 first phase, R27; the time includes the hand-over GEMMs):
+    #    algorithmic FFMA against 128 lanes x 148 SMs x the SM clock under load.
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_INT_PEAKS.json")))
     dfma_peak = peaks["dfma_per_s"]
-    jdb_ms, jdb_n = q["binary64_jacobi"]
-    achieved = counts[mps.CNT_JDB_DFMA] / (jdb_ms / 1e3) if jdb_ms else None
-    traffic = None
+    traffic_tab = {}
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(f"jacobi_db_chi{chi}_p{p}_batch{batch}")
-    # the tensor-core GEMMs (all k_tc_mma launches): int8 MACs issued over their launch time,
-    # against the int8 dense peak = the measured bf16 peak x 2 (nominal 4.5 / 2.25 PFLOP/s) / 2
+        traffic_tab = json.load(open(tfile))
     mp_file = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(mp_file):
         i8_peak = json.load(open(mp_file))["bf16_tflops"] * 1e12
@@ -365,11 +367,37 @@ def main():
     else:
         i8_peak = 2.25e15
         i8_src = "nominal 4.5 POPS int8 dense (B200_PROFILING.md) / 2"
-    tc_ms, tc_n = q["tensor_mma"]
-    tc_rate = counts[mps.CNT_TC_MAC] / (tc_ms / 1e3) if tc_ms else None
-    # the p-bit Jacobi kernel (only the items the first-order finish did not close, R23)
+
+    def kclass(name, bound, unit, count, peak, peak_src, kernel, counts_note, traffic_key):
+        t_ms, n_l = q[name]
+        rate = count / (t_ms / 1e3) if t_ms else None
+        tr = traffic_tab.get(traffic_key)
+        return {"bound": bound, "achieved": rate, "peak": peak, "unit": unit, "frac": (rate / peak) if rate else None,
+                "traffic": tr.get("bytes_per_launch") if isinstance(tr, dict) else tr,
+                "traffic_source": tr.get("source") if isinstance(tr, dict) else None,
+                "kernel": kernel, "peak_source": peak_src, "achieved_counts": counts_note,
+                "ops_per_step": count / args.steps, "kernel_ms_per_step": t_ms / args.steps,
+                "launches_per_step": n_l / args.steps, "share_of_step": t_ms / ms if ms else None}
+
+    sm_mhz = (clk.summary() or {}).get("sm_mhz") or 1965.0
+    classes = {
+        "tensor_gemm": kclass("tensor_mma", "tensor", "int8 MAC/s", counts[mps.CNT_TC_MAC], i8_peak, i8_src,
+                              "k_tc_mma (all launches: contraction, Newton-Schulz, refinement-sweep, A_1 / P, Gram, "
+                              "first-order finish and V-recovery GEMMs; tcgen05 kind::i8, TMEM)",
+                              "MMAs issued x 128 x TC_N x 32 int8 MACs (device counter)", f"tc_mma_chi{chi}_p{p}"),
+        "binary64_jacobi": kclass("binary64_jacobi", "alu", "DFMA/s", counts[mps.CNT_JDB_DFMA], dfma_peak,
+                                  "MEASURED_INT_PEAKS.json dfma_per_s (tools/peaks/int_peak.cu)",
+                                  "k_jacobi_blk<double> (binary64 block Jacobi, fp64 pipe)",
+                                  "algorithmic DFMA per block-pair visit: Gram 4 nc2(nc2+1)/2 M, inner rotations, "
+                                  "W applied to A and V 4 nc2^2 (M + N) (DESIGN.md §4)", f"jacobi_db_chi{chi}_p{p}_batch{batch}"),
+        "binary32_jacobi": kclass("binary32_jacobi", "alu", "FFMA/s", counts[mps.CNT_JSP_FFMA], 128 * 148 * sm_mhz * 1e6,
+                                  "128 FP32 lanes x 148 SMs x the sampled SM clock (B200_PROFILING.md unit counts)",
+                                  "k_jacobi_blk<float> + hand-over (binary32 first phase of the block Jacobi, R27)",
+                                  "algorithmic FFMA per block-pair visit (same formula as the binary64 phase)",
+                                  f"jacobi_sp_chi{chi}_p{p}_batch{batch}"),
+    }
+    dom = max(classes, key=lambda k_: classes[k_]["share_of_step"] or 0.0)
     jac_ms, jac_n = q["jacobi"]
-    jac_exec = executed_imad_wide(counts, chi, p)
     # end to end through the public C API with host buffers (pinned), one step; the device
     # buffers of the timed path are released first (at 512 bits both sets do not fit in HBM)
     e2e = None
@@ -419,27 +447,13 @@ def main():
             "vs_baseline": None, "dtype": f"int32 radix-2^28 limbs (fixed-point columns) + u32-limb float, p={p}",
             "data": "synthetic",
             "config": dict(workload_config(batch, chi, p, nd, world), sweeps_mean=float(np.mean(sweeps))),
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": dfma_peak, "unit": "DFMA/s",
-                         "frac": (achieved / dfma_peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_jacobi_db (binary64 block Jacobi, fp64 pipe)",
-                         "peak_source": "MEASURED_INT_PEAKS.json dfma_per_s (tools/peaks/int_peak.cu)",
-                         "achieved_counts": "algorithmic DFMA per block-pair visit: Gram 4 nc2(nc2+1)/2 M, "
-                                            "inner rotations, W applied to A and V 4 nc2^2 (M + N) (DESIGN.md §4)",
-                         "dfma_per_step": counts[mps.CNT_JDB_DFMA] / args.steps,
-                         "kernel_ms_per_launch": jdb_ms / jdb_n if jdb_n else None,
-                         "share_of_step": jdb_ms / ms if ms else None,
-                         "step_ms": {k: v[0] for k, v in q.items()},
-                         "tensor_gemm": {"bound": "tensor", "achieved": tc_rate, "peak": i8_peak,
-                                         "unit": "int8 MAC/s", "frac": (tc_rate / i8_peak) if tc_rate else None,
-                                         "peak_source": i8_src, "kernel": "k_tc_mma (all launches)",
-                                         "macs_per_step": counts[mps.CNT_TC_MAC] / args.steps,
-                                         "share_of_step": tc_ms / ms if ms else None, "launches": tc_n},
-                         "p_bit_jacobi": {"kernel": "k_jacobi (items not closed by the first-order finish)",
-                                          "executed_imad_wide_per_s": jac_exec / (jac_ms / 1e3) if jac_ms else None,
-                                          "peak": peaks["imad_wide_s32_per_s"],
-                                          "share_of_step": jac_ms / ms if ms else None,
-                                          "counters": {"rotations": counts[0], "pair_evals": counts[1],
-                                                       "u_digit_products": counts[4], "certified_stops": counts[5]}}},
+            "roofline": dict(classes[dom], dominant=dom,
+                             step_ms={k: v[0] / args.steps for k, v in q.items()},
+                             kernels={k: v for k, v in classes.items() if k != dom},
+                             p_bit_jacobi={"kernel": "k_jacobi (items not closed by the first-order finish, R23)",
+                                           "share_of_step": jac_ms / ms if ms else None,
+                                           "counters": {"rotations": counts[0], "pair_evals": counts[1],
+                                                        "u_digit_products": counts[4], "certified_stops": counts[5]}}),
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(),
         }

@@ -171,8 +171,8 @@ def debug_mpf(p: int, op: str, a, b=None):
 
 
 PROF_JACOBI, PROF_CONTRACT, PROF_FINALIZE, PROF_PRECOND, PROF_RECOVER = 0, 1, 2, 3, 4
-PROF_JDB, PROF_XS, PROF_TCMMA = 5, 6, 7  # k_jacobi_db, refinement sweeps, k_tc_mma (inside the above)
-CNT_JDB_DFMA, CNT_TC_MAC = 6, 7  # profile_counts(): algorithmic DFMA of k_jacobi_db, int8 MACs of k_tc_mma
+PROF_JDB, PROF_XS, PROF_TCMMA, PROF_JSP = 5, 6, 7, 8  # binary64 block Jacobi, refinement sweeps, k_tc_mma, binary32 block Jacobi + hand-over (inside the above)
+CNT_JDB_DFMA, CNT_TC_MAC, CNT_JSP_FFMA = 6, 7, 8  # profile_counts(): algorithmic DFMA / FFMA of the block Jacobi phases, int8 MACs of k_tc_mma
 
 
 def profile_enable(on: bool = True):

@@ -42,11 +42,12 @@ enum { PROF_JACOBI = 0, PROF_CONTRACT = 1, PROF_FINALIZE = 2, PROF_PRECOND = 3, 
        PROF_JDB = 5,    // k_jacobi_db (inside PROF_PRECOND)
        PROF_XS = 6,     // refinement sweeps k_xs_params + k_xs_apply (inside PROF_PRECOND)
        PROF_TCMMA = 7,  // every k_tc_mma launch (inside the classes above)
-       PROF_N = 8 };
+       PROF_JSP = 8,    // binary32 phase of the block Jacobi + hand-over (inside PROF_PRECOND, R27)
+       PROF_N = 9 };
 // device counters of the profiling run (mps_profile_counts_n): [0] p-bit rotations, [1] pair
 // evaluations, [2] norm-pass sweeps x M x N, [3] recovery N^2 M, [4] phase-U digit products x M,
 // [5] certified stops, [6] algorithmic DFMA of k_jacobi_db, [7] int8 MACs issued by k_tc_mma
-enum { CNT_JDB_DFMA = 6, CNT_TC_MAC = 7, CNT_N = 16 };
+enum { CNT_JDB_DFMA = 6, CNT_TC_MAC = 7, CNT_JSP_FFMA = 8, CNT_N = 16 };
 void prof_mark(int which, int begin, cudaStream_t st);
 // device buffer of 4 running totals while profiling is on (else null), see k_accum_stats
 unsigned long long* prof_counts();

@@ -38,6 +38,10 @@ struct PreItem {
   // GEMM form of the refinement sweeps (R26): exponents {0, -1} of E and E/2; per sweep
   // the number of pairs applied as sequential exact rotations (the others enter E)
   int64_t* eXs; int* xs_big;
+  // binary32 first phase of the block Jacobi (R27): As, Vs its matrices (null: no such
+  // phase), V0 = binary64 copy of Vs, Rm = V0^H V0, Aj = Theta_d V_d (the binary64 phase then runs
+  // on Aj with V preset in Vd), sweeps_s its sweep count
+  float2* As; float2* Vs; double2* V0; double2* Rm; double2* Aj; int* sweeps_s;
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -66,6 +70,7 @@ __global__ void k_fx_to_d(const PreItem* items) {
       const int32_t* pi = it.A0 + ((size_t)(c * 2 + 1) * L) * M + r;
       const double2 v = make_double2(fx_top_double<L>(pr, M), fx_top_double<L>(pi, M));
       it.Ad[(size_t)c * M + r] = v;
+      if (it.As) it.As[(size_t)c * M + r] = make_float2((float)v.x, (float)v.y);
       s += v.x * v.x + v.y * v.y;
     }
     rmax = fmax(rmax, s);
@@ -76,16 +81,17 @@ __global__ void k_fx_to_d(const PreItem* items) {
 // all-reduce of four sums in 6 shuffles instead of 20: the first two levels exchange half of
 // the values (each lane keeps the pair / the value its lane bits select), then a plain
 // butterfly; finally every lane fetches the four totals from lanes 0..3
-__device__ __forceinline__ void warp_sum4_d(double& a, double& b, double& c, double& d) {
+template <typename T>
+__device__ __forceinline__ void warp_sum4_d(T& a, T& b, T& c, T& d) {
   const int lane = threadIdx.x & 31;
   const bool h16 = lane & 16, h8 = lane & 8;
   // level 16: keep (a, b) if bit 4 clear else (c, d)
-  double x0 = h16 ? c : a, x1 = h16 ? d : b;
-  const double y0 = h16 ? a : c, y1 = h16 ? b : d;
+  T x0 = h16 ? c : a, x1 = h16 ? d : b;
+  const T y0 = h16 ? a : c, y1 = h16 ? b : d;
   x0 += __shfl_xor_sync(0xffffffffu, y0, 16);
   x1 += __shfl_xor_sync(0xffffffffu, y1, 16);
   // level 8: keep x0 if bit 3 clear else x1
-  double z = h8 ? x1 : x0;
+  T z = h8 ? x1 : x0;
   z += __shfl_xor_sync(0xffffffffu, h8 ? x0 : x1, 8);
 #pragma unroll
   for (int off = 4; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
@@ -151,10 +157,10 @@ __host__ __device__ inline int jd_gram_parts(int bs) {
   const int TU = bs * (bs + 1) / 2, P = JD_THREADS / TU;
   return P < 1 ? 1 : (P > 4 ? 4 : P);
 }
-inline size_t jd_smem(int M) {
+inline size_t jd_smem(int M, size_t el = 16) {  // el: bytes of a complex element (16 binary64, 8 binary32)
   const int bs = jd_bs(M), nc2 = 2 * bs;
-  const size_t scr = (size_t)(jd_gram_parts(bs) - 1) * (bs * (bs + 1) / 2) * 4 * 16;
-  return (size_t)nc2 * jd_mp(M) * 16 + (size_t)nc2 * nc2 * 16 + (size_t)nc2 * (nc2 + 1) * 16 + scr + 64;
+  const size_t scr = (size_t)(jd_gram_parts(bs) - 1) * (bs * (bs + 1) / 2) * 4 * el;
+  return (size_t)nc2 * jd_mp(M) * el + (size_t)nc2 * nc2 * el + (size_t)nc2 * (nc2 + 1) * el + scr + 64;
 }
 
 // MPS_JD_PROF=1 (debug): clock64 cycles of thread 0 per phase, summed over CTAs:
@@ -163,22 +169,61 @@ inline size_t jd_smem(int M) {
 static __device__ unsigned long long jd_prof[8];
 static __device__ int jd_prof_on;
 
+// Real type of the block Jacobi: binary64, or binary32 for the first phase (R27)
+__device__ __forceinline__ double2 mk2(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ float2 mk2(float x, float y) { return make_float2(x, y); }
+__device__ __forceinline__ double jd_rsqrt(double x) { return rsqrt(x); }
+__device__ __forceinline__ float jd_rsqrt(float x) { return rsqrtf(x); }
+// one complex element global -> shared (valid = 0: zero fill)
+template <typename T2>
+__device__ __forceinline__ void cp_async_el(void* smem, const void* gmem, bool valid) {
+  if constexpr (sizeof(T2) == 16) {
+    cp_async16(smem, gmem, valid ? 16 : 0);
+  } else {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+  }
+}
+template <typename T> struct JdT;
+template <> struct JdT<double> {
+  using T2 = double2;
+  static constexpr int MINB = JD_MINB;
+  static constexpr double GRAM_OFF = JD_GRAM_OFF, STOP_OFF = 0.0, HUGE_ = 1.0e308, NORM_RATIO = 1048576.0;
+  static __device__ __forceinline__ double2* A(const PreItem& it) { return it.Aj ? it.Aj : it.Ad; }
+  static __device__ __forceinline__ double2* V(const PreItem& it) { return it.Vd; }
+  static __device__ __forceinline__ double tol(int M) { return JD_TOL; }
+  static __device__ __forceinline__ double thr(double tol, double sp, double sq) { return tol * tol * sp * sq; }
+};
+// binary32: Gram-form inner sweeps while a relative off-diagonal exceeds 2^-10 (G's rounding is
+// 2^-24 of the largest column norm^2: norms^2 within 2^8), hand-over to binary64 once a whole sweep
+// saw none above 2^-11 (its rotations leave ~2^-22, the binary32 floor eps sqrt(M) is ~2^-20)
+template <> struct JdT<float> {
+  using T2 = float2;
+  static constexpr int MINB = 1;
+  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 256.0f;
+  static __device__ __forceinline__ float2* A(const PreItem& it) { return it.As; }
+  static __device__ __forceinline__ float2* V(const PreItem& it) { return it.Vs; }
+  static __device__ __forceinline__ float tol(int M) { return 4.0f * M * 5.9604645e-8f; }  // 4 M 2^-24
+  static __device__ __forceinline__ float thr(float tol, float sp, float sq) { return (tol * sp) * (tol * sq); }
+};
+
 // dst[:, s_col[j]] = src (R rows, column stride ld, 2bs columns) x W  (thread: row r, half h)
-__device__ __forceinline__ void jd_apply_w(const double2* src, int ld, double2* dst, int R, const double2* W, int bs,
+template <typename T, typename T2>
+__device__ __forceinline__ void jd_apply_w(const T2* src, int ld, T2* dst, int R, const T2* W, int bs,
                                            const int* s_col) {
   const int nc2 = 2 * bs;
   for (int t = threadIdx.x; t < 2 * R; t += blockDim.x) {
     const int r = t % R, h = t / R;
-    double2 acc[JD_BS_MAX];
+    T2 acc[JD_BS_MAX];
 #pragma unroll
-    for (int j = 0; j < JD_BS_MAX; ++j) acc[j] = make_double2(0.0, 0.0);
+    for (int j = 0; j < JD_BS_MAX; ++j) acc[j] = mk2(T(0), T(0));
 #pragma unroll 2
     for (int l = 0; l < nc2; ++l) {
-      const double2 v = src[(size_t)l * ld + r];
+      const T2 v = src[(size_t)l * ld + r];
 #pragma unroll
       for (int j = 0; j < JD_BS_MAX; ++j) {
         if (j < bs) {
-          const double2 w = W[(size_t)(h * bs + j) * nc2 + l];
+          const T2 w = W[(size_t)(h * bs + j) * nc2 + l];
           acc[j].x = fma(v.x, w.x, fma(-v.y, w.y, acc[j].x));
           acc[j].y = fma(v.x, w.y, fma(v.y, w.x, acc[j].y));
         }
@@ -197,14 +242,14 @@ __device__ __forceinline__ void jd_apply_w(const double2* src, int ld, double2* 
 // rotation parameters of the oracle's formula (R17 form): d = alpha_q - alpha_p,
 // r = sqrt(d^2 + 4|g|^2), c = sqrt((|d| + r) / 2r), s = sgn(d) g / (r c)
 // (two reciprocal square roots, no division: 1/r, c^2 = (|d|/r + 1)/2, 1/c, s = sgn(d) g (1/r)(1/c))
-__device__ __forceinline__ void jd_rot(double sp, double sq, double gr, double gi, double g2, double& c, double& sr,
-                                       double& si) {
-  const double d = sq - sp;
-  const double ir = rsqrt(d * d + 4.0 * g2);
-  const double c2 = 0.5 * fma(fabs(d), ir, 1.0);
-  const double ic = rsqrt(c2);
+template <typename T>
+__device__ __forceinline__ void jd_rot(T sp, T sq, T gr, T gi, T g2, T& c, T& sr, T& si) {
+  const T d = sq - sp;
+  const T ir = jd_rsqrt(d * d + T(4) * g2);
+  const T c2 = T(0.5) * fma(fabs(d), ir, T(1));
+  const T ic = jd_rsqrt(c2);
   c = c2 * ic;
-  const double sc = (d < 0 ? -ir : ir) * ic;
+  const T sc = (d < 0 ? -ir : ir) * ic;
   sr = gr * sc;
   si = gi * sc;
 }
@@ -212,7 +257,10 @@ __device__ __forceinline__ void jd_rot(double sp, double sq, double gr, double g
 // C CTAs (a thread-block cluster when C > 1) share one item: the block pairs of a step are
 // dealt round-robin to the CTAs and the steps are separated by cluster barriers (few items in
 // flight: an MPS layer).  The rotation sequence does not depend on C.
-static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const PreItem* items, int C) {
+template <typename T>
+__global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const PreItem* items, int C) {
+  using T2 = typename JdT<T>::T2;
+  constexpr bool SP = sizeof(T) == 4;  // the binary32 first phase (R27)
   namespace cg = cooperative_groups;
   const int crank = C > 1 ? (int)(blockIdx.x % C) : 0;
   const PreItem it = items[C > 1 ? blockIdx.x / C : blockIdx.x];
@@ -225,21 +273,23 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
   const int bs = jd_bs(M), nb = (N + bs - 1) / bs, nbe = nb + (nb & 1), nc2 = 2 * bs, MP = jd_mp(M);
   const int nh = bs;  // Gram: 2x2 tiles of entries (i, j), (i, j+bs), (i+bs, j), (i+bs, j+bs)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  extern __shared__ double2 jds[];
-  double2* Ab = jds;                       // [2bs][MP] block columns
-  double2* W = jds + (size_t)nc2 * MP;     // [2bs][2bs] column-major
-  double2* G = W + (size_t)nc2 * nc2;      // [2bs][2bs + 1] row-major (Gram form)
-  double2* Gs = G + (size_t)nc2 * (nc2 + 1);  // Gram partial sums of parts 1..P-1
+  extern __shared__ __align__(16) unsigned char jds_raw[];
+  T2* Ab = (T2*)jds_raw;              // [2bs][MP] block columns
+  T2* W = Ab + (size_t)nc2 * MP;     // [2bs][2bs] column-major
+  T2* G = W + (size_t)nc2 * nc2;      // [2bs][2bs + 1] row-major (Gram form)
+  T2* Gs = G + (size_t)nc2 * (nc2 + 1);  // Gram partial sums of parts 1..P-1
   const int GL = nc2 + 1, lgc = __ffs(nc2) - 1;  // nc2 = 2^lgc
   __shared__ int s_any, s_rot, s_gram, s_col[32];
-  __shared__ double s_c[16], s_sr[16], s_si[16];
+  __shared__ T s_c[16], s_sr[16], s_si[16];
   __shared__ int s_on[16], s_p[16], s_q[16];
   __shared__ unsigned long long s_off;  // max rel^2 = |g|^2 / (alpha_p alpha_q) of this CTA's sweep (bits)
-  double2* A = it.Ad;
-  double2* V = it.Vd;
-  for (int t = crank * blockDim.x + threadIdx.x; t < N * N; t += C * blockDim.x)
-    V[t] = make_double2((t % N) == (t / N) ? 1.0 : 0.0, 0.0);
-  const double tol = JD_TOL;
+  T2* A = JdT<T>::A(it);
+  T2* V = JdT<T>::V(it);
+  if (SP && A == nullptr) return;  // item without the binary32 phase
+  if (SP || it.Aj == nullptr)      // (binary64 after a binary32 phase: V is preset, R27)
+    for (int t = crank * blockDim.x + threadIdx.x; t < N * N; t += C * blockDim.x)
+      V[t] = mk2((t % N) == (t / N) ? T(1) : T(0), T(0));
+  const T tol = JdT<T>::tol(M);
   const bool prof = jd_prof_on && threadIdx.x == 0;
   long long tm = prof ? clock64() : 0;
   auto mark = [&](int k) {
@@ -251,9 +301,13 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
   };
   // 1.0 once this thread saw |g|^2 / (alpha_p alpha_q) > JD_GRAM_OFF^2 in the sweep (one atomic per
   // sweep; only that comparison is used, so no division on the rotation path)
+  // (binary32 phase: 2.0 above its Gram-form threshold, 1.0 above the level it stops at)
   double off_t = 0.0;
-  auto note_off = [&](double g2, double sp, double sq) {
-    if (sp > 0 && sq > 0 && g2 > (JD_GRAM_OFF * JD_GRAM_OFF) * (sp * sq)) off_t = 1.0;
+  auto note_off = [&](T g2, T sp, T sq) {
+    if (sp > 0 && sq > 0) {
+      if (g2 > T(JdT<T>::GRAM_OFF * JdT<T>::GRAM_OFF) * (sp * sq)) off_t = SP ? 2.0 : 1.0;
+      else if (SP && off_t < 1.0 && g2 > T(JdT<T>::STOP_OFF * JdT<T>::STOP_OFF) * (sp * sq)) off_t = 1.0;
+    }
   };
   int sweep = 0;
   for (sweep = 1; sweep <= 40; ++sweep) {
@@ -266,7 +320,7 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
     // Gram-form sweep while the previous sweep's largest relative off-diagonal was big
     const bool gram_sweep =
         sweep == 1 || __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[(sweep - 1) & 1]) >
-                          JD_GRAM_OFF * JD_GRAM_OFF;
+                          (SP ? 1.5 : JD_GRAM_OFF * JD_GRAM_OFF);
     for (int step = 0; step < nbe - 1; ++step) {
       for (int bp = crank; bp < nbe / 2; bp += C) {
         int I, J;
@@ -290,7 +344,7 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
         __syncthreads();
         for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {  // (l, r) advance by blockDim
           const int c = s_col[l];  // cp.async: all loads in flight at once (absent columns zero-filled)
-          cp_async16(Ab + (size_t)l * MP + r, c >= 0 ? (const void*)(A + (size_t)c * M + r) : (const void*)A, c >= 0 ? 16 : 0);
+          cp_async_el<T2>(Ab + (size_t)l * MP + r, c >= 0 ? (const void*)(A + (size_t)c * M + r) : (const void*)A, c >= 0);
           r += blockDim.x;
           while (r >= M) { r -= M; ++l; }
         }
@@ -304,20 +358,20 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
           // the others mirrored; thread (tile, part of the rows), parts 1.. sum through Gs
           const int t = threadIdx.x;
           const int TU = nh * (nh + 1) / 2, NP = jd_gram_parts(bs);
-          double2 g[4] = {make_double2(0, 0), make_double2(0, 0), make_double2(0, 0), make_double2(0, 0)};
+          T2 g[4] = {mk2(T(0), T(0)), mk2(T(0), T(0)), mk2(T(0), T(0)), mk2(T(0), T(0))};
           const int tile = t % TU, part = t / TU;
           int ti = 0, tj = tile;  // tile -> (ti, tj), ti <= tj (row ti holds nh - ti tiles)
           while (tj >= nh - ti) { tj -= nh - ti; ++ti; }
           tj += ti;
           if (t < NP * TU) {
             const int r0 = part * M / NP, r1 = (part + 1) * M / NP;
-            const double2* a0 = Ab + (size_t)ti * MP;
-            const double2* a1 = Ab + (size_t)(ti + bs) * MP;
-            const double2* b0 = Ab + (size_t)tj * MP;
-            const double2* b1 = Ab + (size_t)(tj + bs) * MP;
+            const T2* a0 = Ab + (size_t)ti * MP;
+            const T2* a1 = Ab + (size_t)(ti + bs) * MP;
+            const T2* b0 = Ab + (size_t)tj * MP;
+            const T2* b1 = Ab + (size_t)(tj + bs) * MP;
 #pragma unroll 4
             for (int r = r0; r < r1; ++r) {
-              const double2 x0 = a0[r], x1 = a1[r], y0 = b0[r], y1 = b1[r];
+              const T2 x0 = a0[r], x1 = a1[r], y0 = b0[r], y1 = b1[r];
               // conj(x) y
               g[0].x = fma(x0.x, y0.x, fma(x0.y, y0.y, g[0].x)); g[0].y = fma(x0.x, y0.y, fma(-x0.y, y0.x, g[0].y));
               g[1].x = fma(x0.x, y1.x, fma(x0.y, y1.y, g[1].x)); g[1].y = fma(x0.x, y1.y, fma(-x0.y, y1.x, g[1].y));
@@ -334,7 +388,7 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
             for (int pp = 1; pp < NP; ++pp) {  // parts in order: the sum does not depend on timing
 #pragma unroll
               for (int k = 0; k < 4; ++k) {
-                const double2 o = Gs[((size_t)(pp - 1) * TU + tile) * 4 + k];
+                const T2 o = Gs[((size_t)(pp - 1) * TU + tile) * 4 + k];
                 g[k].x += o.x;
                 g[k].y += o.y;
               }
@@ -344,17 +398,17 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
             G[(size_t)(ti + bs) * GL + tj] = g[2];
             G[(size_t)(ti + bs) * GL + tj + bs] = g[3];
             if (ti != tj) {  // G(b, a) = conj G(a, b)
-              G[(size_t)tj * GL + ti] = make_double2(g[0].x, -g[0].y);
-              G[(size_t)(tj + bs) * GL + ti] = make_double2(g[1].x, -g[1].y);
-              G[(size_t)tj * GL + ti + bs] = make_double2(g[2].x, -g[2].y);
-              G[(size_t)(tj + bs) * GL + ti + bs] = make_double2(g[3].x, -g[3].y);
+              G[(size_t)tj * GL + ti] = mk2(g[0].x, -g[0].y);
+              G[(size_t)(tj + bs) * GL + ti] = mk2(g[1].x, -g[1].y);
+              G[(size_t)tj * GL + ti + bs] = mk2(g[2].x, -g[2].y);
+              G[(size_t)(tj + bs) * GL + ti + bs] = mk2(g[3].x, -g[3].y);
             }
           }
           __syncthreads();
           if (warp == 0) {  // column norms^2 within 2^20: Gram form for this block pair (lane = column)
-            double mx = 0, mn = 1.0e308;  // 1e308: no valid column
+            T mx = 0, mn = JdT<T>::HUGE_;  // HUGE_: no valid column
             if (lane < nc2) {
-              const double a = G[(size_t)lane * GL + lane].x;
+              const T a = G[(size_t)lane * GL + lane].x;
               if (s_col[lane] >= 0 && a > 0) { mx = a; mn = a; }
             }
 #pragma unroll
@@ -362,11 +416,11 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
               mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
               mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             }
-            if (lane == 0) s_gram = mn == 1.0e308 || mx <= mn * 1048576.0;
+            if (lane == 0) s_gram = mn == JdT<T>::HUGE_ || mx <= mn * JdT<T>::NORM_RATIO;
           }
         }
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
-          W[t] = make_double2((t % nc2) == (t / nc2) ? 1.0 : 0.0, 0.0);
+          W[t] = mk2((t % nc2) == (t / nc2) ? T(1) : T(0), T(0));
         __syncthreads();
         if (prof && gram_sweep) {  // [7]: Gram products + mode decision (moved out of "inner")
           const long long t = clock64();
@@ -382,12 +436,12 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
               inner_pair(s2, i, p, q);
               int on = 0;
               if (s_col[p] >= 0 && s_col[q] >= 0) {
-                const double sp = G[(size_t)p * GL + p].x, sq = G[(size_t)q * GL + q].x;
-                const double2 gg = G[(size_t)p * GL + q];
-                const double g2 = gg.x * gg.x + gg.y * gg.y;
+                const T sp = G[(size_t)p * GL + p].x, sq = G[(size_t)q * GL + q].x;
+                const T2 gg = G[(size_t)p * GL + q];
+                const T g2 = gg.x * gg.x + gg.y * gg.y;
                 note_off(g2, sp, sq);
-                if (g2 > tol * tol * sp * sq && g2 != 0.0) {
-                  double c, sr, si;
+                if (g2 > JdT<T>::thr(tol, sp, sq) && g2 != T(0)) {
+                  T c, sr, si;
                   jd_rot(sp, sq, gg.x, gg.y, g2, c, sr, si);
                   s_c[i] = c; s_sr[i] = sr; s_si[i] = si;
                   on = 1;
@@ -405,25 +459,25 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
               if (t < bs * bs) {
                 const int a = t / bs, b = t % bs;
                 const int pa = s_p[a], qa = s_q[a], pb = s_p[b], qb = s_q[b];
-                double2 b00 = G[(size_t)pa * GL + pb], b01 = G[(size_t)pa * GL + qb];
-                double2 b10 = G[(size_t)qa * GL + pb], b11 = G[(size_t)qa * GL + qb];
+                T2 b00 = G[(size_t)pa * GL + pb], b01 = G[(size_t)pa * GL + qb];
+                T2 b10 = G[(size_t)qa * GL + pb], b11 = G[(size_t)qa * GL + qb];
                 if (s_on[b]) {  // columns:  x' = c x - conj(s) y,  y' = s x + c y
-                  const double c = s_c[b], sr = s_sr[b], si = s_si[b];
-                  double2 x = b00, y = b01;
-                  b00 = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-                  b01 = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                  const T c = s_c[b], sr = s_sr[b], si = s_si[b];
+                  T2 x = b00, y = b01;
+                  b00 = mk2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                  b01 = mk2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
                   x = b10; y = b11;
-                  b10 = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-                  b11 = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                  b10 = mk2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                  b11 = mk2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
                 }
                 if (s_on[a]) {  // rows:  x' = c x - s y,  y' = conj(s) x + c y
-                  const double c = s_c[a], sr = s_sr[a], si = s_si[a];
-                  double2 x = b00, y = b10;
-                  b00 = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
-                  b10 = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
+                  const T c = s_c[a], sr = s_sr[a], si = s_si[a];
+                  T2 x = b00, y = b10;
+                  b00 = mk2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
+                  b10 = mk2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
                   x = b01; y = b11;
-                  b01 = make_double2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
-                  b11 = make_double2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
+                  b01 = mk2(c * x.x - (sr * y.x - si * y.y), c * x.y - (sr * y.y + si * y.x));
+                  b11 = mk2(sr * x.x + si * x.y + c * y.x, sr * x.y - si * x.x + c * y.y);
                 }
                 if (s_on[a] | s_on[b]) {
                   G[(size_t)pa * GL + pb] = b00; G[(size_t)pa * GL + qb] = b01;
@@ -433,12 +487,12 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
               const int i = t >> lgc, k = t & (nc2 - 1);
               if (!s_on[i]) continue;
               const int p = s_p[i], q = s_q[i];
-              const double c = s_c[i], sr = s_sr[i], si = s_si[i];
-              double2* wp = W + (size_t)p * nc2 + k;
-              double2* wq = W + (size_t)q * nc2 + k;
-              const double2 x = *wp, y = *wq;
-              *wp = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-              *wq = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+              const T c = s_c[i], sr = s_sr[i], si = s_si[i];
+              T2* wp = W + (size_t)p * nc2 + k;
+              T2* wq = W + (size_t)q * nc2 + k;
+              const T2 x = *wp, y = *wq;
+              *wp = mk2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+              *wq = mk2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
             }
             __syncthreads();
           }
@@ -448,34 +502,34 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
               int p, q;
               inner_pair(s2, i, p, q);
               if (s_col[p] < 0 || s_col[q] < 0) continue;
-              double2* ap = Ab + (size_t)p * MP;
-              double2* aq = Ab + (size_t)q * MP;
-              double sp = 0, sq = 0, gr = 0, gi = 0;
+              T2* ap = Ab + (size_t)p * MP;
+              T2* aq = Ab + (size_t)q * MP;
+              T sp = 0, sq = 0, gr = 0, gi = 0;
               for (int r = lane; r < M; r += 32) {
-                const double2 x = ap[r], y = aq[r];
+                const T2 x = ap[r], y = aq[r];
                 sp += x.x * x.x + x.y * x.y;
                 sq += y.x * y.x + y.y * y.y;
                 gr += x.x * y.x + x.y * y.y;
                 gi += x.x * y.y - x.y * y.x;
               }
               warp_sum4_d(sp, sq, gr, gi);
-              const double g2 = gr * gr + gi * gi;
+              const T g2 = gr * gr + gi * gi;
               if (lane == 0) note_off(g2, sp, sq);
-              if (!(g2 > tol * tol * sp * sq) || g2 == 0.0) continue;
+              if (!(g2 > JdT<T>::thr(tol, sp, sq)) || g2 == T(0)) continue;
               if (lane == 0) s_rot = 1;
-              double c, sr, si;
+              T c, sr, si;
               jd_rot(sp, sq, gr, gi, g2, c, sr, si);
               for (int r = lane; r < M; r += 32) {
-                const double2 x = ap[r], y = aq[r];
-                ap[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-                aq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                const T2 x = ap[r], y = aq[r];
+                ap[r] = mk2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                aq[r] = mk2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
               }
-              double2* wp = W + (size_t)p * nc2;
-              double2* wq = W + (size_t)q * nc2;
+              T2* wp = W + (size_t)p * nc2;
+              T2* wq = W + (size_t)q * nc2;
               for (int r = lane; r < nc2; r += 32) {
-                const double2 x = wp[r], y = wq[r];
-                wp[r] = make_double2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
-                wq[r] = make_double2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
+                const T2 x = wp[r], y = wq[r];
+                wp[r] = mk2(c * x.x - (sr * y.x + si * y.y), c * x.y - (sr * y.y - si * y.x));
+                wq[r] = mk2(sr * x.x - si * x.y + c * y.x, sr * x.y + si * x.x + c * y.y);
               }
             }
             __syncthreads();
@@ -488,12 +542,12 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
           if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * bs * bs + 8ull * bs * nc2u);
           else f = (unsigned long long)nin * bs * (16ull * Mu + 8ull * nc2u);
           if (s_rot) f += 4ull * nc2u * nc2u * (Mu + Nu);
-          atomicAdd(&it.cnt[CNT_JDB_DFMA], f);
+          atomicAdd(&it.cnt[SP ? CNT_JSP_FFMA : CNT_JDB_DFMA], f);
         }
         if (s_rot) {  // block-uniform
           if (threadIdx.x == 0) s_any = 1;
           if (s_gram) {
-            jd_apply_w(Ab, MP, A, M, W, bs, s_col);  // A[:, cols] = Ab W
+            jd_apply_w<T, T2>(Ab, MP, A, M, W, bs, s_col);  // A[:, cols] = Ab W
           } else {
             for (int l = threadIdx.x / M, r = threadIdx.x % M; l < nc2;) {
               const int c = s_col[l];
@@ -505,17 +559,17 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
           __syncthreads();  // Ab is free now
           mark(2);
           // stage V[:, cols] (N <= M rows) in its place, then V[:, cols] = Vb W
-          double2* Vb = Ab;  // [2bs][N]
+          T2* Vb = Ab;  // [2bs][N]
           for (int l = threadIdx.x / N, r = threadIdx.x % N; l < nc2;) {
             const int c = s_col[l];
-            cp_async16(Vb + (size_t)l * N + r, c >= 0 ? (const void*)(V + (size_t)c * N + r) : (const void*)V, c >= 0 ? 16 : 0);
+            cp_async_el<T2>(Vb + (size_t)l * N + r, c >= 0 ? (const void*)(V + (size_t)c * N + r) : (const void*)V, c >= 0);
             r += blockDim.x;
             while (r >= N) { r -= N; ++l; }
           }
           cp_commit();
           cp_wait<0>();
           __syncthreads();
-          jd_apply_w(Vb, N, V, N, W, bs, s_col);
+          jd_apply_w<T, T2>(Vb, N, V, N, W, bs, s_col);
         }
         __syncthreads();
         mark(3);
@@ -532,9 +586,100 @@ static __global__ void __launch_bounds__(JD_THREADS, JD_MINB) k_jacobi_db(const 
     csync();
     const int any = *(volatile int*)&it.anyflag[sweep & 1];
     if (!any) break;
+    // binary32 phase: every pair of this sweep was already below the hand-over level when it was
+    // evaluated (its rotations leave ~ that level squared): the binary64 phase takes over
+    if (SP && __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]) < 0.5) break;
   }
-  if (crank == 0 && threadIdx.x == 0) *it.sweeps_d = sweep;
+  if (crank == 0 && threadIdx.x == 0) *(SP ? it.sweeps_s : it.sweeps_d) = sweep;
+  if (jac_trace_items && crank == 0 && threadIdx.x == 0 && (int)(blockIdx.x / C) < jac_trace_items)
+    printf("block Jacobi (%s) item %d M %d N %d: %d sweeps\n", SP ? "binary32" : "binary64", (int)(blockIdx.x / C), M, N, sweep);
   if (prof) atomicAdd(&jd_prof[5], (unsigned long long)sweep);
+}
+
+// ---------------------------------------------------------------------------- R27 hand-over
+// binary32 phase -> binary64 phase: V0 = (binary64) Vs;  Rm = V0^H V0;  Vd = V0 (3 I - Rm) / 2 (one
+// Newton-Schulz step: Vs is unitary to ~1e-6 only, Vd to ~1e-12);  Aj = Theta_d Vd.
+static __global__ void __launch_bounds__(256) k_sp_to_dp(const PreItem* items) {
+  const PreItem it = items[blockIdx.y];
+  if (it.N == 0 || it.Vs == nullptr) return;
+  const size_t n = (size_t)it.N * it.N;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    const float2 v = it.Vs[t];
+    it.V0[t] = make_double2((double)v.x, (double)v.y);
+  }
+}
+// Batched complex binary64 GEMM for the hand-over, column-major, 64 x 64 tiles, 256 threads with a
+// 4 x 4 register tile each.  which: 0: Rm = V0^H V0 (N x N x N);  1: Vd = 1.5 V0 - 0.5 V0 Rm;
+// 2: Aj = Ad Vd (M x N x N).
+static __global__ void __launch_bounds__(256) k_zgemm_handover(const PreItem* items, int which) {
+  const PreItem it = items[blockIdx.z];
+  if (it.N == 0 || it.Vs == nullptr) return;
+  const int N = it.N, M = it.M;
+  const int rows = which == 2 ? M : N, cols = N, K = N;
+  const double2* A = which == 2 ? it.Ad : it.V0;
+  const double2* B = which == 0 ? it.V0 : (which == 1 ? it.Rm : it.Vd);
+  double2* C = which == 0 ? it.Rm : (which == 1 ? it.Vd : it.Aj);
+  const int lda = which == 2 ? M : N, ldb = N, ldc = rows;
+  const bool conjA = which == 0;
+  const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+  if (r0 >= rows || c0 >= cols) return;
+  __shared__ double2 As_[16][65], Bs_[16][65];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    __syncthreads();
+    for (int w = threadIdx.x; w < 16 * 64; w += 256) {
+      double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
+      if (!conjA) {  // A(r, k) at A[k lda + r]: r fastest
+        const int e = w % 64, kk = w / 64;
+        if (r0 + e < rows && k0 + kk < K) va = A[(size_t)(k0 + kk) * lda + r0 + e];
+        As_[kk][e] = va;
+      } else {       // A^H(r, k) = conj A(k, r) at A[r lda + k]: k fastest
+        const int kk = w % 16, e = w / 16;
+        if (r0 + e < rows && k0 + kk < K) {
+          va = A[(size_t)(r0 + e) * lda + k0 + kk];
+          va.y = -va.y;
+        }
+        As_[kk][e] = va;
+      }
+      {              // B(k, c) at B[c ldb + k]: k fastest
+        const int kk = w % 16, e = w / 16;
+        if (c0 + e < cols && k0 + kk < K) vb = B[(size_t)(c0 + e) * ldb + k0 + kk];
+        Bs_[kk][e] = vb;
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 16; ++kk) {
+      double2 a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As_[kk][tx + 16 * i]; b[i] = Bs_[kk][ty + 16 * i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[i][j].x = fma(a[i].x, b[j].x, fma(-a[i].y, b[j].y, acc[i][j].x));
+          acc[i][j].y = fma(a[i].x, b[j].y, fma(a[i].y, b[j].x, acc[i][j].y));
+        }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = r0 + tx + 16 * i, c = c0 + ty + 16 * j;
+      if (r >= rows || c >= cols) continue;
+      double2 v = acc[i][j];
+      if (which == 1) {
+        const double2 x = it.V0[(size_t)c * N + r];
+        v = make_double2(1.5 * x.x - 0.5 * v.x, 1.5 * x.y - 0.5 * v.y);
+      }
+      C[(size_t)c * ldc + r] = v;
+    }
 }
 
 // binary64 v (|v| <= 1) -> L balanced digits at exponent 1 (value = sum d_k 2^(28k) 2^(1-28L)), exact

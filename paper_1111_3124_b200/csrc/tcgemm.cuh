@@ -31,19 +31,19 @@
 namespace mpsb {
 
 #ifndef TC_N_   // tile shape switches (development A/B builds)
-#define TC_N_ 64
+#define TC_N_ 128
 #endif
 #ifndef TC_GCH_
 #define TC_GCH_ (512 / TC_N_)
 #endif
 #ifndef TC_WARPS_
-#define TC_WARPS_ 8
+#define TC_WARPS_ 4
 #endif
 #ifndef TC_SBK_
-#define TC_SBK_ 16
+#define TC_SBK_ 6
 #endif
 #ifndef TC_NSTG_
-#define TC_NSTG_ 2
+#define TC_NSTG_ 3
 #endif
 constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
 constexpr int TC_N = TC_N_;   // output columns per CTA = MMA N

@@ -214,13 +214,25 @@ static __global__ void k_fo_fail(const FoItem<NL>* items, int n, int L) {
   if (blockIdx.x == 0 && threadIdx.x == 0) { *it.ok = 0; *it.done = 0; }
 }
 
+// the binary32 first phase of the block Jacobi (R27) is on unless MPS_JD_SP=0
+inline bool use_jd_sp() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("MPS_JD_SP");
+    on = e ? (atoi(e) != 0) : 1;
+  }
+  return on != 0;
+}
+constexpr int JD_SP_MIN_N = 32;  // smaller items: binary64 only
+
 // preconditioner buffers of one item: Ad, Vd (binary64), X_a, X_b, D (fixed N x N; for a square
 // item the last X buffer also holds P = A0 X_{n-1}), eMix[N], scalars
 template <int L>
 inline size_t pre_bytes(int M, int N) {
   return align_up(16 * (size_t)M * N) + align_up(16 * (size_t)N * N) + 3 * mat_bytes(N, N, L) + align_up(8 * (size_t)N) +
          256 + align_up(4 * (size_t)N * (L + 1)) + align_up(8 * (size_t)N) +  // + recovery coefficients
-         xs_rec_bytes(N);                                                      // + refinement sweep records
+         xs_rec_bytes(N) +                                                     // + refinement sweep records
+         align_up(16 * (size_t)M * N) + 2 * align_up(16 * (size_t)N * N);      // + Aj (As), V0, Rm (Vs) of R27
 }
 
 // preconditioner buffers carved from q (layout of pre_bytes)
@@ -240,6 +252,8 @@ struct PreBufs {
   int4* xs_rec;  // refinement sweep records
   int64_t* eXs;  // [2] = {0, -1}: exponents of E and E / 2 (GEMM form of the refinement sweeps)
   int* xs_big;   // pairs of the current refinement sweep applied as sequential rotations
+  double2 *Aj, *V0, *Rm;  // R27: Theta_d V_d (the binary32 A aliases it), V0, V0^H V0 (the binary32 V aliases it)
+  int* sweeps_s;
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
 };
 template <int L>
@@ -263,6 +277,10 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.eXs = (int64_t*)(q + 112);
   b.xs_big = (int*)(q + 128);
   b.xs_rec = (int4*)((char*)b.rexp + align_up(8 * (size_t)N));
+  b.Aj = (double2*)((char*)b.xs_rec + xs_rec_bytes(N));
+  b.V0 = (double2*)((char*)b.Aj + align_up(16 * (size_t)M * N));
+  b.Rm = (double2*)((char*)b.V0 + align_up(16 * (size_t)N * N));
+  b.sweeps_s = (int*)(q + 136);
   return b;
 }
 // descriptors of one item's preconditioner (gt[k * stride], k = 0 .. 2 ns_iters): the
@@ -276,6 +294,10 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
   constexpr int NSIT = ns_iters<L>();
   *pi = PreItem{M, N, A0, eA0, pb.Ad, pb.Vd, pb.rowmax, pb.sweeps_d, pb.Xa, pb.eOne, pb.eA1, pb.anyflag, pb.offmax,
                 nullptr, nullptr, nullptr, nullptr, prof_counts()};
+  if (use_jd_sp() && N >= JD_SP_MIN_N) {  // a per-item choice
+    pi->As = (float2*)pb.Aj; pi->Vs = (float2*)pb.Rm; pi->V0 = pb.V0; pi->Rm = pb.Rm; pi->Aj = pb.Aj;
+  }
+  pi->sweeps_s = pb.sweeps_s;
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -395,14 +417,16 @@ template <int L>
 inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, int maxN, cudaStream_t st) {
   constexpr int NSIT = ns_iters<L>();
   int nl = 0;
+  jacobi_trace_init();
   k_pre_init<<<(n + 255) / 256, 256, 0, st>>>(dpre, n); ++nl;
   k_fx_to_d<L><<<dim3(std::max(1, (maxM + 255) / 256), n), 256, 0, st>>>(dpre); ++nl;
-  smem_optin((const void*)k_jacobi_db, 226 * 1024);  // + static
   {
     // few items (an MPS layer): C CTAs per item share its block pairs (cluster barriers per step)
     // shared memory for the largest staging of any item: the block size depends on M, and
     // jd_smem is not monotone in M (bs halves above M = 320 and M = 640)
-    const size_t smem = std::max(std::max(jd_smem(std::min(maxM, 320)), jd_smem(std::min(maxM, 640))), jd_smem(maxM));
+    auto smem_for = [&](size_t el) {
+      return std::max(std::max(jd_smem(std::min(maxM, 320), el), jd_smem(std::min(maxM, 640), el)), jd_smem(maxM, el));
+    };
     static int jprof = -1;
     if (jprof < 0) {
       const char* e = getenv("MPS_JD_PROF");
@@ -412,40 +436,55 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
         cudaMemcpyToSymbol(jd_prof_on, &one, sizeof(int));
       }
     }
-    if (jprof) {
-      const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      cudaMemcpyToSymbolAsync(jd_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
-    }
     int C = 1;
     const int bpairs = ((maxN + jd_bs(maxM) - 1) / jd_bs(maxM) + 1) / 2;
     while (C < 8 && n * C * 2 <= 148 && C * 2 <= bpairs) C *= 2;
+    auto run_phase = [&](auto kernel, size_t smem, const char* name) {
+      smem_optin((const void*)kernel, (int)smem);
+      if (jprof) {
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbolAsync(jd_prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st);
+      }
+      if (C == 1) {
+        kernel<<<n, JD_THREADS, smem, st>>>(dpre, 1);
+      } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(n * C, 1, 1);
+        cfg.blockDim = dim3(JD_THREADS, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kernel, dpre, C);
+      }
+      ++nl;
+      if (jprof) {
+        unsigned long long h[8];
+        cudaMemcpyFromSymbolAsync(h, jd_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "%s cycles (thread 0, sum over CTAs): stage %.4e gram %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu (Gram form %llu) sweeps %llu (items %d)\n",
+                name, (double)h[0], (double)h[7], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
+      }
+    };
+    if (use_jd_sp() && maxN >= JD_SP_MIN_N) {  // binary32 first phase and the hand-over (R27); items
+                                               // without it (As == nullptr) exit at once
+      prof_mark(PROF_JSP, 1, st);
+      run_phase(k_jacobi_blk<float>, smem_for(8), "k_jacobi_blk<float>");
+      k_sp_to_dp<<<dim3(32, n), 256, 0, st>>>(dpre); ++nl;
+      const dim3 gN((maxN + 63) / 64, (maxN + 63) / 64, n), gM((maxM + 63) / 64, (maxN + 63) / 64, n);
+      k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 0); ++nl;
+      k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 1); ++nl;
+      k_zgemm_handover<<<gM, 256, 0, st>>>(dpre, 2); ++nl;
+      prof_mark(PROF_JSP, 0, st);
+    }
     prof_mark(PROF_JDB, 1, st);
-    if (C == 1) {
-      k_jacobi_db<<<n, JD_THREADS, smem, st>>>(dpre, 1);
-    } else {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(n * C, 1, 1);
-      cfg.blockDim = dim3(JD_THREADS, 1, 1);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = st;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = C;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      cudaLaunchKernelEx(&cfg, k_jacobi_db, dpre, C);
-    }
+    run_phase(k_jacobi_blk<double>, smem_for(16), "k_jacobi_blk<double>");
     prof_mark(PROF_JDB, 0, st);
-    ++nl;
-    if (jprof) {
-      unsigned long long h[8];
-      cudaMemcpyFromSymbolAsync(h, jd_prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st);
-      cudaStreamSynchronize(st);
-      fprintf(stderr, "k_jacobi_db cycles (thread 0, sum over CTAs): stage %.4e gram %.4e inner %.4e write %.4e vupd %.4e  block pairs %llu (Gram form %llu) sweeps %llu (items %d)\n",
-              (double)h[0], (double)h[7], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
-    }
   }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
   const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
