@@ -195,12 +195,12 @@ template <> struct JdT<double> {
   static __device__ __forceinline__ double thr(double tol, double sp, double sq) { return tol * tol * sp * sq; }
 };
 // binary32: Gram-form inner sweeps while a relative off-diagonal exceeds 2^-10 (G's rounding is
-// 2^-24 of the largest column norm^2: norms^2 within 2^8), hand-over to binary64 once a whole sweep
+// 2^-24 of the largest column norm^2: norms^2 within 2^10, so a pair of small columns is resolved to 2^-14), hand-over to binary64 once a whole sweep
 // saw none above 2^-11 (its rotations leave ~2^-22, the binary32 floor eps sqrt(M) is ~2^-20)
 template <> struct JdT<float> {
   using T2 = float2;
   static constexpr int MINB = 1;
-  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 256.0f;
+  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 1024.0f;
   static __device__ __forceinline__ float2* A(const PreItem& it) { return it.As; }
   static __device__ __forceinline__ float2* V(const PreItem& it) { return it.Vs; }
   static __device__ __forceinline__ float tol(int M) { return 4.0f * M * 5.9604645e-8f; }  // 4 M 2^-24
@@ -453,11 +453,14 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
               s_q[i] = q;
             }
             __syncthreads();
-            // one pass: every 2x2 block (pairs a, b) of G becomes J_a^H G_ab J_b, and the
-            // columns p, q of W of every rotating pair are rotated
+            // one pass: every 2x2 block (pairs a <= b) of the Hermitian G becomes J_a^H G_ab J_b
+            // (the blocks below the diagonal are its mirror images), and the columns p, q of W of
+            // every rotating pair are rotated
             for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
-              if (t < bs * bs) {
-                const int a = t / bs, b = t % bs;
+              if (t < bs * (bs + 1) / 2) {
+                int a = 0, b = t;  // t -> (a, b), a <= b (row a holds bs - a blocks)
+                while (b >= bs - a) { b -= bs - a; ++a; }
+                b += a;
                 const int pa = s_p[a], qa = s_q[a], pb = s_p[b], qb = s_q[b];
                 T2 b00 = G[(size_t)pa * GL + pb], b01 = G[(size_t)pa * GL + qb];
                 T2 b10 = G[(size_t)qa * GL + pb], b11 = G[(size_t)qa * GL + qb];
@@ -482,6 +485,10 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
                 if (s_on[a] | s_on[b]) {
                   G[(size_t)pa * GL + pb] = b00; G[(size_t)pa * GL + qb] = b01;
                   G[(size_t)qa * GL + pb] = b10; G[(size_t)qa * GL + qb] = b11;
+                  if (a != b) {  // G(j, i) = conj G(i, j)
+                    G[(size_t)pb * GL + pa] = mk2(b00.x, -b00.y); G[(size_t)qb * GL + pa] = mk2(b01.x, -b01.y);
+                    G[(size_t)pb * GL + qa] = mk2(b10.x, -b10.y); G[(size_t)qb * GL + qa] = mk2(b11.x, -b11.y);
+                  }
                 }
               }
               const int i = t >> lgc, k = t & (nc2 - 1);
@@ -539,7 +546,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
         if (it.cnt && threadIdx.x == 0) {  // algorithmic DFMA of this visit (bench.py roofline)
           const unsigned long long nc2u = nc2, Mu = M, Nu = N;
           unsigned long long f = 0;
-          if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * bs * bs + 8ull * bs * nc2u);
+          if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * (bs * (bs + 1) / 2) + 8ull * bs * nc2u);
           else f = (unsigned long long)nin * bs * (16ull * Mu + 8ull * nc2u);
           if (s_rot) f += 4ull * nc2u * nc2u * (Mu + Nu);
           atomicAdd(&it.cnt[SP ? CNT_JSP_FFMA : CNT_JDB_DFMA], f);
@@ -585,6 +592,9 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     }
     csync();
     const int any = *(volatile int*)&it.anyflag[sweep & 1];
+    if (jac_trace_items > 1000 && crank == 0 && threadIdx.x == 0 && (int)(blockIdx.x / C) == 0)
+      printf("  block Jacobi (%s) sweep %d: %s form, rotated %d, off flag %.1f\n", SP ? "binary32" : "binary64", sweep,
+             gram_sweep ? "Gram" : "column", any, __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]));
     if (!any) break;
     // binary32 phase: every pair of this sweep was already below the hand-over level when it was
     // evaluated (its rotations leave ~ that level squared): the binary64 phase takes over
@@ -597,28 +607,31 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
 }
 
 // ---------------------------------------------------------------------------- R27 hand-over
-// binary32 phase -> binary64 phase: V0 = (binary64) Vs;  Rm = V0^H V0;  Vd = V0 (3 I - Rm) / 2 (one
-// Newton-Schulz step: Vs is unitary to ~1e-6 only, Vd to ~1e-12);  Aj = Theta_d Vd.
+// binary32 phase -> binary64 phase: Vd = (binary64) Vs, then two Newton-Schulz steps in binary64,
+// Rm = Vd^H Vd, V0 = Vd (3 I - Rm) / 2;  Rm = V0^H V0, Vd = V0 (3 I - Rm) / 2  (Vs is unitary to
+// ~1e-5 only; the rotations of the binary64 phase keep whatever defect V starts with, and the
+// fixed-point Newton-Schulz schedule (NsSched) expects a basis unitary to ~2^-45);  Aj = Theta_d Vd.
 static __global__ void __launch_bounds__(256) k_sp_to_dp(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
   if (it.N == 0 || it.Vs == nullptr) return;
   const size_t n = (size_t)it.N * it.N;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
     const float2 v = it.Vs[t];
-    it.V0[t] = make_double2((double)v.x, (double)v.y);
+    it.Vd[t] = make_double2((double)v.x, (double)v.y);
   }
 }
 // Batched complex binary64 GEMM for the hand-over, column-major, 64 x 64 tiles, 256 threads with a
-// 4 x 4 register tile each.  which: 0: Rm = V0^H V0 (N x N x N);  1: Vd = 1.5 V0 - 0.5 V0 Rm;
-// 2: Aj = Ad Vd (M x N x N).
-static __global__ void __launch_bounds__(256) k_zgemm_handover(const PreItem* items, int which) {
+// 4 x 4 register tile each.  which: 0: Rm = X^H X (N x N x N);  1: Y = 1.5 X - 0.5 X Rm, with
+// (X, Y) = (Vd, V0) in Newton-Schulz step 0 and (V0, Vd) in step 1;  2: Aj = Ad Vd (M x N x N).
+static __global__ void __launch_bounds__(256) k_zgemm_handover(const PreItem* items, int which, int nsstep) {
   const PreItem it = items[blockIdx.z];
   if (it.N == 0 || it.Vs == nullptr) return;
   const int N = it.N, M = it.M;
   const int rows = which == 2 ? M : N, cols = N, K = N;
-  const double2* A = which == 2 ? it.Ad : it.V0;
-  const double2* B = which == 0 ? it.V0 : (which == 1 ? it.Rm : it.Vd);
-  double2* C = which == 0 ? it.Rm : (which == 1 ? it.Vd : it.Aj);
+  const double2* X = nsstep ? it.V0 : it.Vd;
+  const double2* A = which == 2 ? it.Ad : X;
+  const double2* B = which == 0 ? X : (which == 1 ? it.Rm : it.Vd);
+  double2* C = which == 0 ? it.Rm : (which == 1 ? (nsstep ? it.Vd : it.V0) : it.Aj);
   const int lda = which == 2 ? M : N, ldb = N, ldc = rows;
   const bool conjA = which == 0;
   const int r0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
@@ -675,7 +688,7 @@ static __global__ void __launch_bounds__(256) k_zgemm_handover(const PreItem* it
       if (r >= rows || c >= cols) continue;
       double2 v = acc[i][j];
       if (which == 1) {
-        const double2 x = it.V0[(size_t)c * N + r];
+        const double2 x = X[(size_t)c * N + r];
         v = make_double2(1.5 * x.x - 0.5 * v.x, 1.5 * x.y - 0.5 * v.y);
       }
       C[(size_t)c * ldc + r] = v;

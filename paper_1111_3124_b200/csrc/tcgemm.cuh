@@ -140,6 +140,7 @@ __host__ __device__ constexpr uint32_t tc_idesc(int M, int N) {
   return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+#if TC_SLICE_BITS == 7
 // ---------------------------------------------------------------------------- slicing
 // Operand A of the item (rows x K): plane ri of op(A)(r, k) in the LG-digit frame (digits
 // D0 .. L-1 of the stored value).  conjA: A is stored K x rows, op(A) = A^H.
@@ -264,6 +265,143 @@ __global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int firs
   }
 }
 
+#else
+// ---------------------------------------------------------------------------- slicing (8-bit)
+// A thread owns 16 consecutive k of one row x of a tile (half a tile row: one 16-byte line of a
+// core matrix), keeps their running values in 16 int64 and writes every finished slice as ONE
+// 16-byte store; the 8 lanes of consecutive x fill a 128-byte core matrix.  (The first version
+// wrote single bytes, 16 useful bytes per 32-byte sector: the slicing kernels took half as long
+// as the MMAs, profiles/r02_launches_v56.csv.)
+struct TcAcc16 { int64_t a[16]; };
+__device__ __forceinline__ uint4 tc_emit16(TcAcc16& t, bool last) {
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t u = last ? (uint32_t)(t.a[i] & 255) : (uint32_t)(tc_bal8(t.a[i]) & 255);
+    w[i >> 2] |= u << (8 * (i & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// 16 consecutive ints p[0..15] (the first nv valid, the rest 0); vector loads when aligned
+__device__ __forceinline__ void tc_load16(const int32_t* p, int nv, bool neg, int32_t (&v)[16]) {
+  if (nv == 16 && (((uintptr_t)p) & 15) == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int4 t = __ldg((const int4*)p + q);
+      v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = i < nv ? __ldg(p + i) : 0;
+  }
+  if (neg) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = -v[i];
+  }
+}
+// byte offset of the 16-byte line (x, k group kg) of a tile
+__device__ __forceinline__ int tc_line(int x, int kg) { return (((x >> 3) * 2 + kg) << 7) + ((x & 7) << 4); }
+
+// digit j of 16 values enters the running values; the slices it completes are stored
+template <int LG, bool NEG2>
+__device__ __forceinline__ void tc_slice_digit(int j, const int32_t (&v)[16], TcAcc16& ap, TcAcc16& an, int8_t* o1, int8_t* o2,
+                                               size_t sstride) {
+  const int sh = 28 * j - 8 * ((7 * j) / 2);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    ap.a[i] += (int64_t)v[i] << sh;
+    if (NEG2) an.a[i] += (int64_t)(-v[i]) << sh;
+  }
+  for (int sl = (7 * j) / 2; sl < (7 * (j + 1)) / 2; ++sl) {
+    *(uint4*)(o1 + (size_t)sl * sstride) = tc_emit16(ap, false);
+    if (NEG2) *(uint4*)(o2 + (size_t)sl * sstride) = tc_emit16(an, false);
+  }
+}
+template <int LG, bool NEG2>
+__device__ __forceinline__ void tc_slice_tail(TcAcc16& ap, TcAcc16& an, int8_t* o1, int8_t* o2, size_t sstride) {
+  constexpr int S = tc_ns<LG>();
+  for (int sl = (7 * LG) / 2; sl < S; ++sl) {
+    *(uint4*)(o1 + (size_t)sl * sstride) = tc_emit16(ap, sl == S - 1);
+    if (NEG2) *(uint4*)(o2 + (size_t)sl * sstride) = tc_emit16(an, sl == S - 1);
+  }
+}
+
+// Operand A of the item (rows x K): plane ri of op(A)(r, k) in the LG-digit frame (digits
+// D0 .. L-1 of the stored value).  conjA: A is stored K x rows, op(A) = A^H.
+// Block (tile r, k block) of 128 x 32 entries; 256 threads = 128 rows x 2 k groups.
+template <int L, int LG>
+__global__ void __launch_bounds__(256) k_tc_slice_a(const GemmT* items, int first, TcDims dm) {
+  constexpr int S = tc_ns<LG>(), D0 = L - LG;
+  const int item = first + blockIdx.z;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const int ri = blockIdx.y, rt = blockIdx.x % dm.tilesR, kbk = blockIdx.x / dm.tilesR;
+  if (rt * TC_M >= it.rows || kbk * TC_K >= it.K) return;  // tiles no MMA reads
+  const size_t sstride = (size_t)dm.tilesR * dm.kb * TC_ATILE;  // between slices
+  const int x = threadIdx.x % TC_M, kg = threadIdx.x / TC_M;
+  int8_t* out = dm.A + blockIdx.z * dm.a_item + (size_t)ri * S * sstride + ((size_t)rt * dm.kb + kbk) * TC_ATILE + tc_line(x, kg);
+  const int r = rt * TC_M + x, k0 = kbk * TC_K + 16 * kg;
+  const int nv = r < it.rows ? max(0, min(16, it.K - k0)) : 0;
+  TcAcc16 ap, an;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) ap.a[i] = 0;
+#pragma unroll 1
+  for (int j = 0; j < LG; ++j) {
+    int32_t v[16];
+    if (D0 + j < 0 || nv == 0) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = 0;
+    } else if (!it.conjA) {  // op(A)(r, k) = A(r, k): rows contiguous (coalesced across the lanes)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = i < nv ? __ldg(it.A + ((size_t)((k0 + i) * 2 + ri) * L + D0 + j) * it.lda + r) : 0;
+    } else {                 // op(A)(r, k) = conj A(k, r): k contiguous
+      tc_load16(it.A + ((size_t)(r * 2 + ri) * L + D0 + j) * it.lda + k0, nv, ri != 0, v);
+    }
+    tc_slice_digit<LG, false>(j, v, ap, an, out, out, sstride);
+  }
+  tc_slice_tail<LG, false>(ap, an, out, out, sstride);
+}
+
+// Operand B (K x cols), logical column c = physical column colmap[c] (c < ncols): planes
+// 0 re, 1 im, 2 -im.  Block (tile c, k block) of TC_N x 32 entries; thread = (column, k group).
+template <int L, int LG>
+__global__ void __launch_bounds__(256) k_tc_slice_b(const GemmT* items, int first, TcDims dm) {
+  constexpr int S = tc_ns<LG>(), D0 = L - LG;
+  const int item = first + blockIdx.z;
+  const GemmT it = items[item];
+  if (it.rows <= 0 || it.cols <= 0) return;
+  const int ri = blockIdx.y, ct = blockIdx.x % dm.tilesC, kbk = blockIdx.x / dm.tilesC;
+  const int ncols = it.ncols_dev ? min(*it.ncols_dev, it.cols) : it.cols;
+  if (ct * TC_N >= ncols || kbk * TC_K >= it.K) return;  // tiles no MMA reads
+  const size_t sstride = (size_t)dm.tilesC * dm.kb * TC_BTILE;
+  const size_t pstride = (size_t)S * sstride;
+  for (int e = threadIdx.x; e < TC_N * 2; e += 256) {
+    const int x = e % TC_N, kg = e / TC_N;
+    int8_t* out = dm.B + blockIdx.z * dm.b_item + (size_t)ri * pstride + ((size_t)ct * dm.kb + kbk) * TC_BTILE + tc_line(x, kg);
+    const int c = ct * TC_N + x, k0 = kbk * TC_K + 16 * kg;
+    const int nv = c < ncols ? max(0, min(16, it.K - k0)) : 0;
+    const int pc = nv ? (it.colmap ? it.colmap[c] : c) : 0;
+    TcAcc16 ap, an;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { ap.a[i] = 0; an.a[i] = 0; }
+#pragma unroll 1
+    for (int j = 0; j < LG; ++j) {
+      int32_t v[16];
+      if (D0 + j < 0 || nv == 0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0;
+      } else {
+        tc_load16(it.B + ((size_t)(pc * 2 + ri) * L + D0 + j) * it.ldb + k0, nv, false, v);
+      }
+      if (ri) tc_slice_digit<LG, true>(j, v, ap, an, out, out + pstride, sstride);   // plane 2: -im
+      else tc_slice_digit<LG, false>(j, v, ap, an, out, out, sstride);
+    }
+    if (ri) tc_slice_tail<LG, true>(ap, an, out, out + pstride, sstride);
+    else tc_slice_tail<LG, false>(ap, an, out, out, sstride);
+  }
+}
+
+#endif
 // ---------------------------------------------------------------------------- MMA
 // 1 in exactly one lane of the (converged) warp
 __device__ __forceinline__ uint32_t tc_elect() {

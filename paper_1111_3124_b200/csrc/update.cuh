@@ -477,9 +477,11 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       run_phase(k_jacobi_blk<float>, smem_for(8), "k_jacobi_blk<float>");
       k_sp_to_dp<<<dim3(32, n), 256, 0, st>>>(dpre); ++nl;
       const dim3 gN((maxN + 63) / 64, (maxN + 63) / 64, n), gM((maxM + 63) / 64, (maxN + 63) / 64, n);
-      k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 0); ++nl;
-      k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 1); ++nl;
-      k_zgemm_handover<<<gM, 256, 0, st>>>(dpre, 2); ++nl;
+      for (int nsstep = 0; nsstep < 2; ++nsstep) {
+        k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 0, nsstep); ++nl;
+        k_zgemm_handover<<<gN, 256, 0, st>>>(dpre, 1, nsstep); ++nl;
+      }
+      k_zgemm_handover<<<gM, 256, 0, st>>>(dpre, 2, 0); ++nl;
       prof_mark(PROF_JSP, 0, st);
     }
     prof_mark(PROF_JDB, 1, st);

@@ -305,12 +305,116 @@ __global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
            XD, (int)blockIdx.x, N, s_nrot, NP * (N - 1), gemm ? s_nbig : s_nrot, s_emax, xs_alpha[0].hi, s_tr);
 }
 
+// GEMM form (R26), parallel over the pairs: every pair's coefficient comes from the Gram matrix as
+// it stands at the start of the sweep, diagonal included (k_xs_params updates the column norms
+// rotation by rotation, a change of relative order |s|^2 in alpha_q - alpha_p), so no pair waits
+// for another: thread t = (step, i) of the round-robin order, record slot t.  Small pairs go to E,
+// the others get a rotation record (R17 in full) for k_xs_apply and are counted in *xs_big
+// (zeroed by k_xs_zero).
+template <int L, int XD>
+__global__ void __launch_bounds__(256) k_xs_emat(const PreItem* items, int sel) {
+  using T = XsT<XD>;
+  const PreItem it = items[blockIdx.y];
+  const int N = it.N, NP = N / 2;
+  if (N < 2 || it.X1 == nullptr) return;
+  int32_t* E = sel ? it.X1 : it.X;
+  extern __shared__ dd xs_alpha[];  // [N]
+  __shared__ double s_tr;
+  __shared__ int s_nbig, s_nrot, s_emax;
+  for (int p = threadIdx.x; p < N; p += blockDim.x) xs_alpha[p] = xs_g_dd<L, XD>(it.G + ((size_t)(p * 2) * L) * N + p, N);
+  if (threadIdx.x == 0) { s_nbig = 0; s_nrot = 0; s_emax = -9999; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int p = 0; p < N; ++p) t += fmax(xs_alpha[p].hi, 0.0);  // (in this order in every CTA)
+    s_tr = t;
+  }
+  __syncthreads();
+  const double floor2 = ldexp(1.0, -2 * (28 * XD - 50));
+  const double negl = ldexp(s_tr, -400);
+  const double thr2 = ldexp(1.0, -2 * (14 * XD + 44));
+  const int npairs = NP * (N - 1);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < npairs; t += gridDim.x * blockDim.x) {
+    const int step = t / NP, i = t % NP;
+    int p, q;
+    rr_pair(N, step, i, p, q);
+    int4* rec = it.xs_rec + (size_t)t * (T::REC / 4);
+    int flag = 0;
+    const dd ap = xs_alpha[p], aq = xs_alpha[q];
+    const double pa = ap.hi * aq.hi;
+    if (ap.hi > negl && aq.hi > negl && pa > floor2) {
+      const int32_t* gp = it.G + ((size_t)(q * 2) * L) * N + p;  // G(p, q), column q
+      const dd gr = xs_g_dd<L, XD>(gp, N), gi = xs_g_dd<L, XD>(gp + (size_t)L * N, N);
+      const dd g2 = dd_add(dd_mul(gr, gr), dd_mul(gi, gi));
+      if (g2.hi > thr2 * pa) {
+        const dd d = dd_add(aq, dd_neg(ap));
+        int32_t Kr[XD], Ki[XD];
+        dd sr = {0.0, 0.0}, si = {0.0, 0.0};
+        bool small = false;
+        if (g2.hi <= 8.673617379884035e-19 * (d.hi * d.hi)) {  // |gamma|^2 <= 2^-60 d^2: s = gamma / d
+          const dd inv = dd_div({1.0, 0.0}, d);
+          sr = xs_round_grid<XD>(dd_mul(inv, gr), Kr);
+          si = xs_round_grid<XD>(dd_mul(inv, gi), Ki);
+          small = fabs(sr.hi) < ldexp(1.0, -T::EBIG) && fabs(si.hi) < ldexp(1.0, -T::EBIG);
+        }
+        if (small) {
+          flag = 4;
+          int32_t* e1 = E + ((size_t)(q * 2) * L + (L - XD)) * N + p;
+          int32_t* e2 = E + ((size_t)(p * 2) * L + (L - XD)) * N + q;
+#pragma unroll
+          for (int k = 0; k < XD; ++k) {
+            e1[(size_t)k * N] = Kr[k];
+            e1[(size_t)(L + k) * N] = Ki[k];
+            e2[(size_t)k * N] = -Kr[k];
+            e2[(size_t)(L + k) * N] = Ki[k];
+          }
+        } else {  // a sequential exact rotation (R17), as k_xs_params
+          const dd ad = d.hi < 0 ? dd_neg(d) : d;
+          const dd r = dd_sqrt(dd_add(dd_mul(d, d), dd_scale(g2, 2)));
+          const dd c = dd_sqrt(dd_div(dd_add(ad, r), dd_scale(r, 1)));
+          dd sc = dd_div({1.0, 0.0}, dd_mul(r, c));
+          if (d.hi < 0) sc = dd_neg(sc);
+          int32_t Kc[XD];
+          sr = xs_round_grid<XD>(dd_mul(sc, gr), Kr);
+          si = xs_round_grid<XD>(dd_mul(sc, gi), Ki);
+          const dd u = dd_add(dd_mul(sr, sr), dd_mul(si, si));
+          xs_round_grid<XD>(dd_neg(dd_div(u, dd_add_d(dd_sqrt(dd_add_d(dd_neg(u), 1.0)), 1.0))), Kc);
+          int32_t w[3 * T::P];
+#pragma unroll
+          for (int k = 0; k < T::P; ++k) {
+            w[k] = k < XD ? Kc[k] : 0;
+            w[T::P + k] = k < XD ? Kr[k] : 0;
+            w[2 * T::P + k] = k < XD ? Ki[k] : 0;
+          }
+#pragma unroll
+          for (int k = 0; k < 3 * T::P / 4; ++k) rec[k] = make_int4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+          flag = 1;
+          atomicAdd(&s_nbig, 1);
+        }
+        if (jac_trace_items) {
+          atomicAdd(&s_nrot, 1);
+          int ex;
+          frexp(fmax(fabs(sr.hi), fabs(si.hi)), &ex);
+          atomicMax(&s_emax, ex);
+        }
+      }
+    }
+    rec[3 * T::P / 4] = make_int4(flag, 0, 0, 0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && s_nbig) atomicAdd(it.xs_big, s_nbig);
+  if (jac_trace_items && threadIdx.x == 0 && (int)blockIdx.y < jac_trace_items && blockIdx.x == 0)
+    printf("xsweep(%d digits, GEMM form) item %d N %d: CTA 0 rotated %d pairs (%d as sequential rotations), max |s| < 2^%d, trace %.6e\n",
+           XD, (int)blockIdx.y, N, s_nrot, s_nbig, s_emax, s_tr);
+}
+
 // GEMM form: zero E (all L digits) before k_xs_params scatters the rotation coefficients into it
 template <int L>
 __global__ void __launch_bounds__(256) k_xs_zero(const PreItem* items, int sel) {
   const PreItem it = items[blockIdx.y];
   if (it.N < 2 || it.X1 == nullptr) return;
   int4* E = (int4*)(sel ? it.X1 : it.X);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && it.xs_big) *it.xs_big = 0;
   const size_t n4 = (size_t)it.N * it.N * 2 * L / 4;  // N even: a multiple of 4 ints
   for (size_t w = (size_t)blockIdx.x * blockDim.x + threadIdx.x; w < n4; w += (size_t)gridDim.x * blockDim.x)
     E[w] = make_int4(0, 0, 0, 0);
@@ -520,8 +624,8 @@ inline int launch_xs_emat(const PreItem* d, int n, int maxN, int sel, cudaStream
   if (n <= 0 || maxN < 2) return 0;
   jacobi_trace_init();
   k_xs_zero<L><<<dim3(32, n), 256, 0, st>>>(d, sel);
-  const int thr = std::min(1024, std::max(32, ((maxN / 2 + 31) / 32) * 32));
-  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d, sel, 1);
+  const int npairs = (maxN / 2) * (maxN - 1);
+  k_xs_emat<L, XD><<<dim3(std::max(1, std::min(64, (npairs + 255) / 256)), n), 256, (size_t)maxN * sizeof(dd), st>>>(d, sel);
   return 2;
 }
 
