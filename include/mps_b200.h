@@ -173,8 +173,12 @@ int mps_stats(mps_state* st, char* json, size_t cap);
  *   sweeps  batch ints (Jacobi sweeps, the final check-only sweep included)
  *   theta_debug: NULL, or batch*(2chi)^2 complex: Theta' column-major; when given,
  *                the call stops after the contraction (slice test).
- * Host<->device copies are part of the call (pinned host buffers make them DMA-speed).  The
- * device buffers come from a grow-only arena kept between calls (calls are serialised). */
+ * Host<->device copies are part of the call (pinned host buffers make them DMA-speed).  Batches
+ * of 592 items or more are processed in chunks of 296 items (two waves of the one-CTA-per-SM
+ * kernels): the copies of one chunk run on two internal streams while another chunk computes on
+ * cuda_stream; every item's result is independent of the chunking.  The device buffers come
+ * from a grow-only arena kept between calls (calls are serialised).  The call returns after all
+ * copies have completed. */
 int mps_bench_update_batch(int prec_bits, int chi, int chi_max, int batch, double trunc_thr,
                            const void* A, const void* B, const void* lam_l, const void* lam_m,
                            const void* lam_r, const void* U, void* sigma, int* k_out, void* A_out,

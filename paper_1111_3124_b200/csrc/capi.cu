@@ -209,7 +209,17 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   const size_t nAo = (size_t)batch * 2 * chi * chi_max * cb;
   const size_t nLo = (size_t)batch * chi_max * rb;
   const size_t nTh = (size_t)batch * 4 * chi * chi * cb;
-  const size_t ws = mps_update_batch_workspace(p, chi, batch);
+  // The batch is processed in chunks so that the host<->device copies of one chunk overlap the
+  // kernels of another (copy-in stream -> compute on st -> copy-out stream, ordered by events):
+  // chunks of 296 items (two waves of the one-CTA-per-SM kernels on 148 SMs), so the chunked
+  // launches fill the same number of waves as one launch of the whole batch.  One workspace,
+  // sized for the largest chunk, serves all chunks (they compute one after the other on st).
+  // MPS_E2E_CHUNK=<items> overrides the chunk size (0: one chunk).
+  static const int chunk_env = getenv("MPS_E2E_CHUNK") ? atoi(getenv("MPS_E2E_CHUNK")) : -1;
+  int chunk = chunk_env > 0 ? chunk_env : (chunk_env == 0 || batch < 2 * 296 || theta_debug ? batch : 296);
+  chunk = std::min(chunk, batch);
+  const int nchunks = (batch + chunk - 1) / chunk;
+  const size_t ws = mps_update_batch_workspace(p, chi, chunk);
   size_t tot = 0;
   auto slot = [&](size_t n) { size_t o = tot; tot += align_up(n); return o; };
   size_t oA = slot(nA), oB = slot(nA), oll = slot(lam_l ? nLam : 0), olm = slot(lam_m ? nLam : 0),
@@ -221,6 +231,7 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   static std::mutex arena_mu;
   static char* arena = nullptr;
   static size_t arena_sz = 0;
+  static cudaStream_t s_in = nullptr, s_out = nullptr;
   std::lock_guard<std::mutex> lock(arena_mu);
   if (arena_sz < tot) {
     if (arena) cudaFree(arena);
@@ -229,40 +240,80 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
     if (cudaMalloc(&arena, tot) != cudaSuccess) return MPS_ENOMEM;
     arena_sz = tot;
   }
+  if (nchunks > 1 && !s_in) {
+    if (cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) != cudaSuccess)
+      return MPS_ECUDA;
+  }
   char* d = arena;
-  cudaMemcpyAsync(d + oA, A, nA, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d + oB, B, nA, cudaMemcpyHostToDevice, st);
-  if (lam_l) cudaMemcpyAsync(d + oll, lam_l, nLam, cudaMemcpyHostToDevice, st);
-  if (lam_m) cudaMemcpyAsync(d + olm, lam_m, nLam, cudaMemcpyHostToDevice, st);
-  if (lam_r) cudaMemcpyAsync(d + olr, lam_r, nLam, cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(d + oU, U, nU, cudaMemcpyHostToDevice, st);
-  BatchOut o{(uint32_t*)(d + oS), (int*)(d + oK), (uint32_t*)(d + oAo), (uint32_t*)(d + oBo),
-             (uint32_t*)(d + oLo), (int*)(d + oSw), theta_debug ? (uint32_t*)(d + oTh) : nullptr, nullptr};
-  cudaMemsetAsync(d + oAo, 0, nAo, st);
-  cudaMemsetAsync(d + oBo, 0, nAo, st);
+  // per-item sizes (the arrays are item-major)
+  const size_t iA = nA / batch, iLam = nLam / batch, iU = nU / batch, iSig = nSig / batch, iAo = nAo / batch,
+               iLo = nLo / batch, iTh = nTh / batch;
+  std::vector<cudaEvent_t> ev_in(nchunks), ev_done(nchunks);
+  cudaStream_t cin = nchunks > 1 ? s_in : st, cout_ = nchunks > 1 ? s_out : st;
+  cudaEvent_t ev_start = nullptr;
+  if (nchunks > 1) {  // the copies start after the work already queued on st
+    cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    cudaEventRecord(ev_start, st);
+    cudaStreamWaitEvent(cin, ev_start, 0);
+    cudaStreamWaitEvent(cout_, ev_start, 0);
+  }
+  for (int c = 0; c < nchunks; ++c) {  // every host -> device copy is queued first
+    const size_t f = (size_t)c * chunk, cnt = std::min<size_t>(chunk, batch - f);
+    cudaMemcpyAsync(d + oA + f * iA, (const char*)A + f * iA, cnt * iA, cudaMemcpyHostToDevice, cin);
+    cudaMemcpyAsync(d + oB + f * iA, (const char*)B + f * iA, cnt * iA, cudaMemcpyHostToDevice, cin);
+    if (lam_l) cudaMemcpyAsync(d + oll + f * iLam, (const char*)lam_l + f * iLam, cnt * iLam, cudaMemcpyHostToDevice, cin);
+    if (lam_m) cudaMemcpyAsync(d + olm + f * iLam, (const char*)lam_m + f * iLam, cnt * iLam, cudaMemcpyHostToDevice, cin);
+    if (lam_r) cudaMemcpyAsync(d + olr + f * iLam, (const char*)lam_r + f * iLam, cnt * iLam, cudaMemcpyHostToDevice, cin);
+    cudaMemcpyAsync(d + oU + f * iU, (const char*)U + f * iU, cnt * iU, cudaMemcpyHostToDevice, cin);
+    if (nchunks > 1) {
+      cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_done[c], cudaEventDisableTiming);
+      cudaEventRecord(ev_in[c], cin);
+    }
+  }
   std::vector<unsigned char> hd;
-  int nl;
-  const uint32_t* ll = lam_l ? (const uint32_t*)(d + oll) : nullptr;
-  const uint32_t* lm = lam_m ? (const uint32_t*)(d + olm) : nullptr;
-  const uint32_t* lr = lam_r ? (const uint32_t*)(d + olr) : nullptr;
-  if (p <= 280)
-    nl = launch_update2_batch<Tier280>(p, chi, chi_max, batch, thr, (const uint32_t*)(d + oA),
-                                       (const uint32_t*)(d + oB), ll, lm, lr, (const uint32_t*)(d + oU), o,
-                                       d + oWs, st, hd);
-  else
-    nl = launch_update2_batch<Tier512>(p, chi, chi_max, batch, thr, (const uint32_t*)(d + oA),
-                                       (const uint32_t*)(d + oB), ll, lm, lr, (const uint32_t*)(d + oU), o,
-                                       d + oWs, st, hd);
+  int nl = 0;
+  for (int c = 0; c < nchunks; ++c) {
+    const size_t f = (size_t)c * chunk, cnt = std::min<size_t>(chunk, batch - f);
+    if (nchunks > 1) cudaStreamWaitEvent(st, ev_in[c], 0);
+    BatchOut o{(uint32_t*)(d + oS + f * iSig), (int*)(d + oK) + f, (uint32_t*)(d + oAo + f * iAo),
+               (uint32_t*)(d + oBo + f * iAo), (uint32_t*)(d + oLo + f * iLo), (int*)(d + oSw) + f,
+               theta_debug ? (uint32_t*)(d + oTh + f * iTh) : nullptr, nullptr};
+    cudaMemsetAsync(d + oAo + f * iAo, 0, cnt * iAo, st);
+    cudaMemsetAsync(d + oBo + f * iAo, 0, cnt * iAo, st);
+    const uint32_t* ll = lam_l ? (const uint32_t*)(d + oll + f * iLam) : nullptr;
+    const uint32_t* lm = lam_m ? (const uint32_t*)(d + olm + f * iLam) : nullptr;
+    const uint32_t* lr = lam_r ? (const uint32_t*)(d + olr + f * iLam) : nullptr;
+    if (p <= 280)
+      nl += launch_update2_batch<Tier280>(p, chi, chi_max, (int)cnt, thr, (const uint32_t*)(d + oA + f * iA),
+                                          (const uint32_t*)(d + oB + f * iA), ll, lm, lr,
+                                          (const uint32_t*)(d + oU + f * iU), o, d + oWs, st, hd);
+    else
+      nl += launch_update2_batch<Tier512>(p, chi, chi_max, (int)cnt, thr, (const uint32_t*)(d + oA + f * iA),
+                                          (const uint32_t*)(d + oB + f * iA), ll, lm, lr,
+                                          (const uint32_t*)(d + oU + f * iU), o, d + oWs, st, hd);
+    if (nchunks > 1) {
+      cudaEventRecord(ev_done[c], st);
+      cudaStreamWaitEvent(cout_, ev_done[c], 0);
+    }
+    if (theta_debug) cudaMemcpyAsync((char*)theta_debug + f * iTh, d + oTh + f * iTh, cnt * iTh, cudaMemcpyDeviceToHost, cout_);
+    if (sigma) cudaMemcpyAsync((char*)sigma + f * iSig, d + oS + f * iSig, cnt * iSig, cudaMemcpyDeviceToHost, cout_);
+    if (k_out) cudaMemcpyAsync(k_out + f, (int*)(d + oK) + f, 4 * cnt, cudaMemcpyDeviceToHost, cout_);
+    if (A_out) cudaMemcpyAsync((char*)A_out + f * iAo, d + oAo + f * iAo, cnt * iAo, cudaMemcpyDeviceToHost, cout_);
+    if (B_out) cudaMemcpyAsync((char*)B_out + f * iAo, d + oBo + f * iAo, cnt * iAo, cudaMemcpyDeviceToHost, cout_);
+    if (lam_out) cudaMemcpyAsync((char*)lam_out + f * iLo, d + oLo + f * iLo, cnt * iLo, cudaMemcpyDeviceToHost, cout_);
+    if (sweeps) cudaMemcpyAsync(sweeps + f, (int*)(d + oSw) + f, 4 * cnt, cudaMemcpyDeviceToHost, cout_);
+  }
   g_last_launches = nl;
-  if (theta_debug) cudaMemcpyAsync(theta_debug, d + oTh, nTh, cudaMemcpyDeviceToHost, st);
-  if (sigma) cudaMemcpyAsync(sigma, d + oS, nSig, cudaMemcpyDeviceToHost, st);
-  if (k_out) cudaMemcpyAsync(k_out, d + oK, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
-  if (A_out) cudaMemcpyAsync(A_out, d + oAo, nAo, cudaMemcpyDeviceToHost, st);
-  if (B_out) cudaMemcpyAsync(B_out, d + oBo, nAo, cudaMemcpyDeviceToHost, st);
-  if (lam_out) cudaMemcpyAsync(lam_out, d + oLo, nLo, cudaMemcpyDeviceToHost, st);
-  if (sweeps) cudaMemcpyAsync(sweeps, d + oSw, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st);
   cudaError_t e = cudaGetLastError();  // launch errors first (not sticky)
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess && nchunks > 1) e = cudaStreamSynchronize(cout_);
+  if (e == cudaSuccess && nchunks > 1) e = cudaStreamSynchronize(cin);
+  if (nchunks > 1) {
+    for (int c = 0; c < nchunks; ++c) { cudaEventDestroy(ev_in[c]); cudaEventDestroy(ev_done[c]); }
+    cudaEventDestroy(ev_start);
+  }
   if (e != cudaSuccess) {
     fprintf(stderr, "mps_b200: CUDA error %s\n", cudaGetErrorString(e));
     return MPS_ECUDA;

@@ -195,12 +195,15 @@ template <> struct JdT<double> {
   static __device__ __forceinline__ double thr(double tol, double sp, double sq) { return tol * tol * sp * sq; }
 };
 // binary32: Gram-form inner sweeps while a relative off-diagonal exceeds 2^-10 (G's rounding is
-// 2^-24 of the largest column norm^2: norms^2 within 2^10, so a pair of small columns is resolved to 2^-14), hand-over to binary64 once a whole sweep
+// 2^-24 of the largest column norm^2: norms^2 within 2^8; 2^10 measured slower: one more sweep), hand-over to binary64 once a whole sweep
 // saw none above 2^-11 (its rotations leave ~2^-22, the binary32 floor eps sqrt(M) is ~2^-20)
 template <> struct JdT<float> {
   using T2 = float2;
-  static constexpr int MINB = 1;
-  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 1024.0f;
+#ifndef JD_SP_MINB  // CTAs per SM of the binary32 phase (2: 64 registers per thread, 96 KB of shared memory each)
+#define JD_SP_MINB 1
+#endif
+  static constexpr int MINB = JD_SP_MINB;
+  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 256.0f;
   static __device__ __forceinline__ float2* A(const PreItem& it) { return it.As; }
   static __device__ __forceinline__ float2* V(const PreItem& it) { return it.Vs; }
   static __device__ __forceinline__ float tol(int M) { return 4.0f * M * 5.9604645e-8f; }  // 4 M 2^-24
@@ -453,14 +456,12 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
               s_q[i] = q;
             }
             __syncthreads();
-            // one pass: every 2x2 block (pairs a <= b) of the Hermitian G becomes J_a^H G_ab J_b
-            // (the blocks below the diagonal are its mirror images), and the columns p, q of W of
-            // every rotating pair are rotated
+            // one pass: every 2x2 block (pairs a, b) of G becomes J_a^H G_ab J_b, and the
+            // columns p, q of W of every rotating pair are rotated  (forming only the blocks a <= b of
+            // the Hermitian G and mirroring them measured slower: k_jacobi_blk<double> 161 -> 168 ms)
             for (int t = threadIdx.x; t < bs * nc2; t += blockDim.x) {
-              if (t < bs * (bs + 1) / 2) {
-                int a = 0, b = t;  // t -> (a, b), a <= b (row a holds bs - a blocks)
-                while (b >= bs - a) { b -= bs - a; ++a; }
-                b += a;
+              if (t < bs * bs) {
+                const int a = t / bs, b = t % bs;
                 const int pa = s_p[a], qa = s_q[a], pb = s_p[b], qb = s_q[b];
                 T2 b00 = G[(size_t)pa * GL + pb], b01 = G[(size_t)pa * GL + qb];
                 T2 b10 = G[(size_t)qa * GL + pb], b11 = G[(size_t)qa * GL + qb];
@@ -485,10 +486,6 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
                 if (s_on[a] | s_on[b]) {
                   G[(size_t)pa * GL + pb] = b00; G[(size_t)pa * GL + qb] = b01;
                   G[(size_t)qa * GL + pb] = b10; G[(size_t)qa * GL + qb] = b11;
-                  if (a != b) {  // G(j, i) = conj G(i, j)
-                    G[(size_t)pb * GL + pa] = mk2(b00.x, -b00.y); G[(size_t)qb * GL + pa] = mk2(b01.x, -b01.y);
-                    G[(size_t)pb * GL + qa] = mk2(b10.x, -b10.y); G[(size_t)qb * GL + qa] = mk2(b11.x, -b11.y);
-                  }
                 }
               }
               const int i = t >> lgc, k = t & (nc2 - 1);
@@ -546,7 +543,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
         if (it.cnt && threadIdx.x == 0) {  // algorithmic DFMA of this visit (bench.py roofline)
           const unsigned long long nc2u = nc2, Mu = M, Nu = N;
           unsigned long long f = 0;
-          if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * (bs * (bs + 1) / 2) + 8ull * bs * nc2u);
+          if (s_gram) f = 4ull * (nc2u * (nc2u + 1) / 2) * Mu + (unsigned long long)nin * (16ull * bs * bs + 8ull * bs * nc2u);
           else f = (unsigned long long)nin * bs * (16ull * Mu + 8ull * nc2u);
           if (s_rot) f += 4ull * nc2u * nc2u * (Mu + Nu);
           atomicAdd(&it.cnt[SP ? CNT_JSP_FFMA : CNT_JDB_DFMA], f);

@@ -45,12 +45,17 @@ namespace mpsb {
 #ifndef TC_NSTG_
 #define TC_NSTG_ 3
 #endif
+#ifndef TC_PRODUCER  // 1: a fifth warp streams the stage tiles; the MMA warps never wait for a buffer to drain
+#define TC_PRODUCER 1
+#endif
 constexpr int TC_M = 128;  // output rows per CTA = MMA M = TMEM lanes
 constexpr int TC_N = TC_N_;   // output columns per CTA = MMA N
 constexpr int TC_K = 32;   // k per MMA instruction (kind::i8)
 constexpr int TC_GCH = TC_GCH_;   // slice-weight groups per chunk: TC_GCH accumulators x TC_N columns = 512 TMEM columns
 constexpr int TC_WARPS = TC_WARPS_;  // warps of k_tc_mma: warp w issues the MMAs of groups d0 + w (TC_GCH / TC_WARPS each)
 constexpr int TC_SBK = TC_SBK_;  // A slices per pipeline stage (with the <= TC_SBK + TC_GCH - 1 B slices they meet)
+constexpr int TC_THREADS = (TC_WARPS_ + (TC_PRODUCER ? 1 : 0)) * 32;
+constexpr int TC_LOADER = TC_PRODUCER ? TC_WARPS_ : 0;  // the warp that issues the bulk copies
 constexpr int TC_NSTG = TC_NSTG_;  // shared-memory stage buffers (bulk copies run TC_NSTG - 1 stages ahead of the MMAs)
 static_assert(TC_GCH * TC_N <= 512 && TC_GCH % TC_WARPS == 0 && TC_WARPS % 4 == 0, "TMEM columns / warp roles");
 constexpr int TC_STAGE = TC_SBK * 4096 + (TC_SBK + TC_GCH - 1) * TC_N * 32;  // bytes of one stage buffer
@@ -425,7 +430,7 @@ __device__ __forceinline__ void tc_mbar_wait(uint32_t bar, uint32_t parity) {
 // issued, into the buffer the previous stage's MMAs release); after a chunk all warps drain its accumulators to the
 // group-sum scratch (tcgen05.ld).  Slice ranges: A s in [SA0, S), B t in [SB0, SB1).
 template <int LG, int SA0, int SB0, int SB1>
-__global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tc_mma(const GemmT* items, int first, TcDims dm) {
   constexpr int S = tc_ns<LG>(), DLO = tc_dlo<LG>(), NG = tc_ng<LG>(), DHI = tc_dhi<LG>();
   constexpr int NCH = (NG + TC_GCH - 1) / TC_GCH;
   constexpr uint32_t IDESC = tc_idesc(TC_M, TC_N);
@@ -514,7 +519,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
     const int8_t* Bp = Bb + (size_t)bp * S * b_s + ((size_t)ct * dm.kb + g.kbk) * TC_BTILE;
     const uint32_t bytes = (uint32_t)((g.s1 - g.s0 + 1) * TC_ATILE + (g.t1 - g.t0 + 1) * TC_BTILE);
     const uint32_t fb = tc_smem(&bar_full[b]);
-    if (warp != 0 || !tc_elect()) return;
+    if (warp != TC_LOADER || !tc_elect()) return;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(bytes));
     int8_t* buf = tcs + (size_t)b * TC_STAGE;
     for (int s = g.s0; s <= g.s1; ++s)
@@ -537,7 +542,26 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
   unsigned long long nmma = 0;  // MMAs this warp issued (profiling)
   // every warp follows the stage sequence (warp-uniform values, elect.sync-predicated issue): warp 0
   // also streams the tiles, TC_NSTG - 1 stages ahead; warp w issues the MMAs of its groups of the chunk
-  if (chunk_start(cur, 0)) {
+  auto consumer_sync = [&]() {  // the MMA warps only (the producer warp runs on its own)
+    if (TC_PRODUCER) asm volatile("bar.sync 1, %0;\n" ::"n"(TC_WARPS * 32) : "memory");
+    else __syncthreads();
+  };
+  if (TC_PRODUCER && warp == TC_LOADER) {
+    // producer warp: keeps TC_NSTG stages in flight; a buffer is refilled as soon as the MMAs of
+    // the stage that used it have completed (tcgen05.commit of every MMA warp on its "empty" barrier)
+    if (chunk_start(nxt, 0)) {
+      more = true;
+      while (more) {
+        if (nld >= TC_NSTG) tc_mbar_wait(tc_smem(&bar_empty[nld % TC_NSTG]), ((nld - TC_NSTG) / TC_NSTG) & 1);
+        load_stage(nxt, nld % TC_NSTG);
+        ++nld;
+        more = next_stage(nxt);
+      }
+    }
+    return;
+  }
+  const bool have = chunk_start(cur, 0);
+  if (!TC_PRODUCER && have) {
     nxt = cur;
     more = true;
     for (int k = 0; k < TC_NSTG - 1 && more; ++k) {
@@ -583,7 +607,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
                 tc_smem(&bar_empty[b])));
         // prefetch stage i + TC_NSTG - 1 into the buffer of stage i - 1 once that stage's MMAs released
         // it (the MMAs of stage i are queued behind them, so the tensor pipe does not drain)
-        if (more) {
+        if (!TC_PRODUCER && more) {
           if (nld >= TC_NSTG) tc_mbar_wait(tc_smem(&bar_empty[nld % TC_NSTG]), ((nld - TC_NSTG) / TC_NSTG) & 1);
           load_stage(nxt, nld % TC_NSTG);
           ++nld;
@@ -601,7 +625,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
       }
     }
     if (lane == 0) atomicOr(&s_started, started);
-    __syncthreads();
+    consumer_sync();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t stg = s_started;
     // drain: warp w reads TMEM lanes 32 (w % 4) .. + 31 (rows) of groups d0 + w / 4, + 2, ...
@@ -631,7 +655,7 @@ __global__ void __launch_bounds__(TC_WARPS * 32, 1) k_tc_mma(const GemmT* items,
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
-    __syncthreads();  // the next chunk's MMAs overwrite the accumulators
+    consumer_sync();  // the next chunk's MMAs overwrite the accumulators
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(512));
   if (dm.cnt && lane == 0 && nmma) atomicAdd(&dm.cnt[CNT_TC_MAC], nmma * (unsigned long long)(TC_M * TC_N * TC_K));
@@ -731,7 +755,7 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
     k_tc_slice_b<L, LG><<<dim3(dm.tilesC * dm.kb, 2, cnt), 256, 0, st>>>(d_items, f, dm);
     check("slice_b");
     prof_mark(PROF_TCMMA, 1, st);
-    k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), TC_WARPS * 32, smem, st>>>(d_items, f, dm);
+    k_tc_mma<LG, SA0, SB0, SB1><<<dim3(dm.tilesR * dm.tilesC * 2, cnt), TC_THREADS, smem, st>>>(d_items, f, dm);
     prof_mark(PROF_TCMMA, 0, st);
     check("mma");
     const int ne = dm.tilesR * TC_M * dm.tilesC * TC_N;
