@@ -174,7 +174,7 @@ int mps_stats(mps_state* st, char* json, size_t cap);
  *   theta_debug: NULL, or batch*(2chi)^2 complex: Theta' column-major; when given,
  *                the call stops after the contraction (slice test).
  * Host<->device copies are part of the call (pinned host buffers make them DMA-speed).  Batches
- * of 592 items or more are processed in chunks of 296 items (two waves of the one-CTA-per-SM
+ * of more than 592 items are processed in chunks of 592 items (four waves of the one-CTA-per-SM
  * kernels): the copies of one chunk run on two internal streams while another chunk computes on
  * cuda_stream; every item's result is independent of the chunking.  The device buffers come
  * from a grow-only arena kept between calls (calls are serialised).  The call returns after all

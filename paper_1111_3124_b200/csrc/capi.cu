@@ -211,12 +211,14 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   const size_t nTh = (size_t)batch * 4 * chi * chi * cb;
   // The batch is processed in chunks so that the host<->device copies of one chunk overlap the
   // kernels of another (copy-in stream -> compute on st -> copy-out stream, ordered by events):
-  // chunks of 296 items (two waves of the one-CTA-per-SM kernels on 148 SMs), so the chunked
-  // launches fill the same number of waves as one launch of the whole batch.  One workspace,
+  // chunks of 592 items (four waves of the one-CTA-per-SM kernels on 148 SMs, two of the
+  // two-CTA-per-SM ones), so the chunked launches fill the same number of waves as one launch of the
+  // whole batch (1024 = 592 + 432: 4 + 3 waves); smaller chunks overlap more of the copies but run
+  // the kernels less efficiently (296-item chunks: 1.39 instead of 1.28 ms per item, measured).  One workspace,
   // sized for the largest chunk, serves all chunks (they compute one after the other on st).
   // MPS_E2E_CHUNK=<items> overrides the chunk size (0: one chunk).
   static const int chunk_env = getenv("MPS_E2E_CHUNK") ? atoi(getenv("MPS_E2E_CHUNK")) : -1;
-  int chunk = chunk_env > 0 ? chunk_env : (chunk_env == 0 || batch < 2 * 296 || theta_debug ? batch : 296);
+  int chunk = chunk_env > 0 ? chunk_env : (chunk_env == 0 || batch <= 592 || theta_debug ? batch : 592);
   chunk = std::min(chunk, batch);
   const int nchunks = (batch + chunk - 1) / chunk;
   const size_t ws = mps_update_batch_workspace(p, chi, chunk);
@@ -249,11 +251,13 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   // per-item sizes (the arrays are item-major)
   const size_t iA = nA / batch, iLam = nLam / batch, iU = nU / batch, iSig = nSig / batch, iAo = nAo / batch,
                iLo = nLo / batch, iTh = nTh / batch;
-  std::vector<cudaEvent_t> ev_in(nchunks), ev_done(nchunks);
+  static const bool e2e_trace = getenv("MPS_E2E_TRACE") != nullptr;  // debug: per-chunk event times
+  const unsigned evflags = e2e_trace ? cudaEventDefault : cudaEventDisableTiming;
+  std::vector<cudaEvent_t> ev_in(nchunks), ev_done(nchunks), ev_out(nchunks);
   cudaStream_t cin = nchunks > 1 ? s_in : st, cout_ = nchunks > 1 ? s_out : st;
   cudaEvent_t ev_start = nullptr;
   if (nchunks > 1) {  // the copies start after the work already queued on st
-    cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_start, evflags);
     cudaEventRecord(ev_start, st);
     cudaStreamWaitEvent(cin, ev_start, 0);
     cudaStreamWaitEvent(cout_, ev_start, 0);
@@ -267,8 +271,9 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
     if (lam_r) cudaMemcpyAsync(d + olr + f * iLam, (const char*)lam_r + f * iLam, cnt * iLam, cudaMemcpyHostToDevice, cin);
     cudaMemcpyAsync(d + oU + f * iU, (const char*)U + f * iU, cnt * iU, cudaMemcpyHostToDevice, cin);
     if (nchunks > 1) {
-      cudaEventCreateWithFlags(&ev_in[c], cudaEventDisableTiming);
-      cudaEventCreateWithFlags(&ev_done[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev_in[c], evflags);
+      cudaEventCreateWithFlags(&ev_done[c], evflags);
+      cudaEventCreateWithFlags(&ev_out[c], evflags);
       cudaEventRecord(ev_in[c], cin);
     }
   }
@@ -304,6 +309,7 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
     if (B_out) cudaMemcpyAsync((char*)B_out + f * iAo, d + oBo + f * iAo, cnt * iAo, cudaMemcpyDeviceToHost, cout_);
     if (lam_out) cudaMemcpyAsync((char*)lam_out + f * iLo, d + oLo + f * iLo, cnt * iLo, cudaMemcpyDeviceToHost, cout_);
     if (sweeps) cudaMemcpyAsync(sweeps + f, (int*)(d + oSw) + f, 4 * cnt, cudaMemcpyDeviceToHost, cout_);
+    if (nchunks > 1) cudaEventRecord(ev_out[c], cout_);
   }
   g_last_launches = nl;
   cudaError_t e = cudaGetLastError();  // launch errors first (not sticky)
@@ -311,7 +317,15 @@ int mps_bench_update_batch(int p, int chi, int chi_max, int batch, double thr, c
   if (e == cudaSuccess && nchunks > 1) e = cudaStreamSynchronize(cout_);
   if (e == cudaSuccess && nchunks > 1) e = cudaStreamSynchronize(cin);
   if (nchunks > 1) {
-    for (int c = 0; c < nchunks; ++c) { cudaEventDestroy(ev_in[c]); cudaEventDestroy(ev_done[c]); }
+    if (e2e_trace && e == cudaSuccess)
+      for (int c = 0; c < nchunks; ++c) {
+        float a = 0, b = 0, o = 0;
+        cudaEventElapsedTime(&a, ev_start, ev_in[c]);
+        cudaEventElapsedTime(&b, ev_start, ev_done[c]);
+        cudaEventElapsedTime(&o, ev_start, ev_out[c]);
+        fprintf(stderr, "e2e chunk %d: inputs on the device at %.1f ms, computed at %.1f ms, outputs on the host at %.1f ms\n", c, a, b, o);
+      }
+    for (int c = 0; c < nchunks; ++c) { cudaEventDestroy(ev_in[c]); cudaEventDestroy(ev_done[c]); cudaEventDestroy(ev_out[c]); }
     cudaEventDestroy(ev_start);
   }
   if (e != cudaSuccess) {

@@ -42,6 +42,7 @@ struct PreItem {
   // phase), V0 = binary64 copy of Vs, Rm = V0^H V0, Aj = Theta_d V_d (the binary64 phase then runs
   // on Aj with V preset in Vd), sweeps_s its sweep count
   float2* As; float2* Vs; double2* V0; double2* Rm; double2* Aj; int* sweeps_s;
+  int* sp_bad;  // [1] set when the binary32 phase left a V that is not unitary to 1e-6 after one Newton-Schulz step
 };
 
 static __global__ void k_pre_init(const PreItem* items, int n) {
@@ -70,7 +71,6 @@ __global__ void k_fx_to_d(const PreItem* items) {
       const int32_t* pi = it.A0 + ((size_t)(c * 2 + 1) * L) * M + r;
       const double2 v = make_double2(fx_top_double<L>(pr, M), fx_top_double<L>(pi, M));
       it.Ad[(size_t)c * M + r] = v;
-      if (it.As) it.As[(size_t)c * M + r] = make_float2((float)v.x, (float)v.y);
       s += v.x * v.x + v.y * v.y;
     }
     rmax = fmax(rmax, s);
@@ -168,6 +168,7 @@ inline size_t jd_smem(int M, size_t el = 16) {  // el: bytes of a complex elemen
 // [6] block pairs in Gram form, [7] Gram products (cycles)
 static __device__ unsigned long long jd_prof[8];
 static __device__ int jd_prof_on;
+static __device__ int jd_sp_maxsweeps = 40;  // debug (MPS_JD_SP_SWEEPS): cap of the binary32 phase
 
 // Real type of the block Jacobi: binary64, or binary32 for the first phase (R27)
 __device__ __forceinline__ double2 mk2(double x, double y) { return make_double2(x, y); }
@@ -193,6 +194,7 @@ template <> struct JdT<double> {
   static __device__ __forceinline__ double2* V(const PreItem& it) { return it.Vd; }
   static __device__ __forceinline__ double tol(int M) { return JD_TOL; }
   static __device__ __forceinline__ double thr(double tol, double sp, double sq) { return tol * tol * sp * sq; }
+  static __device__ __forceinline__ bool ok(double, double) { return true; }
 };
 // binary32: Gram-form inner sweeps while a relative off-diagonal exceeds 2^-10 (G's rounding is
 // 2^-24 of the largest column norm^2: norms^2 within 2^8; 2^10 measured slower: one more sweep), hand-over to binary64 once a whole sweep
@@ -200,14 +202,20 @@ template <> struct JdT<double> {
 template <> struct JdT<float> {
   using T2 = float2;
 #ifndef JD_SP_MINB  // CTAs per SM of the binary32 phase (2: 64 registers per thread, 96 KB of shared memory each)
-#define JD_SP_MINB 1
+#define JD_SP_MINB 2
 #endif
   static constexpr int MINB = JD_SP_MINB;
-  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = 256.0f;
+  #ifndef JD_SP_NORM_RATIO
+#define JD_SP_NORM_RATIO 256.0f
+#endif
+  static constexpr float GRAM_OFF = 9.765625e-4f, STOP_OFF = 4.8828125e-4f, HUGE_ = 3.0e38f, NORM_RATIO = JD_SP_NORM_RATIO;
   static __device__ __forceinline__ float2* A(const PreItem& it) { return it.As; }
   static __device__ __forceinline__ float2* V(const PreItem& it) { return it.Vs; }
   static __device__ __forceinline__ float tol(int M) { return 4.0f * M * 5.9604645e-8f; }  // 4 M 2^-24
   static __device__ __forceinline__ float thr(float tol, float sp, float sq) { return (tol * sp) * (tol * sq); }
+  // columns below 1e-15 of the largest (norms^2 below 1e-30 after k_d_to_s's scaling) are left to the
+  // binary64 phase: their products underflow binary32
+  static __device__ __forceinline__ bool ok(float sp, float sq) { return sp > 1e-30f && sq > 1e-30f; }
 };
 
 // dst[:, s_col[j]] = src (R rows, column stride ld, 2bs columns) x W  (thread: row r, half h)
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
   T2* G = W + (size_t)nc2 * nc2;      // [2bs][2bs + 1] row-major (Gram form)
   T2* Gs = G + (size_t)nc2 * (nc2 + 1);  // Gram partial sums of parts 1..P-1
   const int GL = nc2 + 1, lgc = __ffs(nc2) - 1;  // nc2 = 2^lgc
-  __shared__ int s_any, s_rot, s_gram, s_col[32];
+  __shared__ int s_any, s_rot, s_gram, s_col[32], s_ngram;
   __shared__ T s_c[16], s_sr[16], s_si[16];
   __shared__ int s_on[16], s_p[16], s_q[16];
   __shared__ unsigned long long s_off;  // max rel^2 = |g|^2 / (alpha_p alpha_q) of this CTA's sweep (bits)
@@ -313,8 +321,9 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     }
   };
   int sweep = 0;
-  for (sweep = 1; sweep <= 40; ++sweep) {
-    if (threadIdx.x == 0) { s_any = 0; s_off = 0ull; }
+  const int maxsweeps = SP ? jd_sp_maxsweeps : 40;
+  for (sweep = 1; sweep <= maxsweeps; ++sweep) {
+    if (threadIdx.x == 0) { s_any = 0; s_off = 0ull; s_ngram = 0; }
     if (crank == 0 && threadIdx.x == 0) {
       *(volatile int*)&it.anyflag[sweep & 1] = 0;
       *(volatile unsigned long long*)&it.offmax[sweep & 1] = 0ull;
@@ -419,7 +428,13 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
               mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
               mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
             }
-            if (lane == 0) s_gram = mn == JdT<T>::HUGE_ || mx <= mn * JdT<T>::NORM_RATIO;
+            if (lane == 0) {
+              s_gram = mn == JdT<T>::HUGE_ || mx <= mn * JdT<T>::NORM_RATIO;
+              if (jac_trace_items > 1000 && blockIdx.x == 0) {
+                s_ngram += s_gram;
+                if (step == 1 && bp == 0) printf("    sweep %d step 1 block pair 0: norms^2 min %.3e max %.3e\n", sweep, (double)mn, (double)mx);
+              }
+            }
           }
         }
         for (int t = threadIdx.x; t < nc2 * nc2; t += blockDim.x)
@@ -443,7 +458,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
                 const T2 gg = G[(size_t)p * GL + q];
                 const T g2 = gg.x * gg.x + gg.y * gg.y;
                 note_off(g2, sp, sq);
-                if (g2 > JdT<T>::thr(tol, sp, sq) && g2 != T(0)) {
+                if (g2 > JdT<T>::thr(tol, sp, sq) && g2 != T(0) && JdT<T>::ok(sp, sq)) {
                   T c, sr, si;
                   jd_rot(sp, sq, gg.x, gg.y, g2, c, sr, si);
                   s_c[i] = c; s_sr[i] = sr; s_si[i] = si;
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
               warp_sum4_d(sp, sq, gr, gi);
               const T g2 = gr * gr + gi * gi;
               if (lane == 0) note_off(g2, sp, sq);
-              if (!(g2 > JdT<T>::thr(tol, sp, sq)) || g2 == T(0)) continue;
+              if (!(g2 > JdT<T>::thr(tol, sp, sq)) || g2 == T(0) || !JdT<T>::ok(sp, sq)) continue;
               if (lane == 0) s_rot = 1;
               T c, sr, si;
               jd_rot(sp, sq, gr, gi, g2, c, sr, si);
@@ -590,8 +605,8 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     csync();
     const int any = *(volatile int*)&it.anyflag[sweep & 1];
     if (jac_trace_items > 1000 && crank == 0 && threadIdx.x == 0 && (int)(blockIdx.x / C) == 0)
-      printf("  block Jacobi (%s) sweep %d: %s form, rotated %d, off flag %.1f\n", SP ? "binary32" : "binary64", sweep,
-             gram_sweep ? "Gram" : "column", any, __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]));
+      printf("  block Jacobi (%s) sweep %d: %s form (%d block pairs), rotated %d, off flag %.1f\n", SP ? "binary32" : "binary64", sweep,
+             gram_sweep ? "Gram" : "column", s_ngram, any, __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]));
     if (!any) break;
     // binary32 phase: every pair of this sweep was already below the hand-over level when it was
     // evaluated (its rotations leave ~ that level squared): the binary64 phase takes over
@@ -608,10 +623,27 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
 // Rm = Vd^H Vd, V0 = Vd (3 I - Rm) / 2;  Rm = V0^H V0, Vd = V0 (3 I - Rm) / 2  (Vs is unitary to
 // ~1e-5 only; the rotations of the binary64 phase keep whatever defect V starts with, and the
 // fixed-point Newton-Schulz schedule (NsSched) expects a basis unitary to ~2^-45);  Aj = Theta_d Vd.
+// binary32 copy of Theta_d for the first phase, scaled by a power of two so that its largest row
+// norm is ~1 (the block exponent of Theta' may sit far above its entries: unscaled, the squared
+// column norms of a circuit's Theta' reached 1e-14 and their products underflowed binary32)
+static __global__ void __launch_bounds__(256) k_d_to_s(const PreItem* items) {
+  const PreItem it = items[blockIdx.y];
+  if (it.N == 0 || it.As == nullptr) return;
+  const double rm = __longlong_as_double((long long)*it.rowmax);
+  int ex = 0;
+  if (rm > 0) frexp(rm, &ex);
+  const double sc = ldexp(1.0, -(ex / 2));
+  const size_t n = (size_t)it.M * it.N;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
+    const double2 v = it.Ad[t];
+    it.As[t] = make_float2((float)(v.x * sc), (float)(v.y * sc));
+  }
+}
 static __global__ void __launch_bounds__(256) k_sp_to_dp(const PreItem* items) {
   const PreItem it = items[blockIdx.y];
   if (it.N == 0 || it.Vs == nullptr) return;
   const size_t n = (size_t)it.N * it.N;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *it.sp_bad = 0;
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (size_t)gridDim.x * blockDim.x) {
     const float2 v = it.Vs[t];
     it.Vd[t] = make_double2((double)v.x, (double)v.y);
@@ -684,12 +716,57 @@ static __global__ void __launch_bounds__(256) k_zgemm_handover(const PreItem* it
       const int r = r0 + tx + 16 * i, c = c0 + ty + 16 * j;
       if (r >= rows || c >= cols) continue;
       double2 v = acc[i][j];
+      if (which == 0 && nsstep == 1) {  // V after one step must be unitary to 1e-6 (NaN fails the test too)
+        if (!(fabs(v.x - (r == c ? 1.0 : 0.0)) <= 1e-6) || !(fabs(v.y) <= 1e-6)) atomicOr(it.sp_bad, 1);
+      }
       if (which == 1) {
         const double2 x = X[(size_t)c * N + r];
         v = make_double2(1.5 * x.x - 0.5 * v.x, 1.5 * x.y - 0.5 * v.y);
+        if (nsstep == 1 && *it.sp_bad) v = make_double2(r == c ? 1.0 : 0.0, 0.0);  // binary64 phase from scratch
       }
+      if (which == 2 && *it.sp_bad) v = it.Ad[(size_t)c * M + r];
       C[(size_t)c * ldc + r] = v;
     }
+}
+
+// debug (MPS_JACOBI_TRACE > 2000): defects of the hand-over / of the final binary64 pair (A, V) of item 0
+static __global__ void k_dbg_pair(const PreItem* items, int stage) {
+  const PreItem it = items[0];
+  if (it.N == 0 || it.Aj == nullptr) return;
+  const int N = it.N, M = it.M;
+  __shared__ double s_u, s_a, s_m;
+  if (threadIdx.x == 0) { s_u = 0; s_a = 0; s_m = 0; }
+  __syncthreads();
+  double eu = 0, ea = 0, am = 0;
+  for (int t = threadIdx.x; t < N * N; t += blockDim.x) {
+    const int r = t % N, c = t / N;
+    double2 acc = make_double2(r == c ? -1.0 : 0.0, 0.0);
+    for (int k = 0; k < N; ++k) {
+      const double2 x = it.Vd[(size_t)r * N + k], y = it.Vd[(size_t)c * N + k];
+      acc.x += x.x * y.x + x.y * y.y;
+      acc.y += x.x * y.y - x.y * y.x;
+    }
+    eu = fmax(eu, fmax(fabs(acc.x), fabs(acc.y)));
+  }
+  for (int t = threadIdx.x; t < M * N; t += blockDim.x) {
+    const int r = t % M, c = t / M;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < N; ++k) {
+      const double2 x = it.Ad[(size_t)k * M + r], y = it.Vd[(size_t)c * N + k];
+      acc.x += x.x * y.x - x.y * y.y;
+      acc.y += x.x * y.y + x.y * y.x;
+    }
+    const double2 z = it.Aj[(size_t)c * M + r];
+    ea = fmax(ea, fmax(fabs(acc.x - z.x), fabs(acc.y - z.y)));
+    am = fmax(am, fmax(fabs(z.x), fabs(z.y)));
+  }
+  atomicMax((unsigned long long*)&s_u, (unsigned long long)__double_as_longlong(eu));
+  atomicMax((unsigned long long*)&s_a, (unsigned long long)__double_as_longlong(ea));
+  atomicMax((unsigned long long*)&s_m, (unsigned long long)__double_as_longlong(am));
+  __syncthreads();
+  if (threadIdx.x == 0)
+    printf("  hand-over check (%s) M %d N %d: max |V^H V - I| %.3e, max |A - Theta_d V| %.3e (max |A| %.3e)\n",
+           stage ? "after the binary64 phase" : "before the binary64 phase", M, N, s_u, s_a, s_m);
 }
 
 // binary64 v (|v| <= 1) -> L balanced digits at exponent 1 (value = sum d_k 2^(28k) 2^(1-28L)), exact

@@ -45,6 +45,9 @@ namespace mpsb {
 #ifndef TC_NSTG_
 #define TC_NSTG_ 3
 #endif
+#ifndef TC_PACKED  // 1: the drain combines the groups of a chunk into one int64 per entry (half the scratch traffic)
+#define TC_PACKED 1
+#endif
 #ifndef TC_PRODUCER  // 1: a fifth warp streams the stage tiles; the MMA warps never wait for a buffer to drain
 #define TC_PRODUCER 1
 #endif
@@ -88,7 +91,8 @@ struct TcDims {
   size_t a_item, b_item, g_item;  // scratch bytes per item
   int8_t* A;                     // [item][plane 2][S][tilesR][kb][4096]
   int8_t* B;                     // [item][plane 3: re, im, -im][S][tilesC][kb][1024]
-  int32_t* G;                    // [item][plane 2][NG][tilesC * 32][tilesR * 128]
+  int32_t* G;                    // [item][plane 2][NG][tilesC * TC_N][tilesR * 128] group sums, or (TC_PACKED)
+                                 // int64 [item][plane 2][NCH][tilesC * TC_N][tilesR * 128] chunk sums
   int bisect;                    // debug (MPS_TC_BISECT): bit 0 no MMA, bit 1 no drain, bit 2 no staging
   unsigned long long* cnt;       // profiling counters (CNT_TC_MAC), or null
 };
@@ -628,6 +632,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_mma(const GemmT* items, in
     consumer_sync();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t stg = s_started;
+    if constexpr (TC_PACKED) {
+      // drain: warp w owns TMEM lanes 32 w .. + 31 (rows); the chunk's groups are combined into
+      // sum_j g_j 2^(8 j) (|g_j| < 2^30, TC_GCH <= 4: below 2^55) and stored as one int64 per entry
+      static_assert(TC_WARPS == 4 && TC_GCH <= 4 && TC_SB == 8, "packed drain: one owner per entry, 32-bit span");
+      const int row = rt * TC_M + 32 * warp + lane;
+      int64_t* g64 = (int64_t*)Gb + (((size_t)plane * NCH + ch) * RCc + (size_t)ct * TC_N) * RRr + row;
+#pragma unroll 1
+      for (int h = 0; h < TC_N / 32; ++h) {
+        int64_t acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0;
+        for (int d = d0; d <= d1; ++d) {
+          if (!(((stg >> (d - d0)) & 1u) && !(dm.bisect & 2))) continue;  // warp-uniform
+          uint32_t v[32];
+          const uint32_t addr = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((d - d0) * TC_N + 32 * h);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+              "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+                "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+                "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+              : "r"(addr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n");
+          const int sh = 8 * (d - d0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] += (int64_t)(int32_t)v[j] << sh;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) g64[(size_t)(32 * h + j) * RRr] = acc[j];
+      }
+    } else {
     // drain: warp w reads TMEM lanes 32 (w % 4) .. + 31 (rows) of groups d0 + w / 4, + 2, ...
     const int row = rt * TC_M + 32 * (warp & 3) + lane;
     for (int d = d0 + (warp >> 2); d <= d1; d += TC_WARPS / 4) {
@@ -653,6 +689,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tc_mma(const GemmT* items, in
 #pragma unroll
         for (int j = 0; j < 32; ++j) g[(size_t)(32 * h + j) * RRr] = (int32_t)v[j];
       }
+    }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
     consumer_sync();  // the next chunk's MMAs overwrite the accumulators
@@ -681,17 +718,33 @@ __global__ void __launch_bounds__(256) k_tc_epi(const GemmT* items, int first, T
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < it.rows * ncols; t += gridDim.x * blockDim.x) {
     const int r = t % it.rows, c = t / it.rows;
     if (it.upper && r > c) continue;
-    int64_t acc[2][LG + 3];
+    int64_t acc[2][LG + 4];
 #pragma unroll
     for (int ri = 0; ri < 2; ++ri) {
 #pragma unroll
-      for (int j = 0; j < LG + 3; ++j) acc[ri][j] = 0;
+      for (int j = 0; j < LG + 4; ++j) acc[ri][j] = 0;
+      if constexpr (TC_PACKED) {
+        // chunk sums v = sum_j g_j 2^(8 j) at bit 8 d0 of the product: low 28 bits and the rest
+        // go to two adjacent digit columns (each term < 2^55 after its shift of < 28 bits)
+        constexpr int NCH = (NG + TC_GCH - 1) / TC_GCH;
+        const int64_t* G64 = (const int64_t*)Gb;
 #pragma unroll
-      for (int q = 0; q < NG; ++q) {
-        const int d = DLO + q;
-        const int64_t v = Gb[(((size_t)ri * NG + q) * RCc + c) * RRr + r];
-        if (TC_SB == 7) acc[ri][d / 4 - (LG - 2)] += v * ((int64_t)1 << (7 * (d % 4)));
-        else acc[ri][(8 * d) / 28 - (LG - 2)] += v * ((int64_t)1 << (8 * d - 28 * ((8 * d) / 28)));
+        for (int q = 0; q < NCH; ++q) {
+          const int bit = 8 * (DLO + q * TC_GCH), col = bit / 28 - (LG - 2), sh = bit - 28 * (bit / 28);
+          const int64_t v = G64[(((size_t)ri * NCH + q) * RCc + c) * RRr + r];
+          const int64_t hi = v >> 28, lo = v - (hi << 28);
+          acc[ri][col] += lo << sh;
+          acc[ri][col + 1] += hi << sh;
+        }
+        acc[ri][LG + 2] += acc[ri][LG + 3] * ((int64_t)1 << 28);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NG; ++q) {
+          const int d = DLO + q;
+          const int64_t v = Gb[(((size_t)ri * NG + q) * RCc + c) * RRr + r];
+          if (TC_SB == 7) acc[ri][d / 4 - (LG - 2)] += v * ((int64_t)1 << (7 * (d % 4)));
+          else acc[ri][(8 * d) / 28 - (LG - 2)] += v * ((int64_t)1 << (8 * d - 28 * ((8 * d) / 28)));
+        }
       }
       acc[ri][LG + 1] += acc[ri][LG + 2] * ((int64_t)1 << 28);  // column 2LG (the top slices' carry)
     }
@@ -729,7 +782,8 @@ inline int launch_gemm_tc(const GemmT* d_items, int n, int maxR, int maxC, int m
   dm.kb = (maxK + TC_K - 1) / TC_K;
   dm.a_item = align_up((size_t)2 * S * dm.tilesR * dm.kb * TC_ATILE);
   dm.b_item = align_up((size_t)3 * S * dm.tilesC * dm.kb * TC_BTILE);
-  dm.g_item = align_up((size_t)2 * NG * dm.tilesC * TC_N * dm.tilesR * TC_M * 4);
+  dm.g_item = TC_PACKED ? align_up((size_t)2 * ((NG + TC_GCH - 1) / TC_GCH) * dm.tilesC * TC_N * dm.tilesR * TC_M * 8)
+                        : align_up((size_t)2 * NG * dm.tilesC * TC_N * dm.tilesR * TC_M * 4);
   const size_t per = dm.a_item + dm.b_item + dm.g_item;
   const size_t budget = (size_t)3 << 30;
   const int chunk = (int)std::max<size_t>(1, std::min<size_t>(n, budget / per));

@@ -253,7 +253,7 @@ struct PreBufs {
   int64_t* eXs;  // [2] = {0, -1}: exponents of E and E / 2 (GEMM form of the refinement sweeps)
   int* xs_big;   // pairs of the current refinement sweep applied as sequential rotations
   double2 *Aj, *V0, *Rm;  // R27: Theta_d V_d (the binary32 A aliases it), V0, V0^H V0 (the binary32 V aliases it)
-  int* sweeps_s;
+  int *sweeps_s, *sp_bad;
   int32_t* Xfin() const { return (ns_iters<L>() % 2) ? Xb : Xa; }
 };
 template <int L>
@@ -281,6 +281,7 @@ inline PreBufs<L> carve_pre(char* q, int M, int N) {
   b.V0 = (double2*)((char*)b.Aj + align_up(16 * (size_t)M * N));
   b.Rm = (double2*)((char*)b.V0 + align_up(16 * (size_t)N * N));
   b.sweeps_s = (int*)(q + 136);
+  b.sp_bad = (int*)(q + 140);
   return b;
 }
 // descriptors of one item's preconditioner (gt[k * stride], k = 0 .. 2 ns_iters): the
@@ -298,6 +299,7 @@ inline void pre_descs(const PreBufs<L>& pb, int M, int N, const int32_t* A0, con
     pi->As = (float2*)pb.Aj; pi->Vs = (float2*)pb.Rm; pi->V0 = pb.V0; pi->Rm = pb.Rm; pi->Aj = pb.Aj;
   }
   pi->sweeps_s = pb.sweeps_s;
+  pi->sp_bad = pb.sp_bad;
   for (int k = 0; k < NSIT; ++k) {
     int32_t* Xc = (k % 2) ? pb.Xb : pb.Xa;
     int32_t* Xn = (k % 2) ? pb.Xa : pb.Xb;
@@ -471,9 +473,16 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
                 name, (double)h[0], (double)h[7], (double)h[1], (double)h[2], (double)h[3], h[4], h[6], h[5], n);
       }
     };
+    static int spcap = -2;
+    if (spcap == -2) {
+      const char* e = getenv("MPS_JD_SP_SWEEPS");
+      spcap = e ? atoi(e) : -1;
+      if (spcap >= 0) cudaMemcpyToSymbol(jd_sp_maxsweeps, &spcap, sizeof(int));
+    }
     if (use_jd_sp() && maxN >= JD_SP_MIN_N) {  // binary32 first phase and the hand-over (R27); items
                                                // without it (As == nullptr) exit at once
       prof_mark(PROF_JSP, 1, st);
+      k_d_to_s<<<dim3(32, n), 256, 0, st>>>(dpre); ++nl;
       run_phase(k_jacobi_blk<float>, smem_for(8), "k_jacobi_blk<float>");
       k_sp_to_dp<<<dim3(32, n), 256, 0, st>>>(dpre); ++nl;
       const dim3 gN((maxN + 63) / 64, (maxN + 63) / 64, n), gM((maxM + 63) / 64, (maxN + 63) / 64, n);
@@ -484,9 +493,12 @@ inline int launch_pre(const PreItem* dpre, const GemmT* dgt, int n, int maxM, in
       k_zgemm_handover<<<gM, 256, 0, st>>>(dpre, 2, 0); ++nl;
       prof_mark(PROF_JSP, 0, st);
     }
+    static const bool dbgpair = getenv("MPS_JACOBI_TRACE") && atoi(getenv("MPS_JACOBI_TRACE")) > 2000;
+    if (dbgpair) k_dbg_pair<<<1, 512, 0, st>>>(dpre, 0);
     prof_mark(PROF_JDB, 1, st);
     run_phase(k_jacobi_blk<double>, smem_for(16), "k_jacobi_blk<double>");
     prof_mark(PROF_JDB, 0, st);
+    if (dbgpair) k_dbg_pair<<<1, 512, 0, st>>>(dpre, 1);
   }
   k_d_to_fx<L><<<dim3(std::max(1, std::min(64, (maxN * maxN + 255) / 256)), n), 256, 0, st>>>(dpre); ++nl;
   const int tNN = ((maxN + GT_TILE - 1) / GT_TILE) * ((maxN + GT_TILE - 1) / GT_TILE);
