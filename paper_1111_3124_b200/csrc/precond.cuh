@@ -147,6 +147,9 @@ constexpr int JD_MINB = JD_BS_MAX >= 16 ? 1 : 3;
 #ifndef JD_CROSS  // 1: block pairs after the first step of a sweep rotate only their cross pairs
 #define JD_CROSS 1
 #endif
+#ifndef JD_LAST_OFF
+#define JD_LAST_OFF 1e-8  // a column-form sweep whose pairs were all below this is the last one
+#endif
 #ifndef JD_GRAM_OFF
 #define JD_GRAM_OFF 1e-6  // Gram-form inner sweeps while max |gamma| / sqrt(alpha_p alpha_q) exceeds this
 #endif
@@ -318,6 +321,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     if (sp > 0 && sq > 0) {
       if (g2 > T(JdT<T>::GRAM_OFF * JdT<T>::GRAM_OFF) * (sp * sq)) off_t = SP ? 2.0 : 1.0;
       else if (SP && off_t < 1.0 && g2 > T(JdT<T>::STOP_OFF * JdT<T>::STOP_OFF) * (sp * sq)) off_t = 1.0;
+      else if (!SP && off_t < 0.25 && g2 > T(JD_LAST_OFF * JD_LAST_OFF) * (sp * sq)) off_t = 0.25;
     }
   };
   int sweep = 0;
@@ -332,7 +336,7 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     // Gram-form sweep while the previous sweep's largest relative off-diagonal was big
     const bool gram_sweep =
         sweep == 1 || __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[(sweep - 1) & 1]) >
-                          (SP ? 1.5 : JD_GRAM_OFF * JD_GRAM_OFF);
+                          (SP ? 1.5 : 0.5);  // flag levels of note_off
     for (int step = 0; step < nbe - 1; ++step) {
       for (int bp = crank; bp < nbe / 2; bp += C) {
         int I, J;
@@ -611,6 +615,10 @@ __global__ void __launch_bounds__(JD_THREADS, JdT<T>::MINB) k_jacobi_blk(const P
     // binary32 phase: every pair of this sweep was already below the hand-over level when it was
     // evaluated (its rotations leave ~ that level squared): the binary64 phase takes over
     if (SP && __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]) < 0.5) break;
+    // binary64, column form: every pair of this sweep was below JD_LAST_OFF when it was evaluated, so its
+    // rotations leave relative off-diagonals of order JD_LAST_OFF^2 / gap, below tol: the rotation-free
+    // sweep that would confirm it is not run (the p-bit stages decide convergence, R19)
+    if (!SP && !gram_sweep && __longlong_as_double((long long)*(volatile unsigned long long*)&it.offmax[sweep & 1]) < 0.2) break;
   }
   if (crank == 0 && threadIdx.x == 0) *(SP ? it.sweeps_s : it.sweeps_d) = sweep;
   if (jac_trace_items && crank == 0 && threadIdx.x == 0 && (int)(blockIdx.x / C) < jac_trace_items)

@@ -364,12 +364,16 @@ inline void pre_skip_descs(const PreBufs<L>& pb, PreItem* pi, GemmT* gt, size_t 
   for (int k = 0; k < pre_slots<L>(); ++k)
     gt[k * stride] = GemmT{nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, 1, pb.eOne, nullptr, nullptr, 0, 0, 0, 0, 0, 0, nullptr};
 }
-// One GemmT launch over n items: the tensor-core path (tcgemm.cuh) for the 280-bit tier (its
-// 41 slice tiles of A and B fit shared memory; the 512-bit tier's 77 do not) unless
-// MPS_TC=0, else (or when its scratch cannot be allocated) the IMAD.WIDE kernel.  Launch count.
+// One GemmT launch over n items: the tensor-core path (tcgemm.cuh; LG <= TC_MAX_LG digits: with
+// the staged pipeline any slice count fits, at 19 digits a slice-weight group sums <= 68 pairs x
+// K <= 512 products < 2^14, below 2^30) unless MPS_TC=0, else (or when its scratch cannot be
+// allocated) the IMAD.WIDE kernel.  Launch count.
+#ifndef TC_MAX_LG
+#define TC_MAX_LG 19
+#endif
 template <int L, int LG, int Z, int NZA = 0, int NZB = 0, int ZOUT = 0>
 inline int run_gemm(const GemmT* d, int n, int maxR, int maxC, int maxK, dim3 grid, cudaStream_t st) {
-  if constexpr (LG <= 10) {
+  if constexpr (LG <= TC_MAX_LG) {
     if (tc_enabled() && maxR > 0 && maxC > 0 && maxK > 0) {
       const int nl = launch_gemm_tc<L, LG, Z, NZA, NZB, ZOUT>(d, n, maxR, maxC, maxK, st);
       if (nl >= 0) return nl;
@@ -740,7 +744,7 @@ int launch_update2(int p, double thr, const Upd2Args* a, int n, void* ws, cudaSt
   // a1 contraction: the thread-per-element k_gemm measured 10% faster than the tiled
   // k_gemm_t at K = chi (92.7 vs 102.5 ms for 296 chi=128 items; with the three-product
   // k_gemm_t still 1.5% slower per bench step, v26); hgc stays as the tiled form
-  if (L <= 10 && tc_enabled()) {  // on the tensor cores (tcgemm.cuh), as the GemmT form hgc
+  if (L <= TC_MAX_LG && tc_enabled()) {  // on the tensor cores (tcgemm.cuh), as the GemmT form hgc
     int mr = 0, mc = 0, mk = 0;
     for (int b = 0; b < n; ++b) {
       mr = std::max(mr, hgc[b].rows);
