@@ -171,20 +171,17 @@ __device__ __forceinline__ dd xs_g_dd(const int32_t* p, size_t ld) {
 // g = G_pq); s is rounded to the XD-digit grid and c - 1 = -|s|^2 / (1 + sqrt(1 - |s|^2))
 // computed from the rounded s, so that the rotation is unitary to ~2^-(28 XD).
 // sel: 0 rotates PreItem::X1 (after Newton-Schulz iteration 0), 1 PreItem::X (iteration 1).
-// gemm: pairs with small s are written into E (the X buffer the sweep does not rotate: sel 0 ->
-// PreItem::X, 1 -> X1; zeroed by k_xs_zero) instead of being flagged for k_xs_apply; *xs_big
-// receives the number of pairs left to k_xs_apply.
+// (Sequential form only, MPS_XS_GEMM=0; the GEMM form computes its coefficients in k_xs_emat.)
 template <int L, int XD>
-__global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
+__global__ void k_xs_params(const PreItem* items) {
   using T = XsT<XD>;
   const PreItem it = items[blockIdx.x];
   const int N = it.N, NP = N / 2;
   if (N < 2 || it.X1 == nullptr) return;
-  int32_t* E = sel ? it.X1 : it.X;
   extern __shared__ dd xs_alpha[];  // [N]
   __shared__ double s_tr;
-  __shared__ int s_nrot, s_nbig, s_emax;
-  if (threadIdx.x == 0) { s_nbig = 0; s_emax = -9999; }
+  __shared__ int s_nrot, s_emax;
+  if (threadIdx.x == 0) s_emax = -9999;
   for (int p = threadIdx.x; p < N; p += blockDim.x) xs_alpha[p] = xs_g_dd<L, XD>(it.G + ((size_t)(p * 2) * L) * N + p, N);
   if (threadIdx.x == 0) s_nrot = 0;
   __syncthreads();
@@ -213,37 +210,7 @@ __global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
         const dd gr = xs_g_dd<L, XD>(gp, N), gi = xs_g_dd<L, XD>(gp + (size_t)L * N, N);
         const dd g2 = dd_add(dd_mul(gr, gr), dd_mul(gi, gi));
         const dd d = dd_add(aq, dd_neg(ap));
-        // GEMM form, |gamma|^2 <= 2^-60 d^2 (every pair but the near-degenerate ones): the rotation
-        // to first order, s = gamma / d (R17's s = sgn(d) gamma / (r c) has r c = |d| (1 + O(|gamma|^2
-        // / d^2)): relative 2^-60 in a coefficient whose residual is second order anyway), c = 1
-        if (gemm && g2.hi > thr2 * pa && g2.hi <= 8.673617379884035e-19 * (d.hi * d.hi)) {
-          const dd inv = dd_div({1.0, 0.0}, d);
-          int32_t Kr[XD], Ki[XD];
-          const dd sr = xs_round_grid<XD>(dd_mul(inv, gr), Kr);
-          const dd si = xs_round_grid<XD>(dd_mul(inv, gi), Ki);
-          if (fabs(sr.hi) < ldexp(1.0, -T::EBIG) && fabs(si.hi) < ldexp(1.0, -T::EBIG)) {
-            flag = 4;
-            int32_t* e1 = E + ((size_t)(q * 2) * L + (L - XD)) * N + p;
-            int32_t* e2 = E + ((size_t)(p * 2) * L + (L - XD)) * N + q;
-#pragma unroll
-            for (int k = 0; k < XD; ++k) {
-              e1[(size_t)k * N] = Kr[k];
-              e1[(size_t)(L + k) * N] = Ki[k];
-              e2[(size_t)k * N] = -Kr[k];
-              e2[(size_t)(L + k) * N] = Ki[k];
-            }
-            if (jac_trace_items) {
-              atomicAdd(&s_nrot, 1);
-              int ex;
-              frexp(fmax(fabs(sr.hi), fabs(si.hi)), &ex);
-              atomicMax(&s_emax, ex);
-            }
-            const dd tg = dd_mul(g2, inv);  // t |g| to first order (signed like d)
-            xs_alpha[p] = dd_add(ap, dd_neg(tg));
-            xs_alpha[q] = dd_add(aq, tg);
-          }
-        }
-        if (flag == 0 && g2.hi > thr2 * pa) {
+        if (g2.hi > thr2 * pa) {
           const dd ad = d.hi < 0 ? dd_neg(d) : d;
           const dd r = dd_sqrt(dd_add(dd_mul(d, d), dd_scale(g2, 2)));
           const dd c = dd_sqrt(dd_div(dd_add(ad, r), dd_scale(r, 1)));
@@ -269,21 +236,6 @@ __global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
 #pragma unroll
           for (int k = 0; k < 3 * T::P / 4; ++k) rec[k] = make_int4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
           flag = 1 | ((zc && zs) ? 2 : 0);
-          if (gemm && fabs(sr.hi) < ldexp(1.0, -T::EBIG) && fabs(si.hi) < ldexp(1.0, -T::EBIG)) {
-            // E_pq = s (row p, column q), E_qp = -conj(s); top XD of the L stored digits
-            flag = 4;
-            int32_t* e1 = E + ((size_t)(q * 2) * L + (L - XD)) * N + p;
-            int32_t* e2 = E + ((size_t)(p * 2) * L + (L - XD)) * N + q;
-#pragma unroll
-            for (int k = 0; k < XD; ++k) {
-              e1[(size_t)k * N] = Kr[k];
-              e1[(size_t)(L + k) * N] = Ki[k];
-              e2[(size_t)k * N] = -Kr[k];
-              e2[(size_t)(L + k) * N] = Ki[k];
-            }
-          } else if (gemm) {
-            atomicAdd(&s_nbig, 1);
-          }
           if (jac_trace_items) {
             atomicAdd(&s_nrot, 1);
             int ex;
@@ -299,10 +251,10 @@ __global__ void k_xs_params(const PreItem* items, int sel, int gemm) {
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0 && it.xs_big) *it.xs_big = gemm ? s_nbig : -1;
+  if (threadIdx.x == 0 && it.xs_big) *it.xs_big = -1;  // k_xs_apply applies every record
   if (jac_trace_items && threadIdx.x == 0 && (int)blockIdx.x < jac_trace_items)
-    printf("xsweep(%d digits) item %d N %d rotated %d of %d pairs (%d as sequential rotations), max |s| < 2^%d, alpha0 %.6e trace %.6e\n",
-           XD, (int)blockIdx.x, N, s_nrot, NP * (N - 1), gemm ? s_nbig : s_nrot, s_emax, xs_alpha[0].hi, s_tr);
+    printf("xsweep(%d digits, sequential) item %d N %d rotated %d of %d pairs, max |s| < 2^%d, alpha0 %.6e trace %.6e\n",
+           XD, (int)blockIdx.x, N, s_nrot, NP * (N - 1), s_emax, xs_alpha[0].hi, s_tr);
 }
 
 // GEMM form (R26), parallel over the pairs: every pair's coefficient comes from the Gram matrix as
@@ -615,7 +567,7 @@ inline int launch_xsweep(const PreItem* d, int n, int maxN, int sel, cudaStream_
   if (n <= 0 || maxN < 2) return 0;
   jacobi_trace_init();
   const int thr = std::min(1024, std::max(32, ((maxN / 2 + 31) / 32) * 32));
-  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d, sel, 0);
+  k_xs_params<L, XD><<<n, thr, (size_t)maxN * sizeof(dd), st>>>(d);
   return 1 + launch_xs_apply<L, XD>(d, n, maxN, sel, st);
 }
 // GEMM form, first half: E from G (the caller then runs the two GEMMs, k_xs_copy and launch_xs_apply)

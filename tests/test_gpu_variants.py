@@ -10,6 +10,8 @@ parity tests in a subprocess with a debug switch (the switches are read once per
                        tensor cores (tcgemm.cuh; the 512-bit tier always uses k_gemm_t)
   MPS_XSWEEP=0         no 112-bit refinement sweep of the preconditioner's basis between the first
                        two Newton-Schulz iterations (R22)
+  MPS_JD_SP=0          the block Jacobi of the preconditioner runs in binary64 from the start (no binary32
+                       first phase and hand-over, R27)
   MPS_XS_GEMM=0        the refinement sweeps apply their rotations sequentially (k_xs_apply) instead of as
                        the two GEMMs X + X F, F = E + E E / 2 (R26)
   MPS_FO=0             the last p-bit sweep runs as k_jacobi instead of the first-order GEMM finish (R23)
@@ -28,9 +30,9 @@ TESTS = ["tests/test_gpu_update2.py::test_update_parity", "tests/test_gpu_mps.py
 
 
 @pytest.mark.parametrize("switch", ["MPS_NO_PRECOND", "MPS_ACCUMULATE_V", "MPS_NS_FORCE_ZERR", "MPS_NO_CERT", "MPS_TC",
-                                    "MPS_XSWEEP", "MPS_XS_GEMM", "MPS_FO"])
+                                    "MPS_XSWEEP", "MPS_XS_GEMM", "MPS_FO", "MPS_JD_SP"])
 def test_path_parity(switch):
-    env = dict(os.environ, **{switch: "0" if switch in ("MPS_TC", "MPS_XSWEEP", "MPS_XS_GEMM", "MPS_FO") else "1"})
+    env = dict(os.environ, **{switch: "0" if switch in ("MPS_TC", "MPS_XSWEEP", "MPS_XS_GEMM", "MPS_FO", "MPS_JD_SP") else "1"})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider"] + TESTS, cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
