@@ -201,8 +201,9 @@ int mps_last_launch_count(void);
  * launching stream.  which: 0 p-bit Jacobi SVD kernel (a3), 1 contraction+gate (a1-a2),
  * 2 truncate+split (a4-a5), 3 binary64 preconditioner + Newton-Schulz + refinement sweeps +
  * A_1 = Theta' X + first-order finish (R19, R22, R23), 4 recovery of V (R16); inside
- * those: 5 the binary64 block Jacobi kernel, 6 the refinement sweeps, 7 every tensor-core MMA
- * kernel.  enable(1) clears and starts recording; query syncs and sums the durations. */
+ * those: 5 the binary64 phase of the block Jacobi, 6 the refinement-sweep kernels, 7 every
+ * tensor-core MMA kernel, 8 the binary32 phase of the block Jacobi and its hand-over (R27).
+ * enable(1) clears and starts recording; query syncs and sums the durations. */
 int mps_profile_enable(int on);
 int mps_profile_query(int which, double* total_ms, int* launches);
 /* Totals over the Jacobi problems run since mps_profile_enable(1): [0] rotations applied,
@@ -211,7 +212,8 @@ int mps_profile_query(int which, double* total_ms, int* launches);
  * (zero-digit variants counted exactly), [5] Jacobi problems that ended on the certified
  * stop instead of a rotation-free sweep (R21), [6] algorithmic DFMA of the binary64
  * block Jacobi (Gram, inner rotations, W applications as formed), [7] int8 multiply-accumulates
- * issued to the tensor cores (MMAs x 128 x 64 x 32).  mps_profile_counts returns [0..3],
+ * issued to the tensor cores (MMAs x 128 x 128 x 32), [8] algorithmic FFMA of the binary32 phase
+ * of the block Jacobi.  mps_profile_counts returns [0..3],
  * mps_profile_counts_n the first n (1..16; the rest reserved, 0).  bench.py derives the
  * roofline fractions from them. */
 int mps_profile_counts(long long* out4);

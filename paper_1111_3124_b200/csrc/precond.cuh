@@ -1,7 +1,8 @@
 // Mixed-precision preconditioning of the one-sided Jacobi SVD (R19).
 //
 //   Theta' (fixed point, p bits)  --k_fx_to_d-->  Theta_d (binary64, scaled by 2^-e)
-//   one-sided Jacobi in binary64 on Theta_d     -->  V_d  (unitary to ~1e-14)
+//   one-sided block Jacobi on Theta_d, first in binary32, then in binary64 (R27)
+//                                                -->  V_d  (unitary to ~1e-14)
 //   X_0 = V_d (exact digits), Newton-Schulz in fixed point:
 //       D_k = I - X_k^H X_k,   X_{k+1} = X_k + X_k D_k / 2        (quadratic: 2^-45 -> 2^-90 -> ...)
 //   A_1 = Theta' X   (exactly unitary X to the working precision)

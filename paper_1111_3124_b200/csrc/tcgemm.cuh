@@ -1,25 +1,27 @@
-// Tensor-core multiprecision GEMM: the GemmT products of the preconditioner (A_1 = Theta' X,
-// P = Theta' X_{n-1}, A_1 = P + P D/2) and of the recovery of V (V = Theta'^H A Sigma^-2), on
-// the 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM) instead of the
-// IMAD.WIDE pipe (DESIGN.md §4 "Tensor cores").
+// Tensor-core multiprecision GEMM: every GemmT product of the update (the contraction, the
+// Newton-Schulz iterations, the refinement-sweep GEMMs, A_1 = Theta' X / P = Theta' X_{n-1} /
+// A_1 = P + P D/2, the Gram matrices and A_1 (I + E) of the first-order finish, the recovery of
+// V) on the 5th-generation tensor cores (tcgen05.mma kind::i8, accumulators in TMEM) instead of
+// the IMAD.WIDE pipe (DESIGN.md §4 "Tensor cores").
 //
 // Every p-bit operand value of the LG-digit frame (balanced radix-2^28 int32 digits) is
-// re-sliced EXACTLY into S = 4 LG + 1 signed slices, x = sum_s u_s 2^(7s): three balanced 7-bit
-// slices and a fourth (|u| <= 128) per digit, the last slice the carry out of the top digit.  A real product of two values is then
-// sum_{s,t} u_s v_t 2^(7(s+t)), and a real GEMM C = A B is, per slice-weight group d = s + t,
-// the int8 GEMM sum_{s+t=d} A_s B_t with exact int32 accumulation (each term <= 2^14, K <= 512,
-// <= 41 pairs per group, 2 real GEMMs per complex plane: < 2^30).  Groups d >= 4 (LG - 2) are
-// formed (a superset of the digit pairs i + j >= LG - 2 the IMAD path keeps, so the truncated
-// product is at least as accurate); the epilogue combines the groups into the int64 digit
-// columns of the IMAD path and runs the same rounding / store code (gemm_t_store).  Complex:
-// Re C = Ar Br + Ai (-Bi), Im C = Ar Bi + Ai Br (4 real products, accumulated in TMEM).
+// re-sliced EXACTLY into S = floor((7 LG + 1) / 2) + 1 balanced base-256 slices of the whole
+// value, x = sum_s u_s 2^(8s), u_s in [-128, 127] (TC_SLICE_BITS = 7 keeps the first version:
+// four 7-bit slices per digit).  A real product of two values is then sum_{s,t} u_s v_t 2^(8(s+t)),
+// and a real GEMM C = A B is, per slice-weight group d = s + t, the int8 GEMM
+// sum_{s+t=d} A_s B_t with exact int32 accumulation (each term <= 2^14, K <= 512, <= 68 pairs per
+// group at 19 digits: < 2^30).  Groups of weight >= 2^(28 (LG - 2)) are formed (a superset of the
+// digit pairs i + j >= LG - 2 the IMAD path keeps, so the truncated product is at least as
+// accurate); the epilogue combines them into the int64 digit columns of the IMAD path and runs
+// the same rounding / store code (gemm_t_store).  Complex: Re C = Ar Br + Ai (-Bi),
+// Im C = Ar Bi + Ai Br (4 real products, accumulated in TMEM).
 //
-// Kernels per chunk of items: k_tc_slice_a / k_tc_slice_b (digits -> int8 slice tiles in the
-// UMMA K-major no-swizzle layout, so that staging is a straight copy), k_tc_mma (one CTA per
-// 128 x 32 output tile and plane: 16 groups at a time in TMEM (16 x 32 of its 512 columns),
-// for each group chunk, term and k block the needed slice tiles of A (4 KB) and B (1 KB) are
-// staged by cp.async and one thread issues the pair MMAs; the group sums are drained by
-// tcgen05.ld to global memory), k_tc_epi (one thread per output entry).
+// Kernels per scratch chunk of items: k_tc_slice_a / k_tc_slice_b (digits -> int8 slice tiles in
+// the UMMA K-major no-swizzle layout, so that staging is a straight bulk copy), k_tc_mma (one CTA
+// per 128 x TC_N output tile and plane: TC_GCH groups at a time in TMEM; a producer warp streams
+// stages of TC_SBK A-slice tiles and the B-slice tiles they meet into TC_NSTG shared-memory
+// buffers with cp.async.bulk + mbarrier transaction counts, TC_WARPS warps issue the MMAs of
+// their group and drain the chunk sums with tcgen05.ld), k_tc_epi (one thread per output entry).
 #pragma once
 #include <cstdio>
 #include <cstdlib>
