@@ -47,24 +47,24 @@ def key(i: int):
     return (gen.SEED0 + 4, layer, site)
 
 
-def inputs(i: int):
+def inputs(i: int, chi: int = CHI):
     _, _, dl, dm, dr = ITEMS[i]
-    return gen.canonical_update_inputs(P, CHI, dl, dm, dr, *key(i))
+    return gen.canonical_update_inputs(P, chi, dl, dm, dr, *key(i))
 
 
-def grid(i: int):
-    N = 2 * CHI
+def grid(i: int, chi: int = CHI):
+    N = 2 * chi
     g = gen.rng(*key(i), 0x9A1D)
     rows = sorted(set([0, N - 1] + g.choice(N, NGRID - 2, replace=False).tolist()))
     cols = sorted(set([0, N - 1] + g.choice(N, NGRID - 2, replace=False).tolist()))
     return rows[:NGRID], cols[:NGRID]
 
 
-def pmax(GL, GR, lam, lam_l, lam_r):
-    gl = R.cplx_to_complex128(GL).reshape(2, CHI, CHI) * R.to_float64(lam_l)[None, :, None]
-    gr = R.cplx_to_complex128(GR).reshape(2, CHI, CHI) * R.to_float64(lam_r)[None, None, :]
-    gl = gl.reshape(2 * CHI, CHI)
-    gr = gr.transpose(1, 0, 2).reshape(CHI, 2 * CHI)
+def pmax(GL, GR, lam, lam_l, lam_r, chi: int = CHI):
+    gl = R.cplx_to_complex128(GL).reshape(2, chi, chi) * R.to_float64(lam_l)[None, :, None]
+    gr = R.cplx_to_complex128(GR).reshape(2, chi, chi) * R.to_float64(lam_r)[None, None, :]
+    gl = gl.reshape(2 * chi, chi)
+    gr = gr.transpose(1, 0, 2).reshape(chi, 2 * chi)
     return float(np.abs((gl * R.to_float64(lam)[None, :]) @ gr).max())
 
 
@@ -72,25 +72,29 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--item", type=int, action="append", required=True)
     ap.add_argument("--outdir", default=os.path.join(ROOT, "tests", "golden"))
+    ap.add_argument("--chi", type=int, default=CHI,
+                    help="bond dimension of the window (configs[4] saturates at 256: ~5 h per item on one core; "
+                         "128 is the half-size stand-in, ~45 min)")
     a = ap.parse_args()
+    chi = a.chi
     for it in a.item:
-        A, B, ll, lm, lr, U = inputs(it)
+        A, B, ll, lm, lr, U = inputs(it, chi)
         t0 = time.time()
-        o = oracle.update2_batch(P, 1, CHI, CHI, CHI, CHI, THR, A, B, U, lam_l=ll, lam_m=lm, lam_r=lr, nthreads=1)
+        o = oracle.update2_batch(P, 1, chi, chi, chi, chi, THR, A, B, U, lam_l=ll, lam_m=lm, lam_r=lr, nthreads=1)
         secs = time.time() - t0
         k = int(o["k"][0])
-        rows, cols = grid(it)
-        Ps = p_sample(P, CHI, k, o["GL"], o["GR"], o["lam"], rows, cols, lam_l=ll, lam_r=lr)
+        rows, cols = grid(it, chi)
+        Ps = p_sample(P, chi, k, o["GL"], o["GR"], o["lam"], rows, cols, lam_l=ll, lam_r=lr)
         res = {
             "what": "oracle two-site update of a configs[4]-shaped gate (tools/make_cfg5_golden.py, oracle/ only)",
-            "prec": P, "chi": CHI, "item": it, "chi_max": CHI, "thr": THR, "spec": list(ITEMS[it]),
+            "prec": P, "chi": chi, "item": it, "chi_max": chi, "thr": THR, "spec": list(ITEMS[it]),
             "key": list(key(it)),
             "sigma": o["sigma"].tobytes().hex(), "k": k, "lam": o["lam"].tobytes().hex(),
             "sweeps": int(o["sweeps"][0]), "P_rows": rows, "P_cols": cols, "P": Ps.tobytes().hex(),
-            "Pmax": pmax(o["GL"], o["GR"], o["lam"], ll, lr),
+            "Pmax": pmax(o["GL"], o["GR"], o["lam"], ll, lr, chi),
             "seconds": secs, "threads": 1, "cpu": platform.processor() or platform.machine(),
         }
-        out = os.path.join(a.outdir, f"cfg5_p{P}_chi{CHI}_item{it}.json")
+        out = os.path.join(a.outdir, f"cfg5_p{P}_chi{chi}_item{it}.json")
         with open(out, "w") as f:
             json.dump(res, f)
         print("wrote", out, f"{secs:.0f}s sweeps {res['sweeps']} k {k}", flush=True)
