@@ -1,7 +1,7 @@
 #!/bin/bash
 # One gpurun call of the build -> measure loop for a switchable path: a short parity check,
 # then bench lines of the default library and with the switch set (A/B on one box).
-#   bash tools/gpu_ab.sh <tag> <ENV=VALUE> [pytest targets...]
+#   bash tools/jobs/gpu_ab.sh <tag> <ENV=VALUE> [pytest targets...]
 set -u
 TAG=$1; AB=$2; shift 2
 OUT=gpurun_out

@@ -1,7 +1,7 @@
 #!/bin/bash
 # One gpurun call of the build -> measure loop: GPU test suite, bench lines of the default
 # library and of an A/B library (optional), whole-circuit timings.  Usage on the GPU box:
-#   bash tools/gpu_check.sh <tag> [ab_library.so] [extra pytest args]
+#   bash tools/jobs/gpu_check.sh <tag> [ab_library.so] [extra pytest args]
 set -u
 TAG=$1
 AB=${2:-}

@@ -1,7 +1,7 @@
 #!/bin/bash
 # A/B of a development build of the library (MPS_B200_SO) against the default one on one box:
 # parity tests with the alternative build, then bench lines of both.
-#   bash tools/gpu_job_s8.sh <tag> <alt .so> [pytest targets...]
+#   bash tools/jobs/gpu_job_s8.sh <tag> <alt .so> [pytest targets...]
 set -u
 TAG=$1; ALT=$2; shift 2
 OUT=gpurun_out; mkdir -p $OUT

@@ -1,6 +1,6 @@
 #!/bin/bash
 # v56: full GPU suite + smoke on the default build, launch list of one bench step, bench lines of
-# development builds.   bash tools/gpu_job_v56.sh <tag> [name=path.so ...]
+# development builds.   bash tools/jobs/gpu_job_v56.sh <tag> [name=path.so ...]
 set -u
 TAG=$1; shift
 OUT=gpurun_out; mkdir -p $OUT

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of development builds (MPS_B200_SO) on one box: for each library a short parity run and a
-# bench line.   bash tools/gpu_job_variants.sh <tag> <name=path.so> ...
+# bench line.   bash tools/jobs/gpu_job_variants.sh <tag> <name=path.so> ...
 set -u
 TAG=$1; shift
 OUT=gpurun_out; mkdir -p $OUT

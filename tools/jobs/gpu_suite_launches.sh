@@ -1,6 +1,6 @@
 #!/bin/bash
 # One gpurun call: the full GPU test suite, smoke(), and the launch list of one bench step.
-#   bash tools/gpu_suite_launches.sh <tag>
+#   bash tools/jobs/gpu_suite_launches.sh <tag>
 set -u
 TAG=${1:-cur}
 OUT=gpurun_out
